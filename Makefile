@@ -1,0 +1,35 @@
+# Builds the B200-native engine: paper_2504_06408_b200/libspgemm_b200.so
+# (sm_100a only) and the parity oracle (oracle/).  `make -j` from the repo root.
+NVCC      ?= nvcc
+ARCH      ?= -gencode arch=compute_100a,code=sm_100a
+NVFLAGS   ?= -O3 -std=c++17 -lineinfo $(ARCH) -Xcompiler -fPIC,-fvisibility=hidden -Xptxas -warn-spills \
+             --expt-relaxed-constexpr -Iinclude
+PKG       := paper_2504_06408_b200
+SRC       := $(PKG)/csrc
+BUILD     := build
+CU_SRCS   := $(wildcard $(SRC)/*.cu)
+CXX_SRCS  := $(wildcard $(SRC)/*.cpp)
+OBJS      := $(patsubst $(SRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS)) $(patsubst $(SRC)/%.cpp,$(BUILD)/%.cpp.o,$(CXX_SRCS))
+HDRS      := $(wildcard $(SRC)/*.cuh) $(wildcard $(SRC)/*.h) include/spgemm_b200.h
+LIB       := $(PKG)/libspgemm_b200.so
+
+all: $(LIB) oracle
+
+$(BUILD)/%.o: $(SRC)/%.cu $(HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(BUILD)/%.cpp.o: $(SRC)/%.cpp $(HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -x c++ -c $< -o $@
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lnccl -lrt -lpthread
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -rf $(BUILD) $(LIB)
+
+.PHONY: all oracle clean

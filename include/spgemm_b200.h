@@ -1,0 +1,254 @@
+/*
+ * spgemm_b200.h — C-ABI of the B200-native distributed semiring SpGEMM engine.
+ *
+ * This is the drop-in boundary for the reference library `spsumma`
+ * (/root/reference/proj/include/spsumma, header-only C++20).  Each entry point
+ * below names the reference interface it replaces (file:line relative to that
+ * directory).  Plain pointers and sizes only: no C++ or torch types cross it.
+ * The reference-shaped C++ facade in include/spsumma_b200.hpp sits on top.
+ *
+ * Conventions
+ *  - Semirings are identified by SPG_SR_* ids (the reference's closed
+ *    SemiringId table, semiring.hpp:122-149, plus the two BASELINE semirings).
+ *  - Host matrices (spg_hcsr) use the reference's index width: int64 offsets
+ *    and int64 indices (common.hpp:10), values in ValueCodec byte layout
+ *    (serialize.hpp:29-76; bool = 1 byte 0/1).
+ *  - Device matrices (spg_dcsr) use int64 offsets and int32 block-local
+ *    indices; values have the same byte layout as on the host.
+ *  - A CSR and a CSC share the struct: `ptr` runs over rows (CSR) or columns
+ *    (CSC); nrows/ncols are always the logical dims.
+ *  - Every call returns an spg_status; the message of the last failure is in
+ *    spg_last_error(ctx) (or spg_last_error(NULL) for calls without a ctx).
+ *    Status codes map 1:1 onto the reference exception classes
+ *    (common.hpp:12-73) so the C++ facade rethrows the matching type.
+ */
+#ifndef SPGEMM_B200_H
+#define SPGEMM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPG_API __attribute__((visibility("default")))
+
+/* semiring ids: 0-3 are the reference built-ins (semiring.hpp:43-120) */
+enum {
+  SPG_SR_ARITHMETIC = 0,   /* double (+, x)                       semiring.hpp:43-54 */
+  SPG_SR_MINPLUS = 1,      /* double (min, +), zero = +inf         semiring.hpp:59-72 */
+  SPG_SR_BOOLEAN = 2,      /* bool (or, and), 1 byte               semiring.hpp:75-86 */
+  SPG_SR_MINSELECT = 3,    /* {double, int64}, non-commutative mul semiring.hpp:97-120 */
+  SPG_SR_TROPICAL_I32 = 4, /* int32 (min, saturating +)            BASELINE config 2 */
+  SPG_SR_MAXTIMES = 5,     /* {double w, uint64 tag} (max, x)      BASELINE config 5 */
+  SPG_SR_COUNT = 6
+};
+
+/* status codes (reference exception classes, common.hpp:12-73) */
+enum {
+  SPG_OK = 0,
+  SPG_ERR_SHAPE = 1,                 /* ShapeError */
+  SPG_ERR_GRID = 2,                  /* GridError */
+  SPG_ERR_UNSUPPORTED_SEMIRING = 3,  /* UnsupportedSemiringError */
+  SPG_ERR_PROTOCOL = 4,              /* ProtocolError */
+  SPG_ERR_MALFORMED = 5,             /* MalformedInputError */
+  SPG_ERR_INVALID_RANGE = 6,         /* InvalidRangeError */
+  SPG_ERR_INTERNAL = 7,              /* InternalError */
+  SPG_ERR_ABORTED = 8,               /* AbortedError */
+  SPG_ERR_DEADLOCK = 9,              /* DeadlockError */
+  SPG_ERR_CUDA = 10,                 /* CUDA runtime failure */
+  SPG_ERR_OOM = 11,                  /* device or host allocation failure */
+  SPG_ERR_NCCL = 12,                 /* NCCL failure (surfaces as ProtocolError) */
+  SPG_ERR_ARG = 13                   /* invalid argument (null pointer, bad id) */
+};
+
+/* communication paths / modes (comm.hpp:14-55) */
+enum { SPG_PATH_HOST = 0, SPG_PATH_DEVICE = 1 };
+enum { SPG_COMM_HOST_ONLY = 0, SPG_COMM_DEVICE_ONLY = 1, SPG_COMM_HYBRID = 2 };
+/* device transport for the device path */
+enum { SPG_DEV_NCCL = 0, SPG_DEV_P2P = 1 };
+/* scopes (fabric.hpp:34-43) */
+enum { SPG_SCOPE_ROW = 0, SPG_SCOPE_COL = 1 };
+
+typedef struct spg_ctx spg_ctx;
+typedef struct spg_comm spg_comm;
+
+/* host CSR/CSC in the reference layout (formats.hpp:39-86) */
+typedef struct {
+  int64_t nrows, ncols, nnz;
+  int64_t* ptr; /* nseg + 1 */
+  int64_t* idx; /* nnz */
+  void* vals;   /* nnz * spg_value_size(sr) bytes */
+} spg_hcsr;
+
+/* host DCSC (formats.hpp:56-70): jc[njc] nonempty column ids, cp[njc + 1] */
+typedef struct {
+  int64_t nrows, ncols, nnz, njc;
+  int64_t* jc;
+  int64_t* cp;
+  int64_t* rowids;
+  void* vals;
+} spg_hdcsc;
+
+/* device CSR/CSC */
+typedef struct {
+  int64_t nrows, ncols, nnz;
+  int64_t* ptr; /* device, nseg + 1 */
+  int32_t* idx; /* device, nnz */
+  void* vals;   /* device, nnz * value size */
+} spg_dcsr;
+
+/* per-call statistics of a local multiply / merge */
+typedef struct {
+  int64_t products;        /* F: intermediate products (flops = 2F) */
+  int64_t nnz_out;
+  int64_t rows_per_bin[8]; /* 0: empty, 1: warp-ESC, 2-5: hash tables, 6: dense */
+  double ms_analyse;       /* row products + binning + offsets */
+  double ms_numeric;       /* accumulate kernels */
+  double ms_compact;       /* output scan + compaction */
+  double ms_total;
+  int64_t kernels;         /* kernels launched by the call */
+} spg_mult_stats;
+
+/* ---------------------------------------------------------------- misc */
+SPG_API const char* spg_version(void);
+SPG_API const char* spg_last_error(const spg_ctx* ctx); /* ctx may be NULL */
+SPG_API int spg_value_size(int sr);
+SPG_API int spg_semiring_by_name(const char* name); /* semiring_by_name, semiring.hpp:125-133; -1 if unknown */
+SPG_API const char* spg_semiring_name(int sr);
+SPG_API int spg_semiring_is_commutative(int sr);  /* SR::is_commutative_mul */
+
+/* ------------------------------------------------------------- context */
+SPG_API int spg_ctx_create(int device, spg_ctx** out);
+SPG_API void spg_ctx_destroy(spg_ctx* ctx);
+SPG_API void* spg_ctx_stream(spg_ctx* ctx);                 /* cudaStream_t */
+SPG_API int spg_ctx_set_stream(spg_ctx* ctx, void* stream); /* borrow a caller stream */
+SPG_API int spg_ctx_sync(spg_ctx* ctx);
+SPG_API uint64_t spg_ctx_kernel_launches(const spg_ctx* ctx);
+/* bytes of device scratch the numeric pass may hold at once (0 = auto: 40% of free HBM) */
+SPG_API int spg_ctx_set_scratch_budget(spg_ctx* ctx, uint64_t bytes);
+
+/* ---------------------------------------------------- device matrices */
+SPG_API int spg_dcsr_alloc(spg_ctx* ctx, int sr, int64_t nrows, int64_t ncols, int64_t nseg,
+                           int64_t nnz, spg_dcsr* out);
+SPG_API int spg_dcsr_free(spg_ctx* ctx, spg_dcsr* m);
+/* H2D of a host CSR (or CSC) with int64 -> int32 index narrowing on device */
+SPG_API int spg_upload(spg_ctx* ctx, int sr, const spg_hcsr* h, int is_csc, spg_dcsr* out);
+/* D2H into library-allocated host arrays (free with spg_hcsr_free) */
+SPG_API int spg_download(spg_ctx* ctx, int sr, const spg_dcsr* d, int is_csc, spg_hcsr* out);
+SPG_API void spg_hcsr_free(spg_hcsr* h);
+
+/* --------------------------------------------------- hot path (device) */
+/* C = A (x) B over sr.  Replaces esc_multiply (local_spgemm.hpp:83-156);
+ * same result contract: products mul(a_ik, b_kj), folded per (i, j), zeros
+ * dropped, columns strictly increasing.  ShapeError when a.ncols != b.nrows. */
+SPG_API int spg_local_multiply(spg_ctx* ctx, int sr, const spg_dcsr* a, const spg_dcsr* b,
+                               spg_dcsr* c, spg_mult_stats* stats);
+
+/* Merges C^T partials (CSR, dims block_cols x block_rows each) into the CSC
+ * C block.  Replaces merge_partials (summa.hpp:122-172): folds with SR::add,
+ * drops zeros; InternalError on an extents mismatch.  `stages`/`rounds`
+ * order the fold (stage-major, round-minor) and may be NULL (list order). */
+SPG_API int spg_merge_partials(spg_ctx* ctx, int sr, int nparts, const spg_dcsr* parts,
+                               const int* stages, const int* rounds, int64_t block_rows,
+                               int64_t block_cols, spg_dcsr* c_csc, spg_mult_stats* stats);
+
+/* matrix_checksum (checksum.hpp:20-38) of a device CSR (is_csc = 0) or CSC. */
+SPG_API int spg_checksum(spg_ctx* ctx, int sr, const spg_dcsr* m, int is_csc, uint64_t* out);
+
+/* csr_row_slice / csr_col_slice (summa.hpp:57-98) on device. */
+SPG_API int spg_csr_slice(spg_ctx* ctx, int sr, const spg_dcsr* m, int by_rows, int64_t begin,
+                          int64_t end, spg_dcsr* out);
+
+/* prepare_block (summa.hpp:30-53): host CSC (dcsc == NULL) or DCSC block ->
+ * device CSR of the block's transpose (dcsc_decompress on device, then the
+ * zero-copy reinterpretation).  UnsupportedSemiringError for minselect. */
+SPG_API int spg_prepare_block(spg_ctx* ctx, int sr, const spg_hcsr* csc, const spg_hdcsc* dcsc,
+                              spg_dcsr* prepared);
+
+/* ------------------------------------- reference-shaped host drop-ins */
+/* esc_multiply on host CSR operands (local_spgemm.hpp:83-85): H2D, device
+ * multiply, D2H.  The output arrays are library-allocated (spg_hcsr_free). */
+SPG_API int spg_esc_multiply(spg_ctx* ctx, int sr, const spg_hcsr* a, const spg_hcsr* b,
+                             spg_hcsr* c, spg_mult_stats* stats);
+
+/* generate_rmat<SR>(scale, edge_factor, seed) (rmat.hpp:15-60), bit-identical
+ * tuples, normalised row-major.  Returns host COO arrays (free with spg_free). */
+SPG_API int spg_generate_rmat(int sr, int scale, double edge_factor, uint64_t seed,
+                              int64_t* nrows, int64_t* nnz, int64_t** rows, int64_t** cols,
+                              void** vals);
+/* Erdos-Renyi-style generator with `d` column draws per row (counter-based,
+ * deduplicated) and a 3D 27-point stencil Laplacian
+ * (config 4).  value_mode 0: from_real(0.5 + u01); 1: maxtimes {0.5+u01, hash}. */
+SPG_API int spg_generate_er(int sr, int64_t n, int d, uint64_t seed, int value_mode,
+                            int64_t* nnz, int64_t** rows, int64_t** cols, void** vals);
+SPG_API int spg_generate_stencil27(int sr, int64_t N, int64_t* nrows, int64_t* nnz,
+                                   int64_t** rows, int64_t** cols, void** vals);
+/* normalised COO (row-major, unique) -> CSR / CSC host arrays, no copies of
+ * the reference's fold semantics needed (input already unique). */
+SPG_API int spg_coo_to_csr(int sr, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rows,
+                           const int64_t* cols, const void* vals, int to_csc, spg_hcsr* out);
+SPG_API void spg_free(void* p);
+
+/* ------------------------------------------------ distributed (SUMMA) */
+/* Grid helpers: block_range (dist_matrix.hpp:23-28), round_range
+ * (summa.hpp:103-107), and the pr x pc stage schedule (common refinement of
+ * A's column blocks and B's row blocks; equals the reference's q stages for
+ * a square grid).  Pure host functions, usable without a GPU. */
+SPG_API void spg_block_range(int64_t n, int q, int idx, int64_t* begin, int64_t* end);
+SPG_API void spg_round_range(int64_t n, int rounds, int round, int64_t* begin, int64_t* end);
+typedef struct {
+  int64_t lo, hi;    /* global inner-dimension interval */
+  int a_col_block;   /* A panel root column (grid col) */
+  int b_row_block;   /* B panel root row (grid row) */
+  int64_t a_off;     /* interval start relative to A's column block */
+  int64_t b_off;     /* interval start relative to B's row block */
+} spg_stage;
+SPG_API int spg_summa_schedule(int64_t inner, int pr, int pc, spg_stage* out, int cap);
+
+/* One process per GPU.  `job` names the shared-memory rendezvous segment
+ * (same on every rank of a job); rank = grid_row * pc + grid_col. */
+SPG_API int spg_comm_create(const char* job, int world, int rank, int pr, int pc, int device,
+                            uint64_t staging_bytes, spg_comm** out);
+SPG_API void spg_comm_destroy(spg_comm* comm);
+SPG_API const char* spg_comm_last_error(const spg_comm* comm);
+SPG_API int spg_comm_barrier(spg_comm* comm);
+/* Rank::exchange_sizes (fabric.hpp:335-338): host path always. */
+SPG_API int spg_exchange_sizes(spg_comm* comm, int scope, int root, int64_t triple[3]);
+/* Rank::bcast (fabric.hpp:343-349) of a device buffer; path chosen by
+ * choose_path(bytes, {mode, threshold}) (comm.hpp:45-55).  *path_out gets
+ * SPG_PATH_HOST or SPG_PATH_DEVICE.  `root` is the scope-local index. */
+SPG_API int spg_bcast(spg_comm* comm, int scope, int root, void* dev_buf, uint64_t bytes,
+                      int mode, uint64_t threshold, int* path_out);
+SPG_API int spg_comm_set_device_transport(spg_comm* comm, int transport);
+
+typedef struct {
+  int two_round;      /* SummaOptions::two_round (summa.hpp:174-177) */
+  int comm_mode;      /* CommConfig::mode (comm.hpp:36-39) */
+  uint64_t threshold; /* CommConfig::threshold_bytes */
+} spg_summa_opts;
+
+/* CostLedger (cost_ledger.hpp:31-56) with measured instead of modelled time. */
+typedef struct {
+  double ms[5]; /* prepare, broadcast, local_multiply, merge, copy */
+  uint64_t host_bcasts, device_bcasts, bytes_host_path, bytes_device_path;
+  uint64_t size_exchanges, local_multiply_calls, skipped_stages, peak_bcast_buffer_bytes;
+  int64_t products; /* F over this rank's local multiplies */
+  double ms_total;  /* time-to-C on this rank */
+} spg_ledger;
+
+/* summa25_multiply (summa.hpp:248-349), one rank's program.  a_block /
+ * b_block are this rank's host blocks as CSC, or DCSC when the dcsc pointer
+ * is non-NULL (LocalBlock, dist_matrix.hpp:41-53).  a_nrows.. are the global
+ * dims.  Output: this rank's C block as device CSC (block_rows x block_cols). */
+SPG_API int spg_summa25_multiply(spg_comm* comm, spg_ctx* ctx, int sr, int64_t a_nrows,
+                                 int64_t a_ncols, int64_t b_ncols, const spg_hcsr* a_csc,
+                                 const spg_hdcsc* a_dcsc, const spg_hcsr* b_csc,
+                                 const spg_hdcsc* b_dcsc, const spg_summa_opts* opts,
+                                 spg_dcsr* c_csc, spg_ledger* ledger);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPGEMM_B200_H */

@@ -1,0 +1,577 @@
+// The extern "C" boundary (include/spgemm_b200.h): contexts, device
+// matrices, the local multiply / merge / checksum / slice / prepare entry
+// points and the host-array drop-ins.  Every function converts C++
+// exceptions into an SPG_ERR_* status + last-error message.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "instantiate.cuh"
+#include "layout.cuh"
+
+extern "C" const spg::SrOps* spg_ops_arithmetic();
+extern "C" const spg::SrOps* spg_ops_minplus();
+extern "C" const spg::SrOps* spg_ops_boolean();
+extern "C" const spg::SrOps* spg_ops_minselect();
+extern "C" const spg::SrOps* spg_ops_tropical_i32();
+extern "C" const spg::SrOps* spg_ops_maxtimes();
+
+namespace spg {
+void gen_rmat(int, int, double, uint64_t, int64_t*, int64_t*, int64_t**, int64_t**, void**);
+void gen_er(int, int64_t, int, uint64_t, int, int64_t*, int64_t**, int64_t**, void**);
+void gen_stencil27(int, int64_t, int64_t*, int64_t*, int64_t**, int64_t**, void**);
+
+thread_local std::string g_last_error;
+
+const SrOps* ops_for(int sr) {
+  switch (sr) {
+    case SPG_SR_ARITHMETIC: return spg_ops_arithmetic();
+    case SPG_SR_MINPLUS: return spg_ops_minplus();
+    case SPG_SR_BOOLEAN: return spg_ops_boolean();
+    case SPG_SR_MINSELECT: return spg_ops_minselect();
+    case SPG_SR_TROPICAL_I32: return spg_ops_tropical_i32();
+    case SPG_SR_MAXTIMES: return spg_ops_maxtimes();
+  }
+  fail(SPG_ERR_ARG, "unknown semiring id " + std::to_string(sr));
+}
+
+template <class F>
+int guarded(spg_ctx* c, F&& f) {
+  try {
+    f();
+    return SPG_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    if (c) c->last_error = e.what();
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    if (c) c->last_error = g_last_error;
+    return SPG_ERR_OOM;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    if (c) c->last_error = e.what();
+    return SPG_ERR_INTERNAL;
+  }
+}
+
+void need(bool ok, const char* what) {
+  if (!ok) fail(SPG_ERR_ARG, what);
+}
+
+void use_device(spg_ctx* c) { SPG_CUDA(cudaSetDevice(c->device)); }
+
+// Host CSR/CSC -> device (int64 -> int32 narrowing on device).
+void upload(spg_ctx* c, int vs, const spg_hcsr* h, int is_csc, spg_dcsr* d) {
+  const int64_t nseg = is_csc ? h->ncols : h->nrows;
+  const int64_t bound = is_csc ? h->nrows : h->ncols;
+  need(h->nrows >= 0 && h->ncols >= 0 && h->nnz >= 0, "negative dims");
+  if (bound > INT32_MAX) fail(SPG_ERR_INVALID_RANGE, "block dimension exceeds int32 indices");
+  if (h->ptr == nullptr) fail(SPG_ERR_ARG, "null offsets");
+  if (h->ptr[0] != 0 || h->ptr[nseg] != h->nnz)
+    fail(SPG_ERR_MALFORMED, "offset array is not a monotone [0..nnz] map");
+  d->nrows = h->nrows;
+  d->ncols = h->ncols;
+  d->nnz = h->nnz;
+  d->ptr = dalloc<int64_t>(c, nseg + 1);
+  d->idx = dalloc<int32_t>(c, h->nnz);
+  d->vals = dalloc<char>(c, (size_t)vs * h->nnz);
+  SPG_CUDA(cudaMemcpyAsync(d->ptr, h->ptr, sizeof(int64_t) * (nseg + 1), cudaMemcpyHostToDevice, c->stream));
+  if (h->nnz > 0) {
+    DBuf<int64_t> wide(c, h->nnz);
+    SPG_CUDA(cudaMemcpyAsync(wide.p, h->idx, sizeof(int64_t) * h->nnz, cudaMemcpyHostToDevice, c->stream));
+    narrow_indices(c, wide.p, d->idx, h->nnz, bound);
+    SPG_CUDA(cudaMemcpyAsync(d->vals, h->vals, (size_t)vs * h->nnz, cudaMemcpyHostToDevice, c->stream));
+  }
+}
+
+void download(spg_ctx* c, int vs, const spg_dcsr* d, int is_csc, spg_hcsr* h) {
+  const int64_t nseg = is_csc ? d->ncols : d->nrows;
+  h->nrows = d->nrows;
+  h->ncols = d->ncols;
+  h->nnz = d->nnz;
+  h->ptr = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * (nseg + 1)));
+  h->idx = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * std::max<int64_t>(d->nnz, 1)));
+  h->vals = std::malloc((size_t)vs * std::max<int64_t>(d->nnz, 1));
+  if (!h->ptr || !h->idx || !h->vals) fail(SPG_ERR_OOM, "host allocation failed");
+  SPG_CUDA(cudaMemcpyAsync(h->ptr, d->ptr, sizeof(int64_t) * (nseg + 1), cudaMemcpyDeviceToHost, c->stream));
+  if (d->nnz > 0) {
+    DBuf<int64_t> wide(c, d->nnz);
+    widen_indices(c, d->idx, wide.p, d->nnz);
+    SPG_CUDA(cudaMemcpyAsync(h->idx, wide.p, sizeof(int64_t) * d->nnz, cudaMemcpyDeviceToHost, c->stream));
+    SPG_CUDA(cudaMemcpyAsync(h->vals, d->vals, (size_t)vs * d->nnz, cudaMemcpyDeviceToHost, c->stream));
+  }
+  SPG_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+void free_dcsr(spg_ctx* c, spg_dcsr* m) {
+  dfree(c, m->ptr);
+  dfree(c, m->idx);
+  dfree(c, m->vals);
+  m->ptr = nullptr;
+  m->idx = nullptr;
+  m->vals = nullptr;
+}
+
+}  // namespace spg
+
+using namespace spg;
+
+extern "C" {
+
+const char* spg_version(void) { return "spgemm_b200 0.1 (sm_100a)"; }
+
+const char* spg_last_error(const spg_ctx* ctx) {
+  return ctx ? ctx->last_error.c_str() : g_last_error.c_str();
+}
+
+int spg_value_size(int sr) {
+  try {
+    return ops_for(sr)->value_size;
+  } catch (...) {
+    return -1;
+  }
+}
+
+int spg_semiring_by_name(const char* name) {
+  if (!name) return -1;
+  for (int s = 0; s < SPG_SR_COUNT; ++s)
+    if (std::strcmp(name, ops_for(s)->name) == 0) return s;
+  g_last_error = std::string("unknown semiring '") + name +
+                 "' (expected arithmetic, minplus, boolean, minselect, tropical_i32, or maxtimes)";
+  return -1;
+}
+
+const char* spg_semiring_name(int sr) {
+  try {
+    return ops_for(sr)->name;
+  } catch (...) {
+    return nullptr;
+  }
+}
+
+int spg_semiring_is_commutative(int sr) {
+  try {
+    return ops_for(sr)->commutative ? 1 : 0;
+  } catch (...) {
+    return -1;
+  }
+}
+
+int spg_ctx_create(int device, spg_ctx** out) {
+  return guarded(nullptr, [&] {
+    need(out != nullptr, "null out");
+    auto* c = new spg_ctx();
+    try {
+      c->device = device;
+      SPG_CUDA(cudaSetDevice(device));
+      SPG_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+      SPG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+      SPG_CUDA(cudaDeviceGetDefaultMemPool(&c->pool, device));
+      uint64_t thr = UINT64_MAX;  // keep freed blocks cached in the pool
+      SPG_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+void spg_ctx_destroy(spg_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->cub_tmp) cudaFreeAsync(c->cub_tmp, c->stream);
+  cudaStreamSynchronize(c->stream);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+void* spg_ctx_stream(spg_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int spg_ctx_set_stream(spg_ctx* c, void* stream) {
+  return guarded(c, [&] {
+    need(c != nullptr, "null ctx");
+    SPG_CUDA(cudaStreamSynchronize(c->stream));
+    if (c->own_stream) SPG_CUDA(cudaStreamDestroy(c->stream));
+    c->stream = static_cast<cudaStream_t>(stream);
+    c->own_stream = false;
+  });
+}
+
+int spg_ctx_sync(spg_ctx* c) {
+  return guarded(c, [&] { SPG_CUDA(cudaStreamSynchronize(c->stream)); });
+}
+
+uint64_t spg_ctx_kernel_launches(const spg_ctx* c) { return c ? c->launches : 0; }
+
+int spg_ctx_set_scratch_budget(spg_ctx* c, uint64_t bytes) {
+  return guarded(c, [&] { c->scratch_budget = bytes; });
+}
+
+int spg_dcsr_alloc(spg_ctx* c, int sr, int64_t nrows, int64_t ncols, int64_t nseg, int64_t nnz, spg_dcsr* out) {
+  return guarded(c, [&] {
+    need(c && out, "null argument");
+    use_device(c);
+    const int vs = ops_for(sr)->value_size;
+    out->nrows = nrows;
+    out->ncols = ncols;
+    out->nnz = nnz;
+    out->ptr = dalloc<int64_t>(c, nseg + 1);
+    out->idx = dalloc<int32_t>(c, nnz);
+    out->vals = dalloc<char>(c, (size_t)vs * nnz);
+  });
+}
+
+int spg_dcsr_free(spg_ctx* c, spg_dcsr* m) {
+  return guarded(c, [&] {
+    need(c && m, "null argument");
+    use_device(c);
+    free_dcsr(c, m);
+  });
+}
+
+int spg_upload(spg_ctx* c, int sr, const spg_hcsr* h, int is_csc, spg_dcsr* out) {
+  return guarded(c, [&] {
+    need(c && h && out, "null argument");
+    use_device(c);
+    upload(c, ops_for(sr)->value_size, h, is_csc, out);
+  });
+}
+
+int spg_download(spg_ctx* c, int sr, const spg_dcsr* d, int is_csc, spg_hcsr* out) {
+  return guarded(c, [&] {
+    need(c && d && out, "null argument");
+    use_device(c);
+    download(c, ops_for(sr)->value_size, d, is_csc, out);
+  });
+}
+
+void spg_hcsr_free(spg_hcsr* h) {
+  if (!h) return;
+  std::free(h->ptr);
+  std::free(h->idx);
+  std::free(h->vals);
+  h->ptr = nullptr;
+  h->idx = nullptr;
+  h->vals = nullptr;
+}
+
+int spg_local_multiply(spg_ctx* c, int sr, const spg_dcsr* a, const spg_dcsr* b, spg_dcsr* out,
+                       spg_mult_stats* st) {
+  return guarded(c, [&] {
+    need(c && a && b && out, "null argument");
+    use_device(c);
+    // local_spgemm.hpp:14-21
+    if (a->ncols != b->nrows)
+      fail(SPG_ERR_SHAPE, "cannot multiply " + std::to_string(a->nrows) + "x" + std::to_string(a->ncols) +
+                              " by " + std::to_string(b->nrows) + "x" + std::to_string(b->ncols));
+    if (b->ncols > INT32_MAX) fail(SPG_ERR_INVALID_RANGE, "output width exceeds int32 indices");
+    ops_for(sr)->local_multiply(c, a, b, out, st);
+  });
+}
+
+int spg_merge_partials(spg_ctx* c, int sr, int nparts, const spg_dcsr* parts, const int* stages,
+                       const int* rounds, int64_t block_rows, int64_t block_cols, spg_dcsr* out,
+                       spg_mult_stats* st) {
+  return guarded(c, [&] {
+    need(c && out && (nparts == 0 || parts), "null argument");
+    use_device(c);
+    std::vector<int> order(nparts);
+    for (int i = 0; i < nparts; ++i) order[i] = i;
+    if (stages && rounds)  // stable (stage, round) order, summa.hpp:125-129
+      std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+        return stages[x] != stages[y] ? stages[x] < stages[y] : rounds[x] < rounds[y];
+      });
+    std::vector<spg_dcsr> ps;
+    for (int i : order) {
+      const spg_dcsr& p = parts[i];
+      if (p.nrows != block_cols || p.ncols != block_rows)  // summa.hpp:133-138
+        fail(SPG_ERR_INTERNAL, "partial extents " + std::to_string(p.nrows) + "x" + std::to_string(p.ncols) +
+                                   " do not match the " + std::to_string(block_rows) + "x" +
+                                   std::to_string(block_cols) + " output block");
+      ps.push_back(p);
+    }
+    // CSR of C^T (block_cols x block_rows) == CSC of C
+    ops_for(sr)->merge(c, nparts, ps.data(), block_cols, block_rows, out, st);
+    out->nrows = block_rows;
+    out->ncols = block_cols;
+  });
+}
+
+int spg_checksum(spg_ctx* c, int sr, const spg_dcsr* m, int is_csc, uint64_t* out) {
+  return guarded(c, [&] {
+    need(c && m && out, "null argument");
+    use_device(c);
+    *out = ops_for(sr)->checksum(c, m, is_csc);
+  });
+}
+
+int spg_csr_slice(spg_ctx* c, int sr, const spg_dcsr* m, int by_rows, int64_t begin, int64_t end,
+                  spg_dcsr* out) {
+  return guarded(c, [&] {
+    need(c && m && out, "null argument");
+    use_device(c);
+    const int vs = ops_for(sr)->value_size;
+    const int64_t lim = by_rows ? m->nrows : m->ncols;
+    if (begin < 0 || end < begin || end > lim) fail(SPG_ERR_INVALID_RANGE, "slice range outside the matrix");
+    if (by_rows) {
+      int64_t lo = 0, hi = 0;
+      SPG_CUDA(cudaMemcpyAsync(&lo, m->ptr + begin, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+      SPG_CUDA(cudaMemcpyAsync(&hi, m->ptr + end, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+      SPG_CUDA(cudaStreamSynchronize(c->stream));
+      out->nrows = end - begin;
+      out->ncols = m->ncols;
+      out->nnz = hi - lo;
+      out->ptr = dalloc<int64_t>(c, end - begin + 1);
+      out->idx = dalloc<int32_t>(c, hi - lo);
+      out->vals = dalloc<char>(c, (size_t)vs * (hi - lo));
+      slice_rows_into(c, *m, begin, end, vs, *out);
+    } else {
+      out->nrows = m->nrows;
+      out->ncols = end - begin;
+      out->ptr = dalloc<int64_t>(c, m->nrows + 1);
+      DBuf<int64_t> cnt(c, m->nrows + 1);
+      slice_cols_count(c, *m, begin, end, cnt.p);
+      exclusive_scan_i64(c, cnt.p, out->ptr, m->nrows + 1);
+      out->nnz = d2h_scalar(c, out->ptr + m->nrows);
+      out->idx = dalloc<int32_t>(c, out->nnz);
+      out->vals = dalloc<char>(c, (size_t)vs * out->nnz);
+      slice_cols_fill(c, *m, begin, end, vs, *out);
+    }
+  });
+}
+
+}  // extern "C"
+
+namespace spg {
+
+// prepare_block (summa.hpp:30-53): device CSR of the block's transpose.
+void prepare_block(spg_ctx* c, int sr, const spg_hcsr* csc, const spg_hdcsc* dcsc, spg_dcsr* out) {
+  const SrOps* ops = ops_for(sr);
+  if (!ops->commutative)
+    fail(SPG_ERR_UNSUPPORTED_SEMIRING,
+         std::string("semiring '") + ops->name +
+             "' has a non-commutative multiplication; the distributed transpose-reinterpretation path "
+             "supports commutative semirings only");
+  const int vs = ops->value_size;
+  if (dcsc) {
+    // dcsc_decompress checks (formats.hpp:222-242), done on the host arrays
+    if (dcsc->njc < 0 || (dcsc->njc > 0 && (!dcsc->jc || !dcsc->cp)))
+      fail(SPG_ERR_MALFORMED, "dcsc_decompress: bad cp offset array");
+    if (dcsc->cp[0] != 0 || dcsc->cp[dcsc->njc] != dcsc->nnz)
+      fail(SPG_ERR_MALFORMED, "dcsc_decompress: bad cp offset array");
+    int64_t prev = -1;
+    for (int64_t i = 0; i < dcsc->njc; ++i) {
+      if (dcsc->cp[i + 1] < dcsc->cp[i]) fail(SPG_ERR_MALFORMED, "dcsc_decompress: bad cp offset array");
+      const int64_t col = dcsc->jc[i];
+      if (col <= prev || col >= dcsc->ncols)
+        fail(SPG_ERR_MALFORMED, "dcsc_decompress: jc column id " + std::to_string(col) +
+                                    " out of range or not strictly increasing");
+      prev = col;
+    }
+    if (dcsc->nrows > INT32_MAX) fail(SPG_ERR_INVALID_RANGE, "block dimension exceeds int32 indices");
+    // transposed view: rows = block cols, cols = block rows
+    out->nrows = dcsc->ncols;
+    out->ncols = dcsc->nrows;
+    out->nnz = dcsc->nnz;
+    out->ptr = dalloc<int64_t>(c, dcsc->ncols + 1);
+    out->idx = dalloc<int32_t>(c, dcsc->nnz);
+    out->vals = dalloc<char>(c, (size_t)vs * dcsc->nnz);
+    DBuf<int64_t> jc(c, dcsc->njc), cp(c, dcsc->njc + 1);
+    if (dcsc->njc > 0)
+      SPG_CUDA(cudaMemcpyAsync(jc.p, dcsc->jc, sizeof(int64_t) * dcsc->njc, cudaMemcpyHostToDevice, c->stream));
+    SPG_CUDA(cudaMemcpyAsync(cp.p, dcsc->cp, sizeof(int64_t) * (dcsc->njc + 1), cudaMemcpyHostToDevice, c->stream));
+    dcsc_colptr(c, dcsc->ncols, dcsc->njc, jc.p, cp.p, out->ptr);
+    if (dcsc->nnz > 0) {
+      DBuf<int64_t> wide(c, dcsc->nnz);
+      SPG_CUDA(cudaMemcpyAsync(wide.p, dcsc->rowids, sizeof(int64_t) * dcsc->nnz, cudaMemcpyHostToDevice, c->stream));
+      narrow_indices(c, wide.p, out->idx, dcsc->nnz, dcsc->nrows);
+      SPG_CUDA(cudaMemcpyAsync(out->vals, dcsc->vals, (size_t)vs * dcsc->nnz, cudaMemcpyHostToDevice, c->stream));
+    }
+  } else {
+    spg_dcsr d{};
+    upload(c, vs, csc, /*is_csc=*/1, &d);
+    // reinterpret_transpose (formats.hpp:255-264): the CSC arrays read as CSR
+    out->nrows = csc->ncols;
+    out->ncols = csc->nrows;
+    out->nnz = csc->nnz;
+    out->ptr = d.ptr;
+    out->idx = d.idx;
+    out->vals = d.vals;
+  }
+}
+
+}  // namespace spg
+
+extern "C" {
+
+int spg_prepare_block(spg_ctx* c, int sr, const spg_hcsr* csc, const spg_hdcsc* dcsc, spg_dcsr* prepared) {
+  return guarded(c, [&] {
+    need(c && prepared && (csc || dcsc), "null argument");
+    use_device(c);
+    prepare_block(c, sr, csc, dcsc, prepared);
+  });
+}
+
+int spg_esc_multiply(spg_ctx* c, int sr, const spg_hcsr* a, const spg_hcsr* b, spg_hcsr* out,
+                     spg_mult_stats* st) {
+  return guarded(c, [&] {
+    need(c && a && b && out, "null argument");
+    use_device(c);
+    if (a->ncols != b->nrows)
+      fail(SPG_ERR_SHAPE, "cannot multiply " + std::to_string(a->nrows) + "x" + std::to_string(a->ncols) +
+                              " by " + std::to_string(b->nrows) + "x" + std::to_string(b->ncols));
+    const SrOps* ops = ops_for(sr);
+    spg_dcsr da{}, db{}, dc{};
+    upload(c, ops->value_size, a, 0, &da);
+    upload(c, ops->value_size, b, 0, &db);
+    try {
+      ops->local_multiply(c, &da, &db, &dc, st);
+      download(c, ops->value_size, &dc, 0, out);
+    } catch (...) {
+      free_dcsr(c, &da);
+      free_dcsr(c, &db);
+      free_dcsr(c, &dc);
+      throw;
+    }
+    free_dcsr(c, &da);
+    free_dcsr(c, &db);
+    free_dcsr(c, &dc);
+  });
+}
+
+int spg_generate_rmat(int sr, int scale, double ef, uint64_t seed, int64_t* nrows, int64_t* nnz, int64_t** rows,
+                      int64_t** cols, void** vals) {
+  return guarded(nullptr, [&] {
+    need(nrows && nnz && rows && cols && vals, "null argument");
+    gen_rmat(sr, scale, ef, seed, nrows, nnz, rows, cols, vals);
+  });
+}
+
+int spg_generate_er(int sr, int64_t n, int d, uint64_t seed, int mode, int64_t* nnz, int64_t** rows,
+                    int64_t** cols, void** vals) {
+  return guarded(nullptr, [&] {
+    need(nnz && rows && cols && vals, "null argument");
+    gen_er(sr, n, d, seed, mode, nnz, rows, cols, vals);
+  });
+}
+
+int spg_generate_stencil27(int sr, int64_t N, int64_t* nrows, int64_t* nnz, int64_t** rows, int64_t** cols,
+                           void** vals) {
+  return guarded(nullptr, [&] {
+    need(nrows && nnz && rows && cols && vals, "null argument");
+    gen_stencil27(sr, N, nrows, nnz, rows, cols, vals);
+  });
+}
+
+int spg_coo_to_csr(int sr, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rows, const int64_t* cols,
+                   const void* vals, int to_csc, spg_hcsr* out) {
+  return guarded(nullptr, [&] {
+    need(out && (nnz == 0 || (rows && cols && vals)), "null argument");
+    const int vs = ops_for(sr)->value_size;
+    const int64_t nseg = to_csc ? ncols : nrows;
+    out->nrows = nrows;
+    out->ncols = ncols;
+    out->nnz = nnz;
+    out->ptr = static_cast<int64_t*>(std::calloc(nseg + 1, sizeof(int64_t)));
+    out->idx = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * std::max<int64_t>(nnz, 1)));
+    out->vals = std::malloc((size_t)vs * std::max<int64_t>(nnz, 1));
+    if (!out->ptr || !out->idx || !out->vals) fail(SPG_ERR_OOM, "host allocation failed");
+    const int64_t* seg = to_csc ? cols : rows;
+    const int64_t* oth = to_csc ? rows : cols;
+    for (int64_t k = 0; k < nnz; ++k) {
+      if (rows[k] < 0 || rows[k] >= nrows || cols[k] < 0 || cols[k] >= ncols)
+        fail(SPG_ERR_MALFORMED, "coo tuple outside the matrix");
+      ++out->ptr[seg[k] + 1];
+    }
+    for (int64_t s = 0; s < nseg; ++s) out->ptr[s + 1] += out->ptr[s];
+    std::vector<int64_t> cur(out->ptr, out->ptr + nseg);
+    const char* v = static_cast<const char*>(vals);
+    char* ov = static_cast<char*>(out->vals);
+    for (int64_t k = 0; k < nnz; ++k) {  // stable counting sort by segment
+      const int64_t p = cur[seg[k]]++;
+      out->idx[p] = oth[k];
+      std::memcpy(ov + (size_t)vs * p, v + (size_t)vs * k, vs);
+    }
+  });
+}
+
+void spg_free(void* p) { std::free(p); }
+
+void spg_block_range(int64_t n, int q, int idx, int64_t* begin, int64_t* end) {
+  // dist_matrix.hpp:23-28: larger ranges first
+  const int64_t base = n / q, extra = n % q;
+  const int64_t b = idx * base + std::min<int64_t>(idx, extra);
+  *begin = b;
+  *end = b + base + (idx < extra ? 1 : 0);
+}
+
+void spg_round_range(int64_t n, int rounds, int round, int64_t* begin, int64_t* end) {
+  // summa.hpp:103-107: first half gets ceil(n/2)
+  if (rounds == 1) {
+    *begin = 0;
+    *end = n;
+    return;
+  }
+  const int64_t mid = (n + 1) / 2;
+  *begin = round == 0 ? 0 : mid;
+  *end = round == 0 ? mid : n;
+}
+
+int spg_summa_schedule(int64_t inner, int pr, int pc, spg_stage* out, int cap) {
+  // Square grids: exactly the reference's q stages (summa.hpp:290-306),
+  // empty blocks included.  pr x pc grids: the common refinement of A's pc
+  // column blocks and B's pr row blocks of the inner dimension (empty
+  // intervals dropped), so every stage has one A-panel owner and one
+  // B-panel owner.
+  if (pr < 1 || pc < 1 || inner < 0) return -SPG_ERR_GRID;
+  auto owner = [](int64_t total, int q, int64_t x) {
+    // block_index_of (dist_matrix.hpp:31-37)
+    const int64_t base = total / q, extra = total % q, wide = extra * (base + 1);
+    if (x < wide) return (int)(x / (base + 1));
+    return (int)(extra + (x - wide) / base);
+  };
+  std::vector<spg_stage> st;
+  if (pr == pc) {
+    for (int s = 0; s < pr; ++s) {
+      int64_t b, e;
+      spg_block_range(inner, pr, s, &b, &e);
+      st.push_back(spg_stage{b, e, s, s, 0, 0});
+    }
+  } else {
+    std::vector<int64_t> cuts{0, inner};
+    for (int j = 1; j < pc; ++j) {
+      int64_t b, e;
+      spg_block_range(inner, pc, j, &b, &e);
+      cuts.push_back(b);
+    }
+    for (int i = 1; i < pr; ++i) {
+      int64_t b, e;
+      spg_block_range(inner, pr, i, &b, &e);
+      cuts.push_back(b);
+    }
+    std::sort(cuts.begin(), cuts.end());
+    cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
+    for (size_t k = 0; k + 1 < cuts.size(); ++k) {
+      const int64_t lo = cuts[k], hi = cuts[k + 1];
+      if (hi <= lo) continue;
+      spg_stage s{lo, hi, owner(inner, pc, lo), owner(inner, pr, lo), 0, 0};
+      int64_t ab, ae, bb, be;
+      spg_block_range(inner, pc, s.a_col_block, &ab, &ae);
+      spg_block_range(inner, pr, s.b_row_block, &bb, &be);
+      s.a_off = lo - ab;
+      s.b_off = lo - bb;
+      st.push_back(s);
+    }
+  }
+  for (size_t k = 0; k < st.size() && (int)k < cap && out; ++k) out[k] = st[k];
+  return (int)st.size();
+}
+
+}  // extern "C"

@@ -1,0 +1,124 @@
+// Per-semiring instantiation of the device pipeline.  Each built-in semiring
+// gets its own translation unit (sr_*.cu) containing one SPG_INSTANTIATE; a
+// user-defined semiring is added the same way from the user's own .cu file
+// and registered at run time with spg_register_semiring() — the analogue of
+// instantiating the reference's templates with a new SemiringLike type
+// (semiring.hpp:28-40).
+#pragma once
+#include "rows_driver.cuh"
+
+namespace spg {
+
+SPG_HD uint64_t splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+// checksum.hpp:25-33: FNV-1a over the ValueCodec bytes, mixed with the
+// coordinates.
+template <class V>
+SPG_HD uint64_t tuple_hash(int64_t row, int64_t col, const V& v) {
+  const uint8_t* b = reinterpret_cast<const uint8_t*>(&v);
+  uint64_t fh = 0xcbf29ce484222325ULL;
+#pragma unroll
+  for (int k = 0; k < (int)sizeof(V); ++k) fh = (fh ^ b[k]) * 0x100000001b3ULL;
+  uint64_t h = splitmix64((uint64_t)row);
+  h ^= splitmix64((uint64_t)col + 0x9e3779b97f4a7c15ULL);
+  h ^= fh;
+  return splitmix64(h);
+}
+
+// K8: order-free content checksum, warp per segment, one atomic per CTA.
+template <class V>
+__global__ void __launch_bounds__(256) checksum_kernel(int64_t nseg, const int64_t* __restrict__ ptr,
+                                                       const int32_t* __restrict__ idx,
+                                                       const V* __restrict__ vals, int is_csc,
+                                                       unsigned long long* out) {
+  __shared__ unsigned long long part[8];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long acc = 0;
+  for (int64_t s = warp; s < nseg; s += nwarps) {
+    const int64_t b = ptr[s], e = ptr[s + 1];
+    for (int64_t t = b + lane; t < e; t += 32) {
+      const int64_t other = idx[t];
+      acc += is_csc ? tuple_hash(other, s, vals[t]) : tuple_hash(s, other, vals[t]);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) part[wid] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long s = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += part[w];
+    atomicAdd(out, s);
+  }
+}
+
+struct SrOps {
+  int id;
+  const char* name;
+  int value_size;
+  bool commutative;
+  void (*local_multiply)(spg_ctx*, const spg_dcsr*, const spg_dcsr*, spg_dcsr*, spg_mult_stats*);
+  // parts are CSR with identical dims (rows x cols); output rows x cols
+  void (*merge)(spg_ctx*, int, const spg_dcsr*, int64_t, int64_t, spg_dcsr*, spg_mult_stats*);
+  uint64_t (*checksum)(spg_ctx*, const spg_dcsr*, int);
+};
+
+template <class SR>
+struct OpsImpl {
+  using V = typename SR::value_type;
+
+  static void local_multiply(spg_ctx* c, const spg_dcsr* a, const spg_dcsr* b, spg_dcsr* out,
+                             spg_mult_stats* st) {
+    MulSource<SR> src{a->ptr, a->idx, static_cast<const V*>(a->vals),
+                      b->ptr, b->idx, static_cast<const V*>(b->vals), a->nrows};
+    run_rows<SR>(c, src, b->ncols, out, st);
+  }
+
+  static void merge(spg_ctx* c, int nparts, const spg_dcsr* parts, int64_t rows, int64_t cols,
+                    spg_dcsr* out, spg_mult_stats* st) {
+    if (nparts > kMaxMergeParts) fail(SPG_ERR_ARG, "merge: too many partials");
+    MergeSource<SR> src{};
+    src.nparts = nparts;
+    src.nrows = rows;
+    for (int q = 0; q < nparts; ++q) {
+      src.p.ptr[q] = parts[q].ptr;
+      src.p.idx[q] = parts[q].idx;
+      src.p.val[q] = parts[q].vals;
+    }
+    run_rows<SR>(c, src, cols, out, st);
+  }
+
+  static uint64_t checksum(spg_ctx* c, const spg_dcsr* m, int is_csc) {
+    const int64_t nseg = is_csc ? m->ncols : m->nrows;
+    DBuf<unsigned long long> acc(c, 1);
+    SPG_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(unsigned long long), c->stream));
+    if (nseg > 0 && m->nnz > 0) {
+      const int grid = grid_for(c, nseg, 8, 8);
+      checksum_kernel<V><<<grid, 256, 0, c->stream>>>(nseg, m->ptr, m->idx, static_cast<const V*>(m->vals),
+                                                      is_csc, acc.p);
+      SPG_LAUNCH_CHECK();
+      ++c->launches;
+    }
+    const unsigned long long s = d2h_scalar(c, acc.p);
+    return splitmix64((uint64_t)m->nrows * 31 + (uint64_t)m->ncols) + s;
+  }
+};
+
+template <class SR>
+const SrOps* ops_instance() {
+  static const SrOps o{SR::id, SR::name, (int)sizeof(typename SR::value_type), SR::is_commutative_mul,
+                       &OpsImpl<SR>::local_multiply, &OpsImpl<SR>::merge, &OpsImpl<SR>::checksum};
+  return &o;
+}
+
+}  // namespace spg
+
+#define SPG_INSTANTIATE(SR, FN) \
+  extern "C" const spg::SrOps* FN() { return spg::ops_instance<SR>(); }

@@ -1,0 +1,166 @@
+// Width-generic layout kernels (see layout.cuh).
+#include <cub/device/device_scan.cuh>
+
+#include "layout.cuh"
+
+namespace spg {
+
+namespace {
+
+__global__ void narrow_kernel(const int64_t* __restrict__ in, int32_t* __restrict__ out, int64_t n,
+                              int64_t bound, int* bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = in[i];
+    if (v < 0 || v >= bound) *bad = 1;
+    out[i] = (int32_t)v;
+  }
+}
+
+__global__ void widen_kernel(const int32_t* __restrict__ in, int64_t* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+
+__global__ void rebase_rowptr_kernel(const int64_t* __restrict__ in, int64_t* __restrict__ out, int64_t n1) {
+  const int64_t base = in[0];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n1;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[i] - base;
+}
+
+__device__ __forceinline__ int64_t lower_bound_i32(const int32_t* a, int64_t lo, int64_t hi, int64_t x) {
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)a[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void col_count_kernel(int64_t nrows, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                                 int64_t b, int64_t e, int64_t* __restrict__ cnt) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lo = ptr[r], hi = ptr[r + 1];
+    const int64_t f = lower_bound_i32(idx, lo, hi, b);
+    const int64_t t = lower_bound_i32(idx, f, hi, e);
+    cnt[r] = t - f;
+  }
+}
+
+template <class T>
+__global__ void col_fill_kernel(int64_t nrows, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                                const T* __restrict__ vals, int64_t b, int64_t e,
+                                const int64_t* __restrict__ optr, int32_t* __restrict__ oidx,
+                                T* __restrict__ ovals) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < nrows; r += nwarps) {
+    const int64_t o = optr[r], n = optr[r + 1] - o;
+    if (n == 0) continue;
+    const int64_t f = lower_bound_i32(idx, ptr[r], ptr[r + 1], b);
+    for (int64_t k = lane; k < n; k += 32) {
+      oidx[o + k] = (int32_t)(idx[f + k] - b);
+      ovals[o + k] = vals[f + k];
+    }
+  }
+}
+
+__global__ void dcsc_scatter_kernel(int64_t njc, const int64_t* __restrict__ jc, const int64_t* __restrict__ cp,
+                                    int64_t* __restrict__ lens) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < njc;
+       i += (int64_t)gridDim.x * blockDim.x)
+    lens[jc[i]] = cp[i + 1] - cp[i];
+}
+
+int blocks_for(spg_ctx* c, int64_t n, int threads = 256) {
+  const int64_t want = (n + threads - 1) / threads;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->sm_count * 16));
+}
+
+}  // namespace
+
+void exclusive_scan_i64(spg_ctx* c, const int64_t* in, int64_t* out, int64_t n) {
+  size_t bytes = 0;
+  SPG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, c->stream));
+  ensure_cub_tmp(c, bytes);
+  SPG_CUDA(cub::DeviceScan::ExclusiveSum(c->cub_tmp, bytes, in, out, n, c->stream));
+  ++c->launches;
+}
+
+void inclusive_scan_i64(spg_ctx* c, const int64_t* in, int64_t* out, int64_t n) {
+  size_t bytes = 0;
+  SPG_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, in, out, n, c->stream));
+  ensure_cub_tmp(c, bytes);
+  SPG_CUDA(cub::DeviceScan::InclusiveSum(c->cub_tmp, bytes, in, out, n, c->stream));
+  ++c->launches;
+}
+
+void narrow_indices(spg_ctx* c, const int64_t* in, int32_t* out, int64_t n, int64_t bound) {
+  if (n == 0) return;
+  DBuf<int> bad(c, 1);
+  SPG_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c->stream));
+  narrow_kernel<<<blocks_for(c, n), 256, 0, c->stream>>>(in, out, n, bound, bad.p);
+  SPG_LAUNCH_CHECK();
+  ++c->launches;
+  if (d2h_scalar(c, bad.p))
+    fail(SPG_ERR_MALFORMED, "index outside [0, " + std::to_string(bound) + ")");
+}
+
+void widen_indices(spg_ctx* c, const int32_t* in, int64_t* out, int64_t n) {
+  if (n == 0) return;
+  widen_kernel<<<blocks_for(c, n), 256, 0, c->stream>>>(in, out, n);
+  SPG_LAUNCH_CHECK();
+  ++c->launches;
+}
+
+void slice_rows_into(spg_ctx* c, const spg_dcsr& m, int64_t b, int64_t e, int vs, const spg_dcsr& out) {
+  rebase_rowptr_kernel<<<blocks_for(c, e - b + 1), 256, 0, c->stream>>>(m.ptr + b, out.ptr, e - b + 1);
+  SPG_LAUNCH_CHECK();
+  ++c->launches;
+  if (out.nnz > 0) {
+    int64_t lo = 0;
+    SPG_CUDA(cudaMemcpyAsync(&lo, m.ptr + b, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    SPG_CUDA(cudaStreamSynchronize(c->stream));
+    SPG_CUDA(cudaMemcpyAsync(out.idx, m.idx + lo, sizeof(int32_t) * out.nnz, cudaMemcpyDeviceToDevice, c->stream));
+    SPG_CUDA(cudaMemcpyAsync(out.vals, static_cast<const char*>(m.vals) + (size_t)vs * lo,
+                             (size_t)vs * out.nnz, cudaMemcpyDeviceToDevice, c->stream));
+  }
+}
+
+void slice_cols_count(spg_ctx* c, const spg_dcsr& m, int64_t b, int64_t e, int64_t* cnt) {
+  SPG_CUDA(cudaMemsetAsync(cnt + m.nrows, 0, sizeof(int64_t), c->stream));
+  if (m.nrows == 0) return;
+  col_count_kernel<<<blocks_for(c, m.nrows), 256, 0, c->stream>>>(m.nrows, m.ptr, m.idx, b, e, cnt);
+  SPG_LAUNCH_CHECK();
+  ++c->launches;
+}
+
+void slice_cols_fill(spg_ctx* c, const spg_dcsr& m, int64_t b, int64_t e, int vs, const spg_dcsr& out) {
+  if (out.nnz == 0 || m.nrows == 0) return;
+  with_vs(vs, [&](auto tag) {
+    using T = typename decltype(tag)::T;
+    col_fill_kernel<T><<<blocks_for(c, m.nrows * 32), 256, 0, c->stream>>>(
+        m.nrows, m.ptr, m.idx, static_cast<const T*>(m.vals), b, e, out.ptr, out.idx, static_cast<T*>(out.vals));
+    SPG_LAUNCH_CHECK();
+    ++c->launches;
+  });
+}
+
+void dcsc_colptr(spg_ctx* c, int64_t ncols, int64_t njc, const int64_t* jc, const int64_t* cp,
+                 int64_t* colptr) {
+  DBuf<int64_t> lens(c, ncols + 1);
+  SPG_CUDA(cudaMemsetAsync(lens.p, 0, sizeof(int64_t) * (ncols + 1), c->stream));
+  if (njc > 0) {
+    // lens[c + 1] = run length of column c
+    dcsc_scatter_kernel<<<blocks_for(c, njc), 256, 0, c->stream>>>(njc, jc, cp, lens.p + 1);
+    SPG_LAUNCH_CHECK();
+    ++c->launches;
+  }
+  inclusive_scan_i64(c, lens.p, colptr, ncols + 1);
+}
+
+}  // namespace spg

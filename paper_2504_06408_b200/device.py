@@ -1,0 +1,140 @@
+"""Per-GPU context and device-resident matrices (C-ABI handles).
+
+A `Context` is the spg_ctx of one GPU: its stream and stream-ordered memory
+pool.  A `DeviceCsr` owns one spg_dcsr (int64 offsets, int32 indices).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._lib import DCsr, HCsr, check, lib
+from .formats import CscMatrix, CsrMatrix
+from .semiring import as_id, dtype_of
+
+
+class Context:
+    def __init__(self, device: int = 0):
+        self.device = device
+        h = C.c_void_p()
+        check(lib.spg_ctx_create(device, C.byref(h)))
+        self.handle = h
+
+    @property
+    def stream(self) -> int:
+        return lib.spg_ctx_stream(self.handle) or 0
+
+    def sync(self):
+        check(lib.spg_ctx_sync(self.handle), self.handle)
+
+    def kernel_launches(self) -> int:
+        return int(lib.spg_ctx_kernel_launches(self.handle))
+
+    def set_scratch_budget(self, nbytes: int):
+        check(lib.spg_ctx_set_scratch_budget(self.handle, int(nbytes)), self.handle)
+
+    def close(self):
+        if self.handle:
+            lib.spg_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default = {}
+
+
+def default_context(device: int = 0) -> Context:
+    if device not in _default:
+        _default[device] = Context(device)
+    return _default[device]
+
+
+def _hcsr(ptr, idx, vals, nrows, ncols):
+    ptr = np.ascontiguousarray(ptr, dtype=np.int64)
+    idx = np.ascontiguousarray(idx, dtype=np.int64)
+    vals = np.ascontiguousarray(vals)
+    h = HCsr(nrows, ncols, idx.shape[0], ptr.ctypes.data_as(C.POINTER(C.c_int64)),
+             idx.ctypes.data_as(C.POINTER(C.c_int64)), vals.ctypes.data_as(C.c_void_p))
+    return h, (ptr, idx, vals)  # keep the arrays alive with the struct
+
+
+def hcsr_of(m):
+    if isinstance(m, CsrMatrix):
+        return _hcsr(m.rowptr, m.colids, m.values, m.nrows, m.ncols)
+    return _hcsr(m.colptr, m.rowids, m.values, m.nrows, m.ncols)
+
+
+def take_hcsr(sr, h: HCsr, is_csc: bool):
+    """Copy a library-allocated spg_hcsr into numpy and free it."""
+    nseg = h.ncols if is_csc else h.nrows
+    ptr = np.ctypeslib.as_array(h.ptr, shape=(nseg + 1,)).copy()
+    nnz = int(h.nnz)
+    idx = np.ctypeslib.as_array(h.idx, shape=(max(nnz, 1),))[:nnz].copy()
+    dt = dtype_of(sr)
+    raw = C.string_at(h.vals, nnz * dt.itemsize) if nnz else b""
+    vals = np.frombuffer(raw, dtype=dt).copy()
+    lib.spg_hcsr_free(C.byref(h))
+    if is_csc:
+        return CscMatrix(int(as_id(sr)), int(h.nrows), int(h.ncols), ptr, idx, vals)
+    return CsrMatrix(int(as_id(sr)), int(h.nrows), int(h.ncols), ptr, idx, vals)
+
+
+class DeviceCsr:
+    """A device CSR (or CSC when is_csc) owned by a Context."""
+
+    def __init__(self, ctx: Context, sr, d: DCsr, is_csc: bool = False):
+        self.ctx = ctx
+        self.sr = as_id(sr)
+        self.d = d
+        self.is_csc = is_csc
+
+    @classmethod
+    def upload(cls, ctx: Context, m) -> "DeviceCsr":
+        is_csc = isinstance(m, CscMatrix)
+        h, keep = hcsr_of(m)
+        d = DCsr()
+        check(lib.spg_upload(ctx.handle, int(m.sr), C.byref(h), int(is_csc), C.byref(d)), ctx.handle)
+        return cls(ctx, m.sr, d, is_csc)
+
+    @property
+    def nrows(self):
+        return int(self.d.nrows)
+
+    @property
+    def ncols(self):
+        return int(self.d.ncols)
+
+    @property
+    def nnz(self):
+        return int(self.d.nnz)
+
+    def download(self):
+        h = HCsr()
+        check(lib.spg_download(self.ctx.handle, int(self.sr), C.byref(self.d), int(self.is_csc), C.byref(h)),
+              self.ctx.handle)
+        return take_hcsr(self.sr, h, self.is_csc)
+
+    def checksum(self) -> int:
+        out = C.c_uint64()
+        check(lib.spg_checksum(self.ctx.handle, int(self.sr), C.byref(self.d), int(self.is_csc), C.byref(out)),
+              self.ctx.handle)
+        return int(out.value)
+
+    def free(self):
+        if self.d is not None and self.d.ptr:
+            lib.spg_dcsr_free(self.ctx.handle, C.byref(self.d))
+        self.d = None
+
+    def __del__(self):
+        try:
+            if self.ctx.handle is not None:
+                self.free()
+        except Exception:
+            pass

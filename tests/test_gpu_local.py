@@ -1,0 +1,148 @@
+"""GPU parity: the sm_100a local multiply / merge / checksum against the
+reference (golden fixtures) and the CPU oracle, through the C-ABI."""
+import numpy as np
+import pytest
+
+import oracle_bind as ob
+from helpers import RTOL, assert_same, to_mat, unpack
+from paper_2504_06408_b200 import (DeviceCsr, errors, esc_multiply, generators, local_multiply,
+                                   matrix_checksum, merge_partials)
+from paper_2504_06408_b200.formats import CscMatrix, CsrMatrix, coo_to_csr
+
+pytestmark = pytest.mark.gpu
+
+
+def test_all_golden_local_cases_bit_exact(golden, ctx):
+    for key in golden["mul_cases"]:
+        sr = int(str(key).split("_")[1])
+        a, b = unpack(golden, key + "_a", sr), unpack(golden, key + "_b", sr)
+        want = unpack(golden, key + "_c", sr)
+        st = {}
+        got = esc_multiply(a, b, ctx=ctx, stats=st)
+        assert_same(got, want, sr)  # integer-valued draws: bit-exact for every semiring
+        assert matrix_checksum(got, ctx=ctx) == int(golden[key + "_csum"][0])
+        assert st["kernels"] > 0
+
+
+def test_spec_examples(golden, ctx):
+    a = CsrMatrix(0, 2, 2, np.array([0, 2, 3]), np.array([0, 1, 1]), np.array([1.0, 2.0, 3.0]))
+    got = esc_multiply(a, a, ctx=ctx)
+    assert got.values.tolist() == [1.0, 8.0, 9.0]
+    assert_same(got, unpack(golden, "spec_aa", 0), 0)
+    w = CsrMatrix(1, 3, 3, np.array([0, 2, 4, 5]), np.array([0, 1, 1, 2, 2]), np.array([0.0, 1.0, 0.0, 2.0, 0.0]))
+    assert_same(esc_multiply(w, w, ctx=ctx), unpack(golden, "spec_ww", 1), 1)
+
+
+def test_config1_er4096_fp64_within_tolerance(golden, ctx):
+    r, c, v = golden["er4096_rows"], golden["er4096_cols"], golden["er4096_vals"]
+    from paper_2504_06408_b200.formats import CooMatrix
+    a = coo_to_csr(CooMatrix(0, 4096, 4096, r, c, v))
+    got = esc_multiply(a, a, ctx=ctx)
+    assert_same(got, unpack(golden, "er4096_c", 0), 0, rtol=RTOL)
+
+
+def test_shape_error(ctx):
+    a = CsrMatrix(0, 2, 3, np.array([0, 0, 0]), np.zeros(0, np.int64), np.zeros(0))
+    b = CsrMatrix(0, 2, 2, np.array([0, 0, 0]), np.zeros(0, np.int64), np.zeros(0))
+    with pytest.raises(errors.ShapeError):
+        esc_multiply(a, b, ctx=ctx)
+
+
+def test_empty_and_zero_sized(ctx):
+    for (m, k, n) in [(0, 0, 0), (5, 0, 7), (0, 4, 3), (6, 6, 6)]:
+        a = CsrMatrix(4, m, k, np.zeros(m + 1, np.int64), np.zeros(0, np.int64), np.zeros(0, np.int32))
+        b = CsrMatrix(4, k, n, np.zeros(k + 1, np.int64), np.zeros(0, np.int64), np.zeros(0, np.int32))
+        got = esc_multiply(a, b, ctx=ctx)
+        assert got.nrows == m and got.ncols == n and got.nnz == 0 and got.rowptr.tolist() == [0] * (m + 1)
+
+
+def _rand(sr, rng, m, k, dens):
+    from golden.make_golden import exact_values
+    mask = rng.random((m, k)) < dens
+    r, c = np.nonzero(mask)
+    vals = exact_values(sr, rng, r.size)
+    ptr = np.concatenate([[0], np.cumsum(np.bincount(r, minlength=m))]).astype(np.int64)
+    return CsrMatrix(sr, m, k, ptr, c.astype(np.int64), vals)
+
+
+@pytest.mark.parametrize("sr", [0, 1, 2, 3, 4, 5])
+def test_every_bin_against_oracle(ctx, sr):
+    """Rows engineered to land in every accumulator bin: empty, <=32 products
+    (warp-ESC), the four hash-table sizes and the dense global accumulator."""
+    rng = np.random.default_rng(100 + sr)
+    n = 40000
+    # B: row k has (k % 97) + 1 entries spread over n columns (sorted, unique)
+    lens = (np.arange(2000) % 97) + 1
+    bptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    bcols = np.concatenate([np.sort(rng.choice(n, L, replace=False)) for L in lens]).astype(np.int64)
+    from golden.make_golden import exact_values
+    b = CsrMatrix(sr, 2000, n, bptr, bcols, exact_values(sr, rng, bcols.size))
+    # A: rows with 0, 1, 3, 20, 120, 600, 1500 entries
+    sizes = [0, 1, 3, 20, 120, 600, 1500, 0, 2, 60]
+    rows = []
+    for s in sizes:
+        rows.append(np.sort(rng.choice(2000, s, replace=False)))
+    aptr = np.concatenate([[0], np.cumsum([len(x) for x in rows])]).astype(np.int64)
+    acols = np.concatenate(rows).astype(np.int64)
+    a = CsrMatrix(sr, len(sizes), 2000, aptr, acols, exact_values(sr, rng, acols.size))
+    st = {}
+    got = esc_multiply(a, b, ctx=ctx, stats=st)
+    want = ob.orc_multiply(to_mat(a), to_mat(b))
+    assert_same(got, want, sr)
+    bins = st["rows_per_bin"]
+    assert bins[0] == 2 and bins[1] >= 1 and bins[6] >= 1, bins
+    assert sum(bins[2:6]) >= 3
+
+
+@pytest.mark.parametrize("sr", [1, 2, 4])
+def test_rmat14_against_reference_checksum(golden, ctx, sr):
+    m = generators.generate_rmat(sr, 12 if sr != 4 else 14, 16.0, 1)
+    a = coo_to_csr(m)
+    d = DeviceCsr.upload(ctx, a)
+    st = {}
+    c = local_multiply(d, d, stats=st)
+    if sr == 4:
+        assert c.nnz == int(golden["rmat14_4_c_nnz"][0])
+        assert c.checksum() == int(golden["rmat14_4_c_csum"][0])
+        assert np.array_equal(np.diff(c.download().rowptr), golden["rmat14_4_c_rownnz"])
+    else:
+        s, z, f, _ = ob.orc_stream(to_mat(a), to_mat(a))
+        assert c.nnz == z and st["products"] == f
+        assert c.checksum() == (ob.orc_seed(a.nrows, a.ncols) + s) % (1 << 64)
+
+
+def test_row_batched_scratch_matches_single_pass(ctx):
+    m = coo_to_csr(generators.generate_rmat(4, 13, 16.0, 5))
+    d = DeviceCsr.upload(ctx, m)
+    full = local_multiply(d, d)
+    ctx.set_scratch_budget(1 << 20)  # 1 MB: forces many row batches
+    try:
+        small = local_multiply(d, d)
+    finally:
+        ctx.set_scratch_budget(0)
+    assert_same(small.download(), full.download(), 4)
+
+
+@pytest.mark.parametrize("sr", [0, 1, 2, 4, 5])
+def test_merge_partials_matches_reference(golden, ctx, sr):
+    parts = [unpack(golden, f"merge_{sr}_p{i}", sr) for i in range(4)]
+    order = golden[f"merge_{sr}_order"]
+    dparts = [DeviceCsr.upload(ctx, p) for p in parts]
+    out = merge_partials(dparts, 40, 30, stages=order[0].tolist(), rounds=order[1].tolist())
+    got = out.download()
+    want = unpack(golden, f"merge_{sr}_c", sr, csc=True)
+    assert isinstance(got, CscMatrix) and got.nrows == 40 and got.ncols == 30
+    assert_same(got, want, sr)
+
+
+def test_merge_extent_mismatch_is_internal_error(ctx):
+    p = DeviceCsr.upload(ctx, CsrMatrix(4, 3, 4, np.zeros(4, np.int64), np.zeros(0, np.int64), np.zeros(0, np.int32)))
+    with pytest.raises(errors.InternalError):
+        merge_partials([p], 5, 5)
+
+
+def test_device_checksum_matches_reference(ctx):
+    rng = np.random.default_rng(9)
+    for sr in (0, 1, 2, 3, 4, 5):
+        m = _rand(sr, rng, 77, 51, 0.1)
+        assert matrix_checksum(m, ctx=ctx) == ob.orc_checksum(to_mat(m))

