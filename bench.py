@@ -229,14 +229,15 @@ def run_single(args):
 
     # e2e: reference-shaped host call esc_multiply(A, A): H2D, multiply, D2H of C
     e2e_times = []
-    for _ in range(max(1, args.e2e_steps)):
+    h2d = 2 * (8 * (a.nrows + 1) + 8 * a.nnz + vs * a.nnz)
+    d2h = 8 * (a.nrows + 1) + (8 + vs) * nnz_c
+    for _ in range(args.e2e_steps):
         t0 = time.perf_counter()
         ch = esc_multiply(a, a, ctx=ctx)
         e2e_times.append(time.perf_counter() - t0)
-    e2e_s = float(np.median(e2e_times))
-    h2d = 2 * (8 * (a.nrows + 1) + 8 * a.nnz + vs * a.nnz)
-    d2h = 8 * (ch.nrows + 1) + 8 * ch.nnz + vs * ch.nnz
-    del ch
+        assert ch.nnz == nnz_c
+        del ch
+    e2e_s = float(np.median(e2e_times)) if e2e_times else float("nan")
 
     cpu = None
     if not args.no_cpu_baseline:

@@ -157,6 +157,15 @@ SPG_API int spg_merge_partials(spg_ctx* ctx, int sr, int nparts, const spg_dcsr*
 /* matrix_checksum (checksum.hpp:20-38) of a device CSR (is_csc = 0) or CSC. */
 SPG_API int spg_checksum(spg_ctx* ctx, int sr, const spg_dcsr* m, int is_csc, uint64_t* out);
 
+/* Sum of the per-tuple checksum terms (no dims seed) with every tuple's
+ * coordinates shifted by (row_off, col_off): the block-local part of the
+ * checksum of a distributed matrix, so ranks' parts add up to the global
+ * matrix_checksum (checksum.hpp:20-38 is order-free). */
+SPG_API int spg_checksum_part(spg_ctx* ctx, int sr, const spg_dcsr* m, int is_csc, int64_t row_off,
+                              int64_t col_off, uint64_t* out);
+/* splitmix64(nrows * 31 + ncols): the dims seed of matrix_checksum. */
+SPG_API uint64_t spg_checksum_seed(int64_t nrows, int64_t ncols);
+
 /* csr_row_slice / csr_col_slice (summa.hpp:57-98) on device. */
 SPG_API int spg_csr_slice(spg_ctx* ctx, int sr, const spg_dcsr* m, int by_rows, int64_t begin,
                           int64_t end, spg_dcsr* out);

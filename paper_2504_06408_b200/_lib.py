@@ -100,6 +100,9 @@ _SIGS = [
     ("spg_merge_partials", C.c_int, [C.c_void_p, C.c_int, C.c_int, _P(DCsr), _P(C.c_int), _P(C.c_int),
                                      C.c_int64, C.c_int64, _P(DCsr), _P(MultStats)]),
     ("spg_checksum", C.c_int, [C.c_void_p, C.c_int, _P(DCsr), C.c_int, _P(C.c_uint64)]),
+    ("spg_checksum_part", C.c_int, [C.c_void_p, C.c_int, _P(DCsr), C.c_int, C.c_int64, C.c_int64,
+                                    _P(C.c_uint64)]),
+    ("spg_checksum_seed", C.c_uint64, [C.c_int64, C.c_int64]),
     ("spg_csr_slice", C.c_int, [C.c_void_p, C.c_int, _P(DCsr), C.c_int, C.c_int64, C.c_int64, _P(DCsr)]),
     ("spg_prepare_block", C.c_int, [C.c_void_p, C.c_int, _P(HCsr), _P(HDcsc), _P(DCsr)]),
     ("spg_esc_multiply", C.c_int, [C.c_void_p, C.c_int, _P(HCsr), _P(HCsr), _P(HCsr), _P(MultStats)]),

@@ -5,9 +5,11 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
+#include "comm.h"
 #include "instantiate.cuh"
 #include "layout.cuh"
 
@@ -55,6 +57,17 @@ int guarded(spg_ctx* c, F&& f) {
     if (c) c->last_error = e.what();
     return SPG_ERR_INTERNAL;
   }
+}
+
+// Runs one rank's distributed program.  Validation errors are symmetric
+// across ranks and leave the fabric usable; anything raised after the first
+// collective tears the peers down (AbortedError on their side).
+int guarded_summa(spg_ctx* c, spg_comm* comm, const std::function<void()>& f) {
+  const int rc = guarded(c, f);
+  if (rc != SPG_OK && comm && rc != SPG_ERR_ABORTED && rc != SPG_ERR_DEADLOCK && rc != SPG_ERR_SHAPE &&
+      rc != SPG_ERR_UNSUPPORTED_SEMIRING && rc != SPG_ERR_ARG && rc != SPG_ERR_GRID)
+    comm_abort(comm, c ? c->last_error : g_last_error);
+  return rc;
 }
 
 void need(bool ok, const char* what) {
@@ -308,8 +321,21 @@ int spg_checksum(spg_ctx* c, int sr, const spg_dcsr* m, int is_csc, uint64_t* ou
   return guarded(c, [&] {
     need(c && m && out, "null argument");
     use_device(c);
-    *out = ops_for(sr)->checksum(c, m, is_csc);
+    *out = splitmix64((uint64_t)m->nrows * 31 + (uint64_t)m->ncols) + ops_for(sr)->checksum_part(c, m, is_csc, 0, 0);
   });
+}
+
+int spg_checksum_part(spg_ctx* c, int sr, const spg_dcsr* m, int is_csc, int64_t row_off, int64_t col_off,
+                      uint64_t* out) {
+  return guarded(c, [&] {
+    need(c && m && out, "null argument");
+    use_device(c);
+    *out = ops_for(sr)->checksum_part(c, m, is_csc, row_off, col_off);
+  });
+}
+
+uint64_t spg_checksum_seed(int64_t nrows, int64_t ncols) {
+  return splitmix64((uint64_t)nrows * 31 + (uint64_t)ncols);
 }
 
 int spg_csr_slice(spg_ctx* c, int sr, const spg_dcsr* m, int by_rows, int64_t begin, int64_t end,

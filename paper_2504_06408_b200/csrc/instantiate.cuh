@@ -35,6 +35,7 @@ template <class V>
 __global__ void __launch_bounds__(256) checksum_kernel(int64_t nseg, const int64_t* __restrict__ ptr,
                                                        const int32_t* __restrict__ idx,
                                                        const V* __restrict__ vals, int is_csc,
+                                                       int64_t row_off, int64_t col_off,
                                                        unsigned long long* out) {
   __shared__ unsigned long long part[8];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -45,7 +46,8 @@ __global__ void __launch_bounds__(256) checksum_kernel(int64_t nseg, const int64
     const int64_t b = ptr[s], e = ptr[s + 1];
     for (int64_t t = b + lane; t < e; t += 32) {
       const int64_t other = idx[t];
-      acc += is_csc ? tuple_hash(other, s, vals[t]) : tuple_hash(s, other, vals[t]);
+      acc += is_csc ? tuple_hash(other + row_off, s + col_off, vals[t])
+                    : tuple_hash(s + row_off, other + col_off, vals[t]);
     }
   }
 #pragma unroll
@@ -67,7 +69,8 @@ struct SrOps {
   void (*local_multiply)(spg_ctx*, const spg_dcsr*, const spg_dcsr*, spg_dcsr*, spg_mult_stats*);
   // parts are CSR with identical dims (rows x cols); output rows x cols
   void (*merge)(spg_ctx*, int, const spg_dcsr*, int64_t, int64_t, spg_dcsr*, spg_mult_stats*);
-  uint64_t (*checksum)(spg_ctx*, const spg_dcsr*, int);
+  // sum of tuple terms with coordinate offsets (no dims seed)
+  uint64_t (*checksum_part)(spg_ctx*, const spg_dcsr*, int, int64_t, int64_t);
 };
 
 template <class SR>
@@ -95,26 +98,25 @@ struct OpsImpl {
     run_rows<SR>(c, src, cols, out, st);
   }
 
-  static uint64_t checksum(spg_ctx* c, const spg_dcsr* m, int is_csc) {
+  static uint64_t checksum_part(spg_ctx* c, const spg_dcsr* m, int is_csc, int64_t row_off, int64_t col_off) {
     const int64_t nseg = is_csc ? m->ncols : m->nrows;
     DBuf<unsigned long long> acc(c, 1);
     SPG_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(unsigned long long), c->stream));
     if (nseg > 0 && m->nnz > 0) {
       const int grid = grid_for(c, nseg, 8, 8);
       checksum_kernel<V><<<grid, 256, 0, c->stream>>>(nseg, m->ptr, m->idx, static_cast<const V*>(m->vals),
-                                                      is_csc, acc.p);
+                                                      is_csc, row_off, col_off, acc.p);
       SPG_LAUNCH_CHECK();
       ++c->launches;
     }
-    const unsigned long long s = d2h_scalar(c, acc.p);
-    return splitmix64((uint64_t)m->nrows * 31 + (uint64_t)m->ncols) + s;
+    return d2h_scalar(c, acc.p);
   }
 };
 
 template <class SR>
 const SrOps* ops_instance() {
   static const SrOps o{SR::id, SR::name, (int)sizeof(typename SR::value_type), SR::is_commutative_mul,
-                       &OpsImpl<SR>::local_multiply, &OpsImpl<SR>::merge, &OpsImpl<SR>::checksum};
+                       &OpsImpl<SR>::local_multiply, &OpsImpl<SR>::merge, &OpsImpl<SR>::checksum_part};
   return &o;
 }
 

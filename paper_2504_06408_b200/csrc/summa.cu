@@ -1,0 +1,255 @@
+// One rank's program of the 2.5D Sparse SUMMA (summa25_multiply,
+// /root/reference/proj/include/spsumma/summa.hpp:248-349), on a pr x pc grid
+// of B200s, one process per GPU.
+//
+//   prepare   : host CSC/DCSC blocks -> device CSR of their transposes
+//               (prepare_block, summa.hpp:30-53; DCSC decompressed on device)
+//   stages    : spg_summa_schedule (= the reference's q stages on a square
+//               grid; the common refinement of the inner splits otherwise)
+//   per round r, stage s (round-major, summa.hpp:290-291):
+//     A panel : owner (i, a_col_block) slices rows [half) of its prepared A
+//               straight into a packed wire buffer (K6), size triple over the
+//               grid row (host path), payload broadcast if nnz > 0
+//     B panel : owner (b_row_block, j) column-slices its prepared B the same
+//               way, broadcast over the grid column
+//     multiply: C^T partial = panB (x) panA (esc(panB, panA), summa.hpp:312)
+//               unless a panel is absent (empty-stage guard, :310-321)
+//   merge     : GPU merge of the partials in (stage, round) order into the
+//               CSC C block (merge_partials, summa.hpp:122-172)
+// The ledger mirrors CostLedger (cost_ledger.hpp:31-56) with measured times.
+#include <algorithm>
+#include <chrono>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "comm.h"
+#include "instantiate.cuh"
+#include "layout.cuh"
+
+namespace spg {
+const SrOps* ops_for(int sr);
+void prepare_block(spg_ctx* c, int sr, const spg_hcsr* csc, const spg_hdcsc* dcsc, spg_dcsr* out);
+void free_dcsr(spg_ctx* c, spg_dcsr* m);
+int guarded_summa(spg_ctx* c, spg_comm* comm, const std::function<void()>& f);
+}  // namespace spg
+
+namespace spg {
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double ms_since(Clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+}
+
+struct Panel {
+  DBuf<char> buf;
+  spg_dcsr view{};
+  uint64_t bytes = 0;
+  bool present = false;
+};
+
+// csr_row_slice of the prepared block into a packed wire buffer.
+void pack_rows(spg_ctx* c, const spg_dcsr& m, int64_t b, int64_t e, int vs, Panel& p) {
+  int64_t lo = 0, hi = 0;
+  SPG_CUDA(cudaMemcpyAsync(&lo, m.ptr + b, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  SPG_CUDA(cudaMemcpyAsync(&hi, m.ptr + e, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  SPG_CUDA(cudaStreamSynchronize(c->stream));
+  const int64_t rows = e - b, nnz = hi - lo;
+  p.bytes = panel_bytes(rows, nnz, vs);
+  p.buf = DBuf<char>(c, p.bytes);
+  p.view = panel_view(p.buf.p, rows, m.ncols, nnz);
+  slice_rows_into(c, m, b, e, vs, p.view);
+}
+
+// csr_col_slice of the prepared block into a packed wire buffer.
+void pack_cols(spg_ctx* c, const spg_dcsr& m, int64_t b, int64_t e, int vs, Panel& p) {
+  DBuf<int64_t> cnt(c, m.nrows + 1), ptr(c, m.nrows + 1);
+  slice_cols_count(c, m, b, e, cnt.p);
+  exclusive_scan_i64(c, cnt.p, ptr.p, m.nrows + 1);
+  const int64_t nnz = d2h_scalar(c, ptr.p + m.nrows);
+  p.bytes = panel_bytes(m.nrows, nnz, vs);
+  p.buf = DBuf<char>(c, p.bytes);
+  p.view = panel_view(p.buf.p, m.nrows, e - b, nnz);
+  SPG_CUDA(cudaMemcpyAsync(p.view.ptr, ptr.p, sizeof(int64_t) * (m.nrows + 1), cudaMemcpyDeviceToDevice, c->stream));
+  slice_cols_fill(c, m, b, e, vs, p.view);
+}
+
+// broadcast_panel (summa.hpp:212-235): size triple always, payload if nnz > 0.
+void broadcast_panel(spg_ctx* c, spg_comm* comm, int scope, int root, bool by_rows, const spg_dcsr& prepared,
+                     int64_t b, int64_t e, int vs, const spg_summa_opts& o, Panel& p, spg_ledger& led) {
+  const bool me = comm_scope_index(comm, scope) == root;
+  int64_t triple[3] = {0, 0, 0};
+  if (me) {
+    if (by_rows) pack_rows(c, prepared, b, e, vs, p);
+    else pack_cols(c, prepared, b, e, vs, p);
+    triple[0] = p.view.nrows;
+    triple[1] = p.view.ncols;
+    triple[2] = p.view.nnz;
+  }
+  const auto t0 = Clock::now();
+  comm_exchange_sizes(comm, scope, root, triple);
+  ++led.size_exchanges;
+  if (triple[2] == 0) {
+    led.ms[1] += ms_since(t0);
+    return;  // summa.hpp:226: empty panels are not broadcast
+  }
+  p.present = true;
+  if (!me) {
+    p.bytes = panel_bytes(triple[0], triple[2], vs);
+    p.buf = DBuf<char>(c, p.bytes);
+    p.view = panel_view(p.buf.p, triple[0], triple[1], triple[2]);
+  }
+  const int path = comm_bcast(comm, scope, root, p.buf.p, p.bytes, o.comm_mode, o.threshold, c->stream, true);
+  if (path == SPG_PATH_HOST) {
+    ++led.host_bcasts;
+    led.bytes_host_path += p.bytes;
+  } else {
+    ++led.device_bcasts;
+    led.bytes_device_path += p.bytes;
+  }
+  led.ms[1] += ms_since(t0);
+}
+
+}  // namespace
+}  // namespace spg
+
+using namespace spg;
+
+extern "C" int spg_summa25_multiply(spg_comm* comm, spg_ctx* c, int sr, int64_t a_nrows, int64_t a_ncols,
+                                    int64_t b_ncols, const spg_hcsr* a_csc, const spg_hdcsc* a_dcsc,
+                                    const spg_hcsr* b_csc, const spg_hdcsc* b_dcsc, const spg_summa_opts* opts,
+                                    spg_dcsr* c_out, spg_ledger* ledger) {
+  return guarded_summa(c, comm, [&] {
+    if (!comm || !c || !c_out || !opts || !(a_csc || a_dcsc) || !(b_csc || b_dcsc)) fail(SPG_ERR_ARG, "null argument");
+    SPG_CUDA(cudaSetDevice(c->device));
+    const SrOps* ops = ops_for(sr);
+    if (!ops->commutative)  // summa.hpp:262-266 via prepare_block :32-37
+      fail(SPG_ERR_UNSUPPORTED_SEMIRING,
+           std::string("semiring '") + ops->name +
+               "' has a non-commutative multiplication; the distributed transpose-reinterpretation path "
+               "supports commutative semirings only");
+    const int vs = ops->value_size;
+    const int pr = comm_pr(comm), pc = comm_pc(comm), i = comm_grid_row(comm), j = comm_grid_col(comm);
+    const int64_t inner = a_ncols;
+    int64_t arb, are, acb, ace, brb, bre, bcb, bce;
+    spg_block_range(a_nrows, pr, i, &arb, &are);
+    spg_block_range(inner, pc, j, &acb, &ace);
+    spg_block_range(inner, pr, i, &brb, &bre);
+    spg_block_range(b_ncols, pc, j, &bcb, &bce);
+    auto dims = [](const spg_hcsr* h, const spg_hdcsc* d, int64_t& r, int64_t& cc) {
+      r = d ? d->nrows : h->nrows;
+      cc = d ? d->ncols : h->ncols;
+    };
+    int64_t ar, ac, br, bc;
+    dims(a_csc, a_dcsc, ar, ac);
+    dims(b_csc, b_dcsc, br, bc);
+    if (ar != are - arb || ac != ace - acb || br != bre - brb || bc != bce - bcb)
+      fail(SPG_ERR_SHAPE, "local blocks do not match the block distribution of " + std::to_string(a_nrows) + "x" +
+                              std::to_string(inner) + " by " + std::to_string(inner) + "x" + std::to_string(b_ncols) +
+                              " on a " + std::to_string(pr) + "x" + std::to_string(pc) + " grid");
+    spg_ledger led{};
+    CommCounters& cc0 = comm_counters(comm);
+    const double copy0 = cc0.ms_copy;
+    const auto t_start = Clock::now();
+
+    // prepare (summa.hpp:278-287)
+    spg_dcsr pa{}, pb{};
+    {
+      const auto t0 = Clock::now();
+      prepare_block(c, sr, a_csc, a_dcsc, &pa);
+      prepare_block(c, sr, b_csc, b_dcsc, &pb);
+      SPG_CUDA(cudaStreamSynchronize(c->stream));
+      led.ms[0] += ms_since(t0);
+    }
+    struct Owned {
+      spg_ctx* c;
+      spg_dcsr* m;
+      ~Owned() { free_dcsr(c, m); }
+    } own_a{c, &pa}, own_b{c, &pb};
+
+    std::vector<spg_stage> stages(pr + pc + 2);
+    const int ns = spg_summa_schedule(inner, pr, pc, stages.data(), (int)stages.size());
+    if (ns < 0) fail(SPG_ERR_GRID, "bad grid");
+    stages.resize(ns);
+    const int rounds = opts->two_round ? 2 : 1;
+
+    struct Part {
+      int stage, round;
+      spg_dcsr m;
+    };
+    std::vector<Part> parts;
+    auto free_parts = [&] {
+      for (auto& p : parts) free_dcsr(c, &p.m);
+      parts.clear();
+    };
+    try {
+      for (int r = 0; r < rounds; ++r) {
+        for (int s = 0; s < ns; ++s) {
+          const spg_stage& st = stages[s];
+          int64_t hb, he;
+          spg_round_range(st.hi - st.lo, rounds, r, &hb, &he);
+          // A panel: rows [a_off + hb, a_off + he) of the prepared A (A's local columns)
+          Panel pana, panb;
+          broadcast_panel(c, comm, SPG_SCOPE_ROW, st.a_col_block, true, pa, st.a_off + hb, st.a_off + he, vs, *opts,
+                          pana, led);
+          // B panel: columns [b_off + hb, b_off + he) of the prepared B (B's local rows)
+          broadcast_panel(c, comm, SPG_SCOPE_COL, st.b_row_block, false, pb, st.b_off + hb, st.b_off + he, vs,
+                          *opts, panb, led);
+          const uint64_t resident = (pana.present ? pana.bytes : 0) + (panb.present ? panb.bytes : 0);
+          if (resident > led.peak_bcast_buffer_bytes) led.peak_bcast_buffer_bytes = resident;
+          if (pana.present && panb.present) {
+            const auto t0 = Clock::now();
+            spg_mult_stats ms{};
+            spg_dcsr ct{};
+            ops->local_multiply(c, &panb.view, &pana.view, &ct, &ms);
+            led.ms[2] += ms_since(t0);
+            led.products += ms.products;
+            ++led.local_multiply_calls;
+            parts.push_back({s, r, ct});
+          } else {
+            ++led.skipped_stages;
+          }
+        }
+      }
+      // merge (summa.hpp:325-328), stage-major / round-minor
+      const auto t0 = Clock::now();
+      std::stable_sort(parts.begin(), parts.end(), [](const Part& x, const Part& y) {
+        return x.stage != y.stage ? x.stage < y.stage : x.round < y.round;
+      });
+      const int64_t block_rows = are - arb, block_cols = bce - bcb;
+      if (parts.empty()) {
+        c_out->nrows = block_rows;
+        c_out->ncols = block_cols;
+        c_out->nnz = 0;
+        c_out->ptr = dalloc<int64_t>(c, block_cols + 1);
+        c_out->idx = dalloc<int32_t>(c, 1);
+        c_out->vals = dalloc<char>(c, vs);
+        SPG_CUDA(cudaMemsetAsync(c_out->ptr, 0, sizeof(int64_t) * (block_cols + 1), c->stream));
+      } else if (parts.size() == 1) {
+        // a single partial already is the CSR of C^T == CSC of C
+        *c_out = parts[0].m;
+        c_out->nrows = block_rows;
+        c_out->ncols = block_cols;
+        parts.clear();
+      } else {
+        std::vector<spg_dcsr> ps;
+        for (auto& p : parts) ps.push_back(p.m);
+        spg_dcsr out{};
+        ops->merge(c, (int)ps.size(), ps.data(), block_cols, block_rows, &out, nullptr);
+        out.nrows = block_rows;
+        out.ncols = block_cols;
+        *c_out = out;
+        free_parts();
+      }
+      SPG_CUDA(cudaStreamSynchronize(c->stream));
+      led.ms[3] += ms_since(t0);
+    } catch (...) {
+      free_parts();
+      throw;
+    }
+    led.ms[4] = comm_counters(comm).ms_copy - copy0;
+    led.ms_total = ms_since(t_start);
+    if (ledger) *ledger = led;
+  });
+}

@@ -1,0 +1,160 @@
+"""Distributed Sparse SUMMA (2.5D) over one process per B200.
+
+Mirrors summa25_multiply (proj/include/spsumma/summa.hpp:248-349) with the
+reference's DistMatrix (dist_matrix.hpp:41-141) generalised from q x q to
+pr x pc grids.  The per-rank program, the broadcasts and the merge run in
+C++/CUDA behind the C-ABI (spg_summa25_multiply); this module only builds
+the host blocks and calls it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import errors
+from ._lib import DCsr, HCsr, HDcsc, Ledger, SummaOpts, check, lib
+from .device import Context, DeviceCsr, hcsr_of
+from .formats import CooMatrix, CscMatrix, DcscMatrix, coo_to_csc, csc_to_dcsc
+from .semiring import as_id
+
+HOST_ONLY, DEVICE_ONLY, HYBRID = 0, 1, 2
+GRIDS = {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}
+
+
+def grid_for(world: int):
+    """pr x pc for the BASELINE GPU counts (1x1, 1x2, 2x2, 2x4); otherwise the
+    most square factorisation with pr <= pc."""
+    if world in GRIDS:
+        return GRIDS[world]
+    pr = int(np.floor(np.sqrt(world)))
+    while world % pr:
+        pr -= 1
+    return pr, world // pr
+
+
+def block_range(n: int, q: int, idx: int):
+    """block_range (dist_matrix.hpp:23-28): larger ranges first."""
+    b, e = C.c_int64(), C.c_int64()
+    lib.spg_block_range(int(n), int(q), int(idx), C.byref(b), C.byref(e))
+    return b.value, e.value
+
+
+@dataclass
+class LocalBlock:
+    """LocalBlock (dist_matrix.hpp:41-53): CSC or DCSC storage + extents."""
+
+    storage: object  # CscMatrix | DcscMatrix
+    rows: tuple
+    cols: tuple
+
+    @property
+    def is_dcsc(self):
+        return isinstance(self.storage, DcscMatrix)
+
+
+def local_block(m: CooMatrix, pr: int, pc: int, i: int, j: int) -> LocalBlock:
+    """Block (i, j) of `m` on a pr x pc grid, stored DCSC when fewer than half
+    of its columns are populated (distribute, dist_matrix.hpp:69-111)."""
+    rb, re = block_range(m.nrows, pr, i)
+    cb, ce = block_range(m.ncols, pc, j)
+    sel = (m.rows >= rb) & (m.rows < re) & (m.cols >= cb) & (m.cols < ce)
+    piece = CooMatrix(m.sr, re - rb, ce - cb, m.rows[sel] - rb, m.cols[sel] - cb, m.values[sel])
+    csc = coo_to_csc(piece)
+    populated = int(np.count_nonzero(np.diff(csc.colptr)))
+    storage = csc_to_dcsc(csc) if 2 * populated < csc.ncols else csc
+    return LocalBlock(storage, (rb, re), (cb, ce))
+
+
+def _block_structs(blk: LocalBlock):
+    s = blk.storage
+    if isinstance(s, DcscMatrix):
+        jc = np.ascontiguousarray(s.jc, dtype=np.int64)
+        cp = np.ascontiguousarray(s.cp, dtype=np.int64)
+        ri = np.ascontiguousarray(s.rowids, dtype=np.int64)
+        v = np.ascontiguousarray(s.values)
+        d = HDcsc(s.nrows, s.ncols, ri.shape[0], jc.shape[0], jc.ctypes.data_as(C.POINTER(C.c_int64)),
+                  cp.ctypes.data_as(C.POINTER(C.c_int64)), ri.ctypes.data_as(C.POINTER(C.c_int64)),
+                  v.ctypes.data_as(C.c_void_p))
+        return None, d, (jc, cp, ri, v)
+    h, keep = hcsr_of(s)
+    return h, None, keep
+
+
+class Comm:
+    """spg_comm: shared-memory rendezvous + pinned staging + NCCL row/column
+    communicators for one rank of a pr x pc grid (rank = i * pc + j)."""
+
+    def __init__(self, job: str, world: int, rank: int, pr: int, pc: int, device: int,
+                 staging_bytes: int = 64 << 20):
+        h = C.c_void_p()
+        rc = lib.spg_comm_create(job.encode(), world, rank, pr, pc, device, staging_bytes, C.byref(h))
+        if rc != 0:
+            raise errors.from_status(rc, lib.spg_comm_last_error(None).decode())
+        self.handle, self.world, self.rank, self.pr, self.pc = h, world, rank, pr, pc
+        self.row, self.col = rank // pc, rank % pc
+
+    def _check(self, rc):
+        if rc != 0:
+            raise errors.from_status(rc, lib.spg_comm_last_error(self.handle).decode())
+
+    def barrier(self):
+        self._check(lib.spg_comm_barrier(self.handle))
+
+    def exchange_sizes(self, scope: int, root: int, triple):
+        """Rank::exchange_sizes (fabric.hpp:335-338); scope 0 = grid row, 1 = column."""
+        t = (C.c_int64 * 3)(*triple)
+        self._check(lib.spg_exchange_sizes(self.handle, scope, root, t))
+        return tuple(t)
+
+    def bcast(self, scope: int, root: int, ptr: int, nbytes: int, mode: int = HYBRID, threshold: int = 0) -> int:
+        """Rank::bcast (fabric.hpp:343-349) of a device (or host) buffer; returns the path taken."""
+        path = C.c_int()
+        self._check(lib.spg_bcast(self.handle, scope, root, C.c_void_p(ptr), int(nbytes), mode, int(threshold),
+                                  C.byref(path)))
+        return path.value
+
+    def set_device_transport(self, transport: int):
+        self._check(lib.spg_comm_set_device_transport(self.handle, transport))
+
+    def close(self):
+        if self.handle:
+            lib.spg_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def summa25_multiply(comm: Comm, ctx: Context, a_block: LocalBlock, b_block: LocalBlock, a_nrows: int,
+                     a_ncols: int, b_ncols: int, two_round: bool = True, mode: int = HYBRID,
+                     threshold: int = 0, sr=None):
+    """One rank's summa25_multiply.  Returns (C block as DeviceCsr CSC, ledger dict)."""
+    sr = as_id(sr if sr is not None else a_block.storage.sr)
+    ah, ad, ka = _block_structs(a_block)
+    bh, bd, kb = _block_structs(b_block)
+    opts = SummaOpts(int(two_round), int(mode), int(threshold))
+    out = DCsr()
+    led = Ledger()
+    rc = lib.spg_summa25_multiply(comm.handle, ctx.handle, int(sr), int(a_nrows), int(a_ncols), int(b_ncols),
+                                  C.byref(ah) if ah is not None else None, C.byref(ad) if ad is not None else None,
+                                  C.byref(bh) if bh is not None else None, C.byref(bd) if bd is not None else None,
+                                  C.byref(opts), C.byref(out), C.byref(led))
+    check(rc, ctx.handle)
+    return DeviceCsr(ctx, sr, out, is_csc=True), led.as_dict()
+
+
+def checksum_part(c: DeviceCsr, row_off: int, col_off: int) -> int:
+    """This block's share of matrix_checksum of the distributed matrix."""
+    out = C.c_uint64()
+    check(lib.spg_checksum_part(c.ctx.handle, int(c.sr), C.byref(c.d), int(c.is_csc), int(row_off), int(col_off),
+                                C.byref(out)), c.ctx.handle)
+    return int(out.value)
+
+
+def checksum_seed(nrows: int, ncols: int) -> int:
+    return int(lib.spg_checksum_seed(int(nrows), int(ncols)))

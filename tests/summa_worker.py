@@ -1,0 +1,93 @@
+"""One rank of a distributed SUMMA parity check (run under torchrun, one
+process per GPU):
+
+    torchrun --standalone --nproc-per-node N tests/summa_worker.py --sr 4 --scale 10
+
+Each rank builds its block of A (R-MAT, identical on every rank), runs the
+CUDA summa25_multiply through the C-ABI, and checks its C block bit-exactly
+against the CPU oracle's product restricted to that block; the per-rank
+checksum parts must add up to the oracle's matrix_checksum of the full C.
+"""
+import argparse
+import os
+import sys
+import uuid
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))
+sys.path.insert(0, HERE)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--sr", type=int, default=4)
+    ap.add_argument("--scale", type=int, default=10)
+    ap.add_argument("--ef", type=float, default=16.0)
+    ap.add_argument("--two-round", type=int, default=1)
+    ap.add_argument("--mode", type=int, default=2)
+    ap.add_argument("--threshold", type=int, default=1 << 14)
+    ap.add_argument("--staging", type=int, default=1 << 16)
+    args = ap.parse_args()
+
+    import torch.distributed as dist
+
+    import oracle_bind as ob
+    from paper_2504_06408_b200 import Context, generators
+    from paper_2504_06408_b200.formats import coo_to_csr
+    from paper_2504_06408_b200.summa import Comm, checksum_part, checksum_seed, grid_for, local_block, \
+        summa25_multiply
+
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    dist.init_process_group("gloo")
+    job = [uuid.uuid4().hex[:12] if rank == 0 else None]
+    dist.broadcast_object_list(job, src=0)
+    pr, pc = grid_for(world)
+    i, j = rank // pc, rank % pc
+
+    m = generators.generate_rmat(args.sr, args.scale, args.ef, 1)
+    n = m.nrows
+    blk = local_block(m, pr, pc, i, j)
+    ctx = Context(local)
+    comm = Comm(job[0], world, rank, pr, pc, local, staging_bytes=args.staging)
+    c, led = summa25_multiply(comm, ctx, blk, blk, n, n, n, two_round=bool(args.two_round), mode=args.mode,
+                              threshold=args.threshold)
+    part = checksum_part(c, blk.rows[0], blk.cols[0])
+    got = c.download()  # CSC of the C block
+
+    a = coo_to_csr(m)
+    want_full = ob.orc_multiply(ob.Mat.of(a), ob.Mat.of(a))
+    # oracle block (rows blk.rows, cols blk.cols) as CSC
+    rb, re = blk.rows
+    cb, ce = blk.cols
+    rr = np.repeat(np.arange(n), np.diff(want_full.ptr))
+    sel = (rr >= rb) & (rr < re) & (want_full.idx >= cb) & (want_full.idx < ce)
+    br, bc, bv = rr[sel] - rb, want_full.idx[sel] - cb, want_full.vals[sel]
+    order = np.lexsort((br, bc))
+    colptr = np.concatenate([[0], np.cumsum(np.bincount(bc, minlength=ce - cb))])
+    ok = (np.array_equal(got.colptr, colptr) and np.array_equal(got.rowids, br[order])
+          and got.values.tobytes() == bv[order].tobytes())
+    import torch
+    t = torch.tensor([part & 0xFFFFFFFF, part >> 32, int(ok), led["local_multiply_calls"],
+                      led["host_bcasts"], led["device_bcasts"]], dtype=torch.int64)
+    parts = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(parts, t)
+    if rank == 0:
+        total = checksum_seed(n, n)
+        for p in parts:
+            total = (total + int(p[0]) + (int(p[1]) << 32)) % (1 << 64)
+        want = ob.orc_checksum(want_full)
+        allok = all(int(p[2]) for p in parts)
+        print(f"[summa_worker] grid {pr}x{pc} sr={args.sr} s{args.scale} two_round={args.two_round} "
+              f"mode={args.mode}: blocks_ok={allok} checksum_ok={total == want} ledger0={led}", flush=True)
+        if not (allok and total == want):
+            sys.exit(1)
+    comm.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

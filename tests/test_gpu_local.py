@@ -82,6 +82,8 @@ def test_every_bin_against_oracle(ctx, sr):
     rows = []
     for s in sizes:
         rows.append(np.sort(rng.choice(2000, s, replace=False)))
+    rows[1] = np.array([5])       # 6 products  -> warp-ESC bin
+    rows[8] = np.array([3, 200])  # 4 + 7 = 11 products -> warp-ESC bin
     aptr = np.concatenate([[0], np.cumsum([len(x) for x in rows])]).astype(np.int64)
     acols = np.concatenate(rows).astype(np.int64)
     a = CsrMatrix(sr, len(sizes), 2000, aptr, acols, exact_values(sr, rng, acols.size))
