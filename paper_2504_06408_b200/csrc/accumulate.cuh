@@ -3,30 +3,39 @@
 // (merge_partials replacement, summa.hpp:122-172).
 //
 // Both operations have the same shape: output row i is the semiring fold of
-// a list of SEGMENTS, each a sorted run of (column, value) items from some
-// CSR row, optionally multiplied on the left by a scalar:
-//   local multiply:  segments of row i = rows k of R for each A entry (i, k),
-//                    item = mul(a_ik, r_kj)                     (Gustavson)
+// a list of SEGMENTS, each a column-sorted run of (column, value) items from
+// some CSR row, optionally multiplied on the left by a scalar:
+//   local multiply:  segments of row i = rows k of R for each L entry (i, k),
+//                    item = mul(l_ik, r_kj)                     (Gustavson)
 //   merge:           segments of row i = row i of each partial, item = value
 // (the merge is the product [I I .. I] * vstack(partials)).  A Source type
 // describes the segments; the kernels below are written once against it.
 //
+// Items are enumerated warp-cooperatively and FLATTENED across segments: a
+// warp takes 32 segments, scans their lengths with shuffles, and each lane
+// locates its item by a 5-step shuffle binary search, so R-MAT's short rows
+// (median ~4 entries) still keep all 32 lanes busy.
+//
 // Pipeline (one call):
-//   K1 analyse   : per-row product count F_i, bound U_i = min(F_i, ncols),
-//                  bin id                                    (warp per row)
-//   K2 bin       : scatter rows into per-bin lists            (smem histogram)
-//   K4 numeric   : per bin
-//        bin 1  F_i <= 32   warp-ESC: products in registers, 32-lane bitonic
-//                           sort on (col, product#), segmented shuffle fold
-//        bin 2-5 U_i <= T/2 CTA hash table of T slots in shared memory
-//                           (T = 512 .. 16K), atomic semiring accumulate,
-//                           compaction + shared-memory bitonic sort
-//        bin 6  larger      dense accumulator in global memory (L2-resident
-//                           per-CTA slab) + bitmap; bitmap scan gives sorted
-//                           output with no sort
-//      each row writes into a scratch slot of U_i entries and reports nnz_i
-//   K7 compact   : rowptr = scan(nnz); copy scratch -> exact-size CSR
+//   K1 analyse : per-row product count F_i, bound U_i = min(F_i, ncols), bin
+//   K2 bin     : scatter rows into per-bin lists (dense bin sorted by F desc)
+//   K4 numeric, per bin, on concurrent streams:
+//      bin 1   F <= 32        warp-ESC: products in registers, 32-lane bitonic
+//                             sort on (col, product#), segmented shuffle fold
+//      bin 2-4 F <= 4096      block-ESC: products placed in product order in
+//                             shared memory, stable block radix sort on the
+//                             column, segmented block scan folds each run
+//                             (deterministic fold order)
+//      bin 6   long rows      dense accumulator over column PANELS of width W
+//                             in shared memory (128 KB), native smem atomics,
+//                             presence bitmap scanned in order -> sorted output,
+//                             accumulator restored while scanning (no clears)
+//      bin 5,7 long rows of   shared-memory hash tables (8K / max slots) +
+//              very wide C    bitonic sort, when panels would be too many
+//      every row writes a scratch slot of U_i entries and reports nnz_i
+//   K7 compact : rowptr = scan(nnz); copy scratch -> exact-size CSR
 #pragma once
+#include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_scan.cuh>
 
 #include "common.cuh"
@@ -34,8 +43,20 @@
 
 namespace spg {
 
-constexpr int kNumBins = 7;
+constexpr int kNumBins = 8;
 constexpr int32_t kEmptyKey = -1;
+constexpr unsigned kFull = 0xffffffffu;
+
+enum Bin : uint8_t {
+  kBinEmpty = 0,
+  kBinWarpEsc = 1,
+  kBinEsc512 = 2,
+  kBinEsc2K = 3,
+  kBinEsc4K = 4,
+  kBinHash8K = 5,
+  kBinDense = 6,
+  kBinHashMax = 7,
+};
 
 // ---------------------------------------------------------------------------
 // Sources
@@ -43,6 +64,7 @@ constexpr int32_t kEmptyKey = -1;
 template <class SR>
 struct MulSource {
   using V = typename SR::value_type;
+  static constexpr bool kMultiSrc = false;
   const int64_t* lptr;
   const int32_t* lidx;
   const V* lval;
@@ -50,23 +72,34 @@ struct MulSource {
   const int32_t* ridx;
   const V* rval;
   int64_t nrows;
+  // panel offsets: poff[k * (npanels + 1) + p] = first entry of R row k with
+  // column >= p * W, relative to rptr[k] (only when npanels > 1)
+  const int32_t* poff = nullptr;
+  int npanels = 1;
 
   __device__ __forceinline__ int64_t seg_begin(int64_t i) const { return lptr[i]; }
   __device__ __forceinline__ int64_t seg_end(int64_t i) const { return lptr[i + 1]; }
-  // Segment s of row i: R row lidx[s], scaled by lval[s].
-  __device__ __forceinline__ void segment(int64_t /*i*/, int64_t s, int64_t& b, int64_t& len,
-                                          const int32_t*& cols, const V*& vals, V& mult) const {
-    const int32_t k = __ldg(lidx + s);
-    b = __ldg(rptr + k);
-    len = __ldg(rptr + k + 1) - b;
-    cols = ridx;
-    vals = rval;
-    mult = lval[s];
-  }
-  __device__ __forceinline__ int64_t seg_len(int64_t /*i*/, int64_t s) const {
+  __device__ __forceinline__ int64_t seg_len(int64_t, int64_t s) const {
     const int32_t k = __ldg(lidx + s);
     return __ldg(rptr + k + 1) - __ldg(rptr + k);
   }
+  // segment s of row i restricted to panel p (p < 0: whole segment)
+  __device__ __forceinline__ void seg(int64_t, int64_t s, int p, int64_t& b, int& len, int& sid, V& mult) const {
+    const int32_t k = __ldg(lidx + s);
+    b = __ldg(rptr + k);
+    if (p < 0) {
+      len = (int)(__ldg(rptr + k + 1) - b);
+    } else {
+      const int32_t* po = poff + (int64_t)k * (npanels + 1) + p;
+      const int32_t lo = __ldg(po), hi = __ldg(po + 1);
+      b += lo;
+      len = hi - lo;
+    }
+    sid = 0;
+    mult = lval[s];
+  }
+  __device__ __forceinline__ int32_t col(int, int64_t u) const { return __ldg(ridx + u); }
+  __device__ __forceinline__ V val(int, int64_t u) const { return rval[u]; }
   __device__ __forceinline__ V item(const V& mult, const V& v) const { return SR::mul(mult, v); }
 };
 
@@ -80,25 +113,42 @@ struct MergeParts {
 template <class SR>
 struct MergeSource {
   using V = typename SR::value_type;
+  static constexpr bool kMultiSrc = true;
   MergeParts p;
   int nparts;
   int64_t nrows;
+  int panel_w = 0;  // panel width for the dense bin (found by binary search)
 
   __device__ __forceinline__ int64_t seg_begin(int64_t) const { return 0; }
   __device__ __forceinline__ int64_t seg_end(int64_t) const { return nparts; }
-  __device__ __forceinline__ void segment(int64_t i, int64_t s, int64_t& b, int64_t& len,
-                                          const int32_t*& cols, const V*& vals, V& mult) const {
-    const int64_t* ptr = p.ptr[s];
-    b = ptr[i];
-    len = ptr[i + 1] - b;
-    cols = p.idx[s];
-    vals = static_cast<const V*>(p.val[s]);
-    mult = SR::one();
-  }
   __device__ __forceinline__ int64_t seg_len(int64_t i, int64_t s) const {
     const int64_t* ptr = p.ptr[s];
     return ptr[i + 1] - ptr[i];
   }
+  __device__ __forceinline__ static int64_t lower_bound(const int32_t* a, int64_t lo, int64_t hi, int64_t x) {
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if ((int64_t)a[mid] < x) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo;
+  }
+  __device__ __forceinline__ void seg(int64_t i, int64_t s, int pnl, int64_t& b, int& len, int& sid, V& mult) const {
+    const int64_t* ptr = p.ptr[s];
+    int64_t lo = ptr[i], hi = ptr[i + 1];
+    if (pnl >= 0) {
+      const int32_t* ix = p.idx[s];
+      const int64_t f = lower_bound(ix, lo, hi, (int64_t)pnl * panel_w);
+      hi = lower_bound(ix, f, hi, (int64_t)(pnl + 1) * panel_w);
+      lo = f;
+    }
+    b = lo;
+    len = (int)(hi - lo);
+    sid = (int)s;
+    mult = SR::one();
+  }
+  __device__ __forceinline__ int32_t col(int sid, int64_t u) const { return p.idx[sid][u]; }
+  __device__ __forceinline__ V val(int sid, int64_t u) const { return static_cast<const V*>(p.val[sid])[u]; }
   __device__ __forceinline__ V item(const V&, const V& v) const { return v; }
 };
 
@@ -114,121 +164,43 @@ inline void rebase_source(MergeSource<SR>& s, int64_t r0) {
 }
 
 // ---------------------------------------------------------------------------
-// Bin geometry per value width
+// Geometry per value width
 // ---------------------------------------------------------------------------
 template <class V>
-struct HashGeom {
-  // largest table whose keys + values fit comfortably in 227 KB of smem
+struct Geom {
+  // hash tables: largest table whose keys + values fit in ~200 KB of smem
   static constexpr int kMaxT = sizeof(V) <= 1 ? 32768 : (sizeof(V) <= 8 ? 16384 : 8192);
+  // dense panel width: 128 KB of accumulator values (64K columns for bool)
+  static constexpr int kPanelW = (131072 / (int)sizeof(V)) > 65536 ? 65536 : (131072 / (int)sizeof(V));
 };
+constexpr int kDenseMaxPanels = 16;   // beyond this many panels prefer hashing
+constexpr int kDenseMinPerPanel = 1024;
 
-// Table size for bins 2..5.
 template <class V>
-__host__ __device__ constexpr int bin_table(int bin) {
-  return bin == 2 ? 512 : bin == 3 ? 2048 : bin == 4 ? 8192 : HashGeom<V>::kMaxT;
-}
-
-// ---------------------------------------------------------------------------
-// K1: per-row analysis
-// ---------------------------------------------------------------------------
-template <class SR, class Src>
-__global__ void __launch_bounds__(256) analyse_rows_kernel(Src src, int64_t ncols_out,
-                                                           int64_t* __restrict__ prods,
-                                                           int64_t* __restrict__ ubound,
-                                                           uint8_t* __restrict__ bins) {
-  using V = typename SR::value_type;
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = warp; i < src.nrows; i += nwarps) {
-    const int64_t sb = src.seg_begin(i), se = src.seg_end(i);
-    int64_t f = 0;
-    for (int64_t s = sb + lane; s < se; s += 32) f += src.seg_len(i, s);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) f += __shfl_xor_sync(0xffffffffu, f, o);
-    if (lane == 0) {
-      const int64_t u = f < ncols_out ? f : ncols_out;
-      uint8_t b;
-      if (f == 0) b = 0;
-      else if (f <= 32) b = 1;
-      else if (u <= bin_table<V>(2) / 2) b = 2;
-      else if (u <= bin_table<V>(3) / 2) b = 3;
-      else if (u <= bin_table<V>(4) / 2) b = 4;
-      else if (u <= bin_table<V>(5) / 2) b = 5;
-      else b = 6;
-      prods[i] = f;
-      ubound[i] = (b == 0) ? 0 : u;
-      bins[i] = b;
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// K2: bin scatter.  counts[b] must be zero on entry; lists are laid out at
-// bin_base[b] (host-computed from a first counting launch).
-// ---------------------------------------------------------------------------
-static __global__ void __launch_bounds__(1024) bin_count_kernel(const uint8_t* __restrict__ bins,
-                                                          int64_t n, unsigned long long* counts) {
-  __shared__ unsigned int h[kNumBins];
-  if (threadIdx.x < kNumBins) h[threadIdx.x] = 0;
-  __syncthreads();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(&h[bins[i]], 1u);
-  __syncthreads();
-  if (threadIdx.x < kNumBins && h[threadIdx.x]) atomicAdd(&counts[threadIdx.x], (unsigned long long)h[threadIdx.x]);
-}
-
-static __global__ void __launch_bounds__(1024) bin_scatter_kernel(const uint8_t* __restrict__ bins,
-                                                            int64_t n,
-                                                            unsigned long long* cursor,  // per bin, starts at base
-                                                            int64_t* __restrict__ lists) {
-  __shared__ unsigned int h[kNumBins];
-  __shared__ unsigned long long base[kNumBins];
-  const int64_t chunk0 = blockIdx.x * (int64_t)blockDim.x;
-  for (int64_t c = chunk0; c < n; c += (int64_t)gridDim.x * blockDim.x) {
-    if (threadIdx.x < kNumBins) h[threadIdx.x] = 0;
-    __syncthreads();
-    const int64_t i = c + threadIdx.x;
-    int b = -1;
-    unsigned int slot = 0;
-    if (i < n) {
-      b = bins[i];
-      if (b != 0) slot = atomicAdd(&h[b], 1u);
-    }
-    __syncthreads();
-    if (threadIdx.x < kNumBins) base[threadIdx.x] = h[threadIdx.x] ? atomicAdd(&cursor[threadIdx.x], (unsigned long long)h[threadIdx.x]) : 0;
-    __syncthreads();
-    if (b > 0) lists[base[b] + slot] = i;
-    __syncthreads();
-  }
-}
-
-static __global__ void zero_empty_rows_kernel(const uint8_t* __restrict__ bins, int64_t n,
-                                       int64_t* __restrict__ rownnz) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    if (bins[i] == 0) rownnz[i] = 0;
+__host__ __device__ inline int npanels_for(int64_t ncols) {
+  return (int)((ncols + Geom<V>::kPanelW - 1) / Geom<V>::kPanelW);
 }
 
 // ---------------------------------------------------------------------------
 // Value shuffles (any width)
 // ---------------------------------------------------------------------------
 template <class V>
-__device__ __forceinline__ V shfl_v(const V& v, int src, unsigned mask = 0xffffffffu) {
-  constexpr int W = (sizeof(V) + 3) / 4;
-  uint32_t w[W];
-  V out;
-  memcpy(w, &v, sizeof(V) <= 4 * W ? sizeof(V) : 0);
-  if constexpr (sizeof(V) < 4) w[0] = (uint32_t)(*reinterpret_cast<const uint8_t*>(&v));
-#pragma unroll
-  for (int k = 0; k < W; ++k) w[k] = __shfl_sync(mask, w[k], src);
+__device__ __forceinline__ V shfl_v(const V& v, int src) {
   if constexpr (sizeof(V) < 4) {
-    *reinterpret_cast<uint8_t*>(&out) = (uint8_t)w[0];
+    const uint32_t w = __shfl_sync(kFull, (uint32_t)(*reinterpret_cast<const uint8_t*>(&v)), src);
+    V out;
+    *reinterpret_cast<uint8_t*>(&out) = (uint8_t)w;
+    return out;
   } else {
+    constexpr int W = sizeof(V) / 4;
+    uint32_t w[W];
+    memcpy(w, &v, sizeof(V));
+#pragma unroll
+    for (int k = 0; k < W; ++k) w[k] = __shfl_sync(kFull, w[k], src);
+    V out;
     memcpy(&out, w, sizeof(V));
+    return out;
   }
-  return out;
 }
 template <class V>
 __device__ __forceinline__ V shfl_xor_v(const V& v, int m) {
@@ -241,13 +213,171 @@ __device__ __forceinline__ V shfl_up_v(const V& v, int d) {
 }
 
 // ---------------------------------------------------------------------------
+// Flattened warp enumeration of the items of segments [s0, s1) of row i
+// (panel p, or whole segments for p < 0), warps striding by `sstride`
+// segments.  f(col, value, seg_index, offset_in_segment) is called once per
+// item; every lane of the warp must call this.
+// ---------------------------------------------------------------------------
+template <class SR, class Src, class F>
+__device__ __forceinline__ void warp_items(const Src& src, int64_t i, int64_t s0, int64_t s1, int p, int64_t sstride,
+                                           F&& f) {
+  using V = typename SR::value_type;
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = s0; base < s1; base += sstride) {
+    const int64_t s = base + lane;
+    int64_t b = 0;
+    int len = 0, sid = 0;
+    V mult = SR::zero();
+    if (s < s1) src.seg(i, s, p, b, len, sid, mult);
+    int incl = len;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int t = __shfl_up_sync(kFull, incl, d);
+      if (lane >= d) incl += t;
+    }
+    const int total = __shfl_sync(kFull, incl, 31);
+    const int excl = incl - len;
+    for (int q0 = 0; q0 < total; q0 += 32) {
+      const int q = q0 + lane;
+      int pos = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const int v = __shfl_sync(kFull, incl, pos + step - 1);
+        if (v <= q) pos += step;
+      }
+      const long long bb = __shfl_sync(kFull, (long long)b, pos);
+      const int ex = __shfl_sync(kFull, excl, pos);
+      const V m = shfl_v(mult, pos);
+      int sd = 0;
+      if constexpr (Src::kMultiSrc) sd = __shfl_sync(kFull, sid, pos);
+      if (q < total) {
+        const int off = q - ex;
+        const int64_t u = bb + off;
+        f(src.col(sd, u), src.item(m, src.val(sd, u)), base + pos, off);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1: per-row analysis and binning policy
+// ---------------------------------------------------------------------------
+template <class SR, class Src>
+__global__ void __launch_bounds__(256) analyse_rows_kernel(Src src, int64_t ncols_out,
+                                                           int64_t* __restrict__ prods,
+                                                           int64_t* __restrict__ ubound,
+                                                           uint8_t* __restrict__ bins) {
+  using V = typename SR::value_type;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int np = npanels_for<V>(ncols_out);
+  for (int64_t i = warp; i < src.nrows; i += nwarps) {
+    const int64_t sb = src.seg_begin(i), se = src.seg_end(i);
+    int64_t f = 0;
+    for (int64_t s = sb + lane; s < se; s += 32) f += src.seg_len(i, s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) f += __shfl_xor_sync(kFull, f, o);
+    if (lane == 0) {
+      const int64_t u = f < ncols_out ? f : ncols_out;
+      const int64_t nseg = se - sb;
+      uint8_t b;
+      if (f == 0) b = kBinEmpty;
+      else if (f <= 32) b = kBinWarpEsc;
+      else if (f <= 512 && nseg <= 512) b = kBinEsc512;
+      else if (f <= 2048 && nseg <= 2048) b = kBinEsc2K;
+      else if (f <= 4096 && nseg <= 4096) b = kBinEsc4K;
+      else if (np <= kDenseMaxPanels || f >= (int64_t)kDenseMinPerPanel * np) b = kBinDense;
+      else if (u <= 4096) b = kBinHash8K;
+      else if (u <= Geom<V>::kMaxT / 2) b = kBinHashMax;
+      else b = kBinDense;
+      prods[i] = f;
+      ubound[i] = (b == kBinEmpty) ? 0 : u;
+      bins[i] = b;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2: bin histogram + scatter into per-bin row lists
+// ---------------------------------------------------------------------------
+static __global__ void __launch_bounds__(1024) bin_count_kernel(const uint8_t* __restrict__ bins, int64_t n,
+                                                                 unsigned long long* counts) {
+  __shared__ unsigned int h[kNumBins];
+  if (threadIdx.x < kNumBins) h[threadIdx.x] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&h[bins[i]], 1u);
+  __syncthreads();
+  if (threadIdx.x < kNumBins && h[threadIdx.x])
+    atomicAdd(&counts[threadIdx.x], (unsigned long long)h[threadIdx.x]);
+}
+
+static __global__ void __launch_bounds__(1024) bin_scatter_kernel(const uint8_t* __restrict__ bins, int64_t n,
+                                                                   unsigned long long* cursor,
+                                                                   int64_t* __restrict__ lists) {
+  __shared__ unsigned int h[kNumBins];
+  __shared__ unsigned long long base[kNumBins];
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+    if (threadIdx.x < kNumBins) h[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t i = c + threadIdx.x;
+    int b = -1;
+    unsigned int slot = 0;
+    if (i < n) {
+      b = bins[i];
+      if (b != kBinEmpty) slot = atomicAdd(&h[b], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < kNumBins)
+      base[threadIdx.x] = h[threadIdx.x] ? atomicAdd(&cursor[threadIdx.x], (unsigned long long)h[threadIdx.x]) : 0;
+    __syncthreads();
+    if (b > 0) lists[base[b] + slot] = i;
+    __syncthreads();
+  }
+}
+
+static __global__ void zero_empty_rows_kernel(const uint8_t* __restrict__ bins, int64_t n, int64_t* __restrict__ rownnz) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (bins[i] == kBinEmpty) rownnz[i] = 0;
+}
+
+// keys[k] = prods[rows[k]] (to sort the dense bin by work, largest first)
+static __global__ void gather_keys_kernel(const int64_t* __restrict__ rows, int64_t n, const int64_t* __restrict__ prods,
+                                          int64_t* __restrict__ keys) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    keys[k] = prods[rows[k]];
+}
+
+// Panel offsets of every R row: poff[k*(np+1) + p] = #entries of row k with
+// column < p * W  (warp per row, lanes binary-search the boundaries).
+static __global__ void __launch_bounds__(256) panel_offsets_kernel(int64_t nrows, const int64_t* __restrict__ rptr,
+                                                                   const int32_t* __restrict__ ridx, int np, int W,
+                                                                   int32_t* __restrict__ poff) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t k = warp; k < nrows; k += nwarps) {
+    const int64_t b = rptr[k], e = rptr[k + 1];
+    for (int p = lane; p <= np; p += 32) {
+      const int64_t x = (int64_t)p * W;
+      int64_t lo = b, hi = e;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int64_t)ridx[mid] < x) lo = mid + 1;
+        else hi = mid;
+      }
+      poff[k * (np + 1) + p] = (int32_t)(lo - b);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K4 bin 1: warp-ESC for rows with <= 32 products
 // ---------------------------------------------------------------------------
 template <class SR, class Src>
-__global__ void __launch_bounds__(256) esc_warp_kernel(Src src, const int64_t* __restrict__ rows,
-                                                       int64_t nrows_bin,
-                                                       const int64_t* __restrict__ off,
-                                                       int32_t* __restrict__ out_cols,
+__global__ void __launch_bounds__(256) esc_warp_kernel(Src src, const int64_t* __restrict__ rows, int64_t nrows_bin,
+                                                       const int64_t* __restrict__ off, int32_t* __restrict__ out_cols,
                                                        typename SR::value_type* __restrict__ out_vals,
                                                        int64_t* __restrict__ rownnz) {
   using V = typename SR::value_type;
@@ -258,27 +388,17 @@ __global__ void __launch_bounds__(256) esc_warp_kernel(Src src, const int64_t* _
     const int64_t i = rows[r];
     uint64_t key = ~0ull;  // (col << 32) | product#  ; ~0 = no item
     V val = SR::zero();
-    int base = 0;
-    const int64_t se = src.seg_end(i);
-    for (int64_t s = src.seg_begin(i); s < se && base < 32; ++s) {
-      int64_t b, len;
-      const int32_t* cols;
-      const V* vals;
-      V mult;
-      src.segment(i, s, b, len, cols, vals, mult);
-      if (lane >= base && lane < base + len) {
-        const int64_t u = b + (lane - base);
-        key = ((uint64_t)(uint32_t)cols[u] << 32) | (uint32_t)lane;
-        val = src.item(mult, vals[u]);
-      }
-      base += (int)len;
-    }
-    // 32-lane bitonic sort by key (unique keys -> deterministic fold order)
+    // every product lands on its own lane, in product order (<= 32 of them)
+    warp_items<SR>(src, i, src.seg_begin(i), src.seg_end(i), -1, 32,
+                   [&](int32_t c, const V& v, int64_t, int) {
+                     key = ((uint64_t)(uint32_t)c << 32) | (uint32_t)lane;
+                     val = v;
+                   });
 #pragma unroll
     for (int k = 2; k <= 32; k <<= 1) {
 #pragma unroll
       for (int j = k >> 1; j > 0; j >>= 1) {
-        const uint64_t okey = __shfl_xor_sync(0xffffffffu, key, j);
+        const uint64_t okey = __shfl_xor_sync(kFull, key, j);
         const V oval = shfl_xor_v(val, j);
         const bool up = (lane & k) == 0;
         const bool lower = (lane & j) == 0;
@@ -291,17 +411,16 @@ __global__ void __launch_bounds__(256) esc_warp_kernel(Src src, const int64_t* _
     }
     const uint32_t col = (uint32_t)(key >> 32);
     const bool valid = key != ~0ull;
-    // segmented inclusive fold over equal columns
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t ocol = __shfl_up_sync(0xffffffffu, col, d);
+      const uint32_t ocol = __shfl_up_sync(kFull, col, d);
       const V oval = shfl_up_v(val, d);
       if (lane >= d && ocol == col) val = SR::add(oval, val);
     }
-    const uint32_t ncol = __shfl_down_sync(0xffffffffu, col, 1);
+    const uint32_t ncol = __shfl_down_sync(kFull, col, 1);
     const bool tail = valid && (lane == 31 || ncol != col);
     const bool keep = tail && !SR::is_zero(val);
-    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    const unsigned m = __ballot_sync(kFull, keep);
     const int pos = __popc(m & ((1u << lane) - 1));
     const int64_t o = off[i];
     if (keep) {
@@ -313,21 +432,251 @@ __global__ void __launch_bounds__(256) esc_warp_kernel(Src src, const int64_t* _
 }
 
 // ---------------------------------------------------------------------------
+// K4 bins 2-4: block-ESC.  Products of one row are placed in product order
+// (segment-major) in shared memory, stably radix-sorted by column, and each
+// run of equal columns is folded by a segmented block scan.
+// ---------------------------------------------------------------------------
+template <class SR>
+struct SegFold {
+  using V = typename SR::value_type;
+  struct T {
+    V v;
+    int head;
+  };
+  __device__ __forceinline__ T operator()(const T& a, const T& b) const {
+    T r;
+    r.head = a.head | b.head;
+    r.v = b.head ? b.v : SR::add(a.v, b.v);
+    return r;
+  }
+};
+
+template <class SR, int THREADS, int ITEMS>
+struct EscSmem {
+  using V = typename SR::value_type;
+  static constexpr int CAP = THREADS * ITEMS;
+  using Sort = cub::BlockRadixSort<uint32_t, THREADS, ITEMS, uint16_t, 6>;
+  using Fold = cub::BlockScan<typename SegFold<SR>::T, THREADS>;
+  using Count = cub::BlockScan<int, THREADS>;
+  union {
+    typename Sort::TempStorage sort;
+    typename Fold::TempStorage fold;
+    typename Count::TempStorage count;
+  } tmp;
+  uint32_t keys[CAP];
+  V vals[CAP];
+  int seg_off[CAP + 1];  // exclusive prefix of segment lengths (<= CAP segments)
+  uint32_t run_cols[CAP + 1];
+};
+
+template <class SR, class Src, int THREADS, int ITEMS>
+__global__ void __launch_bounds__(THREADS) esc_block_kernel(Src src, const int64_t* __restrict__ rows,
+                                                            int64_t nrows_bin, int end_bit,
+                                                            const int64_t* __restrict__ off,
+                                                            int32_t* __restrict__ out_cols,
+                                                            typename SR::value_type* __restrict__ out_vals,
+                                                            int64_t* __restrict__ rownnz) {
+  using V = typename SR::value_type;
+  using S = EscSmem<SR, THREADS, ITEMS>;
+  constexpr int NW = THREADS / 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  S& sm = *reinterpret_cast<S*>(smem_raw);
+  const int wid = threadIdx.x >> 5;
+
+  for (int64_t r = blockIdx.x; r < nrows_bin; r += gridDim.x) {
+    const int64_t i = rows[r];
+    const int64_t sb = src.seg_begin(i), se = src.seg_end(i);
+    const int nseg = (int)(se - sb);  // <= CAP for these bins
+    // 1. exclusive prefix of segment lengths (product order = segment order)
+    int lens[ITEMS];
+    int local = 0;
+#pragma unroll
+    for (int q = 0; q < ITEMS; ++q) {
+      const int s = threadIdx.x * ITEMS + q;
+      lens[q] = s < nseg ? (int)src.seg_len(i, sb + s) : 0;
+      local += lens[q];
+    }
+    int first, total;
+    typename S::Count(sm.tmp.count).ExclusiveSum(local, first, total);
+#pragma unroll
+    for (int q = 0; q < ITEMS; ++q) {
+      const int s = threadIdx.x * ITEMS + q;
+      if (s < nseg) sm.seg_off[s] = first;
+      first += lens[q];
+    }
+    __syncthreads();
+    // 2. expand: each product lands at seg_off[s] + offset-in-segment
+    warp_items<SR>(src, i, sb + wid * 32, se, -1, (int64_t)NW * 32,
+                   [&](int32_t c, const V& v, int64_t s, int o) {
+                     const int pos = sm.seg_off[s - sb] + o;
+                     sm.keys[pos] = (uint32_t)c;
+                     sm.vals[pos] = v;
+                   });
+    __syncthreads();
+    // 3. stable radix sort of (column -> product index), blocked arrangement
+    uint32_t k[ITEMS];
+    uint16_t idx[ITEMS];
+#pragma unroll
+    for (int q = 0; q < ITEMS; ++q) {
+      const int e = threadIdx.x * ITEMS + q;
+      k[q] = e < total ? sm.keys[e] : (1u << end_bit);  // padding sorts last
+      idx[q] = (uint16_t)e;
+    }
+    __syncthreads();
+    typename S::Sort(sm.tmp.sort).Sort(k, idx, 0, end_bit + 1);
+    __syncthreads();
+    // 4. segmented fold of equal-column runs
+#pragma unroll
+    for (int q = 0; q < ITEMS; ++q) sm.run_cols[threadIdx.x * ITEMS + q] = k[q];
+    if (threadIdx.x == 0) sm.run_cols[S::CAP] = 0xffffffffu;
+    __syncthreads();
+    typename SegFold<SR>::T t[ITEMS];
+#pragma unroll
+    for (int q = 0; q < ITEMS; ++q) {
+      const int e = threadIdx.x * ITEMS + q;
+      t[q].head = (e == 0 || sm.run_cols[e - 1] != k[q]) ? 1 : 0;
+      t[q].v = e < total ? sm.vals[idx[q]] : SR::zero();
+    }
+    __syncthreads();
+    typename S::Fold(sm.tmp.fold).InclusiveScan(t, t, SegFold<SR>());
+    __syncthreads();
+    // 5. keep run tails with non-zero value; compact in column order
+    int keep[ITEMS];
+    int nkeep = 0;
+#pragma unroll
+    for (int q = 0; q < ITEMS; ++q) {
+      const int e = threadIdx.x * ITEMS + q;
+      const bool tail = e < total && sm.run_cols[e + 1] != k[q];
+      keep[q] = (tail && !SR::is_zero(t[q].v)) ? 1 : 0;
+      nkeep += keep[q];
+    }
+    int kfirst, ktotal;
+    typename S::Count(sm.tmp.count).ExclusiveSum(nkeep, kfirst, ktotal);
+    const int64_t o = off[i];
+#pragma unroll
+    for (int q = 0; q < ITEMS; ++q) {
+      if (keep[q]) {
+        out_cols[o + kfirst] = (int32_t)k[q];
+        out_vals[o + kfirst] = t[q].v;
+        ++kfirst;
+      }
+    }
+    if (threadIdx.x == 0) rownnz[i] = ktotal;
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5 bin 6: dense accumulator over column panels in shared memory.
+// CTAs pull rows (largest first) from a work counter; for each panel the
+// row's products are accumulated with native smem atomics, then the presence
+// bitmap is scanned in column order to emit sorted output while restoring
+// the accumulator to zero() - so no panel ever needs a separate clear.
+// ---------------------------------------------------------------------------
+template <class SR, class Src, int W, int THREADS>
+__global__ void __launch_bounds__(THREADS) dense_panel_kernel(Src src, const int64_t* __restrict__ rows,
+                                                              int64_t nrows_bin, int npanels,
+                                                              unsigned long long* __restrict__ work,
+                                                              const int64_t* __restrict__ off,
+                                                              int32_t* __restrict__ out_cols,
+                                                              typename SR::value_type* __restrict__ out_vals,
+                                                              int64_t* __restrict__ rownnz) {
+  using V = typename SR::value_type;
+  constexpr int NW = THREADS / 32;
+  constexpr int WORDS = W / 32;
+  constexpr int WPT = (WORDS + THREADS - 1) / THREADS;
+  using Count = cub::BlockScan<int, THREADS>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* acc = reinterpret_cast<V*>(smem_raw);
+  uint32_t* bm = reinterpret_cast<uint32_t*>(smem_raw + sizeof(V) * W);
+  __shared__ typename Count::TempStorage scan_tmp;
+  __shared__ long long s_row;
+  const int wid = threadIdx.x >> 5;
+
+  for (int e = threadIdx.x; e < W; e += THREADS) acc[e] = SR::zero();
+  for (int e = threadIdx.x; e < WORDS; e += THREADS) bm[e] = 0u;
+  __syncthreads();
+  for (;;) {
+    if (threadIdx.x == 0) {
+      const unsigned long long r = atomicAdd(work, 1ull);
+      s_row = r < (unsigned long long)nrows_bin ? (long long)r : -1;
+    }
+    __syncthreads();
+    const long long r = s_row;
+    __syncthreads();
+    if (r < 0) break;
+    const int64_t i = rows[r];
+    const int64_t sb = src.seg_begin(i), se = src.seg_end(i);
+    int64_t written = 0;
+    const int64_t o = off[i];
+    for (int p = 0; p < npanels; ++p) {
+      const int lo = p * W;
+      warp_items<SR>(src, i, sb + wid * 32, se, npanels > 1 ? p : -1, (int64_t)NW * 32,
+                     [&](int32_t c, const V& v, int64_t, int) {
+                       const int cc = c - lo;
+                       atomic_accumulate<SR, true>(&acc[cc], v);
+                       atomicOr(&bm[cc >> 5], 1u << (cc & 31));
+                     });
+      __syncthreads();
+      // ordered scan of the bitmap (thread t owns words [t*WPT, t*WPT+WPT))
+      uint32_t bits[WPT], keepm[WPT];
+      int cnt = 0;
+#pragma unroll
+      for (int q = 0; q < WPT; ++q) {
+        const int w = threadIdx.x * WPT + q;
+        bits[q] = w < WORDS ? bm[w] : 0u;
+        keepm[q] = 0u;
+        for (uint32_t x = bits[q]; x; x &= x - 1) {
+          const int bit = __ffs(x) - 1;
+          if (!SR::is_zero(acc[(w << 5) + bit])) keepm[q] |= 1u << bit;
+        }
+        cnt += __popc(keepm[q]);
+      }
+      int first, total;
+      Count(scan_tmp).ExclusiveSum(cnt, first, total);
+      int64_t pos = o + written + first;
+#pragma unroll
+      for (int q = 0; q < WPT; ++q) {
+        const int w = threadIdx.x * WPT + q;
+        for (uint32_t x = bits[q]; x; x &= x - 1) {
+          const int bit = __ffs(x) - 1;
+          const int cc = (w << 5) + bit;
+          if (keepm[q] & (1u << bit)) {
+            out_cols[pos] = lo + cc;
+            out_vals[pos] = acc[cc];
+            ++pos;
+          }
+          acc[cc] = SR::zero();
+        }
+        if (bits[q]) bm[w] = 0u;
+      }
+      written += total;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) rownnz[i] = written;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Shared-memory bitonic sort of n uint64 keys (pads to a power of two).
 // ---------------------------------------------------------------------------
 template <int THREADS>
 __device__ __forceinline__ void block_bitonic_sort(uint64_t* buf, int n) {
-  int p = 1;
-  while (p < n) p <<= 1;
+  int p = 1, lp = 0;
+  while (p < n) {
+    p <<= 1;
+    ++lp;
+  }
   for (int e = n + threadIdx.x; e < p; e += THREADS) buf[e] = ~0ull;
   __syncthreads();
-  for (int k = 2; k <= p; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
+  for (int lk = 1; lk <= lp; ++lk) {
+    for (int lj = lk - 1; lj >= 0; --lj) {
+      const int j = 1 << lj;
       for (int t = threadIdx.x; t < (p >> 1); t += THREADS) {
-        const int a = 2 * j * (t / j) + (t % j);
+        const int a = ((t >> lj) << (lj + 1)) | (t & (j - 1));
         const int b = a + j;
         const uint64_t x = buf[a], y = buf[b];
-        const bool up = (a & k) == 0;
+        const bool up = ((a >> lk) & 1) == 0;
         if ((x > y) == up) {
           buf[a] = y;
           buf[b] = x;
@@ -343,30 +692,29 @@ __device__ __forceinline__ uint32_t hash_slot(uint32_t col, int log2t) {
 }
 
 // ---------------------------------------------------------------------------
-// K4 bins 2-5: CTA-wide shared-memory hash accumulator, T slots.
+// K4 bins 5,7: CTA-wide shared-memory hash accumulator, T slots (used when the
+// output is so wide that dense panels would be mostly empty).
 // ---------------------------------------------------------------------------
 template <class SR, class Src, int T, int THREADS>
 __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64_t* __restrict__ rows,
-                                                            int64_t nrows_bin,
-                                                            const int64_t* __restrict__ off,
+                                                            int64_t nrows_bin, const int64_t* __restrict__ off,
                                                             int32_t* __restrict__ out_cols,
                                                             typename SR::value_type* __restrict__ out_vals,
                                                             int64_t* __restrict__ rownnz) {
   using V = typename SR::value_type;
-  constexpr int SPT = T / THREADS;  // slots per thread in compaction
+  constexpr int SPT = T / THREADS;
   constexpr int NW = THREADS / 32;
   constexpr int LOG2T = (T == 512) ? 9 : (T == 1024) ? 10 : (T == 2048) ? 11 : (T == 4096) ? 12
                       : (T == 8192) ? 13 : (T == 16384) ? 14 : 15;
   static_assert((1 << LOG2T) == T, "T must be a power of two");
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  V* tvals = reinterpret_cast<V*>(smem_raw);                                // T values
-  int32_t* tkeys = reinterpret_cast<int32_t*>(smem_raw + sizeof(V) * T);    // T keys
-  uint64_t* sortbuf = reinterpret_cast<uint64_t*>(tkeys);                   // aliases keys (<= T/2 entries)
+  V* tvals = reinterpret_cast<V*>(smem_raw);
+  int32_t* tkeys = reinterpret_cast<int32_t*>(smem_raw + sizeof(V) * T);
+  uint64_t* sortbuf = reinterpret_cast<uint64_t*>(tkeys);  // aliases keys (<= T/2 entries)
   using BlockScan = cub::BlockScan<int, THREADS>;
   __shared__ typename BlockScan::TempStorage scan_tmp;
   __shared__ int s_total;
-
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int wid = threadIdx.x >> 5;
   for (int64_t r = blockIdx.x; r < nrows_bin; r += gridDim.x) {
     const int64_t i = rows[r];
     for (int e = threadIdx.x; e < T; e += THREADS) {
@@ -374,39 +722,28 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
       tvals[e] = SR::zero();
     }
     __syncthreads();
-    const int64_t se = src.seg_end(i);
-    for (int64_t s = src.seg_begin(i) + wid; s < se; s += NW) {
-      int64_t b, len;
-      const int32_t* cols;
-      const V* vals;
-      V mult;
-      src.segment(i, s, b, len, cols, vals, mult);
-      for (int64_t u = b + lane; u < b + len; u += 32) {
-        const int32_t c = __ldg(cols + u);
-        const V v = src.item(mult, vals[u]);
-        uint32_t h = hash_slot((uint32_t)c, LOG2T);
-        for (;;) {
-          const int32_t k = *reinterpret_cast<volatile int32_t*>(&tkeys[h]);
-          if (k == c) break;
-          if (k == kEmptyKey) {
-            const int32_t prev = atomicCAS(&tkeys[h], kEmptyKey, c);
-            if (prev == kEmptyKey || prev == c) break;
-          }
-          h = (h + 1) & (T - 1);
-        }
-        atomic_accumulate<SR, true>(&tvals[h], v);
-      }
-    }
+    warp_items<SR>(src, i, src.seg_begin(i) + wid * 32, src.seg_end(i), -1, (int64_t)NW * 32,
+                   [&](int32_t c, const V& v, int64_t, int) {
+                     uint32_t h = hash_slot((uint32_t)c, LOG2T);
+                     for (;;) {
+                       const int32_t k = *reinterpret_cast<volatile int32_t*>(&tkeys[h]);
+                       if (k == c) break;
+                       if (k == kEmptyKey) {
+                         const int32_t prev = atomicCAS(&tkeys[h], kEmptyKey, c);
+                         if (prev == kEmptyKey || prev == c) break;
+                       }
+                       h = (h + 1) & (T - 1);
+                     }
+                     atomic_accumulate<SR, true>(&tvals[h], v);
+                   });
     __syncthreads();
-    // compaction: gather occupied non-zero slots
     int my_slots[SPT];
     int cnt = 0;
 #pragma unroll
     for (int q = 0; q < SPT; ++q) {
       const int e = threadIdx.x * SPT + q;
-      const int32_t k = tkeys[e];
       my_slots[q] = -1;
-      if (k != kEmptyKey && !SR::is_zero(tvals[e])) {
+      if (tkeys[e] != kEmptyKey && !SR::is_zero(tvals[e])) {
         my_slots[q] = e;
         ++cnt;
       }
@@ -416,14 +753,11 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
     uint32_t my_keys[SPT];
 #pragma unroll
     for (int q = 0; q < SPT; ++q) my_keys[q] = my_slots[q] >= 0 ? (uint32_t)tkeys[my_slots[q]] : 0u;
-    __syncthreads();  // all keys read before the sort buffer overwrites them
+    __syncthreads();
     int w = first;
 #pragma unroll
-    for (int q = 0; q < SPT; ++q) {
-      if (my_slots[q] >= 0) {
-        sortbuf[w++] = ((uint64_t)my_keys[q] << 32) | (uint32_t)my_slots[q];
-      }
-    }
+    for (int q = 0; q < SPT; ++q)
+      if (my_slots[q] >= 0) sortbuf[w++] = ((uint64_t)my_keys[q] << 32) | (uint32_t)my_slots[q];
     if (threadIdx.x == 0) s_total = total;
     __syncthreads();
     const int n = s_total;
@@ -440,89 +774,14 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
 }
 
 // ---------------------------------------------------------------------------
-// K5 bin 6: dense accumulator in global memory.  Each CTA owns a slab of
-// ncols values + an ncols-bit presence bitmap (zeroed by the host, restored
-// to zero/zero() after each row so the slab is reusable).
-// ---------------------------------------------------------------------------
-template <class SR, class Src, int THREADS>
-__global__ void __launch_bounds__(THREADS) dense_rows_kernel(Src src, const int64_t* __restrict__ rows,
-                                                             int64_t nrows_bin, int64_t ncols,
-                                                             typename SR::value_type* __restrict__ slabs,
-                                                             uint32_t* __restrict__ bitmaps,
-                                                             const int64_t* __restrict__ off,
-                                                             int32_t* __restrict__ out_cols,
-                                                             typename SR::value_type* __restrict__ out_vals,
-                                                             int64_t* __restrict__ rownnz) {
-  using V = typename SR::value_type;
-  constexpr int NW = THREADS / 32;
-  using BlockScan = cub::BlockScan<int, THREADS>;
-  __shared__ typename BlockScan::TempStorage scan_tmp;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t nwords = (ncols + 31) >> 5;
-  V* dv = slabs + (int64_t)blockIdx.x * ncols;
-  uint32_t* bm = bitmaps + (int64_t)blockIdx.x * nwords;
-  for (int64_t e = threadIdx.x; e < ncols; e += THREADS) dv[e] = SR::zero();
-  __syncthreads();
-  for (int64_t r = blockIdx.x; r < nrows_bin; r += gridDim.x) {
-    const int64_t i = rows[r];
-    const int64_t se = src.seg_end(i);
-    for (int64_t s = src.seg_begin(i) + wid; s < se; s += NW) {
-      int64_t b, len;
-      const int32_t* cols;
-      const V* vals;
-      V mult;
-      src.segment(i, s, b, len, cols, vals, mult);
-      for (int64_t u = b + lane; u < b + len; u += 32) {
-        const int32_t c = __ldg(cols + u);
-        const V v = src.item(mult, vals[u]);
-        atomic_accumulate<SR, false>(&dv[c], v);
-        atomicOr(&bm[c >> 5], 1u << (c & 31));
-      }
-    }
-    __syncthreads();
-    const int64_t o = off[i];
-    int64_t written = 0;
-    for (int64_t w0 = 0; w0 < nwords; w0 += THREADS) {
-      const int64_t w = w0 + threadIdx.x;
-      uint32_t bits = w < nwords ? bm[w] : 0u;
-      uint32_t keep = 0;
-      for (uint32_t x = bits; x; x &= x - 1) {
-        const int bit = __ffs(x) - 1;
-        if (!SR::is_zero(dv[(w << 5) + bit])) keep |= 1u << bit;
-      }
-      const int cnt = __popc(keep);
-      int first, total;
-      BlockScan(scan_tmp).ExclusiveSum(cnt, first, total);
-      int64_t p = o + written + first;
-      for (uint32_t x = bits; x; x &= x - 1) {
-        const int bit = __ffs(x) - 1;
-        const int64_t c = (w << 5) + bit;
-        if (keep & (1u << bit)) {
-          out_cols[p] = (int32_t)c;
-          out_vals[p] = dv[c];
-          ++p;
-        }
-        dv[c] = SR::zero();
-      }
-      if (bits) bm[w] = 0u;
-      written += total;
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) rownnz[i] = written;
-    __syncthreads();
-  }
-}
-
-// ---------------------------------------------------------------------------
-// K7: compaction scratch -> exact CSR (warp per row, 16-byte stores when the
-// run is long enough)
+// K7: compaction scratch -> exact CSR (warp per row, 4-way unrolled)
 // ---------------------------------------------------------------------------
 template <class V>
 __global__ void __launch_bounds__(256) compact_rows_kernel(int64_t nrows, const int64_t* __restrict__ off,
                                                            const int64_t* __restrict__ rowptr,
                                                            const int32_t* __restrict__ sc_cols,
-                                                           const V* __restrict__ sc_vals,
-                                                           int32_t* __restrict__ cols, V* __restrict__ vals) {
+                                                           const V* __restrict__ sc_vals, int32_t* __restrict__ cols,
+                                                           V* __restrict__ vals) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -530,7 +789,21 @@ __global__ void __launch_bounds__(256) compact_rows_kernel(int64_t nrows, const 
     const int64_t d = rowptr[i];
     const int64_t n = rowptr[i + 1] - d;
     const int64_t s = off[i];
-    for (int64_t e = lane; e < n; e += 32) {
+    int64_t e = lane;
+    for (; e + 96 < n; e += 128) {
+      const int32_t c0 = sc_cols[s + e], c1 = sc_cols[s + e + 32], c2 = sc_cols[s + e + 64],
+                    c3 = sc_cols[s + e + 96];
+      const V v0 = sc_vals[s + e], v1 = sc_vals[s + e + 32], v2 = sc_vals[s + e + 64], v3 = sc_vals[s + e + 96];
+      cols[d + e] = c0;
+      cols[d + e + 32] = c1;
+      cols[d + e + 64] = c2;
+      cols[d + e + 96] = c3;
+      vals[d + e] = v0;
+      vals[d + e + 32] = v1;
+      vals[d + e + 64] = v2;
+      vals[d + e + 96] = v3;
+    }
+    for (; e < n; e += 32) {
       cols[d + e] = sc_cols[s + e];
       vals[d + e] = sc_vals[s + e];
     }

@@ -201,6 +201,11 @@ void spg_ctx_destroy(spg_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  for (int k = 0; k < 4; ++k) {
+    if (c->aux[k]) cudaStreamDestroy(c->aux[k]);
+    if (c->aux_ev[k]) cudaEventDestroy(c->aux_ev[k]);
+  }
+  if (c->fork_ev) cudaEventDestroy(c->fork_ev);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
 }

@@ -47,6 +47,9 @@ struct spg_ctx {
   size_t cub_tmp_bytes = 0;
   // per-phase timing of the last local multiply / merge (CUDA events)
   cudaEvent_t ev[8] = {};
+  cudaStream_t aux[4] = {};      // side streams for concurrent bins
+  cudaEvent_t aux_ev[4] = {};
+  cudaEvent_t fork_ev = nullptr;
   uint64_t launches = 0;  // kernels launched by this context (evidence counter)
   size_t scratch_budget = 0;  // bytes the row-batched numeric pass may use (0 = auto)
 };

@@ -1,7 +1,8 @@
 // Host driver for the row-accumulation pipeline in accumulate.cuh: runs
-// analyse -> bin -> numeric (row-batched under a scratch budget) -> compact
-// for any Source, producing an exact-size device CSR.
+// analyse -> bin -> numeric (row-batched under a scratch budget, bins on
+// concurrent streams) -> compact for any Source, producing an exact CSR.
 #pragma once
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -47,31 +48,91 @@ inline int grid_for(spg_ctx* c, int64_t work_items, int per_block, int max_waves
   return (int)std::max<int64_t>(1, std::min<int64_t>(want, cap));
 }
 
+// Forked side streams so independent bins overlap on the SMs.
+struct StreamFork {
+  spg_ctx* c;
+  int n;
+  StreamFork(spg_ctx* ctx, int count) : c(ctx), n(count) {
+    for (int k = 0; k < n; ++k) {
+      if (!c->aux[k]) SPG_CUDA(cudaStreamCreateWithFlags(&c->aux[k], cudaStreamNonBlocking));
+      if (!c->aux_ev[k]) SPG_CUDA(cudaEventCreateWithFlags(&c->aux_ev[k], cudaEventDisableTiming));
+    }
+    if (!c->fork_ev) SPG_CUDA(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
+    SPG_CUDA(cudaEventRecord(c->fork_ev, c->stream));
+    for (int k = 0; k < n; ++k) SPG_CUDA(cudaStreamWaitEvent(c->aux[k], c->fork_ev, 0));
+  }
+  cudaStream_t operator[](int k) const { return c->aux[k % n]; }
+  void join() {
+    for (int k = 0; k < n; ++k) {
+      SPG_CUDA(cudaEventRecord(c->aux_ev[k], c->aux[k]));
+      SPG_CUDA(cudaStreamWaitEvent(c->stream, c->aux_ev[k], 0));
+    }
+  }
+};
+
+template <class K>
+inline void set_smem(K kern, size_t smem) {
+  if (smem > 48 * 1024) SPG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+}
+
+template <class K>
+inline int resident_grid(spg_ctx* c, K kern, int threads, size_t smem, int64_t work) {
+  int per_sm = 1;
+  SPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+  const int64_t cap = (int64_t)c->sm_count * std::max(per_sm, 1);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(work, cap));
+}
+
 template <class SR, class Src, int T, int THREADS>
-void launch_hash(spg_ctx* c, const Src& src, const int64_t* rows, int64_t n, const int64_t* off,
+void launch_hash(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* rows, int64_t n, const int64_t* off,
                  int32_t* sc_cols, typename SR::value_type* sc_vals, int64_t* rownnz) {
   using V = typename SR::value_type;
   const size_t smem = (size_t)T * (sizeof(V) + sizeof(int32_t));
   auto kern = hash_rows_kernel<SR, Src, T, THREADS>;
-  static bool configured = false;  // per template instantiation
-  if (!configured) {
-    SPG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
-  }
-  int per_sm = 1;
-  SPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem));
-  const int64_t cap = (int64_t)c->sm_count * std::max(per_sm, 1);
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(n, cap));
-  kern<<<grid, THREADS, smem, c->stream>>>(src, rows, n, off, sc_cols, sc_vals, rownnz);
+  set_smem(kern, smem);
+  kern<<<resident_grid(c, kern, THREADS, smem, n), THREADS, smem, s>>>(src, rows, n, off, sc_cols, sc_vals, rownnz);
   SPG_LAUNCH_CHECK();
   ++c->launches;
 }
 
+template <class SR, class Src, int THREADS, int ITEMS>
+void launch_esc(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* rows, int64_t n, int end_bit,
+                const int64_t* off, int32_t* sc_cols, typename SR::value_type* sc_vals, int64_t* rownnz) {
+  const size_t smem = sizeof(EscSmem<SR, THREADS, ITEMS>);
+  auto kern = esc_block_kernel<SR, Src, THREADS, ITEMS>;
+  set_smem(kern, smem);
+  kern<<<resident_grid(c, kern, THREADS, smem, n), THREADS, smem, s>>>(src, rows, n, end_bit, off, sc_cols, sc_vals,
+                                                                       rownnz);
+  SPG_LAUNCH_CHECK();
+  ++c->launches;
+}
+
+template <class SR>
+inline void set_panels(MulSource<SR>& s, const int32_t* poff, int np, int) {
+  s.poff = poff;
+  s.npanels = np;
+}
+template <class SR>
+inline void set_panels(MergeSource<SR>& s, const int32_t*, int, int w) {
+  s.panel_w = w;
+}
+template <class SR>
+inline bool needs_poff(const MulSource<SR>&) {
+  return true;
+}
+template <class SR>
+inline bool needs_poff(const MergeSource<SR>&) {
+  return false;
+}
+
 // Runs the pipeline for rows [0, src.nrows) with output width ncols_out.
+// `r_for_panels` (the right operand) is needed to build the panel offsets
+// of the dense bin for a MulSource.
 template <class SR, class Src>
-void run_rows(spg_ctx* c, const Src& src, int64_t ncols_out, spg_dcsr* out, spg_mult_stats* st) {
+void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, spg_mult_stats* st,
+              const spg_dcsr* r_for_panels = nullptr) {
   using V = typename SR::value_type;
-  const int64_t m = src.nrows;
+  const int64_t m = src_in.nrows;
   PhaseTimer tm(c, st != nullptr);
   const uint64_t launches0 = c->launches;
   tm.mark(0);
@@ -89,29 +150,22 @@ void run_rows(spg_ctx* c, const Src& src, int64_t ncols_out, spg_dcsr* out, spg_
     if (st) *st = spg_mult_stats{};
     return;
   }
+  Src src = src_in;
 
   // K1 analyse
   DBuf<int64_t> prods(c, m), ub(c, m + 1), off(c, m + 1), rownnz(c, m + 1);
   DBuf<uint8_t> bins(c, m);
-  {
-    const int grid = grid_for(c, m, 8);
-    analyse_rows_kernel<SR, Src><<<grid, 256, 0, c->stream>>>(src, ncols_out, prods.p, ub.p, bins.p);
-    SPG_LAUNCH_CHECK();
-    ++c->launches;
-  }
+  analyse_rows_kernel<SR, Src><<<grid_for(c, m, 8), 256, 0, c->stream>>>(src, ncols_out, prods.p, ub.p, bins.p);
+  SPG_LAUNCH_CHECK();
+  ++c->launches;
   SPG_CUDA(cudaMemsetAsync(ub.p + m, 0, sizeof(int64_t), c->stream));
   SPG_CUDA(cudaMemsetAsync(rownnz.p + m, 0, sizeof(int64_t), c->stream));
   exclusive_scan(c, ub.p, off.p, m + 1);  // off[m] = total scratch entries
-  // products total (for stats) via scan on prods is not needed on the hot
-  // path; F is reduced from the same array into a scalar below.
-  DBuf<unsigned long long> counts(c, 2 * kNumBins);
-  SPG_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(unsigned long long) * 2 * kNumBins, c->stream));
-  {
-    const int grid = grid_for(c, m, 1024, 2);
-    bin_count_kernel<<<grid, 1024, 0, c->stream>>>(bins.p, m, counts.p);
-    SPG_LAUNCH_CHECK();
-    ++c->launches;
-  }
+  DBuf<unsigned long long> counts(c, kNumBins + 1);
+  SPG_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(unsigned long long) * (kNumBins + 1), c->stream));
+  bin_count_kernel<<<grid_for(c, m, 1024, 2), 1024, 0, c->stream>>>(bins.p, m, counts.p);
+  SPG_LAUNCH_CHECK();
+  ++c->launches;
   unsigned long long hcounts[kNumBins];
   int64_t scratch_total = 0;
   SPG_CUDA(cudaMemcpyAsync(hcounts, counts.p, sizeof(hcounts), cudaMemcpyDeviceToHost, c->stream));
@@ -127,6 +181,24 @@ void run_rows(spg_ctx* c, const Src& src, int64_t ncols_out, spg_dcsr* out, spg_
     ++c->launches;
     products = d2h_scalar(c, fsum.p);
   }
+
+  // Panels for the dense bin.
+  const int W = Geom<V>::kPanelW;
+  const int np = npanels_for<V>(ncols_out);
+  DBuf<int32_t> poff;
+  if (hcounts[kBinDense] > 0 && np > 1) {
+    if (needs_poff(src)) {
+      if (!r_for_panels) fail(SPG_ERR_INTERNAL, "dense panels need the right operand");
+      const spg_dcsr& R = *r_for_panels;
+      poff = DBuf<int32_t>(c, (size_t)R.nrows * (np + 1));
+      panel_offsets_kernel<<<grid_for(c, R.nrows, 8), 256, 0, c->stream>>>(R.nrows, R.ptr, R.idx, np, W, poff.p);
+      SPG_LAUNCH_CHECK();
+      ++c->launches;
+    }
+    set_panels(src, poff.p, np, W);
+  }
+  int end_bit = 0;
+  while ((int64_t{1} << end_bit) < ncols_out) ++end_bit;
 
   // Row batches under the scratch budget (contiguous row ranges).
   size_t budget = c->scratch_budget;
@@ -146,7 +218,6 @@ void run_rows(spg_ctx* c, const Src& src, int64_t ncols_out, spg_dcsr* out, spg_
     const int64_t cap_entries = std::max<int64_t>(1, (int64_t)(budget / per_entry));
     int64_t r0 = 0;
     while (r0 < m) {
-      // largest r1 with hoff[r1] - hoff[r0] <= cap (at least one row)
       int64_t r1 = std::upper_bound(hoff.begin() + r0 + 1, hoff.end(), hoff[r0] + cap_entries) - hoff.begin() - 1;
       if (r1 <= r0) r1 = r0 + 1;
       cuts.push_back(r1);
@@ -155,22 +226,6 @@ void run_rows(spg_ctx* c, const Src& src, int64_t ncols_out, spg_dcsr* out, spg_
   }
   const bool batched = cuts.size() > 2;
   tm.mark(1);
-
-  // Dense slabs (bin 6), sized once for all batches.
-  const int64_t n6_total = (int64_t)hcounts[6];
-  int dense_grid = 0;
-  DBuf<V> slabs;
-  DBuf<uint32_t> bitmaps;
-  const int64_t nwords = (ncols_out + 31) / 32;
-  if (n6_total > 0) {
-    const size_t per_cta = (size_t)ncols_out * sizeof(V) + (size_t)nwords * 4;
-    const size_t slab_budget = (size_t)4 << 30;
-    dense_grid = (int)std::max<int64_t>(1, std::min<int64_t>({n6_total, (int64_t)c->sm_count * 2,
-                                                             (int64_t)(slab_budget / std::max<size_t>(per_cta, 1))}));
-    slabs = DBuf<V>(c, (size_t)dense_grid * ncols_out);
-    bitmaps = DBuf<uint32_t>(c, (size_t)dense_grid * nwords);
-    SPG_CUDA(cudaMemsetAsync(bitmaps.p, 0, sizeof(uint32_t) * dense_grid * nwords, c->stream));
-  }
 
   DBuf<int64_t> lists(c, m);
   DBuf<unsigned long long> cursor(c, kNumBins);
@@ -201,13 +256,11 @@ void run_rows(spg_ctx* c, const Src& src, int64_t ncols_out, spg_dcsr* out, spg_
       if (b > 0) acc += bcount[b];
     }
     SPG_CUDA(cudaMemcpyAsync(cursor.p, base, sizeof(base), cudaMemcpyHostToDevice, c->stream));
-    // lists hold absolute row ids; bins.p + r0 scanning yields ids relative to r0
-    bin_scatter_kernel<<<grid_for(c, r1 - r0, 1024, 2), 1024, 0, c->stream>>>(bins.p + r0, r1 - r0,
-                                                                             cursor.p, lists.p);
+    bin_scatter_kernel<<<grid_for(c, r1 - r0, 1024, 2), 1024, 0, c->stream>>>(bins.p + r0, r1 - r0, cursor.p,
+                                                                             lists.p);
     SPG_LAUNCH_CHECK();
     ++c->launches;
 
-    // scratch for this batch; offsets are relative to off[r0]
     int64_t sc_lo = 0, sc_hi = scratch_total;
     if (batched) {
       SPG_CUDA(cudaMemcpyAsync(&sc_lo, off.p + r0, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
@@ -220,48 +273,86 @@ void run_rows(spg_ctx* c, const Src& src, int64_t ncols_out, spg_dcsr* out, spg_
     // pointers so this batch's window [sc_lo, sc_hi) is what they address.
     int32_t* sccb = sc_cols.p - sc_lo;
     V* scvb = sc_vals.p - sc_lo;
-    // Row ids in `lists` are relative to r0 (bin_scatter ran over bins + r0):
-    // hand the kernels views that start at row r0.
+    // Row ids in `lists` are relative to r0 (bin_scatter ran over bins + r0).
     Src bsrc = src;
     rebase_source(bsrc, r0);
     const int64_t* offb = off.p + r0;
     int64_t* nnzb = rownnz.p + r0;
-
     const int64_t* lb = lists.p;
-    if (bcount[1] > 0) {
-      esc_warp_kernel<SR, Src><<<grid_for(c, bcount[1], 8), 256, 0, c->stream>>>(
-          bsrc, lb + base[1], bcount[1], offb, sccb, scvb, nnzb);
+
+    // dense bin: largest rows first
+    const int64_t nd = bcount[kBinDense];
+    const int64_t* dense_rows = lb + base[kBinDense];
+    DBuf<int64_t> dense_sorted, dk1, dk2;
+    DBuf<unsigned long long> work(c, 1);
+    if (nd > 1) {
+      dk1 = DBuf<int64_t>(c, nd);
+      dk2 = DBuf<int64_t>(c, nd);
+      dense_sorted = DBuf<int64_t>(c, nd);
+      gather_keys_kernel<<<grid_for(c, nd, 256, 4), 256, 0, c->stream>>>(dense_rows, nd, prods.p + r0, dk1.p);
       SPG_LAUNCH_CHECK();
       ++c->launches;
-    }
-    if (bcount[2] > 0) launch_hash<SR, Src, bin_table<V>(2), 128>(c, bsrc, lb + base[2], bcount[2], offb, sccb, scvb, nnzb);
-    if (bcount[3] > 0) launch_hash<SR, Src, bin_table<V>(3), 256>(c, bsrc, lb + base[3], bcount[3], offb, sccb, scvb, nnzb);
-    if (bcount[4] > 0) launch_hash<SR, Src, bin_table<V>(4), 512>(c, bsrc, lb + base[4], bcount[4], offb, sccb, scvb, nnzb);
-    if (bcount[5] > 0) launch_hash<SR, Src, bin_table<V>(5), 1024>(c, bsrc, lb + base[5], bcount[5], offb, sccb, scvb, nnzb);
-    if (bcount[6] > 0) {
-      const int g = (int)std::min<int64_t>(dense_grid, bcount[6]);
-      dense_rows_kernel<SR, Src, 1024><<<g, 1024, 0, c->stream>>>(bsrc, lb + base[6], bcount[6], ncols_out,
-                                                                 slabs.p, bitmaps.p, offb, sccb, scvb, nnzb);
-      SPG_LAUNCH_CHECK();
+      size_t bytes = 0;
+      SPG_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, dk1.p, dk2.p, dense_rows, dense_sorted.p,
+                                                          (int)nd, 0, 64, c->stream));
+      ensure_cub_tmp(c, bytes);
+      SPG_CUDA(cub::DeviceRadixSort::SortPairsDescending(c->cub_tmp, bytes, dk1.p, dk2.p, dense_rows,
+                                                          dense_sorted.p, (int)nd, 0, 64, c->stream));
       ++c->launches;
+      dense_rows = dense_sorted.p;
     }
-    // rows of bin 0 are never visited by a numeric kernel: nnz 0
-    if (bcount[0] > 0) {
+    SPG_CUDA(cudaMemsetAsync(work.p, 0, sizeof(unsigned long long), c->stream));
+    if (bcount[kBinEmpty] > 0) {
       zero_empty_rows_kernel<<<grid_for(c, r1 - r0, 256, 4), 256, 0, c->stream>>>(bins.p + r0, r1 - r0, nnzb);
       SPG_LAUNCH_CHECK();
       ++c->launches;
     }
+
+    StreamFork fk(c, 3);
+    if (nd > 0) {
+      constexpr int DT = 1024;
+      constexpr int PW = Geom<V>::kPanelW;
+      const size_t smem = sizeof(V) * PW + sizeof(uint32_t) * (PW / 32);
+      auto kern = dense_panel_kernel<SR, Src, PW, DT>;
+      set_smem(kern, smem);
+      kern<<<resident_grid(c, kern, DT, smem, nd), DT, smem, fk[0]>>>(bsrc, dense_rows, nd, np, work.p, offb, sccb,
+                                                                      scvb, nnzb);
+      SPG_LAUNCH_CHECK();
+      ++c->launches;
+    }
+    if (bcount[kBinHashMax] > 0)
+      launch_hash<SR, Src, Geom<V>::kMaxT, 1024>(c, fk[1], bsrc, lb + base[kBinHashMax], bcount[kBinHashMax], offb,
+                                                 sccb, scvb, nnzb);
+    if (bcount[kBinHash8K] > 0)
+      launch_hash<SR, Src, 8192, 512>(c, fk[1], bsrc, lb + base[kBinHash8K], bcount[kBinHash8K], offb, sccb, scvb,
+                                      nnzb);
+    if (bcount[kBinEsc4K] > 0)
+      launch_esc<SR, Src, 512, 8>(c, fk[1], bsrc, lb + base[kBinEsc4K], bcount[kBinEsc4K], end_bit, offb, sccb, scvb,
+                                  nnzb);
+    if (bcount[kBinEsc2K] > 0)
+      launch_esc<SR, Src, 256, 8>(c, fk[2], bsrc, lb + base[kBinEsc2K], bcount[kBinEsc2K], end_bit, offb, sccb, scvb,
+                                  nnzb);
+    if (bcount[kBinEsc512] > 0)
+      launch_esc<SR, Src, 128, 4>(c, fk[2], bsrc, lb + base[kBinEsc512], bcount[kBinEsc512], end_bit, offb, sccb,
+                                  scvb, nnzb);
+    if (bcount[kBinWarpEsc] > 0) {
+      esc_warp_kernel<SR, Src><<<grid_for(c, bcount[kBinWarpEsc], 8), 256, 0, fk[2]>>>(
+          bsrc, lb + base[kBinWarpEsc], bcount[kBinWarpEsc], offb, sccb, scvb, nnzb);
+      SPG_LAUNCH_CHECK();
+      ++c->launches;
+    }
+    fk.join();
     tm.mark(2);
     ms_numeric += tm.between(1, 2);
 
     if (!batched) {
       exclusive_scan(c, rownnz.p, out->ptr, m + 1);
-      int64_t nnz = d2h_scalar(c, out->ptr + m);
+      const int64_t nnz = d2h_scalar(c, out->ptr + m);
       out->nnz = nnz;
       out->idx = dalloc<int32_t>(c, (size_t)nnz);
       out->vals = dalloc<V>(c, (size_t)nnz);
-      compact_rows_kernel<V><<<grid_for(c, m, 8), 256, 0, c->stream>>>(
-          m, off.p, out->ptr, sccb, scvb, out->idx, static_cast<V*>(out->vals));
+      compact_rows_kernel<V><<<grid_for(c, m, 8), 256, 0, c->stream>>>(m, off.p, out->ptr, sccb, scvb, out->idx,
+                                                                       static_cast<V*>(out->vals));
       SPG_LAUNCH_CHECK();
       ++c->launches;
     } else {
@@ -273,8 +364,8 @@ void run_rows(spg_ctx* c, const Src& src, int64_t ncols_out, spg_dcsr* out, spg_
       const int64_t bn = d2h_scalar(c, bptr.p + (r1 - r0));
       DBuf<int32_t> pc(c, (size_t)bn);
       DBuf<V> pv(c, (size_t)bn);
-      compact_rows_kernel<V><<<grid_for(c, r1 - r0, 8), 256, 0, c->stream>>>(
-          r1 - r0, offb, bptr.p, sccb, scvb, pc.p, pv.p);
+      compact_rows_kernel<V><<<grid_for(c, r1 - r0, 8), 256, 0, c->stream>>>(r1 - r0, offb, bptr.p, sccb, scvb, pc.p,
+                                                                             pv.p);
       SPG_LAUNCH_CHECK();
       ++c->launches;
       part_cols.push_back(std::move(pc));

@@ -148,3 +148,51 @@ def test_device_checksum_matches_reference(ctx):
     for sr in (0, 1, 2, 3, 4, 5):
         m = _rand(sr, rng, 77, 51, 0.1)
         assert matrix_checksum(m, ctx=ctx) == ob.orc_checksum(to_mat(m))
+
+
+@pytest.mark.parametrize("sr", [0, 2, 4, 5])
+def test_wide_output_uses_hash_bins(ctx, sr):
+    """Outputs wider than 16 dense panels with medium rows go to the hash bins."""
+    rng = np.random.default_rng(7 + sr)
+    from golden.make_golden import exact_values
+    n = 1_200_000
+    lens = rng.integers(30, 120, 400)
+    bptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    bcols = np.concatenate([np.sort(rng.choice(n, L, replace=False)) for L in lens]).astype(np.int64)
+    b = CsrMatrix(sr, 400, n, bptr, bcols, exact_values(sr, rng, bcols.size))
+    rows = [np.sort(rng.choice(400, s, replace=False)) for s in (70, 100, 150, 3, 0, 200)]
+    aptr = np.concatenate([[0], np.cumsum([len(x) for x in rows])]).astype(np.int64)
+    acols = np.concatenate(rows).astype(np.int64)
+    a = CsrMatrix(sr, len(rows), 400, aptr, acols, exact_values(sr, rng, acols.size))
+    st = {}
+    got = esc_multiply(a, b, ctx=ctx, stats=st)
+    assert_same(got, ob.orc_multiply(to_mat(a), to_mat(b)), sr)
+    assert st["rows_per_bin"][5] + st["rows_per_bin"][7] >= 2, st["rows_per_bin"]
+
+
+@pytest.mark.parametrize("sr", [1, 2, 4])
+def test_merge_dense_panels_against_oracle(ctx, sr):
+    """Merging long partial rows over a wide block takes the dense panel path
+    with per-partial binary-searched panel bounds; checked against the oracle
+    product [I I I] . vstack(partials)."""
+    rng = np.random.default_rng(3)
+    from golden.make_golden import exact_values
+    nrows, ncols, K = 6, 200_000, 3
+    parts = []
+    for _ in range(K):
+        rs = [np.sort(rng.choice(ncols, int(rng.integers(2000, 5000)), replace=False)) for _ in range(nrows)]
+        ptr = np.concatenate([[0], np.cumsum([len(x) for x in rs])]).astype(np.int64)
+        idx = np.concatenate(rs).astype(np.int64)
+        parts.append(CsrMatrix(sr, nrows, ncols, ptr, idx, exact_values(sr, rng, idx.size)))
+    dparts = [DeviceCsr.upload(ctx, p) for p in parts]
+    st = {}
+    out = merge_partials(dparts, ncols, nrows, stats=st).download()  # CSC of C == CSR of C^T
+    one = {0: 1.0, 1: 0.0, 2: 1, 4: 0}[sr]
+    L = ob.Mat(sr, nrows, K * nrows, np.arange(0, K * nrows + 1, K),
+               np.array([q * nrows + i for i in range(nrows) for q in range(K)]), np.full(K * nrows, one))
+    R = ob.Mat(sr, K * nrows, ncols, np.concatenate([[0], np.cumsum(np.concatenate([np.diff(p.rowptr) for p in parts]))]),
+               np.concatenate([p.colids for p in parts]), np.concatenate([p.values for p in parts]))
+    want = ob.orc_multiply(L, R)
+    assert np.array_equal(out.colptr, want.ptr) and np.array_equal(out.rowids, want.idx)
+    assert out.values.tobytes() == want.vals.tobytes()
+    assert st["rows_per_bin"][6] == nrows
