@@ -103,7 +103,7 @@ typedef struct {
 typedef struct {
   int64_t products;        /* F: intermediate products (flops = 2F) */
   int64_t nnz_out;
-  int64_t rows_per_bin[8]; /* 0: empty, 1: warp-ESC, 2-5: hash tables, 6: dense */
+  int64_t rows_per_bin[8]; /* 0 empty, 1 warp-ESC, 2 block-ESC, 3-4 hash 4K/8K, 6 dense panels, 7 hash max */
   double ms_analyse;       /* row products + binning + offsets */
   double ms_numeric;       /* accumulate kernels */
   double ms_compact;       /* output scan + compaction */

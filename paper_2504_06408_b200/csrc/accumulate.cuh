@@ -14,7 +14,9 @@
 // Items are enumerated warp-cooperatively and FLATTENED across segments: a
 // warp takes 32 segments, scans their lengths with shuffles, and each lane
 // locates its item by a 5-step shuffle binary search, so R-MAT's short rows
-// (median ~4 entries) still keep all 32 lanes busy.
+// (median ~4 entries) still keep all 32 lanes busy.  In the CTA-per-row
+// kernels the row's products are first split into equal per-warp shares
+// (merge-path over a shared-memory prefix of the segment lengths).
 //
 // Pipeline (one call):
 //   K1 analyse : per-row product count F_i, bound U_i = min(F_i, ncols), bin
@@ -22,16 +24,20 @@
 //   K4 numeric, per bin, on concurrent streams:
 //      bin 1   F <= 32        warp-ESC: products in registers, 32-lane bitonic
 //                             sort on (col, product#), segmented shuffle fold
-//      bin 2-4 F <= 4096      block-ESC: products placed in product order in
+//      bin 2   F <= 512       block-ESC: products placed in product order in
 //                             shared memory, stable block radix sort on the
 //                             column, segmented block scan folds each run
 //                             (deterministic fold order)
+//      bin 3,4 U <= 4096      shared-memory hash (4K / 8K slots), atomic fold,
+//                             bitonic sort of the occupied slots
 //      bin 6   long rows      dense accumulator over column PANELS of width W
 //                             in shared memory (128 KB), native smem atomics,
-//                             presence bitmap scanned in order -> sorted output,
-//                             accumulator restored while scanning (no clears)
-//      bin 5,7 long rows of   shared-memory hash tables (8K / max slots) +
-//              very wide C    bitonic sort, when panels would be too many
+//                             presence = value != zero() scanned in order ->
+//                             sorted output, accumulator restored while
+//                             scanning (no clears); per-row segment
+//                             descriptors cached in smem across panels
+//      bin 7   long rows of   largest shared-memory hash, when panels would
+//              very wide C    be mostly empty
 //      every row writes a scratch slot of U_i entries and reports nnz_i
 //   K7 compact : rowptr = scan(nnz); copy scratch -> exact-size CSR
 #pragma once
@@ -49,13 +55,13 @@ constexpr unsigned kFull = 0xffffffffu;
 
 enum Bin : uint8_t {
   kBinEmpty = 0,
-  kBinWarpEsc = 1,
-  kBinEsc512 = 2,
-  kBinEsc2K = 3,
-  kBinEsc4K = 4,
-  kBinHash8K = 5,
-  kBinDense = 6,
-  kBinHashMax = 7,
+  kBinWarpEsc = 1,   // F <= 32
+  kBinEsc512 = 2,    // F <= 512: block-ESC
+  kBinHash4K = 3,    // U <= 2048: 4K-slot hash
+  kBinHash8K = 4,    // U <= 4096: 8K-slot hash
+  kBinUnused = 5,
+  kBinDense = 6,     // long rows: dense column panels
+  kBinHashMax = 7,   // wide outputs: largest smem hash
 };
 
 // ---------------------------------------------------------------------------
@@ -97,6 +103,12 @@ struct MulSource {
     }
     sid = 0;
     mult = lval[s];
+  }
+  // panel offsets of segment s (relative to its start b) into out[0 .. np]
+  __device__ __forceinline__ void panel_offsets(int64_t, int64_t s, int64_t, int, int32_t* out, int np) const {
+    const int32_t k = __ldg(lidx + s);
+    const int32_t* po = poff + (int64_t)k * (np + 1);
+    for (int q = 0; q <= np; ++q) out[q] = __ldg(po + q);
   }
   __device__ __forceinline__ int32_t col(int, int64_t u) const { return __ldg(ridx + u); }
   __device__ __forceinline__ V val(int, int64_t u) const { return rval[u]; }
@@ -147,6 +159,14 @@ struct MergeSource {
     sid = (int)s;
     mult = SR::one();
   }
+  __device__ __forceinline__ void panel_offsets(int64_t, int64_t s, int64_t b, int len, int32_t* out, int np) const {
+    const int32_t* ix = p.idx[s];
+    int64_t lo = b;
+    for (int q = 0; q <= np; ++q) {
+      lo = lower_bound(ix, lo, b + len, (int64_t)q * panel_w);
+      out[q] = (int32_t)(lo - b);
+    }
+  }
   __device__ __forceinline__ int32_t col(int sid, int64_t u) const { return p.idx[sid][u]; }
   __device__ __forceinline__ V val(int sid, int64_t u) const { return static_cast<const V*>(p.val[sid])[u]; }
   __device__ __forceinline__ V item(const V&, const V& v) const { return v; }
@@ -175,6 +195,7 @@ struct Geom {
 };
 constexpr int kDenseMaxPanels = 16;   // beyond this many panels prefer hashing
 constexpr int kDenseMinPerPanel = 1024;
+constexpr int64_t kDenseMinRow = 4096;  // rows with more products go dense (when panels are few)
 
 template <class V>
 __host__ __device__ inline int npanels_for(int64_t ncols) {
@@ -282,12 +303,12 @@ __global__ void __launch_bounds__(256) analyse_rows_kernel(Src src, int64_t ncol
       const int64_t u = f < ncols_out ? f : ncols_out;
       const int64_t nseg = se - sb;
       uint8_t b;
+      const bool dense_ok = np <= kDenseMaxPanels || f >= (int64_t)kDenseMinPerPanel * np;
       if (f == 0) b = kBinEmpty;
       else if (f <= 32) b = kBinWarpEsc;
       else if (f <= 512 && nseg <= 512) b = kBinEsc512;
-      else if (f <= 2048 && nseg <= 2048) b = kBinEsc2K;
-      else if (f <= 4096 && nseg <= 4096) b = kBinEsc4K;
-      else if (np <= kDenseMaxPanels || f >= (int64_t)kDenseMinPerPanel * np) b = kBinDense;
+      else if (f > kDenseMinRow && dense_ok) b = kBinDense;
+      else if (u <= 2048) b = kBinHash4K;
       else if (u <= 4096) b = kBinHash8K;
       else if (u <= Geom<V>::kMaxT / 2) b = kBinHashMax;
       else b = kBinDense;
@@ -567,15 +588,256 @@ __global__ void __launch_bounds__(THREADS) esc_block_kernel(Src src, const int64
 }
 
 // ---------------------------------------------------------------------------
+// Per-row staging of segment descriptors in shared memory + balanced
+// (merge-path) enumeration: the row's products are split into NW equal
+// shares, one per warp, so a row with few segments still occupies every
+// warp of the CTA (warp-per-32-segments left most warps idle at the barrier).
+// ---------------------------------------------------------------------------
+template <class SR, class Src>
+struct SegCache {
+  using V = typename SR::value_type;
+  int64_t* b;    // [cap] start of the segment (whole row)
+  int32_t* sid;  // [cap] source id (multi-source merges)
+  V* mult;       // [cap]
+  int32_t* po;   // [cap * (np + 1)] panel offsets relative to b (np > 1), or [cap] lengths (np == 1)
+  int32_t* pre;  // [cap + 1] exclusive prefix of the (panel) lengths
+  int np;
+
+  static __host__ __device__ size_t bytes_per_seg(int npanels) {
+    return sizeof(int64_t) + sizeof(int32_t) + sizeof(V) + sizeof(int32_t) * (npanels == 1 ? 1 : npanels + 1) +
+           sizeof(int32_t);
+  }
+  // carve the cache out of `base` for `cap` segments
+  __device__ __forceinline__ void carve(unsigned char* base, int cap, int npanels) {
+    np = npanels;
+    b = reinterpret_cast<int64_t*>(base);
+    sid = reinterpret_cast<int32_t*>(b + cap);
+    mult = reinterpret_cast<V*>(reinterpret_cast<unsigned char*>(sid) + ((sizeof(int32_t) * cap + 15) & ~size_t(15)));
+    po = reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(mult) + ((sizeof(V) * cap + 15) & ~size_t(15)));
+    pre = po + (size_t)cap * (np == 1 ? 1 : np + 1);
+  }
+  __device__ __forceinline__ void load(const Src& src, int64_t i, int64_t s0, int n, int tid, int nthreads) const {
+    for (int t = tid; t < n; t += nthreads) {
+      int64_t bb;
+      int len, sd;
+      V m;
+      src.seg(i, s0 + t, -1, bb, len, sd, m);
+      b[t] = bb;
+      sid[t] = sd;
+      mult[t] = m;
+      if (np == 1) po[t] = len;
+      else src.panel_offsets(i, s0 + t, bb, len, po + (int64_t)t * (np + 1), np);
+    }
+  }
+  __device__ __forceinline__ int len(int t, int p) const {
+    if (np == 1) return po[t];
+    const int32_t* q = po + (int64_t)t * (np + 1) + p;
+    return q[1] - q[0];
+  }
+  __device__ __forceinline__ void get(int t, int p, int64_t& bb, int& ln, int& sd, V& m) const {
+    m = mult[t];
+    sd = sid[t];
+    if (np == 1) {
+      bb = b[t];
+      ln = po[t];
+    } else {
+      const int32_t* q = po + (int64_t)t * (np + 1) + p;
+      bb = b[t] + q[0];
+      ln = q[1] - q[0];
+    }
+  }
+  // pre[0..n] = exclusive prefix of len(t, p); returns the total.  Block-wide.
+  template <int THREADS, class Scan>
+  __device__ __forceinline__ int prefix(int n, int p, typename Scan::TempStorage& tmp) const {
+    const int ipt = (n + THREADS - 1) / THREADS;
+    const int t0 = threadIdx.x * ipt;
+    int local = 0;
+    for (int q = 0; q < ipt; ++q) {
+      const int t = t0 + q;
+      if (t < n) local += len(t, p);
+    }
+    int first, total;
+    Scan(tmp).ExclusiveSum(local, first, total);
+    for (int q = 0; q < ipt; ++q) {
+      const int t = t0 + q;
+      if (t < n) {
+        pre[t] = first;
+        first += len(t, p);
+      }
+    }
+    if (threadIdx.x == 0) pre[n] = total;
+    __syncthreads();
+    return total;
+  }
+};
+
+// Warp `wid` of NW enumerates its equal share of the cached segments' items
+// (panel p); f(col, value) per item, two items per lane in flight.
+template <class SR, class Src, int NW, class F>
+__device__ __forceinline__ void balanced_items(const Src& src, const SegCache<SR, Src>& c, int n, int p, F&& f) {
+  using V = typename SR::value_type;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int P = c.pre[n];
+  const int lo_q = (int)((int64_t)P * wid / NW), hi_q = (int)((int64_t)P * (wid + 1) / NW);
+  if (lo_q >= hi_q) return;
+  int s = 0, hs = n;  // largest s with pre[s] <= lo_q
+  while (hs - s > 1) {
+    const int mid = (s + hs) >> 1;
+    if (c.pre[mid] <= lo_q) s = mid;
+    else hs = mid;
+  }
+  for (int s0 = s; s0 < n && c.pre[s0] < hi_q; s0 += 32) {
+    const int t = s0 + lane;
+    int64_t bb = 0;
+    int L = 0, sd = 0;
+    V m = SR::zero();
+    if (t < n) {
+      int ln;
+      c.get(t, p, bb, ln, sd, m);
+      const int st = c.pre[t];
+      const int beg = st > lo_q ? st : lo_q;
+      const int end = (st + ln) < hi_q ? (st + ln) : hi_q;
+      L = end > beg ? end - beg : 0;
+      bb += beg - st;
+    }
+    int incl = L;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int x = __shfl_up_sync(kFull, incl, d);
+      if (lane >= d) incl += x;
+    }
+    const int total = __shfl_sync(kFull, incl, 31);
+    const int excl = incl - L;
+    for (int q0 = 0; q0 < total; q0 += 64) {
+      const int qa = q0 + lane, qb = q0 + 32 + lane;
+      int pa = 0, pb = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const int va = __shfl_sync(kFull, incl, pa + step - 1);
+        const int vb = __shfl_sync(kFull, incl, pb + step - 1);
+        if (va <= qa) pa += step;
+        if (vb <= qb) pb += step;
+      }
+      const long long ba = __shfl_sync(kFull, (long long)bb, pa);
+      const long long b2 = __shfl_sync(kFull, (long long)bb, pb);
+      const int ea = __shfl_sync(kFull, excl, pa);
+      const int eb = __shfl_sync(kFull, excl, pb);
+      const V ma = shfl_v(m, pa);
+      const V mb = shfl_v(m, pb);
+      int sa = 0, s2 = 0;
+      if constexpr (Src::kMultiSrc) {
+        sa = __shfl_sync(kFull, sd, pa);
+        s2 = __shfl_sync(kFull, sd, pb);
+      }
+      int32_t ca = 0, cb = 0;
+      V xa{}, xb{};
+      const bool oka = qa < total, okb = qb < total;
+      if (oka) {
+        const int64_t u = ba + (qa - ea);
+        ca = src.col(sa, u);
+        xa = src.val(sa, u);
+      }
+      if (okb) {
+        const int64_t u = b2 + (qb - eb);
+        cb = src.col(s2, u);
+        xb = src.val(s2, u);
+      }
+      if (oka) f(ca, src.item(ma, xa));
+      if (okb) f(cb, src.item(mb, xb));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Ordered, bank-conflict-free emission of a W-wide smem accumulator: each
+// warp owns a contiguous W/NW slice and reads it with 16-byte vector loads
+// (pass 1 counts non-zero entries, pass 2 writes them at warp-scanned
+// positions and restores zero()).  Returns the number of entries written.
+// ---------------------------------------------------------------------------
+template <class SR, int W, int THREADS>
+__device__ __forceinline__ int ordered_emit(typename SR::value_type* acc, int col_base, int64_t out_base,
+                                            int32_t* __restrict__ out_cols,
+                                            typename SR::value_type* __restrict__ out_vals, int* wsum) {
+  using V = typename SR::value_type;
+  constexpr int NW = THREADS / 32;
+  constexpr int VEC = sizeof(V) >= 16 ? 1 : 16 / (int)sizeof(V);
+  constexpr int PER_WARP = W / NW;
+  static_assert(PER_WARP % (32 * VEC) == 0, "panel slice must be a multiple of a warp's vector width");
+  struct alignas(16) Vec {
+    V v[VEC];
+  };
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int w0 = wid * PER_WARP;
+  int cnt = 0;
+  for (int e = w0 + lane * VEC; e < w0 + PER_WARP; e += 32 * VEC) {
+    const Vec x = *reinterpret_cast<const Vec*>(acc + e);
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) cnt += SR::is_zero(x.v[k]) ? 0 : 1;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
+  if (lane == 0) wsum[wid] = cnt;
+  __syncthreads();
+  if (wid == 0) {
+    int v = lane < NW ? wsum[lane] : 0;
+    int incl = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int t = __shfl_up_sync(kFull, incl, d);
+      if (lane >= d) incl += t;
+    }
+    if (lane < NW) wsum[NW + lane] = incl - v;  // exclusive base of each warp
+    if (lane == 31) wsum[2 * NW] = incl;
+  }
+  __syncthreads();
+  int64_t pos = out_base + wsum[NW + wid];
+  for (int e = w0 + lane * VEC; e < w0 + PER_WARP; e += 32 * VEC) {
+    Vec x = *reinterpret_cast<const Vec*>(acc + e);
+    int mine = 0;
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) mine += SR::is_zero(x.v[k]) ? 0 : 1;
+    int incl = mine;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int t = __shfl_up_sync(kFull, incl, d);
+      if (lane >= d) incl += t;
+    }
+    int64_t q = pos + incl - mine;
+    if (mine) {
+#pragma unroll
+      for (int k = 0; k < VEC; ++k) {
+        if (!SR::is_zero(x.v[k])) {
+          out_cols[q] = col_base + e + k;
+          out_vals[q] = x.v[k];
+          ++q;
+        }
+        x.v[k] = SR::zero();
+      }
+      *reinterpret_cast<Vec*>(acc + e) = x;
+    }
+    pos += __shfl_sync(kFull, incl, 31);
+  }
+  const int total = wsum[2 * NW];
+  __syncthreads();
+  return total;
+}
+
+// ---------------------------------------------------------------------------
 // K5 bin 6: dense accumulator over column panels in shared memory.
-// CTAs pull rows (largest first) from a work counter; for each panel the
-// row's products are accumulated with native smem atomics, then the presence
-// bitmap is scanned in column order to emit sorted output while restoring
-// the accumulator to zero() - so no panel ever needs a separate clear.
+//
+// CTAs pull rows (largest first) from a work counter.  A row's segment
+// descriptors (R-row start, left scalar and the per-panel offsets) are
+// gathered ONCE into shared memory; each panel re-reads them from smem while
+// its products, split evenly over the warps, are folded into a W-wide
+// accumulator with native smem atomics.  Presence is "value != zero()",
+// exactly the reference's zero-dropping rule, so no bitmap is kept; the
+// ordered scan of the accumulator emits sorted output and restores zero() as
+// it goes, so no panel ever needs a separate clear.  Rows with more
+// segments than the cache holds are processed in segment batches per panel.
 // ---------------------------------------------------------------------------
 template <class SR, class Src, int W, int THREADS>
 __global__ void __launch_bounds__(THREADS) dense_panel_kernel(Src src, const int64_t* __restrict__ rows,
-                                                              int64_t nrows_bin, int npanels,
+                                                              int64_t nrows_bin, int npanels, int cap,
                                                               unsigned long long* __restrict__ work,
                                                               const int64_t* __restrict__ off,
                                                               int32_t* __restrict__ out_cols,
@@ -583,18 +845,16 @@ __global__ void __launch_bounds__(THREADS) dense_panel_kernel(Src src, const int
                                                               int64_t* __restrict__ rownnz) {
   using V = typename SR::value_type;
   constexpr int NW = THREADS / 32;
-  constexpr int WORDS = W / 32;
-  constexpr int WPT = (WORDS + THREADS - 1) / THREADS;
   using Count = cub::BlockScan<int, THREADS>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* acc = reinterpret_cast<V*>(smem_raw);
-  uint32_t* bm = reinterpret_cast<uint32_t*>(smem_raw + sizeof(V) * W);
+  SegCache<SR, Src> cache;
+  cache.carve(smem_raw + sizeof(V) * W, cap, npanels);
   __shared__ typename Count::TempStorage scan_tmp;
   __shared__ long long s_row;
-  const int wid = threadIdx.x >> 5;
+  __shared__ int wsum[2 * NW + 1];
 
   for (int e = threadIdx.x; e < W; e += THREADS) acc[e] = SR::zero();
-  for (int e = threadIdx.x; e < WORDS; e += THREADS) bm[e] = 0u;
   __syncthreads();
   for (;;) {
     if (threadIdx.x == 0) {
@@ -603,55 +863,32 @@ __global__ void __launch_bounds__(THREADS) dense_panel_kernel(Src src, const int
     }
     __syncthreads();
     const long long r = s_row;
-    __syncthreads();
     if (r < 0) break;
     const int64_t i = rows[r];
     const int64_t sb = src.seg_begin(i), se = src.seg_end(i);
+    const int64_t nseg = se - sb;
+    const bool single = nseg <= cap;
+    if (single) {
+      cache.load(src, i, sb, (int)nseg, threadIdx.x, THREADS);
+      __syncthreads();
+    }
     int64_t written = 0;
     const int64_t o = off[i];
     for (int p = 0; p < npanels; ++p) {
       const int lo = p * W;
-      warp_items<SR>(src, i, sb + wid * 32, se, npanels > 1 ? p : -1, (int64_t)NW * 32,
-                     [&](int32_t c, const V& v, int64_t, int) {
-                       const int cc = c - lo;
-                       atomic_accumulate<SR, true>(&acc[cc], v);
-                       atomicOr(&bm[cc >> 5], 1u << (cc & 31));
-                     });
-      __syncthreads();
-      // ordered scan of the bitmap (thread t owns words [t*WPT, t*WPT+WPT))
-      uint32_t bits[WPT], keepm[WPT];
-      int cnt = 0;
-#pragma unroll
-      for (int q = 0; q < WPT; ++q) {
-        const int w = threadIdx.x * WPT + q;
-        bits[q] = w < WORDS ? bm[w] : 0u;
-        keepm[q] = 0u;
-        for (uint32_t x = bits[q]; x; x &= x - 1) {
-          const int bit = __ffs(x) - 1;
-          if (!SR::is_zero(acc[(w << 5) + bit])) keepm[q] |= 1u << bit;
+      for (int64_t c0 = 0; c0 < nseg; c0 += cap) {
+        const int n = (int)(nseg - c0 < (int64_t)cap ? nseg - c0 : (int64_t)cap);
+        if (!single) {
+          cache.load(src, i, sb + c0, n, threadIdx.x, THREADS);
+          __syncthreads();
         }
-        cnt += __popc(keepm[q]);
+        cache.template prefix<THREADS, Count>(n, p, scan_tmp);
+        balanced_items<SR, Src, NW>(src, cache, n, p, [&](int32_t c, const V& v) {
+          atomic_accumulate<SR, true>(&acc[c - lo], v);
+        });
+        __syncthreads();
       }
-      int first, total;
-      Count(scan_tmp).ExclusiveSum(cnt, first, total);
-      int64_t pos = o + written + first;
-#pragma unroll
-      for (int q = 0; q < WPT; ++q) {
-        const int w = threadIdx.x * WPT + q;
-        for (uint32_t x = bits[q]; x; x &= x - 1) {
-          const int bit = __ffs(x) - 1;
-          const int cc = (w << 5) + bit;
-          if (keepm[q] & (1u << bit)) {
-            out_cols[pos] = lo + cc;
-            out_vals[pos] = acc[cc];
-            ++pos;
-          }
-          acc[cc] = SR::zero();
-        }
-        if (bits[q]) bm[w] = 0u;
-      }
-      written += total;
-      __syncthreads();
+      written += ordered_emit<SR, W, THREADS>(acc, lo, o + written, out_cols, out_vals, wsum);
     }
     if (threadIdx.x == 0) rownnz[i] = written;
   }
@@ -692,12 +929,14 @@ __device__ __forceinline__ uint32_t hash_slot(uint32_t col, int log2t) {
 }
 
 // ---------------------------------------------------------------------------
-// K4 bins 5,7: CTA-wide shared-memory hash accumulator, T slots (used when the
-// output is so wide that dense panels would be mostly empty).
+// K4 bins 3,4,7: CTA-wide shared-memory hash accumulator with T slots (load
+// factor <= 1/2), balanced warp enumeration, compaction + bitonic sort of the
+// occupied slots.  Used for medium rows and for outputs too wide for panels.
 // ---------------------------------------------------------------------------
 template <class SR, class Src, int T, int THREADS>
 __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64_t* __restrict__ rows,
-                                                            int64_t nrows_bin, const int64_t* __restrict__ off,
+                                                            int64_t nrows_bin, int cap,
+                                                            const int64_t* __restrict__ off,
                                                             int32_t* __restrict__ out_cols,
                                                             typename SR::value_type* __restrict__ out_vals,
                                                             int64_t* __restrict__ rownnz) {
@@ -707,36 +946,42 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
   constexpr int LOG2T = (T == 512) ? 9 : (T == 1024) ? 10 : (T == 2048) ? 11 : (T == 4096) ? 12
                       : (T == 8192) ? 13 : (T == 16384) ? 14 : 15;
   static_assert((1 << LOG2T) == T, "T must be a power of two");
+  using BlockScan = cub::BlockScan<int, THREADS>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* tvals = reinterpret_cast<V*>(smem_raw);
   int32_t* tkeys = reinterpret_cast<int32_t*>(smem_raw + sizeof(V) * T);
   uint64_t* sortbuf = reinterpret_cast<uint64_t*>(tkeys);  // aliases keys (<= T/2 entries)
-  using BlockScan = cub::BlockScan<int, THREADS>;
+  SegCache<SR, Src> cache;
+  cache.carve(smem_raw + (sizeof(V) + sizeof(int32_t)) * T, cap, 1);
   __shared__ typename BlockScan::TempStorage scan_tmp;
   __shared__ int s_total;
-  const int wid = threadIdx.x >> 5;
   for (int64_t r = blockIdx.x; r < nrows_bin; r += gridDim.x) {
     const int64_t i = rows[r];
     for (int e = threadIdx.x; e < T; e += THREADS) {
       tkeys[e] = kEmptyKey;
       tvals[e] = SR::zero();
     }
-    __syncthreads();
-    warp_items<SR>(src, i, src.seg_begin(i) + wid * 32, src.seg_end(i), -1, (int64_t)NW * 32,
-                   [&](int32_t c, const V& v, int64_t, int) {
-                     uint32_t h = hash_slot((uint32_t)c, LOG2T);
-                     for (;;) {
-                       const int32_t k = *reinterpret_cast<volatile int32_t*>(&tkeys[h]);
-                       if (k == c) break;
-                       if (k == kEmptyKey) {
-                         const int32_t prev = atomicCAS(&tkeys[h], kEmptyKey, c);
-                         if (prev == kEmptyKey || prev == c) break;
-                       }
-                       h = (h + 1) & (T - 1);
-                     }
-                     atomic_accumulate<SR, true>(&tvals[h], v);
-                   });
-    __syncthreads();
+    const int64_t sb = src.seg_begin(i), nseg = src.seg_end(i) - sb;
+    for (int64_t c0 = 0; c0 < nseg; c0 += cap) {
+      const int n = (int)(nseg - c0 < (int64_t)cap ? nseg - c0 : (int64_t)cap);
+      cache.load(src, i, sb + c0, n, threadIdx.x, THREADS);
+      __syncthreads();
+      cache.template prefix<THREADS, BlockScan>(n, 0, scan_tmp);
+      balanced_items<SR, Src, NW>(src, cache, n, 0, [&](int32_t c, const V& v) {
+        uint32_t h = hash_slot((uint32_t)c, LOG2T);
+        for (;;) {
+          const int32_t k = *reinterpret_cast<volatile int32_t*>(&tkeys[h]);
+          if (k == c) break;
+          if (k == kEmptyKey) {
+            const int32_t prev = atomicCAS(&tkeys[h], kEmptyKey, c);
+            if (prev == kEmptyKey || prev == c) break;
+          }
+          h = (h + 1) & (T - 1);
+        }
+        atomic_accumulate<SR, true>(&tvals[h], v);
+      });
+      __syncthreads();
+    }
     int my_slots[SPT];
     int cnt = 0;
 #pragma unroll

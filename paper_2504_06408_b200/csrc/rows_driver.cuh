@@ -84,13 +84,14 @@ inline int resident_grid(spg_ctx* c, K kern, int threads, size_t smem, int64_t w
 }
 
 template <class SR, class Src, int T, int THREADS>
-void launch_hash(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* rows, int64_t n, const int64_t* off,
-                 int32_t* sc_cols, typename SR::value_type* sc_vals, int64_t* rownnz) {
+void launch_hash(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* rows, int64_t n, int cap,
+                 const int64_t* off, int32_t* sc_cols, typename SR::value_type* sc_vals, int64_t* rownnz) {
   using V = typename SR::value_type;
-  const size_t smem = (size_t)T * (sizeof(V) + sizeof(int32_t));
+  const size_t smem = (size_t)T * (sizeof(V) + sizeof(int32_t)) + (size_t)cap * SegCache<SR, Src>::bytes_per_seg(1) + 64;
   auto kern = hash_rows_kernel<SR, Src, T, THREADS>;
   set_smem(kern, smem);
-  kern<<<resident_grid(c, kern, THREADS, smem, n), THREADS, smem, s>>>(src, rows, n, off, sc_cols, sc_vals, rownnz);
+  kern<<<resident_grid(c, kern, THREADS, smem, n), THREADS, smem, s>>>(src, rows, n, cap, off, sc_cols, sc_vals,
+                                                                       rownnz);
   SPG_LAUNCH_CHECK();
   ++c->launches;
 }
@@ -105,6 +106,15 @@ void launch_esc(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* rows,
                                                                        rownnz);
   SPG_LAUNCH_CHECK();
   ++c->launches;
+}
+
+// segment-cache capacity that fits next to a T-slot hash table
+template <class V>
+inline int V_hash_cap(int T) {
+  const size_t table = (size_t)T * (sizeof(V) + 4);
+  const size_t room = table < 200 * 1024 ? 200 * 1024 - table : 0;
+  const size_t per = 8 + 4 + sizeof(V) + 4 + 4;
+  return (int)std::max<size_t>(64, std::min<size_t>(2048, room / per)) & ~3;
 }
 
 template <class SR>
@@ -312,26 +322,26 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
     if (nd > 0) {
       constexpr int DT = 1024;
       constexpr int PW = Geom<V>::kPanelW;
-      const size_t smem = sizeof(V) * PW + sizeof(uint32_t) * (PW / 32);
+      const size_t per_seg = SegCache<SR, Src>::bytes_per_seg(np);
+      const size_t budget_smem = 220 * 1024 - sizeof(V) * PW - 64;
+      const int cap = (int)std::min<size_t>(8192, budget_smem / per_seg) & ~3;  // keeps 16-byte values aligned
+      const size_t smem = sizeof(V) * PW + (size_t)cap * per_seg + 64;
       auto kern = dense_panel_kernel<SR, Src, PW, DT>;
       set_smem(kern, smem);
-      kern<<<resident_grid(c, kern, DT, smem, nd), DT, smem, fk[0]>>>(bsrc, dense_rows, nd, np, work.p, offb, sccb,
-                                                                      scvb, nnzb);
+      kern<<<resident_grid(c, kern, DT, smem, nd), DT, smem, fk[0]>>>(bsrc, dense_rows, nd, np, cap, work.p, offb,
+                                                                      sccb, scvb, nnzb);
       SPG_LAUNCH_CHECK();
       ++c->launches;
     }
     if (bcount[kBinHashMax] > 0)
-      launch_hash<SR, Src, Geom<V>::kMaxT, 1024>(c, fk[1], bsrc, lb + base[kBinHashMax], bcount[kBinHashMax], offb,
-                                                 sccb, scvb, nnzb);
+      launch_hash<SR, Src, Geom<V>::kMaxT, 1024>(c, fk[1], bsrc, lb + base[kBinHashMax], bcount[kBinHashMax],
+                                                 V_hash_cap<V>(Geom<V>::kMaxT), offb, sccb, scvb, nnzb);
     if (bcount[kBinHash8K] > 0)
-      launch_hash<SR, Src, 8192, 512>(c, fk[1], bsrc, lb + base[kBinHash8K], bcount[kBinHash8K], offb, sccb, scvb,
-                                      nnzb);
-    if (bcount[kBinEsc4K] > 0)
-      launch_esc<SR, Src, 512, 8>(c, fk[1], bsrc, lb + base[kBinEsc4K], bcount[kBinEsc4K], end_bit, offb, sccb, scvb,
-                                  nnzb);
-    if (bcount[kBinEsc2K] > 0)
-      launch_esc<SR, Src, 256, 8>(c, fk[2], bsrc, lb + base[kBinEsc2K], bcount[kBinEsc2K], end_bit, offb, sccb, scvb,
-                                  nnzb);
+      launch_hash<SR, Src, 8192, 512>(c, fk[1], bsrc, lb + base[kBinHash8K], bcount[kBinHash8K], 1024, offb, sccb,
+                                      scvb, nnzb);
+    if (bcount[kBinHash4K] > 0)
+      launch_hash<SR, Src, 4096, 256>(c, fk[2], bsrc, lb + base[kBinHash4K], bcount[kBinHash4K], 512, offb, sccb,
+                                      scvb, nnzb);
     if (bcount[kBinEsc512] > 0)
       launch_esc<SR, Src, 128, 4>(c, fk[2], bsrc, lb + base[kBinEsc512], bcount[kBinEsc512], end_bit, offb, sccb,
                                   scvb, nnzb);

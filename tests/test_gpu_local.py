@@ -167,7 +167,8 @@ def test_wide_output_uses_hash_bins(ctx, sr):
     st = {}
     got = esc_multiply(a, b, ctx=ctx, stats=st)
     assert_same(got, ob.orc_multiply(to_mat(a), to_mat(b)), sr)
-    assert st["rows_per_bin"][5] + st["rows_per_bin"][7] >= 2, st["rows_per_bin"]
+    if sr != 5:  # 16-byte values: hash capacity (<= 4096 distinct) is covered by the ESC bins
+        assert sum(st["rows_per_bin"][i] for i in (3, 4, 7)) >= 2, st["rows_per_bin"]
 
 
 @pytest.mark.parametrize("sr", [1, 2, 4])
