@@ -198,8 +198,8 @@ constexpr int kDenseMinPerPanel = 1024;
 constexpr int64_t kDenseMinRow = 4096;  // rows with more products go dense (when panels are few)
 
 template <class V>
-__host__ __device__ inline int npanels_for(int64_t ncols) {
-  return (int)((ncols + Geom<V>::kPanelW - 1) / Geom<V>::kPanelW);
+__host__ __device__ inline int npanels_for(int64_t ncols, int w = Geom<V>::kPanelW) {
+  return (int)((ncols + w - 1) / w);
 }
 
 // ---------------------------------------------------------------------------
@@ -749,73 +749,107 @@ __device__ __forceinline__ void balanced_items(const Src& src, const SegCache<SR
 }
 
 // ---------------------------------------------------------------------------
-// Ordered, bank-conflict-free emission of a W-wide smem accumulator: each
-// warp owns a contiguous W/NW slice and reads it with 16-byte vector loads
-// (pass 1 counts non-zero entries, pass 2 writes them at warp-scanned
-// positions and restores zero()).  Returns the number of entries written.
+// Ordered emission of a W-wide smem accumulator driven by its first-touch
+// bitmap (one bit per column, W/32 words; warp w owns a contiguous slice of
+// W/32/NW words).  Output entries are FLATTENED across lanes: a warp scans the
+// popcounts of 32 words, then each lane takes one output entry per step,
+// finds its word with a 5-step shuffle search and its bit with __fns, so the
+// stores are coalesced and no lane idles on a sparse word.  Positions:
+// block scan over the warps' counts.  Restores zero() and clears the bitmap.
+// Only items != zero() ever set a bit, so the bitmap count is exact unless
+// the fold can cancel back to zero() (fp64 +), which a pre-pass handles.
+// Returns the number of entries written.
 // ---------------------------------------------------------------------------
+template <class SR>
+struct AddCanCancel {
+  static constexpr bool value = SR::id == 0;  // arithmetic (+, x): a + (-a) == 0
+};
+
 template <class SR, int W, int THREADS>
-__device__ __forceinline__ int ordered_emit(typename SR::value_type* acc, int col_base, int64_t out_base,
-                                            int32_t* __restrict__ out_cols,
-                                            typename SR::value_type* __restrict__ out_vals, int* wsum) {
+__device__ __forceinline__ int bitmap_emit(typename SR::value_type* acc, uint32_t* bm, int col_base, int64_t out_base,
+                                           int32_t* __restrict__ out_cols,
+                                           typename SR::value_type* __restrict__ out_vals, int* wsum) {
   using V = typename SR::value_type;
   constexpr int NW = THREADS / 32;
-  constexpr int VEC = sizeof(V) >= 16 ? 1 : 16 / (int)sizeof(V);
-  constexpr int PER_WARP = W / NW;
-  static_assert(PER_WARP % (32 * VEC) == 0, "panel slice must be a multiple of a warp's vector width");
-  struct alignas(16) Vec {
-    V v[VEC];
-  };
+  constexpr int WORDS = W / 32;
+  constexpr int WPW = WORDS / NW;  // words per warp
+  constexpr int ITERS = (WPW + 31) / 32;
+  static_assert(WORDS % NW == 0 && (WPW < 32 || WPW % 32 == 0), "bitmap words must split evenly over the warps");
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int w0 = wid * PER_WARP;
+  const int w0 = wid * WPW;
+  if constexpr (AddCanCancel<SR>::value) {
+    // drop touched entries whose fold cancelled to zero (restoring exact zero() bits)
+    for (int it = 0; it < ITERS; ++it) {
+      const int wl = it * 32 + lane;
+      if (wl >= WPW) break;
+      const int w = w0 + wl;
+      uint32_t x = bm[w];
+      for (uint32_t y = x; y; y &= y - 1) {
+        const int bit = __ffs(y) - 1;
+        if (SR::is_zero(acc[(w << 5) + bit])) {
+          acc[(w << 5) + bit] = SR::zero();
+          x &= ~(1u << bit);
+        }
+      }
+      bm[w] = x;
+    }
+  }
   int cnt = 0;
-  for (int e = w0 + lane * VEC; e < w0 + PER_WARP; e += 32 * VEC) {
-    const Vec x = *reinterpret_cast<const Vec*>(acc + e);
-#pragma unroll
-    for (int k = 0; k < VEC; ++k) cnt += SR::is_zero(x.v[k]) ? 0 : 1;
+  for (int it = 0; it < ITERS; ++it) {
+    const int wl = it * 32 + lane;
+    cnt += wl < WPW ? __popc(bm[w0 + wl]) : 0;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
   if (lane == 0) wsum[wid] = cnt;
   __syncthreads();
   if (wid == 0) {
-    int v = lane < NW ? wsum[lane] : 0;
+    const int v = lane < NW ? wsum[lane] : 0;
     int incl = v;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const int t = __shfl_up_sync(kFull, incl, d);
       if (lane >= d) incl += t;
     }
-    if (lane < NW) wsum[NW + lane] = incl - v;  // exclusive base of each warp
+    if (lane < NW) wsum[NW + lane] = incl - v;
     if (lane == 31) wsum[2 * NW] = incl;
   }
   __syncthreads();
   int64_t pos = out_base + wsum[NW + wid];
-  for (int e = w0 + lane * VEC; e < w0 + PER_WARP; e += 32 * VEC) {
-    Vec x = *reinterpret_cast<const Vec*>(acc + e);
-    int mine = 0;
-#pragma unroll
-    for (int k = 0; k < VEC; ++k) mine += SR::is_zero(x.v[k]) ? 0 : 1;
-    int incl = mine;
+  for (int it = 0; it < ITERS; ++it) {
+    const int wl = it * 32 + lane;
+    const int w = w0 + wl;
+    const uint32_t x = wl < WPW ? bm[w] : 0u;
+    const int c = __popc(x);
+    int incl = c;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const int t = __shfl_up_sync(kFull, incl, d);
       if (lane >= d) incl += t;
     }
-    int64_t q = pos + incl - mine;
-    if (mine) {
+    const int total = __shfl_sync(kFull, incl, 31);
+    const int excl = incl - c;
+    for (int q0 = 0; q0 < total; q0 += 32) {
+      const int q = q0 + lane;
+      int own = 0;
 #pragma unroll
-      for (int k = 0; k < VEC; ++k) {
-        if (!SR::is_zero(x.v[k])) {
-          out_cols[q] = col_base + e + k;
-          out_vals[q] = x.v[k];
-          ++q;
-        }
-        x.v[k] = SR::zero();
+      for (int step = 16; step >= 1; step >>= 1) {
+        const int v = __shfl_sync(kFull, incl, own + step - 1);
+        if (v <= q) own += step;
       }
-      *reinterpret_cast<Vec*>(acc + e) = x;
+      const uint32_t xo = __shfl_sync(kFull, x, own);
+      const int eo = __shfl_sync(kFull, excl, own);
+      if (q < total) {
+        const int bit = (int)__fns(xo, 0, q - eo + 1);
+        const int cc = ((w0 + it * 32 + own) << 5) + bit;
+        const V v = acc[cc];
+        out_cols[pos + q] = col_base + cc;
+        out_vals[pos + q] = v;
+        acc[cc] = SR::zero();
+      }
     }
-    pos += __shfl_sync(kFull, incl, 31);
+    if (x) bm[w] = 0u;
+    pos += total;
   }
   const int total = wsum[2 * NW];
   __syncthreads();
@@ -848,13 +882,15 @@ __global__ void __launch_bounds__(THREADS) dense_panel_kernel(Src src, const int
   using Count = cub::BlockScan<int, THREADS>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* acc = reinterpret_cast<V*>(smem_raw);
+  uint32_t* bm = reinterpret_cast<uint32_t*>(smem_raw + sizeof(V) * W);
   SegCache<SR, Src> cache;
-  cache.carve(smem_raw + sizeof(V) * W, cap, npanels);
+  cache.carve(smem_raw + sizeof(V) * W + sizeof(uint32_t) * (W / 32), cap, npanels);
   __shared__ typename Count::TempStorage scan_tmp;
   __shared__ long long s_row;
   __shared__ int wsum[2 * NW + 1];
 
   for (int e = threadIdx.x; e < W; e += THREADS) acc[e] = SR::zero();
+  for (int e = threadIdx.x; e < W / 32; e += THREADS) bm[e] = 0u;
   __syncthreads();
   for (;;) {
     if (threadIdx.x == 0) {
@@ -884,11 +920,14 @@ __global__ void __launch_bounds__(THREADS) dense_panel_kernel(Src src, const int
         }
         cache.template prefix<THREADS, Count>(n, p, scan_tmp);
         balanced_items<SR, Src, NW>(src, cache, n, p, [&](int32_t c, const V& v) {
-          atomic_accumulate<SR, true>(&acc[c - lo], v);
+          if (SR::is_zero(v)) return;  // add(x, zero) == x: nothing to fold
+          const int cc = c - lo;
+          const V old = atomic_accumulate<SR, true>(&acc[cc], v);
+          if (is_zero_bits<SR>(old)) atomicOr(&bm[cc >> 5], 1u << (cc & 31));  // first touch
         });
         __syncthreads();
       }
-      written += ordered_emit<SR, W, THREADS>(acc, lo, o + written, out_cols, out_vals, wsum);
+      written += bitmap_emit<SR, W, THREADS>(acc, bm, lo, o + written, out_cols, out_vals, wsum);
     }
     if (threadIdx.x == 0) rownnz[i] = written;
   }
@@ -933,28 +972,40 @@ __device__ __forceinline__ uint32_t hash_slot(uint32_t col, int log2t) {
 // factor <= 1/2), balanced warp enumeration, compaction + bitonic sort of the
 // occupied slots.  Used for medium rows and for outputs too wide for panels.
 // ---------------------------------------------------------------------------
+template <int T, int THREADS>
+struct HashSort {
+  static constexpr int ITEMS = T / 2 / THREADS;  // occupied slots <= T/2 (load factor 1/2)
+  using Sort = cub::BlockRadixSort<uint32_t, THREADS, ITEMS, uint16_t, 6>;
+  using Scan = cub::BlockScan<int, THREADS>;
+  union Tmp {
+    typename Sort::TempStorage sort;
+    typename Scan::TempStorage scan;
+  };
+};
+
 template <class SR, class Src, int T, int THREADS>
 __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64_t* __restrict__ rows,
-                                                            int64_t nrows_bin, int cap,
+                                                            int64_t nrows_bin, int cap, int end_bit,
                                                             const int64_t* __restrict__ off,
                                                             int32_t* __restrict__ out_cols,
                                                             typename SR::value_type* __restrict__ out_vals,
                                                             int64_t* __restrict__ rownnz) {
   using V = typename SR::value_type;
+  using HS = HashSort<T, THREADS>;
   constexpr int SPT = T / THREADS;
+  constexpr int ITEMS = HS::ITEMS;
   constexpr int NW = THREADS / 32;
   constexpr int LOG2T = (T == 512) ? 9 : (T == 1024) ? 10 : (T == 2048) ? 11 : (T == 4096) ? 12
                       : (T == 8192) ? 13 : (T == 16384) ? 14 : 15;
   static_assert((1 << LOG2T) == T, "T must be a power of two");
-  using BlockScan = cub::BlockScan<int, THREADS>;
+  static_assert(T <= 65536 * 2, "slot ids must fit 16 bits");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* tvals = reinterpret_cast<V*>(smem_raw);
   int32_t* tkeys = reinterpret_cast<int32_t*>(smem_raw + sizeof(V) * T);
-  uint64_t* sortbuf = reinterpret_cast<uint64_t*>(tkeys);  // aliases keys (<= T/2 entries)
+  typename HS::Tmp* tmp = reinterpret_cast<typename HS::Tmp*>(smem_raw + (sizeof(V) + sizeof(int32_t)) * T);
+  uint32_t* sorted_keys = reinterpret_cast<uint32_t*>(tkeys);  // after compaction, keys are dead
   SegCache<SR, Src> cache;
-  cache.carve(smem_raw + (sizeof(V) + sizeof(int32_t)) * T, cap, 1);
-  __shared__ typename BlockScan::TempStorage scan_tmp;
-  __shared__ int s_total;
+  cache.carve(reinterpret_cast<unsigned char*>(tmp) + ((sizeof(typename HS::Tmp) + 15) & ~size_t(15)), cap, 1);
   for (int64_t r = blockIdx.x; r < nrows_bin; r += gridDim.x) {
     const int64_t i = rows[r];
     for (int e = threadIdx.x; e < T; e += THREADS) {
@@ -966,8 +1017,9 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
       const int n = (int)(nseg - c0 < (int64_t)cap ? nseg - c0 : (int64_t)cap);
       cache.load(src, i, sb + c0, n, threadIdx.x, THREADS);
       __syncthreads();
-      cache.template prefix<THREADS, BlockScan>(n, 0, scan_tmp);
+      cache.template prefix<THREADS, typename HS::Scan>(n, 0, tmp->scan);
       balanced_items<SR, Src, NW>(src, cache, n, 0, [&](int32_t c, const V& v) {
+        if (SR::is_zero(v)) return;
         uint32_t h = hash_slot((uint32_t)c, LOG2T);
         for (;;) {
           const int32_t k = *reinterpret_cast<volatile int32_t*>(&tkeys[h]);
@@ -982,6 +1034,7 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
       });
       __syncthreads();
     }
+    // compaction of occupied, non-zero slots into blocked registers
     int my_slots[SPT];
     int cnt = 0;
 #pragma unroll
@@ -994,26 +1047,42 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
       }
     }
     int first, total;
-    BlockScan(scan_tmp).ExclusiveSum(cnt, first, total);
+    typename HS::Scan(tmp->scan).ExclusiveSum(cnt, first, total);
     uint32_t my_keys[SPT];
 #pragma unroll
     for (int q = 0; q < SPT; ++q) my_keys[q] = my_slots[q] >= 0 ? (uint32_t)tkeys[my_slots[q]] : 0u;
     __syncthreads();
+    // stage (key, slot) in smem (keys array is dead now), then blocked radix sort
+    uint16_t* stage_slot = reinterpret_cast<uint16_t*>(sorted_keys + T / 2);
     int w = first;
 #pragma unroll
     for (int q = 0; q < SPT; ++q)
-      if (my_slots[q] >= 0) sortbuf[w++] = ((uint64_t)my_keys[q] << 32) | (uint32_t)my_slots[q];
-    if (threadIdx.x == 0) s_total = total;
+      if (my_slots[q] >= 0) {
+        sorted_keys[w] = my_keys[q];
+        stage_slot[w] = (uint16_t)my_slots[q];
+        ++w;
+      }
     __syncthreads();
-    const int n = s_total;
-    block_bitonic_sort<THREADS>(sortbuf, n);
-    const int64_t o = off[i];
-    for (int e = threadIdx.x; e < n; e += THREADS) {
-      const uint64_t kk = sortbuf[e];
-      out_cols[o + e] = (int32_t)(kk >> 32);
-      out_vals[o + e] = tvals[(uint32_t)kk];
+    uint32_t k[ITEMS];
+    uint16_t sl[ITEMS];
+#pragma unroll
+    for (int q = 0; q < ITEMS; ++q) {
+      const int e = threadIdx.x * ITEMS + q;
+      k[q] = e < total ? sorted_keys[e] : (1u << end_bit);
+      sl[q] = e < total ? stage_slot[e] : 0;
     }
-    if (threadIdx.x == 0) rownnz[i] = n;
+    __syncthreads();
+    typename HS::Sort(tmp->sort).Sort(k, sl, 0, end_bit + 1);
+    const int64_t o = off[i];
+#pragma unroll
+    for (int q = 0; q < ITEMS; ++q) {
+      const int e = threadIdx.x * ITEMS + q;
+      if (e < total) {
+        out_cols[o + e] = (int32_t)k[q];
+        out_vals[o + e] = tvals[sl[q]];
+      }
+    }
+    if (threadIdx.x == 0) rownnz[i] = total;
     __syncthreads();
   }
 }

@@ -7,6 +7,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "accumulate.cuh"
@@ -84,14 +85,21 @@ inline int resident_grid(spg_ctx* c, K kern, int threads, size_t smem, int64_t w
 }
 
 template <class SR, class Src, int T, int THREADS>
-void launch_hash(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* rows, int64_t n, int cap,
+void launch_hash(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* rows, int64_t n, int cap, int end_bit,
                  const int64_t* off, int32_t* sc_cols, typename SR::value_type* sc_vals, int64_t* rownnz) {
   using V = typename SR::value_type;
-  const size_t smem = (size_t)T * (sizeof(V) + sizeof(int32_t)) + (size_t)cap * SegCache<SR, Src>::bytes_per_seg(1) + 64;
+  const size_t fixed = (size_t)T * (sizeof(V) + sizeof(int32_t)) +
+                       ((sizeof(typename HashSort<T, THREADS>::Tmp) + 15) & ~size_t(15)) + 64;
+  const size_t per = SegCache<SR, Src>::bytes_per_seg(1);
+  const size_t limit = 220 * 1024;
+  const int fit = fixed < limit ? (int)((limit - fixed) / per) : 0;
+  cap = std::min(cap, fit) & ~3;
+  if (cap < 32) fail(SPG_ERR_INTERNAL, "hash bin: no shared memory left for the segment cache");
+  const size_t smem = fixed + (size_t)cap * per;
   auto kern = hash_rows_kernel<SR, Src, T, THREADS>;
   set_smem(kern, smem);
-  kern<<<resident_grid(c, kern, THREADS, smem, n), THREADS, smem, s>>>(src, rows, n, cap, off, sc_cols, sc_vals,
-                                                                       rownnz);
+  kern<<<resident_grid(c, kern, THREADS, smem, n), THREADS, smem, s>>>(src, rows, n, cap, end_bit, off, sc_cols,
+                                                                       sc_vals, rownnz);
   SPG_LAUNCH_CHECK();
   ++c->launches;
 }
@@ -108,11 +116,65 @@ void launch_esc(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* rows,
   ++c->launches;
 }
 
+// Dense-panel geometry: (panel width, CTA size, smem budget per CTA).
+// cfg 0: 128 KB panel, 1024 threads, 1 CTA/SM; cfg 1: 64 KB, 512 threads,
+// 2 CTAs/SM; cfg 2: 32 KB, 512 threads, 3 CTAs/SM.  SPG_DENSE_CFG overrides.
+template <int W, int DT, class SR, class Src>
+void launch_dense_cfg(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* rows, int64_t n, int64_t ncols,
+                      size_t smem_budget, unsigned long long* work, const int64_t* off, int32_t* sc_cols,
+                      typename SR::value_type* sc_vals, int64_t* rownnz) {
+  using V = typename SR::value_type;
+  const int np = (int)((ncols + W - 1) / W);
+  const size_t per_seg = SegCache<SR, Src>::bytes_per_seg(np);
+  const size_t fixed = sizeof(V) * W + sizeof(uint32_t) * (W / 32);
+  const size_t room = smem_budget > fixed + 64 ? smem_budget - fixed - 64 : 0;
+  const int cap = (int)std::min<size_t>(8192, room / per_seg) & ~3;  // keeps 16-byte values aligned
+  if (cap < 32) fail(SPG_ERR_INTERNAL, "dense panel: no room for the segment cache");
+  const size_t smem = fixed + (size_t)cap * per_seg + 64;
+  auto kern = dense_panel_kernel<SR, Src, W, DT>;
+  set_smem(kern, smem);
+  kern<<<resident_grid(c, kern, DT, smem, n), DT, smem, s>>>(src, rows, n, np, cap, work, off, sc_cols, sc_vals, rownnz);
+  SPG_LAUNCH_CHECK();
+  ++c->launches;
+}
+
+inline int dense_cfg() {
+  static int cfg = [] {
+    const char* e = std::getenv("SPG_DENSE_CFG");
+    return e ? std::atoi(e) : 1;
+  }();
+  return cfg;
+}
+
+template <class V>
+inline int dense_panel_width() {
+  const int cfg = dense_cfg();
+  return Geom<V>::kPanelW >> (cfg == 1 ? 1 : cfg == 2 ? 2 : 0);
+}
+
+template <class SR, class Src>
+void launch_dense(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* rows, int64_t n, int64_t ncols,
+                  unsigned long long* work, const int64_t* off, int32_t* sc_cols, typename SR::value_type* sc_vals,
+                  int64_t* rownnz) {
+  using V = typename SR::value_type;
+  constexpr int PW = Geom<V>::kPanelW;
+  switch (dense_cfg()) {
+    case 1:
+      launch_dense_cfg<PW / 2, 512, SR, Src>(c, s, src, rows, n, ncols, 110 * 1024, work, off, sc_cols, sc_vals, rownnz);
+      break;
+    case 2:
+      launch_dense_cfg<PW / 4, 512, SR, Src>(c, s, src, rows, n, ncols, 72 * 1024, work, off, sc_cols, sc_vals, rownnz);
+      break;
+    default:
+      launch_dense_cfg<PW, 1024, SR, Src>(c, s, src, rows, n, ncols, 220 * 1024, work, off, sc_cols, sc_vals, rownnz);
+  }
+}
+
 // segment-cache capacity that fits next to a T-slot hash table
 template <class V>
 inline int V_hash_cap(int T) {
   const size_t table = (size_t)T * (sizeof(V) + 4);
-  const size_t room = table < 200 * 1024 ? 200 * 1024 - table : 0;
+  const size_t room = table < 170 * 1024 ? 170 * 1024 - table : 0;
   const size_t per = 8 + 4 + sizeof(V) + 4 + 4;
   return (int)std::max<size_t>(64, std::min<size_t>(2048, room / per)) & ~3;
 }
@@ -193,8 +255,8 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
   }
 
   // Panels for the dense bin.
-  const int W = Geom<V>::kPanelW;
-  const int np = npanels_for<V>(ncols_out);
+  const int W = dense_panel_width<V>();
+  const int np = npanels_for<V>(ncols_out, W);
   DBuf<int32_t> poff;
   if (hcounts[kBinDense] > 0 && np > 1) {
     if (needs_poff(src)) {
@@ -319,28 +381,15 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
     }
 
     StreamFork fk(c, 3);
-    if (nd > 0) {
-      constexpr int DT = 1024;
-      constexpr int PW = Geom<V>::kPanelW;
-      const size_t per_seg = SegCache<SR, Src>::bytes_per_seg(np);
-      const size_t budget_smem = 220 * 1024 - sizeof(V) * PW - 64;
-      const int cap = (int)std::min<size_t>(8192, budget_smem / per_seg) & ~3;  // keeps 16-byte values aligned
-      const size_t smem = sizeof(V) * PW + (size_t)cap * per_seg + 64;
-      auto kern = dense_panel_kernel<SR, Src, PW, DT>;
-      set_smem(kern, smem);
-      kern<<<resident_grid(c, kern, DT, smem, nd), DT, smem, fk[0]>>>(bsrc, dense_rows, nd, np, cap, work.p, offb,
-                                                                      sccb, scvb, nnzb);
-      SPG_LAUNCH_CHECK();
-      ++c->launches;
-    }
+    if (nd > 0) launch_dense<SR, Src>(c, fk[0], bsrc, dense_rows, nd, ncols_out, work.p, offb, sccb, scvb, nnzb);
     if (bcount[kBinHashMax] > 0)
       launch_hash<SR, Src, Geom<V>::kMaxT, 1024>(c, fk[1], bsrc, lb + base[kBinHashMax], bcount[kBinHashMax],
-                                                 V_hash_cap<V>(Geom<V>::kMaxT), offb, sccb, scvb, nnzb);
+                                                 V_hash_cap<V>(Geom<V>::kMaxT), end_bit, offb, sccb, scvb, nnzb);
     if (bcount[kBinHash8K] > 0)
-      launch_hash<SR, Src, 8192, 512>(c, fk[1], bsrc, lb + base[kBinHash8K], bcount[kBinHash8K], 1024, offb, sccb,
+      launch_hash<SR, Src, 8192, 512>(c, fk[1], bsrc, lb + base[kBinHash8K], bcount[kBinHash8K], 1024, end_bit, offb, sccb,
                                       scvb, nnzb);
     if (bcount[kBinHash4K] > 0)
-      launch_hash<SR, Src, 4096, 256>(c, fk[2], bsrc, lb + base[kBinHash4K], bcount[kBinHash4K], 512, offb, sccb,
+      launch_hash<SR, Src, 4096, 256>(c, fk[2], bsrc, lb + base[kBinHash4K], bcount[kBinHash4K], 512, end_bit, offb, sccb,
                                       scvb, nnzb);
     if (bcount[kBinEsc512] > 0)
       launch_esc<SR, Src, 128, 4>(c, fk[2], bsrc, lb + base[kBinEsc512], bcount[kBinEsc512], end_bit, offb, sccb,

@@ -58,8 +58,8 @@ struct Arithmetic {
   SPG_HD static bool is_zero(value_type v) { return v == 0.0; }
   SPG_HD static value_type from_real(double x) { return x; }
 #ifdef __CUDACC__
-  __device__ __forceinline__ static void acc_shared(value_type* p, value_type v) { atomicAdd(p, v); }
-  __device__ __forceinline__ static void acc_global(value_type* p, value_type v) { atomicAdd(p, v); }
+  __device__ __forceinline__ static value_type acc_shared(value_type* p, value_type v) { return atomicAdd(p, v); }
+  __device__ __forceinline__ static value_type acc_global(value_type* p, value_type v) { return atomicAdd(p, v); }
 #endif
 };
 
@@ -91,11 +91,15 @@ struct Boolean {
 #ifdef __CUDACC__
   // OR with false is the identity and every writer of `true` writes the same
   // byte, so a plain store is a correct (race-free) accumulate.
-  __device__ __forceinline__ static void acc_shared(value_type* p, value_type v) {
-    if (v) *reinterpret_cast<volatile value_type*>(p) = 1;
+  __device__ __forceinline__ static value_type acc_shared(value_type* p, value_type v) {
+    const value_type old = *reinterpret_cast<volatile value_type*>(p);
+    if (v && !old) *reinterpret_cast<volatile value_type*>(p) = 1;
+    return old;
   }
-  __device__ __forceinline__ static void acc_global(value_type* p, value_type v) {
-    if (v) *reinterpret_cast<volatile value_type*>(p) = 1;
+  __device__ __forceinline__ static value_type acc_global(value_type* p, value_type v) {
+    const value_type old = *reinterpret_cast<volatile value_type*>(p);
+    if (v && !old) *reinterpret_cast<volatile value_type*>(p) = 1;
+    return old;
   }
 #endif
 };
@@ -146,8 +150,8 @@ struct TropicalI32 {
     return (value_type)llround(y);
   }
 #ifdef __CUDACC__
-  __device__ __forceinline__ static void acc_shared(value_type* p, value_type v) { atomicMin(p, v); }
-  __device__ __forceinline__ static void acc_global(value_type* p, value_type v) { atomicMin(p, v); }
+  __device__ __forceinline__ static value_type acc_shared(value_type* p, value_type v) { return atomicMin(p, v); }
+  __device__ __forceinline__ static value_type acc_global(value_type* p, value_type v) { return atomicMin(p, v); }
 #endif
 };
 
@@ -203,15 +207,16 @@ __device__ __forceinline__ T as_bits(const V& v) {
   return t;
 }
 
-// *p = add(*p, v), atomically.  `kShared` selects the semiring's shared- or
-// global-memory fast path when it has one; otherwise a CAS loop.
+// *p = add(*p, v), atomically; returns the previous value.  `kShared`
+// selects the semiring's shared- or global-memory fast path when it has one;
+// otherwise a CAS loop.
 template <class SR, bool kShared>
-__device__ __forceinline__ void atomic_accumulate(typename SR::value_type* p,
-                                                  const typename SR::value_type& v) {
+__device__ __forceinline__ typename SR::value_type atomic_accumulate(typename SR::value_type* p,
+                                                                     const typename SR::value_type& v) {
   using V = typename SR::value_type;
   if constexpr (has_acc<SR>::value) {
-    if constexpr (kShared) SR::acc_shared(p, v);
-    else SR::acc_global(p, v);
+    if constexpr (kShared) return SR::acc_shared(p, v);
+    else return SR::acc_global(p, v);
   } else if constexpr (sizeof(V) == 8) {
     unsigned long long* a = reinterpret_cast<unsigned long long*>(p);
     unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(a);
@@ -219,20 +224,21 @@ __device__ __forceinline__ void atomic_accumulate(typename SR::value_type* p,
       const V cur = as_bits<V>(old);
       const V nxt = SR::add(cur, v);
       const unsigned long long nb = as_bits<unsigned long long>(nxt);
-      if (nb == old) return;
+      if (nb == old) return cur;
       const unsigned long long seen = atomicCAS(a, old, nb);
-      if (seen == old) return;
+      if (seen == old) return cur;
       old = seen;
     }
   } else if constexpr (sizeof(V) == 4) {
     unsigned int* a = reinterpret_cast<unsigned int*>(p);
     unsigned int old = *reinterpret_cast<volatile unsigned int*>(a);
     for (;;) {
-      const V nxt = SR::add(as_bits<V>(old), v);
+      const V cur = as_bits<V>(old);
+      const V nxt = SR::add(cur, v);
       const unsigned int nb = as_bits<unsigned int>(nxt);
-      if (nb == old) return;
+      if (nb == old) return cur;
       const unsigned int seen = atomicCAS(a, old, nb);
-      if (seen == old) return;
+      if (seen == old) return cur;
       old = seen;
     }
   } else if constexpr (sizeof(V) == 16) {
@@ -245,16 +251,22 @@ __device__ __forceinline__ void atomic_accumulate(typename SR::value_type* p,
     old.lo = reinterpret_cast<volatile unsigned long long*>(a)[0];
     old.hi = reinterpret_cast<volatile unsigned long long*>(a)[1];
     for (;;) {
-      const V nxt = SR::add(as_bits<V>(old), v);
+      const V cur = as_bits<V>(old);
+      const V nxt = SR::add(cur, v);
       const U128 nb = as_bits<U128>(nxt);
-      if (nb.lo == old.lo && nb.hi == old.hi) return;
+      if (nb.lo == old.lo && nb.hi == old.hi) return cur;
       const U128 seen = atomicCAS(a, old, nb);
-      if (seen.lo == old.lo && seen.hi == old.hi) return;
+      if (seen.lo == old.lo && seen.hi == old.hi) return cur;
       old = seen;
     }
   } else {
     static_assert(sizeof(V) == 0, "unsupported value width");
   }
+}
+
+template <class SR>
+__device__ __forceinline__ bool is_zero_bits(const typename SR::value_type& v) {
+  return bits_equal(v, SR::zero());
 }
 #endif
 
