@@ -189,7 +189,7 @@ inline void rebase_source(MergeSource<SR>& s, int64_t r0) {
 template <class V>
 struct Geom {
   // hash tables: largest table whose keys + values fit in ~200 KB of smem
-  static constexpr int kMaxT = sizeof(V) <= 1 ? 32768 : (sizeof(V) <= 8 ? 16384 : 8192);
+  static constexpr int kMaxT = sizeof(V) <= 4 ? 16384 : 8192;
   // dense panel width: 128 KB of accumulator values (64K columns for bool)
   static constexpr int kPanelW = (131072 / (int)sizeof(V)) > 65536 ? 65536 : (131072 / (int)sizeof(V));
 };
@@ -975,7 +975,7 @@ __device__ __forceinline__ uint32_t hash_slot(uint32_t col, int log2t) {
 template <int T, int THREADS>
 struct HashSort {
   static constexpr int ITEMS = T / 2 / THREADS;  // occupied slots <= T/2 (load factor 1/2)
-  using Sort = cub::BlockRadixSort<uint32_t, THREADS, ITEMS, uint16_t, 6>;
+  using Sort = cub::BlockRadixSort<uint32_t, THREADS, ITEMS, uint16_t, 4>;
   using Scan = cub::BlockScan<int, THREADS>;
   union Tmp {
     typename Sort::TempStorage sort;

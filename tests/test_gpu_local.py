@@ -160,15 +160,14 @@ def test_wide_output_uses_hash_bins(ctx, sr):
     bptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
     bcols = np.concatenate([np.sort(rng.choice(n, L, replace=False)) for L in lens]).astype(np.int64)
     b = CsrMatrix(sr, 400, n, bptr, bcols, exact_values(sr, rng, bcols.size))
-    rows = [np.sort(rng.choice(400, s, replace=False)) for s in (70, 100, 150, 3, 0, 200)]
+    rows = [np.sort(rng.choice(400, s, replace=False)) for s in (10, 20, 40, 3, 0, 50, 150)]
     aptr = np.concatenate([[0], np.cumsum([len(x) for x in rows])]).astype(np.int64)
     acols = np.concatenate(rows).astype(np.int64)
     a = CsrMatrix(sr, len(rows), 400, aptr, acols, exact_values(sr, rng, acols.size))
     st = {}
     got = esc_multiply(a, b, ctx=ctx, stats=st)
     assert_same(got, ob.orc_multiply(to_mat(a), to_mat(b)), sr)
-    if sr != 5:  # 16-byte values: hash capacity (<= 4096 distinct) is covered by the ESC bins
-        assert sum(st["rows_per_bin"][i] for i in (3, 4, 7)) >= 2, st["rows_per_bin"]
+    assert sum(st["rows_per_bin"][i] for i in (3, 4, 7)) >= 2, st["rows_per_bin"]
 
 
 @pytest.mark.parametrize("sr", [1, 2, 4])
