@@ -270,7 +270,124 @@ def run_single(args):
     print(json.dumps(line), flush=True)
 
 
+def run_summa(args):
+    """N GPUs, one process each (torchrun): C = A.A through summa25_multiply on
+    a 1x2 / 2x2 / 2x4 grid.  Time-to-C per step = host-resident distributed
+    blocks -> device-resident merged C blocks (prepare H2D, size exchanges,
+    broadcasts, local multiplies, merge), device-timed, max over ranks."""
+    import uuid
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2504_06408_b200 import Context, generators
+    from paper_2504_06408_b200._lib import check, lib
+    from paper_2504_06408_b200.summa import (DEVICE_ONLY, HOST_ONLY, HYBRID, Comm, checksum_part, checksum_seed,
+                                             grid_for, local_block, summa25_multiply)
+
+    rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29511")
+    torch.cuda.set_device(local)
+    import datetime
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=600))
+    job = [uuid.uuid4().hex[:12] if rank == 0 else None]
+    dist.broadcast_object_list(job, src=0)
+    pr, pc = grid_for(world)
+    i, j = rank // pc, rank % pc
+    mode = {"host": HOST_ONLY, "device": DEVICE_ONLY, "hybrid": HYBRID}[args.comm]
+    thr = args.threshold if args.threshold >= 0 else int(os.environ.get("SPG_HYBRID_THRESHOLD", 1 << 18))
+
+    coo = generators.generate_rmat(4, args.scale, args.ef, args.seed)
+    n = coo.nrows
+    blk = local_block(coo, pr, pc, i, j)
+    del coo
+    stream = torch.cuda.current_stream()
+    ctx = Context(local)
+    check(lib.spg_ctx_set_stream(ctx.handle, C.c_void_p(stream.cuda_stream)), ctx.handle)
+    comm = Comm(job[0], world, rank, pr, pc, local, staging_bytes=64 << 20)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+
+    def step():
+        c, led = summa25_multiply(comm, ctx, blk, blk, n, n, n, two_round=not args.one_round, mode=mode,
+                                  threshold=thr)
+        return c, led
+
+    for _ in range(args.warmup):
+        c, led = step()
+        c.free()
+    times, leds = [], []
+    launches0 = ctx.kernel_launches()
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            c, led = step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+            leds.append(led)
+            if len(times) < args.steps:
+                c.free()
+    launches = ctx.kernel_launches() - launches0
+    part = checksum_part(c, blk.rows[0], blk.cols[0])
+    nnz_blk = c.nnz
+    # e2e: the same call plus the D2H read of this rank's C block (host result)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    c2, _ = step()
+    host_c = c2.download()
+    e2e_local = time.perf_counter() - t0
+    d2h = 8 * (host_c.ncols + 1) + (8 + 4) * host_c.nnz
+    del host_c
+    c2.free()
+    c.free()
+
+    t = torch.tensor(times, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    agg = torch.tensor([float(leds[-1]["products"]), float(nnz_blk), float(part & 0xFFFFFFFF), float(part >> 32),
+                        float(launches), float(d2h)], dtype=torch.float64)
+    dist.all_reduce(agg, op=dist.ReduceOp.SUM)
+    e2e_t = torch.tensor([e2e_local], dtype=torch.float64)
+    dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    ms = float(t.mean())
+    F = int(agg[0])
+    if rank == 0:
+        led0 = leds[-1]
+        csum = (checksum_seed(n, n) + int(agg[2]) + (int(agg[3]) << 32)) % (1 << 64)
+        peak, peak_kind = peaks()
+        h2d = 8 * (blk.storage.ncols + 1) + (8 + 4) * blk.storage.nnz
+        line = {
+            "metric": METRIC, "value": 2.0 * F / (ms * 1e-3) / 1e9, "unit": "Gflop/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": f"rmat{args.scale}_ef{int(args.ef)}_tropical_i32_AxA via summa25_multiply",
+                       "grid": f"{pr}x{pc}", "two_round": not args.one_round, "comm": args.comm,
+                       "threshold_bytes": thr, "products": F, "nnz_C": int(agg[1]), "checksum_C": csum,
+                       "time_to_C_ms": ms, "rank0_ledger": led0,
+                       "l2": "flushed between steps (512 MB write)", "parallelism": f"summa{pr}x{pc}"},
+            "roofline": {"bound": "hbm", "achieved": None, "peak": peak, "unit": "GB/s", "frac": None,
+                         "traffic": None, "note": "per-kernel roofline is reported by the N=1 line"},
+            "cpu_baseline": None,
+            "e2e": {"value": 2.0 * F / float(e2e_t[0]) / 1e9, "unit": "Gflop/s", "h2d_bytes_per_step": 2 * h2d,
+                    "d2h_bytes_per_step": int(agg[5]), "seconds": float(e2e_t[0])},
+            "gpu_launches": int(agg[4]), "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    comm.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
+    if os.environ.get("SPG_DEBUG_HANG"):
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["SPG_DEBUG_HANG"]), exit=True)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -283,6 +400,10 @@ def main():
     ap.add_argument("--cpu-products", type=float, default=0.0,
                     help="products in the CPU sample (default: 3e7 per host core, at most 1e9)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--summa", action="store_true", help="use the SUMMA path even on one GPU (1x1 grid)")
+    ap.add_argument("--one-round", action="store_true", help="SummaOptions::two_round = false")
+    ap.add_argument("--comm", default="hybrid", choices=["host", "device", "hybrid"])
+    ap.add_argument("--threshold", type=int, default=-1, help="hybrid threshold bytes (-1: measured default)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.cpu_products <= 0:
@@ -290,11 +411,10 @@ def main():
     if args.impl == "reference":
         run_reference_arm(args)
         return
-    if args.gpus == 1 and int(os.environ.get("WORLD_SIZE", "1")) == 1:
+    if args.gpus == 1 and int(os.environ.get("WORLD_SIZE", "1")) == 1 and not args.summa:
         run_single(args)
     else:
-        from paper_2504_06408_b200 import summa_bench
-        summa_bench.run(args)
+        run_summa(args)
 
 
 if __name__ == "__main__":

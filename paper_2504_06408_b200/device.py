@@ -71,6 +71,16 @@ def hcsr_of(m):
     return _hcsr(m.colptr, m.rowids, m.values, m.nrows, m.ncols)
 
 
+def copy_out(ptr, n: int, dt) -> np.ndarray:
+    """Copy n values of dtype dt from a raw host pointer (any size; ctypes'
+    string_at truncates sizes to a C int)."""
+    dt = np.dtype(dt)
+    if n == 0 or not ptr:
+        return np.zeros(0, dtype=dt)
+    raw = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_uint8)), shape=(n * dt.itemsize,))
+    return raw.copy().view(dt)
+
+
 def take_hcsr(sr, h: HCsr, is_csc: bool):
     """Copy a library-allocated spg_hcsr into numpy and free it."""
     nseg = h.ncols if is_csc else h.nrows
@@ -78,8 +88,7 @@ def take_hcsr(sr, h: HCsr, is_csc: bool):
     nnz = int(h.nnz)
     idx = np.ctypeslib.as_array(h.idx, shape=(max(nnz, 1),))[:nnz].copy()
     dt = dtype_of(sr)
-    raw = C.string_at(h.vals, nnz * dt.itemsize) if nnz else b""
-    vals = np.frombuffer(raw, dtype=dt).copy()
+    vals = copy_out(h.vals, nnz, dt)
     lib.spg_hcsr_free(C.byref(h))
     if is_csc:
         return CscMatrix(int(as_id(sr)), int(h.nrows), int(h.ncols), ptr, idx, vals)

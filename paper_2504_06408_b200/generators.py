@@ -20,7 +20,8 @@ def _take(sr, nnz, rows, cols, vals):
     dt = dtype_of(sr)
     r = np.ctypeslib.as_array(rows, shape=(max(n, 1),))[:n].copy()
     c = np.ctypeslib.as_array(cols, shape=(max(n, 1),))[:n].copy()
-    v = np.frombuffer(C.string_at(vals, n * dt.itemsize), dtype=dt).copy() if n else np.zeros(0, dt)
+    from .device import copy_out
+    v = copy_out(vals, n, dt)
     lib.spg_free(C.cast(rows, C.c_void_p))
     lib.spg_free(C.cast(cols, C.c_void_p))
     lib.spg_free(vals)

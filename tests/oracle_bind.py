@@ -103,13 +103,20 @@ class Mat:
         return cls(m.sr, m.nrows, m.ncols, m.colptr, m.rowids, m.values, csc=True)
 
 
+def _copy_out(ptr, n, dt):
+    if n == 0 or not ptr:
+        return np.zeros(0, dtype=dt)
+    raw = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_uint8)), shape=(n * dt.itemsize,))
+    return raw.copy().view(dt)
+
+
 def _take_csr(sr, c: Csr, csc=False, free=None):
     nseg = c.ncols if csc else c.nrows
     n = int(c.nnz)
     ptr = np.ctypeslib.as_array(c.ptr, shape=(nseg + 1,)).copy()
     idx = np.ctypeslib.as_array(c.idx, shape=(max(n, 1),))[:n].copy()
     dt = _DT[sr]
-    vals = np.frombuffer(C.string_at(c.vals, n * dt.itemsize), dtype=dt).copy() if n else np.zeros(0, dt)
+    vals = _copy_out(c.vals, n, dt)
     for p in (c.ptr, c.idx):
         free(C.cast(p, C.c_void_p))
     free(c.vals)
@@ -121,7 +128,7 @@ def _take_coo(sr, c: Coo):
     r = np.ctypeslib.as_array(c.rows, shape=(max(n, 1),))[:n].copy()
     cc = np.ctypeslib.as_array(c.cols, shape=(max(n, 1),))[:n].copy()
     dt = _DT[sr]
-    v = np.frombuffer(C.string_at(c.vals, n * dt.itemsize), dtype=dt).copy() if n else np.zeros(0, dt)
+    v = _copy_out(c.vals, n, dt)
     ref.ref_free(C.cast(c.rows, C.c_void_p))
     ref.ref_free(C.cast(c.cols, C.c_void_p))
     ref.ref_free(c.vals)
