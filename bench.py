@@ -101,11 +101,13 @@ class Clocks:
                 "samples": len(sm)}
 
 
-def make_input(scale, ef, seed, sr=4):
+def make_input(scale, ef, seed, sr=4, permute=False):
     from paper_2504_06408_b200 import generators
     from paper_2504_06408_b200.generators import coo_to_csr_fast
     t0 = time.time()
     coo = generators.generate_rmat(sr, scale, ef, seed)
+    if permute:
+        coo = generators.permute_symmetric(coo, seed)
     a = coo_to_csr_fast(coo)
     log(f"[bench] R-MAT s{scale} ef{ef}: n={a.nrows} nnz={a.nnz} (gen {time.time() - t0:.1f}s)")
     return a
@@ -190,7 +192,7 @@ def run_single(args):
 
     sr = 4
     vs = 4
-    a = make_input(args.scale, args.ef, args.seed)
+    a = make_input(args.scale, args.ef, args.seed, permute=args.permute)
     torch.cuda.set_device(0)
     stream = torch.cuda.current_stream()
     ctx = Context(0)
@@ -256,7 +258,7 @@ def run_single(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "int32", "data": "synthetic",
         "config": {"workload": f"rmat{args.scale}_ef{int(args.ef)}_tropical_i32_AxA (BASELINE config 2)",
-                   "grid": "1x1", "products": F, "nnz_A": a.nnz, "nnz_C": nnz_c,
+                   "grid": "1x1", "permuted": bool(args.permute), "products": F, "nnz_A": a.nnz, "nnz_C": nnz_c,
                    "time_to_C_ms": ms, "l2": "flushed between steps (512 MB write)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
@@ -300,6 +302,8 @@ def run_summa(args):
     thr = args.threshold if args.threshold >= 0 else int(os.environ.get("SPG_HYBRID_THRESHOLD", 1 << 18))
 
     coo = generators.generate_rmat(4, args.scale, args.ef, args.seed)
+    if args.permute:
+        coo = generators.permute_symmetric(coo, args.seed)
     n = coo.nrows
     blk = local_block(coo, pr, pc, i, j)
     del coo
@@ -311,7 +315,7 @@ def run_summa(args):
 
     def step():
         c, led = summa25_multiply(comm, ctx, blk, blk, n, n, n, two_round=not args.one_round, mode=mode,
-                                  threshold=thr)
+                                  threshold=thr, fuse_stages=not args.no_fuse)
         return c, led
 
     for _ in range(args.warmup):
@@ -355,6 +359,11 @@ def run_summa(args):
     dist.all_reduce(agg, op=dist.ReduceOp.SUM)
     e2e_t = torch.tensor([e2e_local], dtype=torch.float64)
     dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    mine = torch.tensor([times[-1], leds[-1]["ms_total"]] + [leds[-1]["ms"][k] for k in
+                        ("prepare", "broadcast", "local_multiply", "merge")] + [float(leds[-1]["products"])],
+                        dtype=torch.float64)
+    allr = [torch.zeros_like(mine) for _ in range(world)]
+    dist.all_gather(allr, mine)
     ms = float(t.mean())
     F = int(agg[0])
     if rank == 0:
@@ -367,9 +376,16 @@ def run_summa(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": {"workload": f"rmat{args.scale}_ef{int(args.ef)}_tropical_i32_AxA via summa25_multiply",
-                       "grid": f"{pr}x{pc}", "two_round": not args.one_round, "comm": args.comm,
+                       "grid": f"{pr}x{pc}", "permuted": bool(args.permute), "two_round": not args.one_round,
+                       "fuse_stages": not args.no_fuse,
+                       "comm": args.comm,
                        "threshold_bytes": thr, "products": F, "nnz_C": int(agg[1]), "checksum_C": csum,
-                       "time_to_C_ms": ms, "rank0_ledger": led0,
+                       "time_to_C_ms": ms, "steps_ms_max_over_ranks": [round(float(x), 2) for x in t],
+                       "rank0_ledger": led0,
+                       "per_rank_ms": [{"event": round(float(x[0]), 2), "ledger_total": round(float(x[1]), 2),
+                                        "prepare": round(float(x[2]), 2), "bcast": round(float(x[3]), 2),
+                                        "multiply": round(float(x[4]), 2), "merge": round(float(x[5]), 2),
+                                        "products": int(x[6])} for x in allr],
                        "l2": "flushed between steps (512 MB write)", "parallelism": f"summa{pr}x{pc}"},
             "roofline": {"bound": "hbm", "achieved": None, "peak": peak, "unit": "GB/s", "frac": None,
                          "traffic": None, "note": "per-kernel roofline is reported by the N=1 line"},
@@ -402,6 +418,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--summa", action="store_true", help="use the SUMMA path even on one GPU (1x1 grid)")
     ap.add_argument("--one-round", action="store_true", help="SummaOptions::two_round = false")
+    ap.add_argument("--no-fuse", action="store_true", help="per-stage multiplies + merge_partials (reference structure)")
+    ap.add_argument("--no-permute", dest="permute", action="store_false",
+                    help="use the generator's vertex order (default: relabel vertices by a seeded random "
+                         "permutation, as CombBLAS does, so grid blocks carry equal work; F and nnz(C) unchanged)")
     ap.add_argument("--comm", default="hybrid", choices=["host", "device", "hybrid"])
     ap.add_argument("--threshold", type=int, default=-1, help="hybrid threshold bytes (-1: measured default)")
     args = ap.parse_args()

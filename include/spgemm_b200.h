@@ -236,6 +236,9 @@ typedef struct {
   int two_round;      /* SummaOptions::two_round (summa.hpp:174-177) */
   int comm_mode;      /* CommConfig::mode (comm.hpp:36-39) */
   uint64_t threshold; /* CommConfig::threshold_bytes */
+  int fuse_stages;    /* 1: keep every received panel and run ONE fused local multiply over the
+                         concatenated panels (no partials, no merge; fold order = ascending k);
+                         0: the reference's per-stage multiplies + merge_partials */
 } spg_summa_opts;
 
 /* CostLedger (cost_ledger.hpp:31-56) with measured instead of modelled time. */

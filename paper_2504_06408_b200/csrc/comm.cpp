@@ -10,6 +10,7 @@
 #include <unistd.h>
 
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
@@ -341,6 +342,21 @@ int spg_comm_create(const char* job, int world, int rank, int pr, int pc, int de
       while (c->hdr->uid_ready.load(std::memory_order_acquire) != 1) std::this_thread::sleep_for(std::chrono::milliseconds(1));
       ncclUniqueId id;
       std::memcpy(&id, c->hdr->uid, sizeof(id));
+      // NCCL may print its version banner on stdout; keep stdout clean for
+      // callers that emit machine-readable output (bench.py's JSON line).
+      std::fflush(stdout);
+      const int saved = dup(1);
+      if (saved >= 0) dup2(2, 1);
+      struct Restore {
+        int fd;
+        ~Restore() {
+          if (fd >= 0) {
+            std::fflush(stdout);
+            dup2(fd, 1);
+            close(fd);
+          }
+        }
+      } restore{saved};
       nccl_check(ncclCommInitRank(&c->world_comm, world, id, rank), "ncclCommInitRank");
       nccl_check(ncclCommSplit(c->world_comm, c->row, c->col, &c->row_comm, nullptr), "ncclCommSplit(row)");
       nccl_check(ncclCommSplit(c->world_comm, c->col, c->row, &c->col_comm, nullptr), "ncclCommSplit(col)");

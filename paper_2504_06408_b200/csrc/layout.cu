@@ -1,6 +1,8 @@
 // Width-generic layout kernels (see layout.cuh).
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
+
 #include "layout.cuh"
 
 namespace spg {
@@ -76,6 +78,49 @@ __global__ void dcsc_scatter_kernel(int64_t njc, const int64_t* __restrict__ jc,
     lens[jc[i]] = cp[i + 1] - cp[i];
 }
 
+constexpr int kMaxConcat = 64;
+struct ConcatParts {
+  const int64_t* ptr[kMaxConcat];
+  const int32_t* idx[kMaxConcat];
+  const void* val[kMaxConcat];
+  int64_t shift[kMaxConcat];
+};
+
+__global__ void concat_len_kernel(ConcatParts P, int K, int64_t nrows, int64_t* __restrict__ len) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t l = 0;
+    for (int p = 0; p < K; ++p) l += P.ptr[p][i + 1] - P.ptr[p][i];
+    len[i] = l;
+  }
+}
+
+template <class T>
+__global__ void concat_fill_kernel(ConcatParts P, int K, int64_t nrows, const int64_t* __restrict__ optr,
+                                   int32_t* __restrict__ oidx, T* __restrict__ oval) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < nrows; i += nwarps) {
+    int64_t o = optr[i];
+    for (int p = 0; p < K; ++p) {
+      const int64_t b = P.ptr[p][i], n = P.ptr[p][i + 1] - b;
+      const int32_t sh = (int32_t)P.shift[p];
+      const int32_t* ix = P.idx[p];
+      const T* vv = static_cast<const T*>(P.val[p]);
+      for (int64_t k = lane; k < n; k += 32) {
+        oidx[o + k] = ix[b + k] + sh;
+        oval[o + k] = vv[b + k];
+      }
+      o += n;
+    }
+  }
+}
+
+__global__ void add_offset_kernel(const int64_t* __restrict__ in, int64_t* __restrict__ out, int64_t n, int64_t add) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[i] + add;
+}
+
 int blocks_for(spg_ctx* c, int64_t n, int threads = 256) {
   const int64_t want = (n + threads - 1) / threads;
   return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c->sm_count * 16));
@@ -97,6 +142,77 @@ void inclusive_scan_i64(spg_ctx* c, const int64_t* in, int64_t* out, int64_t n) 
   ensure_cub_tmp(c, bytes);
   SPG_CUDA(cub::DeviceScan::InclusiveSum(c->cub_tmp, bytes, in, out, n, c->stream));
   ++c->launches;
+}
+
+void concat_cols(spg_ctx* c, int K, const spg_dcsr* parts, const int64_t* col_shift, int vs, spg_dcsr* out) {
+  if (K < 1 || K > kMaxConcat) fail(SPG_ERR_ARG, "concat: bad part count");
+  const int64_t nrows = parts[0].nrows;
+  ConcatParts P{};
+  int64_t nnz = 0, ncols = 0;
+  for (int p = 0; p < K; ++p) {
+    if (parts[p].nrows != nrows) fail(SPG_ERR_INTERNAL, "concat_cols: row counts differ");
+    P.ptr[p] = parts[p].ptr;
+    P.idx[p] = parts[p].idx;
+    P.val[p] = parts[p].vals;
+    P.shift[p] = col_shift[p];
+    nnz += parts[p].nnz;
+    ncols = std::max(ncols, col_shift[p] + parts[p].ncols);
+  }
+  out->nrows = nrows;
+  out->ncols = ncols;
+  out->nnz = nnz;
+  out->ptr = dalloc<int64_t>(c, nrows + 1);
+  out->idx = dalloc<int32_t>(c, nnz);
+  out->vals = dalloc<char>(c, (size_t)vs * nnz);
+  DBuf<int64_t> len(c, nrows + 1);
+  SPG_CUDA(cudaMemsetAsync(len.p + nrows, 0, sizeof(int64_t), c->stream));
+  if (nrows > 0) {
+    concat_len_kernel<<<blocks_for(c, nrows), 256, 0, c->stream>>>(P, K, nrows, len.p);
+    SPG_LAUNCH_CHECK();
+    ++c->launches;
+  }
+  exclusive_scan_i64(c, len.p, out->ptr, nrows + 1);
+  if (nnz > 0) {
+    with_vs(vs, [&](auto tag) {
+      using T = typename decltype(tag)::T;
+      concat_fill_kernel<T><<<blocks_for(c, nrows * 32), 256, 0, c->stream>>>(P, K, nrows, out->ptr, out->idx,
+                                                                             static_cast<T*>(out->vals));
+      SPG_LAUNCH_CHECK();
+      ++c->launches;
+    });
+  }
+}
+
+void concat_rows(spg_ctx* c, int K, const spg_dcsr* parts, int64_t ncols, int vs, spg_dcsr* out) {
+  int64_t nrows = 0, nnz = 0;
+  for (int p = 0; p < K; ++p) {
+    nrows += parts[p].nrows;
+    nnz += parts[p].nnz;
+  }
+  out->nrows = nrows;
+  out->ncols = ncols;
+  out->nnz = nnz;
+  out->ptr = dalloc<int64_t>(c, nrows + 1);
+  out->idx = dalloc<int32_t>(c, nnz);
+  out->vals = dalloc<char>(c, (size_t)vs * nnz);
+  int64_t r = 0, z = 0;
+  for (int p = 0; p < K; ++p) {
+    const spg_dcsr& m = parts[p];
+    if (m.nrows > 0) {
+      add_offset_kernel<<<blocks_for(c, m.nrows), 256, 0, c->stream>>>(m.ptr, out->ptr + r, m.nrows, z);
+      SPG_LAUNCH_CHECK();
+      ++c->launches;
+    }
+    if (m.nnz > 0) {
+      SPG_CUDA(cudaMemcpyAsync(out->idx + z, m.idx, sizeof(int32_t) * m.nnz, cudaMemcpyDeviceToDevice, c->stream));
+      SPG_CUDA(cudaMemcpyAsync(static_cast<char*>(out->vals) + (size_t)vs * z, m.vals, (size_t)vs * m.nnz,
+                               cudaMemcpyDeviceToDevice, c->stream));
+    }
+    r += m.nrows;
+    z += m.nnz;
+  }
+  SPG_CUDA(cudaMemcpyAsync(out->ptr + nrows, &nnz, sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+  SPG_CUDA(cudaStreamSynchronize(c->stream));  // &nnz is a host stack value
 }
 
 void narrow_indices(spg_ctx* c, const int64_t* in, int32_t* out, int64_t n, int64_t bound) {

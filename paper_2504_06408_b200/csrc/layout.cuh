@@ -66,6 +66,13 @@ void slice_cols_fill(spg_ctx* c, const spg_dcsr& m, int64_t b, int64_t e, int vs
 void dcsc_colptr(spg_ctx* c, int64_t ncols, int64_t njc, const int64_t* jc, const int64_t* cp,
                  int64_t* colptr);
 void exclusive_scan_i64(spg_ctx* c, const int64_t* in, int64_t* out, int64_t n);
+
+// Horizontal concatenation of K CSR matrices with equal row counts: row i of
+// the result is row i of part 0, then part 1, ... with part p's columns shifted
+// by col_shift[p].  Vertical concatenation (stacking rows) of K CSRs.  Both
+// allocate `out` from the context pool.
+void concat_cols(spg_ctx* c, int K, const spg_dcsr* parts, const int64_t* col_shift, int vs, spg_dcsr* out);
+void concat_rows(spg_ctx* c, int K, const spg_dcsr* parts, int64_t ncols, int vs, spg_dcsr* out);
 void inclusive_scan_i64(spg_ctx* c, const int64_t* in, int64_t* out, int64_t n);
 
 }  // namespace spg

@@ -179,10 +179,18 @@ extern "C" int spg_summa25_multiply(spg_comm* comm, spg_ctx* c, int sr, int64_t 
       spg_dcsr m;
     };
     std::vector<Part> parts;
+    // fused mode: every received panel pair is kept (device memory is ample)
+    struct Kept {
+      int stage, round;
+      Panel a, b;
+      int64_t a_rows, b_cols;  // panel dims (also for absent panels, from the size triples)
+    };
+    std::vector<Kept> kept;
     auto free_parts = [&] {
       for (auto& p : parts) free_dcsr(c, &p.m);
       parts.clear();
     };
+    const int64_t block_rows = are - arb, block_cols = bce - bcb;
     try {
       for (int r = 0; r < rounds; ++r) {
         for (int s = 0; s < ns; ++s) {
@@ -196,6 +204,15 @@ extern "C" int spg_summa25_multiply(spg_comm* comm, spg_ctx* c, int sr, int64_t 
           // B panel: columns [b_off + hb, b_off + he) of the prepared B (B's local rows)
           broadcast_panel(c, comm, SPG_SCOPE_COL, st.b_row_block, false, pb, st.b_off + hb, st.b_off + he, vs,
                           *opts, panb, led);
+          if (opts->fuse_stages) {
+            const uint64_t resident = (pana.present ? pana.bytes : 0) + (panb.present ? panb.bytes : 0);
+            uint64_t total = resident;
+            for (auto& k : kept) total += (k.a.present ? k.a.bytes : 0) + (k.b.present ? k.b.bytes : 0);
+            if (total > led.peak_bcast_buffer_bytes) led.peak_bcast_buffer_bytes = total;
+            if (!(pana.present && panb.present)) ++led.skipped_stages;
+            kept.push_back({s, r, std::move(pana), std::move(panb), he - hb, block_cols});
+            continue;
+          }
           const uint64_t resident = (pana.present ? pana.bytes : 0) + (panb.present ? panb.bytes : 0);
           if (resident > led.peak_bcast_buffer_bytes) led.peak_bcast_buffer_bytes = resident;
           if (pana.present && panb.present) {
@@ -212,38 +229,99 @@ extern "C" int spg_summa25_multiply(spg_comm* comm, spg_ctx* c, int sr, int64_t 
           }
         }
       }
-      // merge (summa.hpp:325-328), stage-major / round-minor
-      const auto t0 = Clock::now();
-      std::stable_sort(parts.begin(), parts.end(), [](const Part& x, const Part& y) {
-        return x.stage != y.stage ? x.stage < y.stage : x.round < y.round;
-      });
-      const int64_t block_rows = are - arb, block_cols = bce - bcb;
-      if (parts.empty()) {
+      if (opts->fuse_stages) {
+        // C^T = [panB_0 | panB_1 | ...] (x) [panA_0; panA_1; ...]  in (stage, round) order
+        // = ascending inner index k, so the fold order equals the serial reference's.
+        const auto t0 = Clock::now();
+        std::stable_sort(kept.begin(), kept.end(), [](const Kept& x, const Kept& y) {
+          return x.stage != y.stage ? x.stage < y.stage : x.round < y.round;
+        });
+        std::vector<spg_dcsr> bs, as;
+        std::vector<int64_t> shift;
+        std::vector<DBuf<int64_t>> empties;  // zero rowptrs for panels that were not broadcast
+        int64_t off = 0;
+        for (auto& k : kept) {
+          auto empty_view = [&](int64_t rows, int64_t cols) {
+            empties.emplace_back(c, rows + 1);
+            SPG_CUDA(cudaMemsetAsync(empties.back().p, 0, sizeof(int64_t) * (rows + 1), c->stream));
+            spg_dcsr v{rows, cols, 0, empties.back().p, nullptr, nullptr};
+            return v;
+          };
+          bs.push_back(k.b.present ? k.b.view : empty_view(block_cols, k.a_rows));
+          as.push_back(k.a.present ? k.a.view : empty_view(k.a_rows, block_rows));
+          shift.push_back(off);
+          off += k.a_rows;
+        }
+        spg_dcsr L{}, R{};
+        if (!kept.empty()) {
+          concat_cols(c, (int)bs.size(), bs.data(), shift.data(), vs, &L);
+          concat_rows(c, (int)as.size(), as.data(), block_rows, vs, &R);
+        }
+        kept.clear();  // panel buffers are released (stream-ordered) once copied
+        empties.clear();
+        struct OwnedLR {
+          spg_ctx* c;
+          spg_dcsr *l, *r;
+          ~OwnedLR() {
+            free_dcsr(c, l);
+            free_dcsr(c, r);
+          }
+        } own_lr{c, &L, &R};
+        spg_mult_stats ms{};
+        spg_dcsr ct{};
+        if (L.nrows == 0 && R.nrows == 0) {
+          L.nrows = block_cols;
+        }
+        if (off == 0) {  // no inner dimension: empty product
+          ct.nrows = block_cols;
+          ct.ncols = block_rows;
+          ct.ptr = dalloc<int64_t>(c, block_cols + 1);
+          ct.idx = dalloc<int32_t>(c, 1);
+          ct.vals = dalloc<char>(c, vs);
+          SPG_CUDA(cudaMemsetAsync(ct.ptr, 0, sizeof(int64_t) * (block_cols + 1), c->stream));
+        } else {
+          ops->local_multiply(c, &L, &R, &ct, &ms);
+          ++led.local_multiply_calls;
+        }
+        led.products += ms.products;
+        *c_out = ct;
         c_out->nrows = block_rows;
         c_out->ncols = block_cols;
-        c_out->nnz = 0;
-        c_out->ptr = dalloc<int64_t>(c, block_cols + 1);
-        c_out->idx = dalloc<int32_t>(c, 1);
-        c_out->vals = dalloc<char>(c, vs);
-        SPG_CUDA(cudaMemsetAsync(c_out->ptr, 0, sizeof(int64_t) * (block_cols + 1), c->stream));
-      } else if (parts.size() == 1) {
-        // a single partial already is the CSR of C^T == CSC of C
-        *c_out = parts[0].m;
-        c_out->nrows = block_rows;
-        c_out->ncols = block_cols;
-        parts.clear();
+        SPG_CUDA(cudaStreamSynchronize(c->stream));
+        led.ms[2] += ms_since(t0);
       } else {
-        std::vector<spg_dcsr> ps;
-        for (auto& p : parts) ps.push_back(p.m);
-        spg_dcsr out{};
-        ops->merge(c, (int)ps.size(), ps.data(), block_cols, block_rows, &out, nullptr);
-        out.nrows = block_rows;
-        out.ncols = block_cols;
-        *c_out = out;
-        free_parts();
+        // merge (summa.hpp:325-328), stage-major / round-minor
+        const auto t0 = Clock::now();
+        std::stable_sort(parts.begin(), parts.end(), [](const Part& x, const Part& y) {
+          return x.stage != y.stage ? x.stage < y.stage : x.round < y.round;
+        });
+        if (parts.empty()) {
+          c_out->nrows = block_rows;
+          c_out->ncols = block_cols;
+          c_out->nnz = 0;
+          c_out->ptr = dalloc<int64_t>(c, block_cols + 1);
+          c_out->idx = dalloc<int32_t>(c, 1);
+          c_out->vals = dalloc<char>(c, vs);
+          SPG_CUDA(cudaMemsetAsync(c_out->ptr, 0, sizeof(int64_t) * (block_cols + 1), c->stream));
+        } else if (parts.size() == 1) {
+          // a single partial already is the CSR of C^T == CSC of C
+          *c_out = parts[0].m;
+          c_out->nrows = block_rows;
+          c_out->ncols = block_cols;
+          parts.clear();
+        } else {
+          std::vector<spg_dcsr> ps;
+          for (auto& p : parts) ps.push_back(p.m);
+          spg_dcsr out{};
+          ops->merge(c, (int)ps.size(), ps.data(), block_cols, block_rows, &out, nullptr);
+          out.nrows = block_rows;
+          out.ncols = block_cols;
+          *c_out = out;
+          free_parts();
+        }
+        SPG_CUDA(cudaStreamSynchronize(c->stream));
+        led.ms[3] += ms_since(t0);
       }
-      SPG_CUDA(cudaStreamSynchronize(c->stream));
-      led.ms[3] += ms_since(t0);
     } catch (...) {
       free_parts();
       throw;

@@ -73,3 +73,16 @@ def coo_to_csr_fast(m: CooMatrix, to_csc: bool = False):
                              rows.ctypes.data_as(C.POINTER(C.c_int64)), cols.ctypes.data_as(C.POINTER(C.c_int64)),
                              vals.ctypes.data_as(C.c_void_p), int(to_csc), C.byref(out)))
     return take_hcsr(m.sr, out, to_csc)
+
+
+def permute_symmetric(m: CooMatrix, seed: int) -> CooMatrix:
+    """Relabel vertices by a seeded random permutation p: A' = P A P^T
+    (entry (i, j) -> (p[i], p[j])), re-normalised row-major.  Work and output
+    size of A'.A' equal those of A.A; CombBLAS applies the same relabeling to
+    balance R-MAT blocks across a process grid."""
+    if m.nrows != m.ncols:
+        raise ValueError("symmetric permutation needs a square matrix")
+    perm = np.random.default_rng(seed).permutation(m.nrows).astype(np.int64)
+    r, c = perm[m.rows], perm[m.cols]
+    order = np.lexsort((c, r))
+    return CooMatrix(m.sr, m.nrows, m.ncols, r[order], c[order], m.values[order])

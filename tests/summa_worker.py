@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--mode", type=int, default=2)
     ap.add_argument("--threshold", type=int, default=1 << 14)
     ap.add_argument("--staging", type=int, default=1 << 16)
+    ap.add_argument("--fuse", type=int, default=1)
     args = ap.parse_args()
 
     import torch.distributed as dist
@@ -53,7 +54,7 @@ def main():
     ctx = Context(local)
     comm = Comm(job[0], world, rank, pr, pc, local, staging_bytes=args.staging)
     c, led = summa25_multiply(comm, ctx, blk, blk, n, n, n, two_round=bool(args.two_round), mode=args.mode,
-                              threshold=args.threshold)
+                              threshold=args.threshold, fuse_stages=bool(args.fuse))
     part = checksum_part(c, blk.rows[0], blk.cols[0])
     got = c.download()  # CSC of the C block
 
@@ -86,7 +87,7 @@ def main():
         allok = all(int(p[2]) for p in parts)
         cs_ok = total == want or args.sr == 0  # fp64 values hash bitwise
         print(f"[summa_worker] grid {pr}x{pc} sr={args.sr} s{args.scale} two_round={args.two_round} "
-              f"mode={args.mode}: blocks_ok={allok} checksum_ok={cs_ok} ledger0={led}", flush=True)
+              f"mode={args.mode} fuse={args.fuse}: blocks_ok={allok} checksum_ok={cs_ok} ledger0={led}", flush=True)
         if not (allok and cs_ok):
             sys.exit(1)
     comm.close()

@@ -25,11 +25,12 @@ def run_worker(nproc, *args, timeout=600):
     return p.stdout
 
 
-@pytest.mark.parametrize("sr,mode,two_round", [(4, 2, 1), (2, 0, 1), (1, 1, 0), (0, 2, 1), (5, 2, 0)])
-def test_summa_all_gpus(sr, mode, two_round):
+@pytest.mark.parametrize("sr,mode,two_round,fuse", [(4, 2, 1, 1), (4, 2, 1, 0), (2, 0, 1, 1), (1, 1, 0, 0),
+                                                     (0, 2, 1, 1), (5, 2, 0, 1), (2, 2, 0, 0)])
+def test_summa_all_gpus(sr, mode, two_round, fuse):
     n = ngpus()
     nproc = 8 if n >= 8 else 4 if n >= 4 else 2 if n >= 2 else 1
-    out = run_worker(nproc, "--sr", sr, "--scale", 10, "--mode", mode, "--two-round", two_round)
+    out = run_worker(nproc, "--sr", sr, "--scale", 10, "--mode", mode, "--two-round", two_round, "--fuse", fuse)
     assert "blocks_ok=True checksum_ok=True" in out
 
 
