@@ -412,7 +412,7 @@ def main():
     ap.add_argument("--scale", type=int, default=18)
     ap.add_argument("--ef", type=float, default=16.0)
     ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-products", type=float, default=0.0,
                     help="products in the CPU sample (default: 3e7 per host core, at most 1e9)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

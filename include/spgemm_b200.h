@@ -135,7 +135,8 @@ SPG_API int spg_dcsr_alloc(spg_ctx* ctx, int sr, int64_t nrows, int64_t ncols, i
 SPG_API int spg_dcsr_free(spg_ctx* ctx, spg_dcsr* m);
 /* H2D of a host CSR (or CSC) with int64 -> int32 index narrowing on device */
 SPG_API int spg_upload(spg_ctx* ctx, int sr, const spg_hcsr* h, int is_csc, spg_dcsr* out);
-/* D2H into library-allocated host arrays (free with spg_hcsr_free) */
+/* D2H into library-allocated host arrays (pinned, recycled by the library:
+ * release with spg_hcsr_free, or each array with spg_free) */
 SPG_API int spg_download(spg_ctx* ctx, int sr, const spg_dcsr* d, int is_csc, spg_hcsr* out);
 SPG_API void spg_hcsr_free(spg_hcsr* h);
 
@@ -198,7 +199,7 @@ SPG_API int spg_generate_stencil27(int sr, int64_t N, int64_t* nrows, int64_t* n
  * the reference's fold semantics needed (input already unique). */
 SPG_API int spg_coo_to_csr(int sr, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rows,
                            const int64_t* cols, const void* vals, int to_csc, spg_hcsr* out);
-SPG_API void spg_free(void* p);
+SPG_API void spg_free(void* p); /* any host array returned by the library */
 
 /* ------------------------------------------------ distributed (SUMMA) */
 /* Grid helpers: block_range (dist_matrix.hpp:23-28), round_range

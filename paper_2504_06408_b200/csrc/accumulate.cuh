@@ -760,6 +760,22 @@ __device__ __forceinline__ void balanced_items(const Src& src, const SegCache<SR
 // the fold can cancel back to zero() (fp64 +), which a pre-pass handles.
 // Returns the number of entries written.
 // ---------------------------------------------------------------------------
+// Position of the k-th (0-based) set bit of x (k < popc(x)); popc bisection.
+__device__ __forceinline__ int nth_set_bit(uint32_t x, int k) {
+  int pos = 0;
+  int c = __popc(x & 0xffffu);
+  if (k >= c) { k -= c; pos += 16; x >>= 16; }
+  c = __popc(x & 0xffu);
+  if (k >= c) { k -= c; pos += 8; x >>= 8; }
+  c = __popc(x & 0xfu);
+  if (k >= c) { k -= c; pos += 4; x >>= 4; }
+  c = __popc(x & 0x3u);
+  if (k >= c) { k -= c; pos += 2; x >>= 2; }
+  c = (int)(x & 1u);
+  if (k >= c) pos += 1;
+  return pos;
+}
+
 template <class SR>
 struct AddCanCancel {
   static constexpr bool value = SR::id == 0;  // arithmetic (+, x): a + (-a) == 0
@@ -840,7 +856,7 @@ __device__ __forceinline__ int bitmap_emit(typename SR::value_type* acc, uint32_
       const uint32_t xo = __shfl_sync(kFull, x, own);
       const int eo = __shfl_sync(kFull, excl, own);
       if (q < total) {
-        const int bit = (int)__fns(xo, 0, q - eo + 1);
+        const int bit = nth_set_bit(xo, q - eo);
         const int cc = ((w0 + it * 32 + own) << 5) + bit;
         const V v = acc[cc];
         out_cols[pos + q] = col_base + cc;

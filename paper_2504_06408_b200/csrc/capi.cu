@@ -6,6 +6,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -100,21 +102,100 @@ void upload(spg_ctx* c, int vs, const spg_hcsr* h, int is_csc, spg_dcsr* d) {
   }
 }
 
+// Caching allocator of pinned host memory for results (D2H at full PCIe
+// speed; page-locking tens of GB per call would cost seconds).  Blocks are
+// recycled by size class; anything not from the cache is plain malloc.
+struct PinnedCache {
+  std::mutex mu;
+  std::multimap<size_t, void*> free_blocks;
+  std::map<void*, size_t> live;
+  size_t cached_bytes = 0;
+
+  static size_t round_up(size_t n) {
+    size_t c = 1 << 20;
+    while (c < n) c <<= 1;
+    return c;
+  }
+  void* get(size_t n) {
+    const size_t cls = round_up(std::max<size_t>(n, 1));
+    {
+      std::lock_guard<std::mutex> g(mu);
+      auto it = free_blocks.lower_bound(cls);
+      if (it != free_blocks.end() && it->first == cls) {
+        void* p = it->second;
+        free_blocks.erase(it);
+        cached_bytes -= cls;
+        live[p] = cls;
+        return p;
+      }
+    }
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, cls, cudaHostAllocPortable) != cudaSuccess) {
+      cudaGetLastError();
+      p = std::malloc(n);  // fall back to pageable memory
+      if (!p) fail(SPG_ERR_OOM, "host allocation failed");
+      return p;
+    }
+    std::lock_guard<std::mutex> g(mu);
+    live[p] = cls;
+    return p;
+  }
+  // returns true when p was a cached pinned block
+  bool put(void* p) {
+    if (!p) return true;
+    std::lock_guard<std::mutex> g(mu);
+    auto it = live.find(p);
+    if (it == live.end()) return false;
+    const size_t cls = it->second;
+    live.erase(it);
+    // keep at most 64 GB cached; release the rest
+    if (cached_bytes + cls > (size_t(64) << 30)) {
+      cudaFreeHost(p);
+      return true;
+    }
+    free_blocks.emplace(cls, p);
+    cached_bytes += cls;
+    return true;
+  }
+};
+
+PinnedCache& pinned() {
+  static PinnedCache* pc = new PinnedCache();  // intentionally leaked: outlives late frees
+  return *pc;
+}
+
+void host_release(void* p) {
+  if (!pinned().put(p)) std::free(p);
+}
+
+__global__ void widen_into_kernel(const int32_t* __restrict__ in, int64_t* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+
 void download(spg_ctx* c, int vs, const spg_dcsr* d, int is_csc, spg_hcsr* h) {
   const int64_t nseg = is_csc ? d->ncols : d->nrows;
   h->nrows = d->nrows;
   h->ncols = d->ncols;
   h->nnz = d->nnz;
-  h->ptr = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * (nseg + 1)));
-  h->idx = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * std::max<int64_t>(d->nnz, 1)));
-  h->vals = std::malloc((size_t)vs * std::max<int64_t>(d->nnz, 1));
-  if (!h->ptr || !h->idx || !h->vals) fail(SPG_ERR_OOM, "host allocation failed");
+  h->ptr = static_cast<int64_t*>(pinned().get(sizeof(int64_t) * (nseg + 1)));
+  h->idx = static_cast<int64_t*>(pinned().get(sizeof(int64_t) * std::max<int64_t>(d->nnz, 1)));
+  h->vals = pinned().get((size_t)vs * std::max<int64_t>(d->nnz, 1));
   SPG_CUDA(cudaMemcpyAsync(h->ptr, d->ptr, sizeof(int64_t) * (nseg + 1), cudaMemcpyDeviceToHost, c->stream));
   if (d->nnz > 0) {
-    DBuf<int64_t> wide(c, d->nnz);
-    widen_indices(c, d->idx, wide.p, d->nnz);
-    SPG_CUDA(cudaMemcpyAsync(h->idx, wide.p, sizeof(int64_t) * d->nnz, cudaMemcpyDeviceToHost, c->stream));
+    // values first (overlaps the widening kernel), then indices widened to
+    // the reference's int64 on device in chunks
     SPG_CUDA(cudaMemcpyAsync(h->vals, d->vals, (size_t)vs * d->nnz, cudaMemcpyDeviceToHost, c->stream));
+    const int64_t chunk = int64_t(1) << 28;
+    DBuf<int64_t> wide(c, (size_t)std::min<int64_t>(chunk, d->nnz));
+    for (int64_t o = 0; o < d->nnz; o += chunk) {
+      const int64_t n = std::min<int64_t>(chunk, d->nnz - o);
+      widen_into_kernel<<<std::min<int64_t>((n + 255) / 256, (int64_t)c->sm_count * 16), 256, 0, c->stream>>>(
+          d->idx + o, wide.p, n);
+      SPG_LAUNCH_CHECK();
+      ++c->launches;
+      SPG_CUDA(cudaMemcpyAsync(h->idx + o, wide.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->stream));
+    }
   }
   SPG_CUDA(cudaStreamSynchronize(c->stream));
 }
@@ -272,9 +353,9 @@ int spg_download(spg_ctx* c, int sr, const spg_dcsr* d, int is_csc, spg_hcsr* ou
 
 void spg_hcsr_free(spg_hcsr* h) {
   if (!h) return;
-  std::free(h->ptr);
-  std::free(h->idx);
-  std::free(h->vals);
+  host_release(h->ptr);
+  host_release(h->idx);
+  host_release(h->vals);
   h->ptr = nullptr;
   h->idx = nullptr;
   h->vals = nullptr;
@@ -533,7 +614,7 @@ int spg_coo_to_csr(int sr, int64_t nrows, int64_t ncols, int64_t nnz, const int6
   });
 }
 
-void spg_free(void* p) { std::free(p); }
+void spg_free(void* p) { host_release(p); }
 
 void spg_block_range(int64_t n, int q, int idx, int64_t* begin, int64_t* end) {
   // dist_matrix.hpp:23-28: larger ranges first

@@ -81,15 +81,40 @@ def copy_out(ptr, n: int, dt) -> np.ndarray:
     return raw.copy().view(dt)
 
 
+class _HostBlock:
+    """Owns one library-allocated host array (pinned, recycled on release)."""
+
+    __slots__ = ("ptr", "__array_interface__")
+
+    def __init__(self, ptr, nbytes):
+        self.ptr = ptr
+        self.__array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3}
+
+    def __del__(self):
+        if self.ptr:
+            lib.spg_free(C.c_void_p(self.ptr))
+            self.ptr = None
+
+
+def view_owned(ptr, n: int, dt) -> np.ndarray:
+    """Zero-copy numpy view of n values at a library-allocated pointer; the
+    memory returns to the library when the array is garbage collected."""
+    dt = np.dtype(dt)
+    addr = C.cast(ptr, C.c_void_p).value
+    if not addr:
+        return np.zeros(n, dtype=dt)
+    raw = np.asarray(_HostBlock(addr, max(n, 1) * dt.itemsize))
+    return raw[: n * dt.itemsize].view(dt)
+
+
 def take_hcsr(sr, h: HCsr, is_csc: bool):
-    """Copy a library-allocated spg_hcsr into numpy and free it."""
+    """Wrap a library-allocated spg_hcsr as numpy arrays (zero copy)."""
     nseg = h.ncols if is_csc else h.nrows
-    ptr = np.ctypeslib.as_array(h.ptr, shape=(nseg + 1,)).copy()
     nnz = int(h.nnz)
-    idx = np.ctypeslib.as_array(h.idx, shape=(max(nnz, 1),))[:nnz].copy()
     dt = dtype_of(sr)
-    vals = copy_out(h.vals, nnz, dt)
-    lib.spg_hcsr_free(C.byref(h))
+    ptr = view_owned(h.ptr, nseg + 1, np.int64)
+    idx = view_owned(h.idx, nnz, np.int64)
+    vals = view_owned(h.vals, nnz, dt)
     if is_csc:
         return CscMatrix(int(as_id(sr)), int(h.nrows), int(h.ncols), ptr, idx, vals)
     return CsrMatrix(int(as_id(sr)), int(h.nrows), int(h.ncols), ptr, idx, vals)
