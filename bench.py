@@ -299,7 +299,9 @@ def run_summa(args):
     pr, pc = grid_for(world)
     i, j = rank // pc, rank % pc
     mode = {"host": HOST_ONLY, "device": DEVICE_ONLY, "hybrid": HYBRID}[args.comm]
-    thr = args.threshold if args.threshold >= 0 else int(os.environ.get("SPG_HYBRID_THRESHOLD", 1 << 18))
+    from paper_2504_06408_b200.summa import measured_threshold
+    thr = args.threshold if args.threshold >= 0 else measured_threshold(pc)      # row scope: fanout pc
+    thr_col = args.threshold if args.threshold >= 0 else measured_threshold(pr)  # column scope: fanout pr
 
     coo = generators.generate_rmat(4, args.scale, args.ef, args.seed)
     if args.permute:
@@ -315,7 +317,7 @@ def run_summa(args):
 
     def step():
         c, led = summa25_multiply(comm, ctx, blk, blk, n, n, n, two_round=not args.one_round, mode=mode,
-                                  threshold=thr, fuse_stages=not args.no_fuse)
+                                  threshold=thr, threshold_col=thr_col, fuse_stages=not args.no_fuse)
         return c, led
 
     for _ in range(args.warmup):
@@ -379,7 +381,9 @@ def run_summa(args):
                        "grid": f"{pr}x{pc}", "permuted": bool(args.permute), "two_round": not args.one_round,
                        "fuse_stages": not args.no_fuse,
                        "comm": args.comm,
-                       "threshold_bytes": thr, "products": F, "nnz_C": int(agg[1]), "checksum_C": csum,
+                       "threshold_bytes": {"row_scope": thr, "col_scope": thr_col,
+                                           "source": "measured crossover (profiles/comm_fanout*.json)"},
+                       "products": F, "nnz_C": int(agg[1]), "checksum_C": csum,
                        "time_to_C_ms": ms, "steps_ms_max_over_ranks": [round(float(x), 2) for x in t],
                        "rank0_ledger": led0,
                        "per_rank_ms": [{"event": round(float(x[0]), 2), "ledger_total": round(float(x[1]), 2),

@@ -237,6 +237,8 @@ typedef struct {
   int two_round;      /* SummaOptions::two_round (summa.hpp:174-177) */
   int comm_mode;      /* CommConfig::mode (comm.hpp:36-39) */
   uint64_t threshold; /* CommConfig::threshold_bytes */
+  uint64_t threshold_col; /* threshold for the grid-column scope (fanout pr); 0 = same as threshold
+                             (which then applies to both scopes; the row scope has fanout pc) */
   int fuse_stages;    /* 1: keep every received panel and run ONE fused local multiply over the
                          concatenated panels (no partials, no merge; fold order = ascending k);
                          0: the reference's per-stage multiplies + merge_partials */

@@ -290,7 +290,7 @@ CscMatrix<SR> summa25_multiply(Comm& comm, Context& ctx, index_t a_nrows, index_
                                const CommConfig& cfg = {}, const SummaOptions& opts = {},
                                spg_ledger* ledger = nullptr) {
   spg_hcsr ha = detail::view_csc(a_block), hb = detail::view_csc(b_block);
-  spg_summa_opts o{opts.two_round ? 1 : 0, static_cast<int>(cfg.mode), cfg.threshold_bytes,
+  spg_summa_opts o{opts.two_round ? 1 : 0, static_cast<int>(cfg.mode), cfg.threshold_bytes, 0,
                    opts.fuse_stages ? 1 : 0};
   spg_dcsr c{};
   ctx.check(spg_summa25_multiply(comm.get(), ctx.get(), SR::id, a_nrows, a_ncols, b_ncols, &ha, nullptr, &hb,

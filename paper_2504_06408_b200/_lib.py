@@ -56,7 +56,7 @@ class Stage(C.Structure):
 
 class SummaOpts(C.Structure):
     _fields_ = [("two_round", C.c_int), ("comm_mode", C.c_int), ("threshold", C.c_uint64),
-                ("fuse_stages", C.c_int)]
+                ("threshold_col", C.c_uint64), ("fuse_stages", C.c_int)]
 
 
 class Ledger(C.Structure):

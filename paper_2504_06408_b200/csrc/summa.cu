@@ -100,7 +100,8 @@ void broadcast_panel(spg_ctx* c, spg_comm* comm, int scope, int root, bool by_ro
     p.buf = DBuf<char>(c, p.bytes);
     p.view = panel_view(p.buf.p, triple[0], triple[1], triple[2]);
   }
-  const int path = comm_bcast(comm, scope, root, p.buf.p, p.bytes, o.comm_mode, o.threshold, c->stream, true);
+  const uint64_t thr = (scope == SPG_SCOPE_COL && o.threshold_col) ? o.threshold_col : o.threshold;
+  const int path = comm_bcast(comm, scope, root, p.buf.p, p.bytes, o.comm_mode, thr, c->stream, true);
   if (path == SPG_PATH_HOST) {
     ++led.host_bcasts;
     led.bytes_host_path += p.bytes;

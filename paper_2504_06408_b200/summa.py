@@ -132,7 +132,7 @@ class Comm:
 
 def summa25_multiply(comm: Comm, ctx: Context, a_block: LocalBlock, b_block: LocalBlock, a_nrows: int,
                      a_ncols: int, b_ncols: int, two_round: bool = True, mode: int = HYBRID,
-                     threshold: int = 0, sr=None, fuse_stages: bool = True):
+                     threshold: int = 0, sr=None, fuse_stages: bool = True, threshold_col: int = 0):
     """One rank's summa25_multiply.  Returns (C block as DeviceCsr CSC, ledger dict).
 
     fuse_stages=True keeps every received panel and runs one fused local
@@ -141,7 +141,7 @@ def summa25_multiply(comm: Comm, ctx: Context, a_block: LocalBlock, b_block: Loc
     sr = as_id(sr if sr is not None else a_block.storage.sr)
     ah, ad, ka = _block_structs(a_block)
     bh, bd, kb = _block_structs(b_block)
-    opts = SummaOpts(int(two_round), int(mode), int(threshold), int(fuse_stages))
+    opts = SummaOpts(int(two_round), int(mode), int(threshold), int(threshold_col), int(fuse_stages))
     out = DCsr()
     led = Ledger()
     rc = lib.spg_summa25_multiply(comm.handle, ctx.handle, int(sr), int(a_nrows), int(a_ncols), int(b_ncols),
@@ -162,3 +162,23 @@ def checksum_part(c: DeviceCsr, row_off: int, col_off: int) -> int:
 
 def checksum_seed(nrows: int, ncols: int) -> int:
     return int(lib.spg_checksum_seed(int(nrows), int(ncols)))
+
+
+def measured_threshold(fanout: int, default: int = 64 << 10) -> int:
+    """Hybrid threshold for a scope of `fanout` ranks: the crossover measured on
+    the box by tools/comm_sweep.py (profiles/comm_fanout<f>.json); the nearest
+    measured fanout is used when the exact one is missing."""
+    import json
+    import os
+    root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles")
+    best = None
+    for f in os.listdir(root) if os.path.isdir(root) else []:
+        if f.startswith("comm_fanout") and f.endswith(".json"):
+            try:
+                k = int(f[len("comm_fanout"):-len(".json")])
+                x = json.load(open(os.path.join(root, f)))["sweep"]["crossover_bytes"]
+            except (ValueError, KeyError, OSError):
+                continue
+            if x and (best is None or abs(k - fanout) < abs(best[0] - fanout)):
+                best = (k, int(x))
+    return best[1] if best else default

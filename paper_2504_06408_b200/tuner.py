@@ -1,0 +1,140 @@
+"""Measured hybrid-communication tuning (replaces the reference's modelled
+tuner: tuner.hpp:17-117 and latency_model.hpp:21-185).
+
+The reference prices the host and device broadcast paths with synthetic
+log-log latency curves; here the curves are MEASURED on the box through the
+real transports (`spg_bcast`: pinned shared-memory staging vs NCCL over
+NVLink), stored in the reference's JSON curve format, and the threshold is
+the measured crossover (`find_crossover`, same bisection contract).
+"""
+from __future__ import annotations
+
+import json
+import math
+import time
+from typing import Dict, List, Optional, Sequence, Tuple
+
+Curve = List[Tuple[float, float]]  # (bytes, seconds), strictly increasing bytes
+
+
+def curve_at(curve: Curve, nbytes: float) -> float:
+    """LatencyCurve::at (latency_model.hpp:44-55): piecewise-linear in log-log,
+    extrapolated by the end segments."""
+    if len(curve) < 2:
+        raise ValueError("latency curve needs at least two sample points")
+    x = math.log(max(nbytes, 1.0))
+    hi = 1
+    while hi + 1 < len(curve) and math.log(curve[hi][0]) < x:
+        hi += 1
+    x0, x1 = math.log(curve[hi - 1][0]), math.log(curve[hi][0])
+    y0, y1 = math.log(curve[hi - 1][1]), math.log(curve[hi][1])
+    return math.exp(y0 + (x - x0) / (x1 - x0) * (y1 - y0))
+
+
+def find_crossover(host, device, lo: int = 1, hi: int = 1 << 30) -> Optional[int]:
+    """find_crossover (tuner.hpp:17-39): smallest size in [lo, hi] where the
+    host path stops being cheaper than the device path (1-byte bisection);
+    None when there is no sign change in range.  `host`/`device` are curves
+    or callables bytes -> seconds (the model's *_path_total)."""
+    if lo >= hi:
+        raise ValueError("find_crossover needs lo < hi")
+    hf = host if callable(host) else (lambda b: curve_at(host, b))
+    df = device if callable(device) else (lambda b: curve_at(device, b))
+
+    def host_minus_device(b):
+        return hf(b) - df(b)
+
+    if host_minus_device(lo) >= 0.0 or host_minus_device(hi) < 0.0:
+        return None
+    while hi - lo > 1:
+        mid = lo + (hi - lo) // 2
+        if host_minus_device(mid) >= 0.0:
+            hi = mid
+        else:
+            lo = mid
+    return hi
+
+
+def default_threshold_ladder(crossover: Optional[int]) -> List[int]:
+    """default_threshold_ladder (tuner.hpp:101-117): 0, s*/32..s*/2, s*..16 s*, inf."""
+    star = crossover if crossover else 1 << 16
+    ladder = [0]
+    for shift in range(5, 0, -1):
+        t = star >> shift
+        if t > 0 and t != ladder[-1]:
+            ladder.append(t)
+    for shift in range(0, 5):
+        t = star << shift
+        if t != ladder[-1]:
+            ladder.append(t)
+    ladder.append((1 << 64) - 1)
+    return ladder
+
+
+def to_reference_json(curves: Dict[str, Curve]) -> dict:
+    """The reference's model file layout (latency_model.hpp:135-148)."""
+    return {"curves": {k: [[float(b), float(t)] for b, t in v] for k, v in curves.items()}}
+
+
+def measure_bcast_curves(comm, sizes: Sequence[int], reps: int = 10, scope: int = 0,
+                         barrier=None, reduce_max=None, device: int = 0) -> Dict[str, Curve]:
+    """Times spg_bcast on this rank's `scope` (0 = grid row, 1 = grid column)
+    for every size through each path: the host path (root D2H into pinned
+    shared memory, peers H2D, pipelined) and the device path (NCCL broadcast
+    over NVLink).  Each sample is the max over ranks of the median of `reps`
+    runs (reduce_max combines across ranks).  Also times plain pinned D2H/H2D
+    copies (the model's copy curves).  Returns curves keyed like the reference
+    model plus `host_path_total` / `device_path_total`."""
+    import torch
+
+    from .summa import DEVICE_ONLY, HOST_ONLY
+
+    buf = torch.empty(max(sizes), dtype=torch.uint8, device=f"cuda:{device}")
+    pinned = torch.empty(max(sizes), dtype=torch.uint8, pin_memory=True)
+    out: Dict[str, Curve] = {"host_path_total": [], "device_path_total": [], "copy_d2h": [], "copy_h2d": []}
+    for nbytes in sizes:
+        for key, mode in (("host_path_total", HOST_ONLY), ("device_path_total", DEVICE_ONLY)):
+            ts = []
+            for r in range(reps + 2):
+                torch.cuda.synchronize()
+                if barrier:
+                    barrier()
+                t0 = time.perf_counter()
+                comm.bcast(scope, 0, buf.data_ptr(), nbytes, mode=mode, threshold=0)
+                torch.cuda.synchronize()
+                if r >= 2:
+                    ts.append(time.perf_counter() - t0)
+            med = sorted(ts)[len(ts) // 2]
+            out[key].append((float(nbytes), reduce_max(med) if reduce_max else med))
+        for key, fn in (("copy_d2h", lambda n: pinned[:n].copy_(buf[:n], non_blocking=True)),
+                        ("copy_h2d", lambda n: buf[:n].copy_(pinned[:n], non_blocking=True))):
+            ts = []
+            for r in range(reps + 2):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                fn(nbytes)
+                torch.cuda.synchronize()
+                if r >= 2:
+                    ts.append(time.perf_counter() - t0)
+            out[key].append((float(nbytes), sorted(ts)[len(ts) // 2]))
+    # reference-format curves: host_bcast is what remains of the host path
+    # after the two staging copies (latency_model.hpp:104-106), floored at 1 ns
+    out["host_bcast"] = [(b, max(t - d - h, 1e-9)) for (b, t), (_, d), (_, h) in
+                         zip(out["host_path_total"], out["copy_d2h"], out["copy_h2d"])]
+    out["device_bcast"] = list(out["device_path_total"])
+    for k in out:  # the reference requires non-decreasing latencies
+        pts, best = [], 0.0
+        for b, t in out[k]:
+            best = max(best, t)
+            pts.append((b, best))
+        out[k] = pts
+    return out
+
+
+def save_model(path: str, curves: Dict[str, Curve], extra: dict | None = None):
+    doc = to_reference_json({k: curves[k] for k in ("host_bcast", "device_bcast", "copy_h2d", "copy_d2h")})
+    doc["measured"] = {k: [[b, t] for b, t in curves[k]] for k in ("host_path_total", "device_path_total")}
+    if extra:
+        doc.update(extra)
+    with open(path, "w") as f:
+        json.dump(doc, f, indent=1)
