@@ -230,6 +230,8 @@ def run_single(args):
     achieved = balg / (ms * 1e-3) / 1e9
 
     # e2e: reference-shaped host call esc_multiply(A, A): H2D, multiply, D2H of C
+    from paper_2504_06408_b200.device import pin
+    unpin = pin(a.rowptr, a.colids, a.values)  # inputs in pinned host memory
     e2e_times = []
     h2d = 2 * (8 * (a.nrows + 1) + 8 * a.nnz + vs * a.nnz)
     d2h = 8 * (a.nrows + 1) + (8 + vs) * nnz_c
@@ -240,6 +242,7 @@ def run_single(args):
         assert ch.nnz == nnz_c
         del ch
     e2e_s = float(np.median(e2e_times)) if e2e_times else float("nan")
+    unpin()
 
     cpu = None
     if not args.no_cpu_baseline:
@@ -296,7 +299,9 @@ def run_summa(args):
     dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=600))
     job = [uuid.uuid4().hex[:12] if rank == 0 else None]
     dist.broadcast_object_list(job, src=0)
-    pr, pc = grid_for(world)
+    pr, pc = (int(x) for x in args.grid.split("x")) if args.grid else grid_for(world)
+    if pr * pc != world:
+        raise SystemExit(f"--grid {args.grid} does not hold {world} ranks")
     i, j = rank // pc, rank % pc
     mode = {"host": HOST_ONLY, "device": DEVICE_ONLY, "hybrid": HYBRID}[args.comm]
     from paper_2504_06408_b200.summa import measured_threshold
@@ -309,6 +314,14 @@ def run_summa(args):
     n = coo.nrows
     blk = local_block(coo, pr, pc, i, j)
     del coo
+    from paper_2504_06408_b200.device import pin
+    st = blk.storage
+    arrays = [getattr(st, k) for k in ("colptr", "jc", "cp", "rowids", "values") if hasattr(st, k)]
+    arrays = [np.ascontiguousarray(x) for x in arrays]
+    for k in ("colptr", "jc", "cp", "rowids", "values"):
+        if hasattr(st, k):
+            setattr(st, k, arrays.pop(0))
+    unpin = pin(*[getattr(st, k) for k in ("colptr", "jc", "cp", "rowids", "values") if hasattr(st, k)])
     stream = torch.cuda.current_stream()
     ctx = Context(local)
     check(lib.spg_ctx_set_stream(ctx.handle, C.c_void_p(stream.cuda_stream)), ctx.handle)
@@ -400,6 +413,7 @@ def run_summa(args):
         }
         print(json.dumps(line), flush=True)
     comm.close()
+    unpin()
     dist.barrier()
     dist.destroy_process_group()
 
@@ -427,6 +441,7 @@ def main():
                     help="use the generator's vertex order (default: relabel vertices by a seeded random "
                          "permutation, as CombBLAS does, so grid blocks carry equal work; F and nnz(C) unchanged)")
     ap.add_argument("--comm", default="hybrid", choices=["host", "device", "hybrid"])
+    ap.add_argument("--grid", default="", help="PRxPC process grid (default 1x1/1x2/2x2/2x4 by GPU count)")
     ap.add_argument("--threshold", type=int, default=-1, help="hybrid threshold bytes (-1: measured default)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup

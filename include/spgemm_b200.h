@@ -126,7 +126,8 @@ SPG_API void* spg_ctx_stream(spg_ctx* ctx);                 /* cudaStream_t */
 SPG_API int spg_ctx_set_stream(spg_ctx* ctx, void* stream); /* borrow a caller stream */
 SPG_API int spg_ctx_sync(spg_ctx* ctx);
 SPG_API uint64_t spg_ctx_kernel_launches(const spg_ctx* ctx);
-/* bytes of device scratch the numeric pass may hold at once (0 = auto: 40% of free HBM) */
+/* bytes of device scratch the single-pass numeric may use (0 = auto: 45% of free
+ * HBM); above it the multiply switches to the exact two-pass mode */
 SPG_API int spg_ctx_set_scratch_budget(spg_ctx* ctx, uint64_t bytes);
 
 /* ---------------------------------------------------- device matrices */
@@ -200,6 +201,10 @@ SPG_API int spg_generate_stencil27(int sr, int64_t N, int64_t* nrows, int64_t* n
 SPG_API int spg_coo_to_csr(int sr, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rows,
                            const int64_t* cols, const void* vals, int to_csc, spg_hcsr* out);
 SPG_API void spg_free(void* p); /* any host array returned by the library */
+/* Page-lock (pin) / unpin caller-owned host memory so uploads run at full
+ * PCIe speed (cudaHostRegister; the caller keeps ownership). */
+SPG_API int spg_host_register(void* p, uint64_t bytes);
+SPG_API int spg_host_unregister(void* p);
 
 /* ------------------------------------------------ distributed (SUMMA) */
 /* Grid helpers: block_range (dist_matrix.hpp:23-28), round_range

@@ -116,6 +116,8 @@ _SIGS = [
     ("spg_coo_to_csr", C.c_int, [C.c_int, C.c_int64, C.c_int64, C.c_int64, _i64p, _i64p, C.c_void_p,
                                  C.c_int, _P(HCsr)]),
     ("spg_free", None, [C.c_void_p]),
+    ("spg_host_register", C.c_int, [C.c_void_p, C.c_uint64]),
+    ("spg_host_unregister", C.c_int, [C.c_void_p]),
     ("spg_block_range", None, [C.c_int64, C.c_int, C.c_int, _i64p, _i64p]),
     ("spg_round_range", None, [C.c_int64, C.c_int, C.c_int, _i64p, _i64p]),
     ("spg_summa_schedule", C.c_int, [C.c_int64, C.c_int, C.c_int, _P(Stage), C.c_int]),

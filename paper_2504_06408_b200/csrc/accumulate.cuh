@@ -40,6 +40,8 @@
 //              very wide C    be mostly empty
 //      every row writes a scratch slot of U_i entries and reports nnz_i
 //   K7 compact : rowptr = scan(nnz); copy scratch -> exact-size CSR
+//   (when the scratch would not fit: a counting pass, exact rowptr, and a
+//    second pass writing straight into C)
 #pragma once
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/block/block_scan.cuh>
@@ -171,17 +173,6 @@ struct MergeSource {
   __device__ __forceinline__ V val(int sid, int64_t u) const { return static_cast<const V*>(p.val[sid])[u]; }
   __device__ __forceinline__ V item(const V&, const V& v) const { return v; }
 };
-
-template <class SR>
-inline void rebase_source(MulSource<SR>& s, int64_t r0) {
-  s.lptr += r0;
-  s.nrows -= r0;
-}
-template <class SR>
-inline void rebase_source(MergeSource<SR>& s, int64_t r0) {
-  for (int q = 0; q < s.nparts; ++q) s.p.ptr[q] += r0;
-  s.nrows -= r0;
-}
 
 // ---------------------------------------------------------------------------
 // Geometry per value width
@@ -444,7 +435,7 @@ __global__ void __launch_bounds__(256) esc_warp_kernel(Src src, const int64_t* _
     const unsigned m = __ballot_sync(kFull, keep);
     const int pos = __popc(m & ((1u << lane) - 1));
     const int64_t o = off[i];
-    if (keep) {
+    if (keep && out_cols) {  // out_cols == nullptr: counting pass
       out_cols[o + pos] = (int32_t)col;
       out_vals[o + pos] = val;
     }
@@ -577,8 +568,10 @@ __global__ void __launch_bounds__(THREADS) esc_block_kernel(Src src, const int64
 #pragma unroll
     for (int q = 0; q < ITEMS; ++q) {
       if (keep[q]) {
-        out_cols[o + kfirst] = (int32_t)k[q];
-        out_vals[o + kfirst] = t[q].v;
+        if (out_cols) {
+          out_cols[o + kfirst] = (int32_t)k[q];
+          out_vals[o + kfirst] = t[q].v;
+        }
         ++kfirst;
       }
     }
@@ -858,9 +851,10 @@ __device__ __forceinline__ int bitmap_emit(typename SR::value_type* acc, uint32_
       if (q < total) {
         const int bit = nth_set_bit(xo, q - eo);
         const int cc = ((w0 + it * 32 + own) << 5) + bit;
-        const V v = acc[cc];
-        out_cols[pos + q] = col_base + cc;
-        out_vals[pos + q] = v;
+        if (out_cols) {
+          out_cols[pos + q] = col_base + cc;
+          out_vals[pos + q] = acc[cc];
+        }
         acc[cc] = SR::zero();
       }
     }
@@ -1064,6 +1058,11 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
     }
     int first, total;
     typename HS::Scan(tmp->scan).ExclusiveSum(cnt, first, total);
+    if (out_cols == nullptr) {  // counting pass: no sort, no output
+      if (threadIdx.x == 0) rownnz[i] = total;
+      __syncthreads();
+      continue;
+    }
     uint32_t my_keys[SPT];
 #pragma unroll
     for (int q = 0; q < SPT; ++q) my_keys[q] = my_slots[q] >= 0 ? (uint32_t)tkeys[my_slots[q]] : 0u;
@@ -1093,7 +1092,7 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
 #pragma unroll
     for (int q = 0; q < ITEMS; ++q) {
       const int e = threadIdx.x * ITEMS + q;
-      if (e < total) {
+      if (e < total && out_cols) {
         out_cols[o + e] = (int32_t)k[q];
         out_vals[o + e] = tvals[sl[q]];
       }

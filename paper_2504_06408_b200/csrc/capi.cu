@@ -616,6 +616,30 @@ int spg_coo_to_csr(int sr, int64_t nrows, int64_t ncols, int64_t nnz, const int6
 
 void spg_free(void* p) { host_release(p); }
 
+int spg_host_register(void* p, uint64_t bytes) {
+  return guarded(nullptr, [&] {
+    if (!p || bytes == 0) return;
+    const cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterPortable);
+    if (e == cudaErrorHostMemoryAlreadyRegistered) {
+      cudaGetLastError();
+      return;
+    }
+    SPG_CUDA(e);
+  });
+}
+
+int spg_host_unregister(void* p) {
+  return guarded(nullptr, [&] {
+    if (!p) return;
+    const cudaError_t e = cudaHostUnregister(p);
+    if (e == cudaErrorHostMemoryNotRegistered) {
+      cudaGetLastError();
+      return;
+    }
+    SPG_CUDA(e);
+  });
+}
+
 void spg_block_range(int64_t n, int q, int idx, int64_t* begin, int64_t* end) {
   // dist_matrix.hpp:23-28: larger ranges first
   const int64_t base = n / q, extra = n % q;

@@ -1,6 +1,7 @@
 // Host driver for the row-accumulation pipeline in accumulate.cuh: runs
-// analyse -> bin -> numeric (row-batched under a scratch budget, bins on
-// concurrent streams) -> compact for any Source, producing an exact CSR.
+// analyse -> bin -> numeric (bins on concurrent streams) -> compact for any
+// Source, producing an exact CSR; falls back to an exact two-pass (count,
+// then write into C) mode when the scratch would exceed the budget.
 #pragma once
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_reduce.cuh>
@@ -149,7 +150,7 @@ inline int dense_cfg() {
 template <class V>
 inline int dense_panel_width() {
   const int cfg = dense_cfg();
-  return Geom<V>::kPanelW >> (cfg == 1 ? 1 : cfg == 2 ? 2 : 0);
+  return Geom<V>::kPanelW >> (cfg == 1 || cfg == 3 ? 1 : cfg == 2 ? 2 : 0);
 }
 
 template <class SR, class Src>
@@ -165,6 +166,10 @@ void launch_dense(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* row
     case 2:
       launch_dense_cfg<PW / 4, 512, SR, Src>(c, s, src, rows, n, ncols, 72 * 1024, work, off, sc_cols, sc_vals, rownnz);
       break;
+    case 3:
+      launch_dense_cfg<PW / 2, 256, SR, Src>(c, s, src, rows, n, ncols, 74 * 1024, work, off, sc_cols, sc_vals, rownnz);
+      break;
+
     default:
       launch_dense_cfg<PW, 1024, SR, Src>(c, s, src, rows, n, ncols, 220 * 1024, work, off, sc_cols, sc_vals, rownnz);
   }
@@ -272,187 +277,120 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
   int end_bit = 0;
   while ((int64_t{1} << end_bit) < ncols_out) ++end_bit;
 
-  // Row batches under the scratch budget (contiguous row ranges).
+  // Output strategy.  Single pass: every row writes into a scratch slot of
+  // U_i entries, then a compaction copies the exact rows into C.  When the
+  // scratch would not fit the budget (very large C), two passes: a counting
+  // pass (no stores) gives the exact rowptr, then the same kernels write
+  // straight into C at rowptr (no scratch, no compaction, C allocated once).
   size_t budget = c->scratch_budget;
   if (budget == 0) {
     size_t fr = 0, tot = 0;
     SPG_CUDA(cudaMemGetInfo(&fr, &tot));
-    budget = (size_t)(fr * 0.4);
+    budget = (size_t)(fr * 0.45);
   }
   const size_t per_entry = sizeof(int32_t) + sizeof(V);
-  std::vector<int64_t> cuts{0};
-  if ((size_t)scratch_total * per_entry <= budget) {
-    cuts.push_back(m);
-  } else {
-    std::vector<int64_t> hoff(m + 1);
-    SPG_CUDA(cudaMemcpyAsync(hoff.data(), off.p, sizeof(int64_t) * (m + 1), cudaMemcpyDeviceToHost, c->stream));
-    SPG_CUDA(cudaStreamSynchronize(c->stream));
-    const int64_t cap_entries = std::max<int64_t>(1, (int64_t)(budget / per_entry));
-    int64_t r0 = 0;
-    while (r0 < m) {
-      int64_t r1 = std::upper_bound(hoff.begin() + r0 + 1, hoff.end(), hoff[r0] + cap_entries) - hoff.begin() - 1;
-      if (r1 <= r0) r1 = r0 + 1;
-      cuts.push_back(r1);
-      r0 = r1;
-    }
-  }
-  const bool batched = cuts.size() > 2;
+  const bool two_pass = (size_t)scratch_total * per_entry > budget;
   tm.mark(1);
 
   DBuf<int64_t> lists(c, m);
   DBuf<unsigned long long> cursor(c, kNumBins);
-  std::vector<DBuf<int32_t>> part_cols;
-  std::vector<DBuf<V>> part_vals;
-  std::vector<int64_t> part_nnz;
   float ms_numeric = 0.f, ms_compact = 0.f;
-
-  for (size_t bi = 0; bi + 1 < cuts.size(); ++bi) {
-    const int64_t r0 = cuts[bi], r1 = cuts[bi + 1];
-    int64_t bcount[kNumBins];
-    if (!batched) {
-      for (int b = 0; b < kNumBins; ++b) bcount[b] = (int64_t)hcounts[b];
-    } else {
-      SPG_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(unsigned long long) * kNumBins, c->stream));
-      bin_count_kernel<<<grid_for(c, r1 - r0, 1024, 2), 1024, 0, c->stream>>>(bins.p + r0, r1 - r0, counts.p);
-      SPG_LAUNCH_CHECK();
-      ++c->launches;
-      unsigned long long hc[kNumBins];
-      SPG_CUDA(cudaMemcpyAsync(hc, counts.p, sizeof(hc), cudaMemcpyDeviceToHost, c->stream));
-      SPG_CUDA(cudaStreamSynchronize(c->stream));
-      for (int b = 0; b < kNumBins; ++b) bcount[b] = (int64_t)hc[b];
-    }
-    unsigned long long base[kNumBins];
+  unsigned long long base[kNumBins];
+  {
     unsigned long long acc = 0;
     for (int b = 0; b < kNumBins; ++b) {
       base[b] = acc;
-      if (b > 0) acc += bcount[b];
+      if (b > 0) acc += hcounts[b];
     }
-    SPG_CUDA(cudaMemcpyAsync(cursor.p, base, sizeof(base), cudaMemcpyHostToDevice, c->stream));
-    bin_scatter_kernel<<<grid_for(c, r1 - r0, 1024, 2), 1024, 0, c->stream>>>(bins.p + r0, r1 - r0, cursor.p,
-                                                                             lists.p);
+  }
+  SPG_CUDA(cudaMemcpyAsync(cursor.p, base, sizeof(base), cudaMemcpyHostToDevice, c->stream));
+  bin_scatter_kernel<<<grid_for(c, m, 1024, 2), 1024, 0, c->stream>>>(bins.p, m, cursor.p, lists.p);
+  SPG_LAUNCH_CHECK();
+  ++c->launches;
+  // dense bin: largest rows first
+  const int64_t nd = (int64_t)hcounts[kBinDense];
+  const int64_t* dense_rows = lists.p + base[kBinDense];
+  DBuf<int64_t> dense_sorted, dk1, dk2;
+  if (nd > 1) {
+    dk1 = DBuf<int64_t>(c, nd);
+    dk2 = DBuf<int64_t>(c, nd);
+    dense_sorted = DBuf<int64_t>(c, nd);
+    gather_keys_kernel<<<grid_for(c, nd, 256, 4), 256, 0, c->stream>>>(dense_rows, nd, prods.p, dk1.p);
     SPG_LAUNCH_CHECK();
     ++c->launches;
+    size_t bytes = 0;
+    SPG_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, dk1.p, dk2.p, dense_rows, dense_sorted.p,
+                                                        (int)nd, 0, 64, c->stream));
+    ensure_cub_tmp(c, bytes);
+    SPG_CUDA(cub::DeviceRadixSort::SortPairsDescending(c->cub_tmp, bytes, dk1.p, dk2.p, dense_rows, dense_sorted.p,
+                                                        (int)nd, 0, 64, c->stream));
+    ++c->launches;
+    dense_rows = dense_sorted.p;
+  }
+  if (hcounts[kBinEmpty] > 0) {
+    zero_empty_rows_kernel<<<grid_for(c, m, 256, 4), 256, 0, c->stream>>>(bins.p, m, rownnz.p);
+    SPG_LAUNCH_CHECK();
+    ++c->launches;
+  }
+  DBuf<unsigned long long> work(c, 1);
 
-    int64_t sc_lo = 0, sc_hi = scratch_total;
-    if (batched) {
-      SPG_CUDA(cudaMemcpyAsync(&sc_lo, off.p + r0, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
-      SPG_CUDA(cudaMemcpyAsync(&sc_hi, off.p + r1, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
-      SPG_CUDA(cudaStreamSynchronize(c->stream));
-    }
-    DBuf<int32_t> sc_cols(c, (size_t)(sc_hi - sc_lo));
-    DBuf<V> sc_vals(c, (size_t)(sc_hi - sc_lo));
-    // Kernels index scratch with the global offsets off[i]; shift the base
-    // pointers so this batch's window [sc_lo, sc_hi) is what they address.
-    int32_t* sccb = sc_cols.p - sc_lo;
-    V* scvb = sc_vals.p - sc_lo;
-    // Row ids in `lists` are relative to r0 (bin_scatter ran over bins + r0).
-    Src bsrc = src;
-    rebase_source(bsrc, r0);
-    const int64_t* offb = off.p + r0;
-    int64_t* nnzb = rownnz.p + r0;
-    const int64_t* lb = lists.p;
-
-    // dense bin: largest rows first
-    const int64_t nd = bcount[kBinDense];
-    const int64_t* dense_rows = lb + base[kBinDense];
-    DBuf<int64_t> dense_sorted, dk1, dk2;
-    DBuf<unsigned long long> work(c, 1);
-    if (nd > 1) {
-      dk1 = DBuf<int64_t>(c, nd);
-      dk2 = DBuf<int64_t>(c, nd);
-      dense_sorted = DBuf<int64_t>(c, nd);
-      gather_keys_kernel<<<grid_for(c, nd, 256, 4), 256, 0, c->stream>>>(dense_rows, nd, prods.p + r0, dk1.p);
-      SPG_LAUNCH_CHECK();
-      ++c->launches;
-      size_t bytes = 0;
-      SPG_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, dk1.p, dk2.p, dense_rows, dense_sorted.p,
-                                                          (int)nd, 0, 64, c->stream));
-      ensure_cub_tmp(c, bytes);
-      SPG_CUDA(cub::DeviceRadixSort::SortPairsDescending(c->cub_tmp, bytes, dk1.p, dk2.p, dense_rows,
-                                                          dense_sorted.p, (int)nd, 0, 64, c->stream));
-      ++c->launches;
-      dense_rows = dense_sorted.p;
-    }
+  // One numeric pass over all bins; `offs` = per-row output offsets, outputs
+  // null for a counting pass.
+  auto numeric = [&](const int64_t* offs, int32_t* ocols, V* ovals) {
     SPG_CUDA(cudaMemsetAsync(work.p, 0, sizeof(unsigned long long), c->stream));
-    if (bcount[kBinEmpty] > 0) {
-      zero_empty_rows_kernel<<<grid_for(c, r1 - r0, 256, 4), 256, 0, c->stream>>>(bins.p + r0, r1 - r0, nnzb);
-      SPG_LAUNCH_CHECK();
-      ++c->launches;
-    }
-
+    const int64_t* lb = lists.p;
     StreamFork fk(c, 3);
-    if (nd > 0) launch_dense<SR, Src>(c, fk[0], bsrc, dense_rows, nd, ncols_out, work.p, offb, sccb, scvb, nnzb);
-    if (bcount[kBinHashMax] > 0)
-      launch_hash<SR, Src, Geom<V>::kMaxT, 1024>(c, fk[1], bsrc, lb + base[kBinHashMax], bcount[kBinHashMax],
-                                                 V_hash_cap<V>(Geom<V>::kMaxT), end_bit, offb, sccb, scvb, nnzb);
-    if (bcount[kBinHash8K] > 0)
-      launch_hash<SR, Src, 8192, 512>(c, fk[1], bsrc, lb + base[kBinHash8K], bcount[kBinHash8K], 1024, end_bit, offb, sccb,
-                                      scvb, nnzb);
-    if (bcount[kBinHash4K] > 0)
-      launch_hash<SR, Src, 4096, 256>(c, fk[2], bsrc, lb + base[kBinHash4K], bcount[kBinHash4K], 512, end_bit, offb, sccb,
-                                      scvb, nnzb);
-    if (bcount[kBinEsc512] > 0)
-      launch_esc<SR, Src, 128, 4>(c, fk[2], bsrc, lb + base[kBinEsc512], bcount[kBinEsc512], end_bit, offb, sccb,
-                                  scvb, nnzb);
-    if (bcount[kBinWarpEsc] > 0) {
-      esc_warp_kernel<SR, Src><<<grid_for(c, bcount[kBinWarpEsc], 8), 256, 0, fk[2]>>>(
-          bsrc, lb + base[kBinWarpEsc], bcount[kBinWarpEsc], offb, sccb, scvb, nnzb);
+    if (nd > 0) launch_dense<SR, Src>(c, fk[0], src, dense_rows, nd, ncols_out, work.p, offs, ocols, ovals, rownnz.p);
+    if (hcounts[kBinHashMax] > 0)
+      launch_hash<SR, Src, Geom<V>::kMaxT, 1024>(c, fk[1], src, lb + base[kBinHashMax], hcounts[kBinHashMax],
+                                                 V_hash_cap<V>(Geom<V>::kMaxT), end_bit, offs, ocols, ovals,
+                                                 rownnz.p);
+    if (hcounts[kBinHash8K] > 0)
+      launch_hash<SR, Src, 8192, 512>(c, fk[1], src, lb + base[kBinHash8K], hcounts[kBinHash8K], 1024, end_bit, offs,
+                                      ocols, ovals, rownnz.p);
+    if (hcounts[kBinHash4K] > 0)
+      launch_hash<SR, Src, 4096, 256>(c, fk[2], src, lb + base[kBinHash4K], hcounts[kBinHash4K], 512, end_bit, offs,
+                                      ocols, ovals, rownnz.p);
+    if (hcounts[kBinEsc512] > 0)
+      launch_esc<SR, Src, 128, 4>(c, fk[2], src, lb + base[kBinEsc512], hcounts[kBinEsc512], end_bit, offs, ocols,
+                                  ovals, rownnz.p);
+    if (hcounts[kBinWarpEsc] > 0) {
+      esc_warp_kernel<SR, Src><<<grid_for(c, hcounts[kBinWarpEsc], 8), 256, 0, fk[2]>>>(
+          src, lb + base[kBinWarpEsc], hcounts[kBinWarpEsc], offs, ocols, ovals, rownnz.p);
       SPG_LAUNCH_CHECK();
       ++c->launches;
     }
     fk.join();
+  };
+
+  if (!two_pass) {
+    DBuf<int32_t> sc_cols(c, (size_t)scratch_total);
+    DBuf<V> sc_vals(c, (size_t)scratch_total);
+    numeric(off.p, sc_cols.p, sc_vals.p);
     tm.mark(2);
-    ms_numeric += tm.between(1, 2);
-
-    if (!batched) {
-      exclusive_scan(c, rownnz.p, out->ptr, m + 1);
-      const int64_t nnz = d2h_scalar(c, out->ptr + m);
-      out->nnz = nnz;
-      out->idx = dalloc<int32_t>(c, (size_t)nnz);
-      out->vals = dalloc<V>(c, (size_t)nnz);
-      compact_rows_kernel<V><<<grid_for(c, m, 8), 256, 0, c->stream>>>(m, off.p, out->ptr, sccb, scvb, out->idx,
-                                                                       static_cast<V*>(out->vals));
-      SPG_LAUNCH_CHECK();
-      ++c->launches;
-    } else {
-      // compact this batch into an exact buffer; the exclusive scan over
-      // rownnz[r0 .. r1] ends with the batch total (the last input, which
-      // belongs to the next batch, is excluded by construction)
-      DBuf<int64_t> bptr(c, r1 - r0 + 1);
-      exclusive_scan(c, rownnz.p + r0, bptr.p, r1 - r0 + 1);
-      const int64_t bn = d2h_scalar(c, bptr.p + (r1 - r0));
-      DBuf<int32_t> pc(c, (size_t)bn);
-      DBuf<V> pv(c, (size_t)bn);
-      compact_rows_kernel<V><<<grid_for(c, r1 - r0, 8), 256, 0, c->stream>>>(r1 - r0, offb, bptr.p, sccb, scvb, pc.p,
-                                                                             pv.p);
-      SPG_LAUNCH_CHECK();
-      ++c->launches;
-      part_cols.push_back(std::move(pc));
-      part_vals.push_back(std::move(pv));
-      part_nnz.push_back(bn);
-    }
-    tm.mark(3);
-    ms_compact += tm.between(2, 3);
-    tm.mark(1);
-  }
-
-  if (batched) {
+    ms_numeric = tm.between(1, 2);
     exclusive_scan(c, rownnz.p, out->ptr, m + 1);
     const int64_t nnz = d2h_scalar(c, out->ptr + m);
     out->nnz = nnz;
     out->idx = dalloc<int32_t>(c, (size_t)nnz);
     out->vals = dalloc<V>(c, (size_t)nnz);
-    int64_t pos = 0;
-    for (size_t k = 0; k < part_nnz.size(); ++k) {
-      if (part_nnz[k] == 0) continue;
-      SPG_CUDA(cudaMemcpyAsync(out->idx + pos, part_cols[k].p, sizeof(int32_t) * part_nnz[k],
-                               cudaMemcpyDeviceToDevice, c->stream));
-      SPG_CUDA(cudaMemcpyAsync(static_cast<V*>(out->vals) + pos, part_vals[k].p, sizeof(V) * part_nnz[k],
-                               cudaMemcpyDeviceToDevice, c->stream));
-      pos += part_nnz[k];
-    }
+    compact_rows_kernel<V><<<grid_for(c, m, 8), 256, 0, c->stream>>>(m, off.p, out->ptr, sc_cols.p, sc_vals.p,
+                                                                     out->idx, static_cast<V*>(out->vals));
+    SPG_LAUNCH_CHECK();
+    ++c->launches;
     tm.mark(3);
-    ms_compact += tm.between(1, 3);
+    ms_compact = tm.between(2, 3);
+  } else {
+    numeric(off.p, nullptr, nullptr);  // counting pass
+    exclusive_scan(c, rownnz.p, out->ptr, m + 1);
+    const int64_t nnz = d2h_scalar(c, out->ptr + m);
+    out->nnz = nnz;
+    out->idx = dalloc<int32_t>(c, (size_t)nnz);
+    out->vals = dalloc<V>(c, (size_t)nnz);
+    numeric(out->ptr, out->idx, static_cast<V*>(out->vals));  // writes straight into C
+    tm.mark(2);
+    ms_numeric = tm.between(1, 2);
+    tm.mark(3);
   }
   if (st) {
     tm.mark(3);

@@ -172,3 +172,19 @@ class DeviceCsr:
                 self.free()
         except Exception:
             pass
+
+
+def pin(*arrays):
+    """Page-lock numpy arrays in place (cudaHostRegister) so their uploads run
+    at full PCIe speed; returns a callable that unpins them."""
+    done = []
+    for a in arrays:
+        if a is None or a.nbytes == 0:
+            continue
+        check(lib.spg_host_register(C.c_void_p(a.ctypes.data), int(a.nbytes)))
+        done.append(a)
+
+    def unpin():
+        for a in done:
+            lib.spg_host_unregister(C.c_void_p(a.ctypes.data))
+    return unpin

@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--threshold", type=int, default=1 << 14)
     ap.add_argument("--staging", type=int, default=1 << 16)
     ap.add_argument("--fuse", type=int, default=1)
+    ap.add_argument("--grid", default="", help="PRxPC (default: the BASELINE grid for the world size)")
     args = ap.parse_args()
 
     import torch.distributed as dist
@@ -45,7 +46,7 @@ def main():
     dist.init_process_group("gloo")
     job = [uuid.uuid4().hex[:12] if rank == 0 else None]
     dist.broadcast_object_list(job, src=0)
-    pr, pc = grid_for(world)
+    pr, pc = (int(x) for x in args.grid.split("x")) if args.grid else grid_for(world)
     i, j = rank // pc, rank % pc
 
     m = generators.generate_rmat(args.sr, args.scale, args.ef, 1)

@@ -113,16 +113,17 @@ def test_rmat14_against_reference_checksum(golden, ctx, sr):
         assert c.checksum() == (ob.orc_seed(a.nrows, a.ncols) + s) % (1 << 64)
 
 
-def test_row_batched_scratch_matches_single_pass(ctx):
-    m = coo_to_csr(generators.generate_rmat(4, 13, 16.0, 5))
+@pytest.mark.parametrize("sr", [0, 2, 4, 5])
+def test_two_pass_mode_matches_single_pass(ctx, sr):
+    m = coo_to_csr(generators.generate_rmat(sr, 13, 16.0, 5))
     d = DeviceCsr.upload(ctx, m)
     full = local_multiply(d, d)
-    ctx.set_scratch_budget(1 << 20)  # 1 MB: forces many row batches
+    ctx.set_scratch_budget(1 << 20)  # 1 MB: forces the count-then-write mode
     try:
         small = local_multiply(d, d)
     finally:
         ctx.set_scratch_budget(0)
-    assert_same(small.download(), full.download(), 4)
+    assert_same(small.download(), full.download(), sr, rtol=RTOL)
 
 
 @pytest.mark.parametrize("sr", [0, 1, 2, 4, 5])

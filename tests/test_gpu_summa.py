@@ -40,3 +40,14 @@ def test_summa_host_path_chunked_staging():
     nproc = 2 if n >= 2 else 1
     out = run_worker(nproc, "--sr", 4, "--scale", 11, "--mode", 0, "--staging", 8192)
     assert "blocks_ok=True checksum_ok=True" in out
+
+
+@pytest.mark.parametrize("grid", ["1x4", "4x1", "1x2", "2x1"])
+def test_summa_rectangular_grids(grid):
+    """Non-square grids use the common-refinement stage schedule."""
+    pr, pc = (int(x) for x in grid.split("x"))
+    if pr * pc > ngpus():
+        pytest.skip(f"needs {pr * pc} GPUs")
+    for fuse in (1, 0):
+        out = run_worker(pr * pc, "--sr", 4, "--scale", 10, "--grid", grid, "--fuse", fuse, "--mode", 2)
+        assert "blocks_ok=True checksum_ok=True" in out
