@@ -65,7 +65,14 @@ class Clocks:
                                          stdout=self.f, stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
-        time.sleep(0.25)
+        # nvidia-smi's NVML start-up takes driver locks that can stall the GPU
+        # for hundreds of ms: wait for its second sample before timing starts
+        t0 = time.time()
+        while self.proc is not None and time.time() - t0 < 10.0:
+            self.f.flush()
+            if os.path.getsize(self.path) > 0 and open(self.path).read().count("\n") >= 2:
+                break
+            time.sleep(0.05)
         return self
 
     def __exit__(self, *exc):
@@ -111,6 +118,30 @@ def make_input(scale, ef, seed, sr=4, permute=False):
     a = coo_to_csr_fast(coo)
     log(f"[bench] R-MAT s{scale} ef{ef}: n={a.nrows} nnz={a.nnz} (gen {time.time() - t0:.1f}s)")
     return a
+
+
+def workload(args):
+    """BASELINE.json configs 2-5: generator, semiring,
+    sizes and the closed-form / measured totals the run must reproduce."""
+    c = args.config
+    if c == 2:
+        return {"gen": "rmat", "sr": 4, "n": 1 << args.scale, "vs": 4, "dtype": "int32",
+                "name": f"rmat{args.scale}_ef{int(args.ef)}_tropical_i32_AxA (BASELINE config 2)",
+                "expect": {"products": 2934326978, "nnz_C": 1281547801} if (args.scale, args.ef) == (18, 16.0)
+                else None}
+    if c == 3:
+        return {"gen": "rmat", "sr": 2, "n": 1 << args.scale, "vs": 1, "dtype": "u8",
+                "name": f"rmat{args.scale}_ef{int(args.ef)}_boolean_AxA (BASELINE config 3)", "expect": None}
+    if c == 4:
+        N = args.stencil_n
+        return {"gen": "stencil27", "sr": 0, "n": N ** 3, "N": N, "vs": 8, "dtype": "f64",
+                "name": f"stencil27_N{N}_fp64_AxA (BASELINE config 4)",
+                "expect": {"products": (9 * N - 10) ** 3, "nnz_C": (5 * N - 6) ** 3}}
+    if c == 5:
+        n = 1 << args.er_log2
+        return {"gen": "er", "sr": 5, "n": n, "d": args.er_d, "value_mode": 1, "vs": 16, "dtype": "f64+u64",
+                "name": f"er2^{args.er_log2}_d{args.er_d}_maxtimes_struct_AxA (BASELINE config 5)", "expect": None}
+    raise SystemExit(f"--config {c}: choose 2, 3, 4 or 5")
 
 
 def b_alg(nnz_l, nrows, F, nnz_c, vs):
@@ -262,13 +293,15 @@ def run_single(args):
         "vs_baseline": None, "dtype": "int32", "data": "synthetic",
         "config": {"workload": f"rmat{args.scale}_ef{int(args.ef)}_tropical_i32_AxA (BASELINE config 2)",
                    "grid": "1x1", "permuted": bool(args.permute), "products": F, "nnz_A": a.nnz, "nnz_C": nnz_c,
-                   "time_to_C_ms": ms, "l2": "flushed between steps (512 MB write)"},
+                   "time_to_C_ms": ms, "steps_ms": [round(float(x), 3) for x in times],
+                   "l2": "flushed between steps (512 MB write)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "note": f"B_alg of the whole local multiply (SURVEY §8d) / its event time; peak {peak_kind}"},
         "cpu_baseline": cpu,
-        "e2e": {"value": 2.0 * F / e2e_s / 1e9, "unit": "Gflop/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "seconds": e2e_s},
+        "e2e": (None if args.e2e_steps <= 0 else
+                {"value": 2.0 * F / e2e_s / 1e9, "unit": "Gflop/s", "h2d_bytes_per_step": h2d,
+                 "d2h_bytes_per_step": d2h, "seconds": e2e_s}),
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
@@ -308,12 +341,23 @@ def run_summa(args):
     thr = args.threshold if args.threshold >= 0 else measured_threshold(pc)      # row scope: fanout pc
     thr_col = args.threshold if args.threshold >= 0 else measured_threshold(pr)  # column scope: fanout pr
 
-    coo = generators.generate_rmat(4, args.scale, args.ef, args.seed)
-    if args.permute:
-        coo = generators.permute_symmetric(coo, args.seed)
-    n = coo.nrows
-    blk = local_block(coo, pr, pc, i, j)
-    del coo
+    t_gen = time.time()
+    wl = workload(args)
+    sr, n = wl["sr"], wl["n"]
+    from paper_2504_06408_b200.summa import block_from_piece, block_range
+    rr, cr = block_range(n, pr, i), block_range(n, pc, j)
+    if wl["gen"] == "rmat":
+        coo = generators.generate_rmat(sr, args.scale, args.ef, args.seed)
+        if args.permute:
+            coo = generators.permute_symmetric(coo, args.seed)
+        blk = local_block(coo, pr, pc, i, j)
+        del coo
+    elif wl["gen"] == "stencil27":
+        blk = block_from_piece(generators.generate_stencil27_block(sr, wl["N"], rr, cr), rr, cr)
+    else:
+        blk = block_from_piece(generators.generate_er_block(sr, n, wl["d"], args.seed, rr, cr,
+                                                            value_mode=wl["value_mode"]), rr, cr)
+    log(f"[bench] rank {rank}: block {rr}x{cr} nnz={blk.storage.nnz} (gen {time.time() - t_gen:.1f}s)")
     from paper_2504_06408_b200.device import pin
     st = blk.storage
     arrays = [getattr(st, k) for k in ("colptr", "jc", "cp", "rowids", "values") if hasattr(st, k)]
@@ -355,17 +399,20 @@ def run_summa(args):
     launches = ctx.kernel_launches() - launches0
     part = checksum_part(c, blk.rows[0], blk.cols[0])
     nnz_blk = c.nnz
-    # e2e: the same call plus the D2H read of this rank's C block (host result)
-    torch.cuda.synchronize()
-    dist.barrier()
-    t0 = time.perf_counter()
-    c2, _ = step()
-    host_c = c2.download()
-    e2e_local = time.perf_counter() - t0
-    d2h = 8 * (host_c.ncols + 1) + (8 + 4) * host_c.nnz
-    del host_c
-    c2.free()
     c.free()
+    # e2e: the same call plus the D2H read of this rank's C block (host
+    # result); skipped (--e2e-steps 0) when C blocks exceed host RAM
+    e2e_local, d2h = float("nan"), 0
+    if args.e2e_steps > 0:
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        c2, _ = step()
+        host_c = c2.download()
+        e2e_local = time.perf_counter() - t0
+        d2h = 8 * (host_c.ncols + 1) + (8 + wl["vs"]) * host_c.nnz
+        del host_c
+        c2.free()
 
     t = torch.tensor(times, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -385,18 +432,24 @@ def run_summa(args):
         led0 = leds[-1]
         csum = (checksum_seed(n, n) + int(agg[2]) + (int(agg[3]) << 32)) % (1 << 64)
         peak, peak_kind = peaks()
-        h2d = 8 * (blk.storage.ncols + 1) + (8 + 4) * blk.storage.nnz
+        h2d = 8 * (blk.storage.ncols + 1) + (8 + wl["vs"]) * blk.storage.nnz
+        nnz_c = int(agg[1])
         line = {
             "metric": METRIC, "value": 2.0 * F / (ms * 1e-3) / 1e9, "unit": "Gflop/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": f"rmat{args.scale}_ef{int(args.ef)}_tropical_i32_AxA via summa25_multiply",
-                       "grid": f"{pr}x{pc}", "permuted": bool(args.permute), "two_round": not args.one_round,
+            "scaling": "strong", "vs_baseline": None, "dtype": wl["dtype"], "data": "synthetic",
+            "config": {"workload": wl["name"] + " via summa25_multiply", "baseline_config": args.config,
+                       "grid": f"{pr}x{pc}", "permuted": bool(args.permute and wl["gen"] == "rmat"),
+                       "two_round": not args.one_round,
                        "fuse_stages": not args.no_fuse,
                        "comm": args.comm,
                        "threshold_bytes": {"row_scope": thr, "col_scope": thr_col,
                                            "source": "measured crossover (profiles/comm_fanout*.json)"},
-                       "products": F, "nnz_C": int(agg[1]), "checksum_C": csum,
+                       "products": F, "nnz_C": nnz_c, "checksum_C": csum,
+                       "expected": wl.get("expect"),
+                       "matches_expected": (None if not wl.get("expect") else
+                                            all({"products": F, "nnz_C": nnz_c}[k] == v
+                                                for k, v in wl["expect"].items())),
                        "time_to_C_ms": ms, "steps_ms_max_over_ranks": [round(float(x), 2) for x in t],
                        "rank0_ledger": led0,
                        "per_rank_ms": [{"event": round(float(x[0]), 2), "ledger_total": round(float(x[1]), 2),
@@ -407,8 +460,9 @@ def run_summa(args):
             "roofline": {"bound": "hbm", "achieved": None, "peak": peak, "unit": "GB/s", "frac": None,
                          "traffic": None, "note": "per-kernel roofline is reported by the N=1 line"},
             "cpu_baseline": None,
-            "e2e": {"value": 2.0 * F / float(e2e_t[0]) / 1e9, "unit": "Gflop/s", "h2d_bytes_per_step": 2 * h2d,
-                    "d2h_bytes_per_step": int(agg[5]), "seconds": float(e2e_t[0])},
+            "e2e": (None if args.e2e_steps <= 0 else
+                    {"value": 2.0 * F / float(e2e_t[0]) / 1e9, "unit": "Gflop/s", "h2d_bytes_per_step": 2 * h2d,
+                     "d2h_bytes_per_step": int(agg[5]), "seconds": float(e2e_t[0])}),
             "gpu_launches": int(agg[4]), "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -427,7 +481,12 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--scale", type=int, default=18)
+    ap.add_argument("--config", type=int, default=2, help="BASELINE.json config (2 = default N=1 line; 3, 4, 5 "
+                    "run through summa25_multiply)")
+    ap.add_argument("--scale", type=int, default=0, help="R-MAT scale (default 18 for config 2, 22 for config 3)")
+    ap.add_argument("--stencil-n", type=int, default=252)
+    ap.add_argument("--er-log2", type=int, default=22)
+    ap.add_argument("--er-d", type=int, default=64)
     ap.add_argument("--ef", type=float, default=16.0)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -445,12 +504,14 @@ def main():
     ap.add_argument("--threshold", type=int, default=-1, help="hybrid threshold bytes (-1: measured default)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.scale <= 0:
+        args.scale = 22 if args.config == 3 else 18
     if args.cpu_products <= 0:
         args.cpu_products = min(1e9, 3e7 * (os.cpu_count() or 1))
     if args.impl == "reference":
         run_reference_arm(args)
         return
-    if args.gpus == 1 and int(os.environ.get("WORLD_SIZE", "1")) == 1 and not args.summa:
+    if args.gpus == 1 and int(os.environ.get("WORLD_SIZE", "1")) == 1 and not args.summa and args.config == 2:
         run_single(args)
     else:
         run_summa(args)

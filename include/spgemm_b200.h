@@ -196,6 +196,14 @@ SPG_API int spg_generate_er(int sr, int64_t n, int d, uint64_t seed, int value_m
                             int64_t* nnz, int64_t** rows, int64_t** cols, void** vals);
 SPG_API int spg_generate_stencil27(int sr, int64_t N, int64_t* nrows, int64_t* nnz,
                                    int64_t** rows, int64_t** cols, void** vals);
+/* The same generators restricted to the block rows [r0, r1) x cols [c0, c1)
+ * (global indices), so each rank of a grid builds only its own block. */
+SPG_API int spg_generate_er_block(int sr, int64_t n, int d, uint64_t seed, int value_mode, int64_t r0,
+                                  int64_t r1, int64_t c0, int64_t c1, int64_t* nnz, int64_t** rows,
+                                  int64_t** cols, void** vals);
+SPG_API int spg_generate_stencil27_block(int sr, int64_t N, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
+                                         int64_t* nrows, int64_t* nnz, int64_t** rows, int64_t** cols,
+                                         void** vals);
 /* normalised COO (row-major, unique) -> CSR / CSC host arrays, no copies of
  * the reference's fold semantics needed (input already unique). */
 SPG_API int spg_coo_to_csr(int sr, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rows,

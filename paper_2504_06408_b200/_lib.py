@@ -113,6 +113,10 @@ _SIGS = [
                                   _P(_i64p), _P(_i64p), _P(C.c_void_p)]),
     ("spg_generate_stencil27", C.c_int, [C.c_int, C.c_int64, _i64p, _i64p, _P(_i64p), _P(_i64p),
                                          _P(C.c_void_p)]),
+    ("spg_generate_er_block", C.c_int, [C.c_int, C.c_int64, C.c_int, C.c_uint64, C.c_int, C.c_int64, C.c_int64,
+                                        C.c_int64, C.c_int64, _i64p, _P(_i64p), _P(_i64p), _P(C.c_void_p)]),
+    ("spg_generate_stencil27_block", C.c_int, [C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                                               _i64p, _i64p, _P(_i64p), _P(_i64p), _P(C.c_void_p)]),
     ("spg_coo_to_csr", C.c_int, [C.c_int, C.c_int64, C.c_int64, C.c_int64, _i64p, _i64p, C.c_void_p,
                                  C.c_int, _P(HCsr)]),
     ("spg_free", None, [C.c_void_p]),

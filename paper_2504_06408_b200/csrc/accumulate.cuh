@@ -1067,14 +1067,84 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
 #pragma unroll
     for (int q = 0; q < SPT; ++q) my_keys[q] = my_slots[q] >= 0 ? (uint32_t)tkeys[my_slots[q]] : 0u;
     __syncthreads();
-    // stage (key, slot) in smem (keys array is dead now), then blocked radix sort
+    // Monotone bucketing by the high column bits (the keys array is dead
+    // now): NB = T/2 buckets (>= occupied slots), counts by shared atomics,
+    // starts by one block scan, in-bucket order by a rank count, output
+    // written straight to its sorted position.  A row whose columns crowd
+    // one bucket (> kBucketMax entries) takes the radix sort below instead.
+    {
+      constexpr int NB = T / 2, NBT = NB / THREADS, kBucketMax = 32;
+      static_assert(NB % THREADS == 0, "bucket count must divide by the CTA size");
+      const int shift = end_bit > LOG2T - 1 ? end_bit - (LOG2T - 1) : 0;
+      int* bstart = tkeys;                                            // NB counters, then starts
+      uint32_t* bkeys = reinterpret_cast<uint32_t*>(tkeys) + NB;      // keys grouped by bucket
+      for (int b = threadIdx.x; b < NB; b += THREADS) bstart[b] = 0;
+      __syncthreads();
+      // the in-bucket arrival rank rides in bits 16..30 of the slot id
+#pragma unroll
+      for (int q = 0; q < SPT; ++q)
+        if (my_slots[q] >= 0) my_slots[q] |= min(atomicAdd(&bstart[my_keys[q] >> shift], 1), 0x7fff) << 16;
+      __syncthreads();
+      int sum = 0, mx = 0;
+#pragma unroll
+      for (int b = 0; b < NBT; ++b) {
+        const int n = bstart[threadIdx.x * NBT + b];
+        sum += n;
+        mx = max(mx, n);
+      }
+      if (!__syncthreads_or(mx > kBucketMax)) {
+        int run;
+        typename HS::Scan(tmp->scan).ExclusiveSum(sum, run);
+#pragma unroll
+        for (int b = 0; b < NBT; ++b) {
+          const int n = bstart[threadIdx.x * NBT + b];
+          bstart[threadIdx.x * NBT + b] = run;
+          run += n;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < SPT; ++q)
+          if (my_slots[q] >= 0) bkeys[bstart[my_keys[q] >> shift] + (my_slots[q] >> 16)] = my_keys[q];
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < SPT; ++q)
+          if (my_slots[q] >= 0) {  // final position replaces the arrival rank
+            const uint32_t key = my_keys[q];
+            const int b = (int)(key >> shift);
+            const int s1 = b + 1 < NB ? bstart[b + 1] : total;
+            int pos = bstart[b];
+            for (int j = pos; j < s1; ++j) pos += bkeys[j] < key;
+            my_slots[q] = (my_slots[q] & 0xffff) | (pos << 16);
+          }
+        __syncthreads();
+        // sorted (key, slot) staging, then coalesced stores of the row
+        uint32_t* skeys = reinterpret_cast<uint32_t*>(bstart);
+        uint16_t* sslot = reinterpret_cast<uint16_t*>(bkeys);
+#pragma unroll
+        for (int q = 0; q < SPT; ++q)
+          if (my_slots[q] >= 0) {
+            skeys[my_slots[q] >> 16] = my_keys[q];
+            sslot[my_slots[q] >> 16] = (uint16_t)(my_slots[q] & 0xffff);
+          }
+        __syncthreads();
+        const int64_t o = off[i];
+        for (int e = threadIdx.x; e < total; e += THREADS) {
+          out_cols[o + e] = (int32_t)skeys[e];
+          out_vals[o + e] = tvals[sslot[e]];
+        }
+        if (threadIdx.x == 0) rownnz[i] = total;
+        __syncthreads();
+        continue;
+      }
+    }
+    // stage (key, slot) in smem, then blocked radix sort
     uint16_t* stage_slot = reinterpret_cast<uint16_t*>(sorted_keys + T / 2);
     int w = first;
 #pragma unroll
     for (int q = 0; q < SPT; ++q)
       if (my_slots[q] >= 0) {
         sorted_keys[w] = my_keys[q];
-        stage_slot[w] = (uint16_t)my_slots[q];
+        stage_slot[w] = (uint16_t)(my_slots[q] & 0xffff);
         ++w;
       }
     __syncthreads();

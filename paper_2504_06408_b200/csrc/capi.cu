@@ -24,8 +24,9 @@ extern "C" const spg::SrOps* spg_ops_maxtimes();
 
 namespace spg {
 void gen_rmat(int, int, double, uint64_t, int64_t*, int64_t*, int64_t**, int64_t**, void**);
-void gen_er(int, int64_t, int, uint64_t, int, int64_t*, int64_t**, int64_t**, void**);
-void gen_stencil27(int, int64_t, int64_t*, int64_t*, int64_t**, int64_t**, void**);
+void gen_er(int, int64_t, int, uint64_t, int, int64_t, int64_t, int64_t, int64_t, int64_t*, int64_t**, int64_t**,
+            void**);
+void gen_stencil27(int, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t*, int64_t*, int64_t**, int64_t**, void**);
 
 thread_local std::string g_last_error;
 
@@ -267,7 +268,15 @@ int spg_ctx_create(int device, spg_ctx** out) {
       SPG_CUDA(cudaDeviceGetDefaultMemPool(&c->pool, device));
       uint64_t thr = UINT64_MAX;  // keep freed blocks cached in the pool
       SPG_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thr));
+      cudaMemPoolProps props{};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = device;
+      SPG_CUDA(cudaMemPoolCreate(&c->big_pool, &props));
+      SPG_CUDA(cudaMemPoolSetAttribute(c->big_pool, cudaMemPoolAttrReleaseThreshold, &thr));
+      mem_snapshot(c);
     } catch (...) {
+      if (c->big_pool) cudaMemPoolDestroy(c->big_pool);
       delete c;
       throw;
     }
@@ -288,6 +297,10 @@ void spg_ctx_destroy(spg_ctx* c) {
   }
   if (c->fork_ev) cudaEventDestroy(c->fork_ev);
   if (c->own_stream) cudaStreamDestroy(c->stream);
+  if (c->big_pool) {
+    cudaDeviceSynchronize();  // buffers the caller freed stream-ordered must be back in the pool
+    cudaMemPoolDestroy(c->big_pool);
+  }
   delete c;
 }
 
@@ -570,7 +583,15 @@ int spg_generate_er(int sr, int64_t n, int d, uint64_t seed, int mode, int64_t* 
                     int64_t** cols, void** vals) {
   return guarded(nullptr, [&] {
     need(nnz && rows && cols && vals, "null argument");
-    gen_er(sr, n, d, seed, mode, nnz, rows, cols, vals);
+    gen_er(sr, n, d, seed, mode, 0, n, 0, n, nnz, rows, cols, vals);
+  });
+}
+
+int spg_generate_er_block(int sr, int64_t n, int d, uint64_t seed, int mode, int64_t r0, int64_t r1, int64_t c0,
+                          int64_t c1, int64_t* nnz, int64_t** rows, int64_t** cols, void** vals) {
+  return guarded(nullptr, [&] {
+    need(nnz && rows && cols && vals, "null argument");
+    gen_er(sr, n, d, seed, mode, r0, r1, c0, c1, nnz, rows, cols, vals);
   });
 }
 
@@ -578,7 +599,15 @@ int spg_generate_stencil27(int sr, int64_t N, int64_t* nrows, int64_t* nnz, int6
                            void** vals) {
   return guarded(nullptr, [&] {
     need(nrows && nnz && rows && cols && vals, "null argument");
-    gen_stencil27(sr, N, nrows, nnz, rows, cols, vals);
+    gen_stencil27(sr, N, 0, N * N * N, 0, N * N * N, nrows, nnz, rows, cols, vals);
+  });
+}
+
+int spg_generate_stencil27_block(int sr, int64_t N, int64_t r0, int64_t r1, int64_t c0, int64_t c1, int64_t* nrows,
+                                 int64_t* nnz, int64_t** rows, int64_t** cols, void** vals) {
+  return guarded(nullptr, [&] {
+    need(nrows && nnz && rows && cols && vals, "null argument");
+    gen_stencil27(sr, N, r0, r1, c0, c1, nrows, nnz, rows, cols, vals);
   });
 }
 

@@ -4,8 +4,10 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -40,7 +42,10 @@ struct spg_ctx {
   int sm_count = 148;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  cudaMemPool_t pool = nullptr;
+  cudaMemPool_t pool = nullptr;      // device default pool: small buffers
+  cudaMemPool_t big_pool = nullptr;  // private pool for buffers >= kBigAlloc (no fragmentation by small ones)
+  size_t free_snap = 0;              // cudaMemGetInfo free bytes at the last snapshot
+  size_t reserved_snap = 0;          // pool bytes reserved at that snapshot
   std::string last_error;
   // cub temporary storage, grown on demand and reused
   void* cub_tmp = nullptr;
@@ -56,15 +61,86 @@ struct spg_ctx {
 
 namespace spg {
 
-// Stream-ordered device allocation from the context's pool.
+// SPG_HOST_TRACE=<ms>: report host calls that block longer than <ms>
+// (stalls there show up as idle gaps inside the device-timed phases).
+struct HostTrace {
+  const char* what;
+  size_t arg;
+  std::chrono::steady_clock::time_point t0;
+  static double limit_ms() {
+    static const double v = [] {
+      const char* e = std::getenv("SPG_HOST_TRACE");
+      return e ? std::atof(e) : -1.0;
+    }();
+    return v;
+  }
+  HostTrace(const char* w, size_t a = 0) : what(w), arg(a), t0(std::chrono::steady_clock::now()) {}
+  ~HostTrace() {
+    const double lim = limit_ms();
+    if (lim < 0) return;
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (ms >= lim) std::fprintf(stderr, "[spg-host] %s (%zu) %.3f ms\n", what, arg, ms);
+  }
+};
+
+// Stream-ordered device allocation.  Large buffers come from the context's
+// private pool, so the many small per-call buffers never split the big
+// cached blocks (a split forces the pool to map fresh memory: tens of ms).
+constexpr size_t kBigAlloc = size_t(16) << 20;
 template <class T>
 T* dalloc(spg_ctx* c, size_t n) {
   if (n == 0) n = 1;
   void* p = nullptr;
-  SPG_CUDA(cudaMallocAsync(&p, n * sizeof(T), c->stream));
+  const size_t bytes = n * sizeof(T);
+  HostTrace ht("cudaMallocAsync", bytes);
+  if (bytes >= kBigAlloc && c->big_pool)
+    SPG_CUDA(cudaMallocFromPoolAsync(&p, bytes, c->big_pool, c->stream));
+  else
+    SPG_CUDA(cudaMallocAsync(&p, bytes, c->stream));
   return static_cast<T*>(p);
 }
+
+// As dalloc, but an out-of-memory result returns nullptr instead of failing.
+template <class T>
+T* try_dalloc(spg_ctx* c, size_t n) {
+  if (n == 0) n = 1;
+  void* p = nullptr;
+  const size_t bytes = n * sizeof(T);
+  const cudaError_t e = (bytes >= kBigAlloc && c->big_pool)
+                            ? cudaMallocFromPoolAsync(&p, bytes, c->big_pool, c->stream)
+                            : cudaMallocAsync(&p, bytes, c->stream);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  SPG_CUDA(e);
+  return static_cast<T*>(p);
+}
+
+inline size_t pool_attr(cudaMemPool_t p, cudaMemPoolAttr a) {
+  uint64_t v = 0;
+  if (p) cudaMemPoolGetAttribute(p, a, &v);
+  return (size_t)v;
+}
+// Re-reads free device memory (cudaMemGetInfo can block for tens of ms, so
+// it runs at context creation and after an allocation failure only).
+inline void mem_snapshot(spg_ctx* c) {
+  size_t fr = 0, tot = 0;
+  SPG_CUDA(cudaMemGetInfo(&fr, &tot));
+  c->free_snap = fr;
+  c->reserved_snap = pool_attr(c->pool, cudaMemPoolAttrReservedMemCurrent) +
+                     pool_attr(c->big_pool, cudaMemPoolAttrReservedMemCurrent);
+}
+// Bytes this context can still allocate: free memory at the snapshot plus
+// what its pools had reserved then, minus what they hold in use now.
+inline size_t mem_available(spg_ctx* c) {
+  const size_t used = pool_attr(c->pool, cudaMemPoolAttrUsedMemCurrent) +
+                      pool_attr(c->big_pool, cudaMemPoolAttrUsedMemCurrent);
+  const size_t have = c->free_snap + c->reserved_snap;
+  return have > used ? have - used : 0;
+}
 inline void dfree(spg_ctx* c, void* p) {
+  HostTrace ht("cudaFreeAsync");
   if (p) SPG_CUDA(cudaFreeAsync(p, c->stream));
 }
 
@@ -86,10 +162,18 @@ struct DBuf {
   }
   ~DBuf() { reset(); }
   void reset() {
+    HostTrace ht("cudaFreeAsync", n * sizeof(T));
     if (p) cudaFreeAsync(p, c->stream);
     p = nullptr;
   }
   T* release() { T* q = p; p = nullptr; return q; }
+  static DBuf adopt(spg_ctx* ctx, T* q, size_t count) {
+    DBuf b;
+    b.c = ctx;
+    b.p = q;
+    b.n = count;
+    return b;
+  }
 };
 
 inline void ensure_cub_tmp(spg_ctx* c, size_t bytes) {

@@ -127,10 +127,11 @@ void rmat(int scale, double edge_factor, uint64_t seed, int64_t* nrows, int64_t*
 }
 
 template <class SR>
-void er(int64_t n, int d, uint64_t seed, int value_mode, int64_t* nnz, int64_t** rows, int64_t** cols,
-        void** vals) {
+void er(int64_t n, int d, uint64_t seed, int value_mode, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
+        int64_t* nnz, int64_t** rows, int64_t** cols, void** vals) {
   using V = typename SR::value_type;
   if (n < 1 || d < 1) fail(SPG_ERR_INVALID_RANGE, "er: need n >= 1 and d >= 1");
+  if (r0 < 0 || r1 > n || r0 > r1 || c0 < 0 || c1 > n || c0 > c1) fail(SPG_ERR_INVALID_RANGE, "er: bad block");
   if (value_mode == 1 && sizeof(V) != 16) fail(SPG_ERR_ARG, "er: value_mode 1 needs a 16-byte value type");
   const uint64_t s = mix64(seed);
   const int T = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
@@ -139,7 +140,7 @@ void er(int64_t n, int d, uint64_t seed, int value_mode, int64_t* nnz, int64_t**
   std::vector<std::thread> ts;
   for (int w = 0; w < T; ++w) {
     ts.emplace_back([&, w] {
-      const int64_t lo = n * w / T, hi = n * (w + 1) / T;
+      const int64_t lo = r0 + (r1 - r0) * w / T, hi = r0 + (r1 - r0) * (w + 1) / T;
       std::vector<std::pair<int64_t, V>> row(d);
       std::vector<int> idx(d);
       for (int64_t i = lo; i < hi; ++i) {
@@ -161,9 +162,10 @@ void er(int64_t n, int d, uint64_t seed, int value_mode, int64_t* nnz, int64_t**
           V acc = row[idx[a]].second;
           int b = a + 1;
           for (; b < d && row[idx[b]].first == row[idx[a]].first; ++b) acc = SR::add(acc, row[idx[b]].second);
-          if (!SR::is_zero(acc)) {
+          const int64_t col = row[idx[a]].first;
+          if (!SR::is_zero(acc) && col >= c0 && col < c1) {
             pr[w].push_back(i);
-            pc[w].push_back(row[idx[a]].first);
+            pc[w].push_back(col);
             pv[w].push_back(acc);
           }
           a = b;
@@ -189,33 +191,52 @@ void er(int64_t n, int d, uint64_t seed, int value_mode, int64_t* nnz, int64_t**
 }
 
 template <class SR>
-void stencil27(int64_t N, int64_t* nrows, int64_t* nnz, int64_t** rows, int64_t** cols, void** vals) {
+void stencil27(int64_t N, int64_t r0, int64_t r1, int64_t c0, int64_t c1, int64_t* nrows, int64_t* nnz,
+               int64_t** rows, int64_t** cols, void** vals) {
   using V = typename SR::value_type;
   if (N < 1) fail(SPG_ERR_INVALID_RANGE, "stencil27: N must be >= 1");
   const int64_t n = N * N * N;
-  const int64_t m = (3 * N - 2) * (3 * N - 2) * (3 * N - 2);
-  int64_t* r = hmalloc<int64_t>(m);
-  int64_t* c = hmalloc<int64_t>(m);
-  V* v = hmalloc<V>(m);
+  if (r0 < 0 || r1 > n || r0 > r1 || c0 < 0 || c1 > n || c0 > c1) fail(SPG_ERR_INVALID_RANGE, "stencil27: bad block");
   const V diag = SR::from_real(26.0), off = SR::from_real(-1.0);
-  int64_t k = 0;
-  for (int64_t z = 0; z < N; ++z)
-    for (int64_t y = 0; y < N; ++y)
-      for (int64_t x = 0; x < N; ++x) {
-        const int64_t i = (z * N + y) * N + x;
+  // rows are independent: threads take contiguous row ranges, then concatenate
+  const int T = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+  std::vector<std::vector<int64_t>> pr(T), pc(T);
+  std::vector<std::vector<V>> pv(T);
+  std::vector<std::thread> ts;
+  for (int w = 0; w < T; ++w) {
+    ts.emplace_back([&, w] {
+      const int64_t lo = r0 + (r1 - r0) * w / T, hi = r0 + (r1 - r0) * (w + 1) / T;
+      for (int64_t i = lo; i < hi; ++i) {
+        const int64_t x = i % N, y = (i / N) % N, z = i / (N * N);
         for (int dz = -1; dz <= 1; ++dz)
           for (int dy = -1; dy <= 1; ++dy)
             for (int dx = -1; dx <= 1; ++dx) {
               const int64_t zz = z + dz, yy = y + dy, xx = x + dx;
               if (zz < 0 || zz >= N || yy < 0 || yy >= N || xx < 0 || xx >= N) continue;
-              r[k] = i;
-              c[k] = (zz * N + yy) * N + xx;
-              v[k] = (dx == 0 && dy == 0 && dz == 0) ? diag : off;
-              ++k;
+              const int64_t col = (zz * N + yy) * N + xx;
+              if (col < c0 || col >= c1) continue;
+              pr[w].push_back(i);
+              pc[w].push_back(col);
+              pv[w].push_back((dx == 0 && dy == 0 && dz == 0) ? diag : off);
             }
       }
+    });
+  }
+  for (auto& t : ts) t.join();
+  size_t m = 0;
+  for (int w = 0; w < T; ++w) m += pr[w].size();
+  int64_t* r = hmalloc<int64_t>(m);
+  int64_t* c = hmalloc<int64_t>(m);
+  V* v = hmalloc<V>(m);
+  size_t o = 0;
+  for (int w = 0; w < T; ++w) {
+    std::memcpy(r + o, pr[w].data(), sizeof(int64_t) * pr[w].size());
+    std::memcpy(c + o, pc[w].data(), sizeof(int64_t) * pc[w].size());
+    std::memcpy(v + o, pv[w].data(), sizeof(V) * pv[w].size());
+    o += pr[w].size();
+  }
   *nrows = n;
-  *nnz = k;
+  *nnz = (int64_t)m;
   *rows = r;
   *cols = c;
   *vals = v;
@@ -240,12 +261,13 @@ void gen_rmat(int sr, int scale, double ef, uint64_t seed, int64_t* nrows, int64
               int64_t** cols, void** vals) {
   with_builtin(sr, [&](auto t) { rmat<decltype(t)>(scale, ef, seed, nrows, nnz, rows, cols, vals); });
 }
-void gen_er(int sr, int64_t n, int d, uint64_t seed, int mode, int64_t* nnz, int64_t** rows, int64_t** cols,
-            void** vals) {
-  with_builtin(sr, [&](auto t) { er<decltype(t)>(n, d, seed, mode, nnz, rows, cols, vals); });
+void gen_er(int sr, int64_t n, int d, uint64_t seed, int mode, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
+            int64_t* nnz, int64_t** rows, int64_t** cols, void** vals) {
+  with_builtin(sr, [&](auto t) { er<decltype(t)>(n, d, seed, mode, r0, r1, c0, c1, nnz, rows, cols, vals); });
 }
-void gen_stencil27(int sr, int64_t N, int64_t* nrows, int64_t* nnz, int64_t** rows, int64_t** cols, void** vals) {
-  with_builtin(sr, [&](auto t) { stencil27<decltype(t)>(N, nrows, nnz, rows, cols, vals); });
+void gen_stencil27(int sr, int64_t N, int64_t r0, int64_t r1, int64_t c0, int64_t c1, int64_t* nrows, int64_t* nnz,
+                   int64_t** rows, int64_t** cols, void** vals) {
+  with_builtin(sr, [&](auto t) { stencil27<decltype(t)>(N, r0, r1, c0, c1, nrows, nnz, rows, cols, vals); });
 }
 
 }  // namespace spg

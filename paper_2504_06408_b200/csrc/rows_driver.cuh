@@ -247,7 +247,10 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
   int64_t scratch_total = 0;
   SPG_CUDA(cudaMemcpyAsync(hcounts, counts.p, sizeof(hcounts), cudaMemcpyDeviceToHost, c->stream));
   SPG_CUDA(cudaMemcpyAsync(&scratch_total, off.p + m, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
-  SPG_CUDA(cudaStreamSynchronize(c->stream));
+  {
+    HostTrace ht("analyse sync");
+    SPG_CUDA(cudaStreamSynchronize(c->stream));
+  }
   int64_t products = 0;
   if (st) {
     size_t bytes = 0;
@@ -283,13 +286,23 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
   // pass (no stores) gives the exact rowptr, then the same kernels write
   // straight into C at rowptr (no scratch, no compaction, C allocated once).
   size_t budget = c->scratch_budget;
-  if (budget == 0) {
-    size_t fr = 0, tot = 0;
-    SPG_CUDA(cudaMemGetInfo(&fr, &tot));
-    budget = (size_t)(fr * 0.45);
-  }
+  if (budget == 0) budget = (size_t)(mem_available(c) * 0.45);
   const size_t per_entry = sizeof(int32_t) + sizeof(V);
-  const bool two_pass = (size_t)scratch_total * per_entry > budget;
+  bool two_pass = (size_t)scratch_total * per_entry > budget;
+  DBuf<int32_t> sc_cols;
+  DBuf<V> sc_vals;
+  if (!two_pass) {  // the estimate can be stale (other allocators): an OOM here means two passes
+    int32_t* pc = try_dalloc<int32_t>(c, (size_t)scratch_total);
+    V* pv = pc ? try_dalloc<V>(c, (size_t)scratch_total) : nullptr;
+    if (pv) {
+      sc_cols = DBuf<int32_t>::adopt(c, pc, (size_t)scratch_total);
+      sc_vals = DBuf<V>::adopt(c, pv, (size_t)scratch_total);
+    } else {
+      if (pc) dfree(c, pc);
+      two_pass = true;
+      mem_snapshot(c);
+    }
+  }
   tm.mark(1);
 
   DBuf<int64_t> lists(c, m);
@@ -364,8 +377,6 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
   };
 
   if (!two_pass) {
-    DBuf<int32_t> sc_cols(c, (size_t)scratch_total);
-    DBuf<V> sc_vals(c, (size_t)scratch_total);
     numeric(off.p, sc_cols.p, sc_vals.p);
     tm.mark(2);
     ms_numeric = tm.between(1, 2);
@@ -378,6 +389,8 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
                                                                      out->idx, static_cast<V*>(out->vals));
     SPG_LAUNCH_CHECK();
     ++c->launches;
+    sc_cols.reset();
+    sc_vals.reset();
     tm.mark(3);
     ms_compact = tm.between(2, 3);
   } else {

@@ -176,12 +176,17 @@ class DeviceCsr:
 
 def pin(*arrays):
     """Page-lock numpy arrays in place (cudaHostRegister) so their uploads run
-    at full PCIe speed; returns a callable that unpins them."""
+    at full PCIe speed; returns a callable that unpins them.  Pinning is a
+    transfer-speed hint: an array the driver refuses to lock (e.g. beyond
+    the host's lockable-memory limit) stays pageable and still uploads."""
     done = []
     for a in arrays:
         if a is None or a.nbytes == 0:
             continue
-        check(lib.spg_host_register(C.c_void_p(a.ctypes.data), int(a.nbytes)))
+        if lib.spg_host_register(C.c_void_p(a.ctypes.data), int(a.nbytes)) != 0:
+            import sys
+            print(f"[spg] pin: {a.nbytes} B left pageable ({lib.spg_last_error(None).decode()})", file=sys.stderr)
+            continue
         done.append(a)
 
     def unpin():

@@ -61,6 +61,31 @@ def generate_stencil27(sr, N: int) -> CooMatrix:
     return CooMatrix(int(sr), nrows.value, nrows.value, r, c, v)
 
 
+def generate_er_block(sr, n: int, d: int, seed: int, rows: tuple, cols: tuple, value_mode: int = 0) -> CooMatrix:
+    """Block rows[0]:rows[1] x cols[0]:cols[1] of generate_er, LOCAL indices."""
+    sr = as_id(sr)
+    nnz = C.c_int64()
+    r_, c_ = C.POINTER(C.c_int64)(), C.POINTER(C.c_int64)()
+    vals = C.c_void_p()
+    check(lib.spg_generate_er_block(int(sr), int(n), int(d), int(seed), int(value_mode), int(rows[0]), int(rows[1]),
+                                    int(cols[0]), int(cols[1]), C.byref(nnz), C.byref(r_), C.byref(c_),
+                                    C.byref(vals)))
+    r, c, v = _take(sr, nnz.value, r_, c_, vals)
+    return CooMatrix(int(sr), rows[1] - rows[0], cols[1] - cols[0], r - rows[0], c - cols[0], v)
+
+
+def generate_stencil27_block(sr, N: int, rows: tuple, cols: tuple) -> CooMatrix:
+    """Block of generate_stencil27 with LOCAL indices."""
+    sr = as_id(sr)
+    nrows, nnz = C.c_int64(), C.c_int64()
+    r_, c_ = C.POINTER(C.c_int64)(), C.POINTER(C.c_int64)()
+    vals = C.c_void_p()
+    check(lib.spg_generate_stencil27_block(int(sr), int(N), int(rows[0]), int(rows[1]), int(cols[0]), int(cols[1]),
+                                           C.byref(nrows), C.byref(nnz), C.byref(r_), C.byref(c_), C.byref(vals)))
+    r, c, v = _take(sr, nnz.value, r_, c_, vals)
+    return CooMatrix(int(sr), rows[1] - rows[0], cols[1] - cols[0], r - rows[0], c - cols[0], v)
+
+
 def coo_to_csr_fast(m: CooMatrix, to_csc: bool = False):
     """Compression of a normalised COO with the library's host routine."""
     from ._lib import HCsr

@@ -61,10 +61,18 @@ def local_block(m: CooMatrix, pr: int, pc: int, i: int, j: int) -> LocalBlock:
     cb, ce = block_range(m.ncols, pc, j)
     sel = (m.rows >= rb) & (m.rows < re) & (m.cols >= cb) & (m.cols < ce)
     piece = CooMatrix(m.sr, re - rb, ce - cb, m.rows[sel] - rb, m.cols[sel] - cb, m.values[sel])
-    csc = coo_to_csc(piece)
+    return block_from_piece(piece, (rb, re), (cb, ce))
+
+
+def block_from_piece(piece: CooMatrix, rows: tuple, cols: tuple) -> LocalBlock:
+    """LocalBlock from a block's COO in LOCAL indices (e.g. the block
+    generators), DCSC when fewer than half of its columns are populated.
+    `piece` must be normalised (row-major sorted, unique)."""
+    from .generators import coo_to_csr_fast
+    csc = coo_to_csr_fast(piece, to_csc=True)
     populated = int(np.count_nonzero(np.diff(csc.colptr)))
     storage = csc_to_dcsc(csc) if 2 * populated < csc.ncols else csc
-    return LocalBlock(storage, (rb, re), (cb, ce))
+    return LocalBlock(storage, tuple(rows), tuple(cols))
 
 
 def _block_structs(blk: LocalBlock):

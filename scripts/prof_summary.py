@@ -17,7 +17,7 @@ for row in r[2:]:
               'l1tex__throughput.avg.pct_of_peak_sustained_active']:
         print("   ", k, d.get(k))
 if len(sys.argv) > 2:
-    sass = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k", sys.argv[2]],
+    sass = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"] + ([] if sys.argv[2] == "-" else ["-k", sys.argv[2]]),
                           capture_output=True, text=True).stdout
     rows = list(csv.reader(sass.splitlines()))
     hdr = rows[1]

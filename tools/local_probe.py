@@ -1,0 +1,56 @@
+#!/usr/bin/env python
+"""Local multiply probe: C = A.A for one generated matrix on cuda:0, per-bin
+row counts and phase times (spg_mult_stats), repeated --reps times.
+
+    python tools/local_probe.py er --n-log2 16 --d 64 --sr maxtimes --value-mode 1
+    python tools/local_probe.py stencil --N 120 --sr arithmetic
+    python tools/local_probe.py rmat --scale 18 --sr tropical_i32
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("kind", choices=["er", "stencil", "rmat"])
+    ap.add_argument("--n-log2", type=int, default=16)
+    ap.add_argument("--d", type=int, default=64)
+    ap.add_argument("--N", type=int, default=100)
+    ap.add_argument("--scale", type=int, default=16)
+    ap.add_argument("--sr", default="maxtimes")
+    ap.add_argument("--value-mode", type=int, default=0)
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--permute", action="store_true")
+    args = ap.parse_args()
+    from paper_2504_06408_b200 import Context, DeviceCsr, generators, local_multiply
+    from paper_2504_06408_b200.semiring import as_id
+
+    sr = as_id(args.sr)
+    t0 = time.time()
+    if args.kind == "er":
+        coo = generators.generate_er(sr, 1 << args.n_log2, args.d, 1, value_mode=args.value_mode)
+    elif args.kind == "stencil":
+        coo = generators.generate_stencil27(sr, args.N)
+    else:
+        coo = generators.generate_rmat(sr, args.scale, 16.0, 1)
+    if args.permute:
+        coo = generators.permute_symmetric(coo, 1)
+    a = generators.coo_to_csr_fast(coo)
+    print(f"gen {time.time() - t0:.1f}s n={a.nrows} nnz={a.nnz}", file=sys.stderr)
+    ctx = Context(0)
+    d = DeviceCsr.upload(ctx, a)
+    for r in range(args.reps):
+        st = {}
+        c = local_multiply(d, d, stats=st)
+        ctx.sync()
+        print(json.dumps({"rep": r, **st}))
+        c.free()
+
+
+if __name__ == "__main__":
+    main()
