@@ -109,6 +109,8 @@ typedef struct {
   double ms_compact;       /* output scan + compaction */
   double ms_total;
   int64_t kernels;         /* kernels launched by the call */
+  int64_t output_mode;     /* 0: U-slot scratch + compaction, 1: exact claims + compaction,
+                              2: two passes (count, then write into C) */
 } spg_mult_stats;
 
 /* ---------------------------------------------------------------- misc */
@@ -209,6 +211,9 @@ SPG_API int spg_generate_stencil27_block(int sr, int64_t N, int64_t r0, int64_t 
 SPG_API int spg_coo_to_csr(int sr, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rows,
                            const int64_t* cols, const void* vals, int to_csc, spg_hcsr* out);
 SPG_API void spg_free(void* p); /* any host array returned by the library */
+/* Page-locked host memory from the library's caching allocator (plain
+ * malloc when the driver refuses); release with spg_free.  NULL on OOM. */
+SPG_API void* spg_host_alloc(uint64_t bytes);
 /* Page-lock (pin) / unpin caller-owned host memory so uploads run at full
  * PCIe speed (cudaHostRegister; the caller keeps ownership). */
 SPG_API int spg_host_register(void* p, uint64_t bytes);

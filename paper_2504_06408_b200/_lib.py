@@ -40,13 +40,13 @@ class MultStats(C.Structure):
     _fields_ = [("products", C.c_int64), ("nnz_out", C.c_int64),
                 ("rows_per_bin", C.c_int64 * 8), ("ms_analyse", C.c_double),
                 ("ms_numeric", C.c_double), ("ms_compact", C.c_double),
-                ("ms_total", C.c_double), ("kernels", C.c_int64)]
+                ("ms_total", C.c_double), ("kernels", C.c_int64), ("output_mode", C.c_int64)]
 
     def as_dict(self):
         return {"products": self.products, "nnz_out": self.nnz_out,
                 "rows_per_bin": list(self.rows_per_bin), "ms_analyse": self.ms_analyse,
                 "ms_numeric": self.ms_numeric, "ms_compact": self.ms_compact,
-                "ms_total": self.ms_total, "kernels": self.kernels}
+                "ms_total": self.ms_total, "kernels": self.kernels, "output_mode": self.output_mode}
 
 
 class Stage(C.Structure):
@@ -117,6 +117,7 @@ _SIGS = [
                                         C.c_int64, C.c_int64, _i64p, _P(_i64p), _P(_i64p), _P(C.c_void_p)]),
     ("spg_generate_stencil27_block", C.c_int, [C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                                                _i64p, _i64p, _P(_i64p), _P(_i64p), _P(C.c_void_p)]),
+    ("spg_host_alloc", C.c_void_p, [C.c_uint64]),
     ("spg_coo_to_csr", C.c_int, [C.c_int, C.c_int64, C.c_int64, C.c_int64, _i64p, _i64p, C.c_void_p,
                                  C.c_int, _P(HCsr)]),
     ("spg_free", None, [C.c_void_p]),

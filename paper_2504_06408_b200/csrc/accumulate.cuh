@@ -61,7 +61,7 @@ enum Bin : uint8_t {
   kBinEsc512 = 2,    // F <= 512: block-ESC
   kBinHash4K = 3,    // U <= 2048: 4K-slot hash
   kBinHash8K = 4,    // U <= 4096: 8K-slot hash
-  kBinUnused = 5,
+  kBinHash2K = 5,    // U <= 1024: 2K-slot hash, 128 threads (many CTAs per SM)
   kBinDense = 6,     // long rows: dense column panels
   kBinHashMax = 7,   // wide outputs: largest smem hash
 };
@@ -299,6 +299,7 @@ __global__ void __launch_bounds__(256) analyse_rows_kernel(Src src, int64_t ncol
       else if (f <= 32) b = kBinWarpEsc;
       else if (f <= 512 && nseg <= 512) b = kBinEsc512;
       else if (f > kDenseMinRow && dense_ok) b = kBinDense;
+      else if (u <= 1024) b = kBinHash2K;
       else if (u <= 2048) b = kBinHash4K;
       else if (u <= 4096) b = kBinHash8K;
       else if (u <= Geom<V>::kMaxT / 2) b = kBinHashMax;
@@ -385,13 +386,58 @@ static __global__ void __launch_bounds__(256) panel_offsets_kernel(int64_t nrows
 }
 
 // ---------------------------------------------------------------------------
+// Where the row kernels put their output.
+//  * direct: row i starts at off[i] (the exact rowptr of C in the second
+//    pass of two-pass mode);
+//  * exact claim ("bump"): a row, once its nnz is known, claims exactly that
+//    many entries of the scratch with one atomicAdd; dense rows claim one
+//    chunk per column panel.  Scratch holds nnz(C) entries, not the
+//    products bound; a claim past `cap` is not stored (overflow => the
+//    driver reruns in direct mode with the exact rowptr it now has);
+//  * cols == nullptr: count only.
+// ---------------------------------------------------------------------------
+template <class V>
+struct RowOut {
+  int32_t* cols = nullptr;
+  V* vals = nullptr;
+  const int64_t* off = nullptr;
+  unsigned long long* bump = nullptr;
+  int64_t cap = 0;
+  int64_t* rowstart = nullptr;  // claim mode: scratch start of row i (-2: dense row, see chunks)
+  int64_t* chunks = nullptr;    // claim mode, dense rows: (start, count) per (dense slot, panel)
+  int64_t* rownnz = nullptr;
+
+  __device__ __forceinline__ bool writes() const { return cols != nullptr; }
+  __device__ __forceinline__ int64_t claim(int64_t n) const {
+    const unsigned long long b = n ? atomicAdd(bump, (unsigned long long)n) : 0ull;
+    return (int64_t)b + n <= cap ? (int64_t)b : -1;
+  }
+  // base of row i's n entries; -1 = do not store
+  __device__ __forceinline__ int64_t claim_row(int64_t i, int64_t n) const {
+    if (!cols) return -1;
+    if (!bump) return off[i];
+    const int64_t b = claim(n);
+    rowstart[i] = b;
+    return b;
+  }
+  // base of dense row i's panel p chunk (n entries, `written` before it)
+  __device__ __forceinline__ int64_t claim_chunk(int64_t i, int64_t slot, int p, int np, int64_t written,
+                                                 int64_t n) const {
+    if (!cols) return -1;
+    if (!bump) return off[i] + written;
+    const int64_t b = claim(n);
+    chunks[2 * (slot * np + p)] = b;
+    chunks[2 * (slot * np + p) + 1] = n;
+    return b;
+  }
+};
+
+// ---------------------------------------------------------------------------
 // K4 bin 1: warp-ESC for rows with <= 32 products
 // ---------------------------------------------------------------------------
 template <class SR, class Src>
 __global__ void __launch_bounds__(256) esc_warp_kernel(Src src, const int64_t* __restrict__ rows, int64_t nrows_bin,
-                                                       const int64_t* __restrict__ off, int32_t* __restrict__ out_cols,
-                                                       typename SR::value_type* __restrict__ out_vals,
-                                                       int64_t* __restrict__ rownnz) {
+                                                       RowOut<typename SR::value_type> out) {
   using V = typename SR::value_type;
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -434,12 +480,16 @@ __global__ void __launch_bounds__(256) esc_warp_kernel(Src src, const int64_t* _
     const bool keep = tail && !SR::is_zero(val);
     const unsigned m = __ballot_sync(kFull, keep);
     const int pos = __popc(m & ((1u << lane) - 1));
-    const int64_t o = off[i];
-    if (keep && out_cols) {  // out_cols == nullptr: counting pass
-      out_cols[o + pos] = (int32_t)col;
-      out_vals[o + pos] = val;
+    int64_t o = 0;
+    if (lane == 0) {
+      o = out.claim_row(i, __popc(m));
+      out.rownnz[i] = __popc(m);
     }
-    if (lane == 0) rownnz[i] = __popc(m);
+    o = __shfl_sync(kFull, o, 0);
+    if (keep && o >= 0) {
+      out.cols[o + pos] = (int32_t)col;
+      out.vals[o + pos] = val;
+    }
   }
 }
 
@@ -484,12 +534,10 @@ struct EscSmem {
 template <class SR, class Src, int THREADS, int ITEMS>
 __global__ void __launch_bounds__(THREADS) esc_block_kernel(Src src, const int64_t* __restrict__ rows,
                                                             int64_t nrows_bin, int end_bit,
-                                                            const int64_t* __restrict__ off,
-                                                            int32_t* __restrict__ out_cols,
-                                                            typename SR::value_type* __restrict__ out_vals,
-                                                            int64_t* __restrict__ rownnz) {
+                                                            RowOut<typename SR::value_type> out) {
   using V = typename SR::value_type;
   using S = EscSmem<SR, THREADS, ITEMS>;
+  __shared__ long long s_base;
   constexpr int NW = THREADS / 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   S& sm = *reinterpret_cast<S*>(smem_raw);
@@ -564,18 +612,22 @@ __global__ void __launch_bounds__(THREADS) esc_block_kernel(Src src, const int64
     }
     int kfirst, ktotal;
     typename S::Count(sm.tmp.count).ExclusiveSum(nkeep, kfirst, ktotal);
-    const int64_t o = off[i];
+    if (threadIdx.x == 0) {
+      s_base = out.claim_row(i, ktotal);
+      out.rownnz[i] = ktotal;
+    }
+    __syncthreads();
+    const int64_t o = s_base;
 #pragma unroll
     for (int q = 0; q < ITEMS; ++q) {
       if (keep[q]) {
-        if (out_cols) {
-          out_cols[o + kfirst] = (int32_t)k[q];
-          out_vals[o + kfirst] = t[q].v;
+        if (o >= 0) {
+          out.cols[o + kfirst] = (int32_t)k[q];
+          out.vals[o + kfirst] = t[q].v;
         }
         ++kfirst;
       }
     }
-    if (threadIdx.x == 0) rownnz[i] = ktotal;
     __syncthreads();
   }
 }
@@ -775,9 +827,9 @@ struct AddCanCancel {
 };
 
 template <class SR, int W, int THREADS>
-__device__ __forceinline__ int bitmap_emit(typename SR::value_type* acc, uint32_t* bm, int col_base, int64_t out_base,
-                                           int32_t* __restrict__ out_cols,
-                                           typename SR::value_type* __restrict__ out_vals, int* wsum) {
+__device__ __forceinline__ int bitmap_emit(typename SR::value_type* acc, uint32_t* bm, int col_base,
+                                           const RowOut<typename SR::value_type>& out, int64_t row, int64_t slot,
+                                           int panel, int npanels, int64_t written, int* wsum, long long* s_base) {
   using V = typename SR::value_type;
   constexpr int NW = THREADS / 32;
   constexpr int WORDS = W / 32;
@@ -821,10 +873,14 @@ __device__ __forceinline__ int bitmap_emit(typename SR::value_type* acc, uint32_
       if (lane >= d) incl += t;
     }
     if (lane < NW) wsum[NW + lane] = incl - v;
-    if (lane == 31) wsum[2 * NW] = incl;
+    if (lane == 31) {
+      wsum[2 * NW] = incl;
+      *s_base = out.claim_chunk(row, slot, panel, npanels, written, incl);
+    }
   }
   __syncthreads();
-  int64_t pos = out_base + wsum[NW + wid];
+  const bool store = *s_base >= 0;
+  int64_t pos = *s_base + wsum[NW + wid];
   for (int it = 0; it < ITERS; ++it) {
     const int wl = it * 32 + lane;
     const int w = w0 + wl;
@@ -851,9 +907,9 @@ __device__ __forceinline__ int bitmap_emit(typename SR::value_type* acc, uint32_
       if (q < total) {
         const int bit = nth_set_bit(xo, q - eo);
         const int cc = ((w0 + it * 32 + own) << 5) + bit;
-        if (out_cols) {
-          out_cols[pos + q] = col_base + cc;
-          out_vals[pos + q] = acc[cc];
+        if (store) {
+          out.cols[pos + q] = col_base + cc;
+          out.vals[pos + q] = acc[cc];
         }
         acc[cc] = SR::zero();
       }
@@ -883,10 +939,7 @@ template <class SR, class Src, int W, int THREADS>
 __global__ void __launch_bounds__(THREADS) dense_panel_kernel(Src src, const int64_t* __restrict__ rows,
                                                               int64_t nrows_bin, int npanels, int cap,
                                                               unsigned long long* __restrict__ work,
-                                                              const int64_t* __restrict__ off,
-                                                              int32_t* __restrict__ out_cols,
-                                                              typename SR::value_type* __restrict__ out_vals,
-                                                              int64_t* __restrict__ rownnz) {
+                                                              RowOut<typename SR::value_type> out) {
   using V = typename SR::value_type;
   constexpr int NW = THREADS / 32;
   using Count = cub::BlockScan<int, THREADS>;
@@ -896,7 +949,7 @@ __global__ void __launch_bounds__(THREADS) dense_panel_kernel(Src src, const int
   SegCache<SR, Src> cache;
   cache.carve(smem_raw + sizeof(V) * W + sizeof(uint32_t) * (W / 32), cap, npanels);
   __shared__ typename Count::TempStorage scan_tmp;
-  __shared__ long long s_row;
+  __shared__ long long s_row, s_base;
   __shared__ int wsum[2 * NW + 1];
 
   for (int e = threadIdx.x; e < W; e += THREADS) acc[e] = SR::zero();
@@ -919,7 +972,7 @@ __global__ void __launch_bounds__(THREADS) dense_panel_kernel(Src src, const int
       __syncthreads();
     }
     int64_t written = 0;
-    const int64_t o = off[i];
+    if (threadIdx.x == 0 && out.bump) out.rowstart[i] = -2;  // chunked: see out.chunks
     for (int p = 0; p < npanels; ++p) {
       const int lo = p * W;
       for (int64_t c0 = 0; c0 < nseg; c0 += cap) {
@@ -937,9 +990,9 @@ __global__ void __launch_bounds__(THREADS) dense_panel_kernel(Src src, const int
         });
         __syncthreads();
       }
-      written += bitmap_emit<SR, W, THREADS>(acc, bm, lo, o + written, out_cols, out_vals, wsum);
+      written += bitmap_emit<SR, W, THREADS>(acc, bm, lo, out, i, r, p, npanels, written, wsum, &s_base);
     }
-    if (threadIdx.x == 0) rownnz[i] = written;
+    if (threadIdx.x == 0) out.rownnz[i] = written;
   }
 }
 
@@ -996,12 +1049,10 @@ struct HashSort {
 template <class SR, class Src, int T, int THREADS>
 __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64_t* __restrict__ rows,
                                                             int64_t nrows_bin, int cap, int end_bit,
-                                                            const int64_t* __restrict__ off,
-                                                            int32_t* __restrict__ out_cols,
-                                                            typename SR::value_type* __restrict__ out_vals,
-                                                            int64_t* __restrict__ rownnz) {
+                                                            RowOut<typename SR::value_type> out) {
   using V = typename SR::value_type;
   using HS = HashSort<T, THREADS>;
+  __shared__ long long s_base;
   constexpr int SPT = T / THREADS;
   constexpr int ITEMS = HS::ITEMS;
   constexpr int NW = THREADS / 32;
@@ -1058,8 +1109,11 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
     }
     int first, total;
     typename HS::Scan(tmp->scan).ExclusiveSum(cnt, first, total);
-    if (out_cols == nullptr) {  // counting pass: no sort, no output
-      if (threadIdx.x == 0) rownnz[i] = total;
+    if (threadIdx.x == 0) {
+      s_base = out.claim_row(i, total);
+      out.rownnz[i] = total;
+    }
+    if (!out.writes()) {  // counting pass: no sort, no output
       __syncthreads();
       continue;
     }
@@ -1127,12 +1181,12 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
             sslot[my_slots[q] >> 16] = (uint16_t)(my_slots[q] & 0xffff);
           }
         __syncthreads();
-        const int64_t o = off[i];
-        for (int e = threadIdx.x; e < total; e += THREADS) {
-          out_cols[o + e] = (int32_t)skeys[e];
-          out_vals[o + e] = tvals[sslot[e]];
-        }
-        if (threadIdx.x == 0) rownnz[i] = total;
+        const int64_t o = s_base;
+        if (o >= 0)
+          for (int e = threadIdx.x; e < total; e += THREADS) {
+            out.cols[o + e] = (int32_t)skeys[e];
+            out.vals[o + e] = tvals[sslot[e]];
+          }
         __syncthreads();
         continue;
       }
@@ -1158,16 +1212,15 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
     }
     __syncthreads();
     typename HS::Sort(tmp->sort).Sort(k, sl, 0, end_bit + 1);
-    const int64_t o = off[i];
+    const int64_t o = s_base;
 #pragma unroll
     for (int q = 0; q < ITEMS; ++q) {
       const int e = threadIdx.x * ITEMS + q;
-      if (e < total && out_cols) {
-        out_cols[o + e] = (int32_t)k[q];
-        out_vals[o + e] = tvals[sl[q]];
+      if (e < total && o >= 0) {
+        out.cols[o + e] = (int32_t)k[q];
+        out.vals[o + e] = tvals[sl[q]];
       }
     }
-    if (threadIdx.x == 0) rownnz[i] = total;
     __syncthreads();
   }
 }
@@ -1175,6 +1228,28 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
 // ---------------------------------------------------------------------------
 // K7: compaction scratch -> exact CSR (warp per row, 4-way unrolled)
 // ---------------------------------------------------------------------------
+// Dense rows: concatenate their per-panel chunks (CTA per row).
+template <class V>
+__global__ void __launch_bounds__(256) compact_chunks_kernel(const int64_t* __restrict__ rows, int64_t nrows_bin,
+                                                             int npanels, const int64_t* __restrict__ chunks,
+                                                             const int64_t* __restrict__ rowptr,
+                                                             const int32_t* __restrict__ sc_cols,
+                                                             const V* __restrict__ sc_vals, int32_t* __restrict__ cols,
+                                                             V* __restrict__ vals) {
+  for (int64_t r = blockIdx.x; r < nrows_bin; r += gridDim.x) {
+    int64_t d = rowptr[rows[r]];
+    for (int p = 0; p < npanels; ++p) {
+      const int64_t s = chunks[2 * (r * npanels + p)], n = chunks[2 * (r * npanels + p) + 1];
+      for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
+        cols[d + e] = sc_cols[s + e];
+        vals[d + e] = sc_vals[s + e];
+      }
+      d += n;
+    }
+  }
+}
+
+// Other rows: row i sits at off[i] of the scratch (off[i] < 0: skip).
 template <class V>
 __global__ void __launch_bounds__(256) compact_rows_kernel(int64_t nrows, const int64_t* __restrict__ off,
                                                            const int64_t* __restrict__ rowptr,
@@ -1187,7 +1262,9 @@ __global__ void __launch_bounds__(256) compact_rows_kernel(int64_t nrows, const 
   for (int64_t i = warp; i < nrows; i += nwarps) {
     const int64_t d = rowptr[i];
     const int64_t n = rowptr[i + 1] - d;
+    if (n == 0) continue;
     const int64_t s = off[i];
+    if (s < 0) continue;
     int64_t e = lane;
     for (; e + 96 < n; e += 128) {
       const int32_t c0 = sc_cols[s + e], c1 = sc_cols[s + e + 32], c2 = sc_cols[s + e + 64],

@@ -131,8 +131,10 @@ struct PinnedCache {
       }
     }
     void* p = nullptr;
+    HostTrace ht("cudaHostAlloc", cls);
     if (cudaHostAlloc(&p, cls, cudaHostAllocPortable) != cudaSuccess) {
       cudaGetLastError();
+      if (HostTrace::limit_ms() >= 0) std::fprintf(stderr, "[spg-host] cudaHostAlloc(%zu) refused: pageable\n", cls);
       p = std::malloc(n);  // fall back to pageable memory
       if (!p) fail(SPG_ERR_OOM, "host allocation failed");
       return p;
@@ -198,6 +200,7 @@ void download(spg_ctx* c, int vs, const spg_dcsr* d, int is_csc, spg_hcsr* h) {
       SPG_CUDA(cudaMemcpyAsync(h->idx + o, wide.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->stream));
     }
   }
+  HostTrace ht("download sync", (size_t)d->nnz);
   SPG_CUDA(cudaStreamSynchronize(c->stream));
 }
 
@@ -288,6 +291,8 @@ void spg_ctx_destroy(spg_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->cub_tmp) cudaFreeAsync(c->cub_tmp, c->stream);
+  for (auto& kv : c->big_free) cudaFreeAsync(kv.second, c->stream);
+  c->big_free.clear();
   cudaStreamSynchronize(c->stream);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
@@ -554,10 +559,19 @@ int spg_esc_multiply(spg_ctx* c, int sr, const spg_hcsr* a, const spg_hcsr* b, s
                               " by " + std::to_string(b->nrows) + "x" + std::to_string(b->ncols));
     const SrOps* ops = ops_for(sr);
     spg_dcsr da{}, db{}, dc{};
-    upload(c, ops->value_size, a, 0, &da);
-    upload(c, ops->value_size, b, 0, &db);
+    {
+      HostTrace ht("esc upload");
+      upload(c, ops->value_size, a, 0, &da);
+      upload(c, ops->value_size, b, 0, &db);
+      SPG_CUDA(cudaStreamSynchronize(c->stream));
+    }
     try {
-      ops->local_multiply(c, &da, &db, &dc, st);
+      {
+        HostTrace ht("esc local multiply");
+        ops->local_multiply(c, &da, &db, &dc, st);
+        SPG_CUDA(cudaStreamSynchronize(c->stream));
+      }
+      HostTrace ht("esc download");
       download(c, ops->value_size, &dc, 0, out);
     } catch (...) {
       free_dcsr(c, &da);
@@ -645,14 +659,20 @@ int spg_coo_to_csr(int sr, int64_t nrows, int64_t ncols, int64_t nnz, const int6
 
 void spg_free(void* p) { host_release(p); }
 
+void* spg_host_alloc(uint64_t bytes) {
+  try {
+    return pinned().get((size_t)bytes);
+  } catch (...) {
+    return nullptr;
+  }
+}
+
 int spg_host_register(void* p, uint64_t bytes) {
   return guarded(nullptr, [&] {
     if (!p || bytes == 0) return;
     const cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterPortable);
-    if (e == cudaErrorHostMemoryAlreadyRegistered) {
-      cudaGetLastError();
-      return;
-    }
+    if (e != cudaSuccess) cudaGetLastError();  // not sticky: later launches must not see it
+    if (e == cudaErrorHostMemoryAlreadyRegistered) return;
     SPG_CUDA(e);
   });
 }
@@ -661,10 +681,8 @@ int spg_host_unregister(void* p) {
   return guarded(nullptr, [&] {
     if (!p) return;
     const cudaError_t e = cudaHostUnregister(p);
-    if (e == cudaErrorHostMemoryNotRegistered) {
-      cudaGetLastError();
-      return;
-    }
+    if (e != cudaSuccess) cudaGetLastError();
+    if (e == cudaErrorHostMemoryNotRegistered) return;
     SPG_CUDA(e);
   });
 }

@@ -4,10 +4,13 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <unordered_map>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -44,6 +47,12 @@ struct spg_ctx {
   bool own_stream = false;
   cudaMemPool_t pool = nullptr;      // device default pool: small buffers
   cudaMemPool_t big_pool = nullptr;  // private pool for buffers >= kBigAlloc (no fragmentation by small ones)
+  // Cache of large device buffers: freed blocks are kept and handed out
+  // again (stream-ordered on `stream`) to requests of nearly the same size,
+  // so steady-state calls never map fresh memory.
+  std::multimap<size_t, void*> big_free;
+  std::unordered_map<void*, size_t> big_live;
+  size_t big_cached = 0;
   size_t free_snap = 0;              // cudaMemGetInfo free bytes at the last snapshot
   size_t reserved_snap = 0;          // pool bytes reserved at that snapshot
   std::string last_error;
@@ -87,34 +96,72 @@ struct HostTrace {
 // private pool, so the many small per-call buffers never split the big
 // cached blocks (a split forces the pool to map fresh memory: tens of ms).
 constexpr size_t kBigAlloc = size_t(16) << 20;
-template <class T>
-T* dalloc(spg_ctx* c, size_t n) {
-  if (n == 0) n = 1;
-  void* p = nullptr;
-  const size_t bytes = n * sizeof(T);
-  HostTrace ht("cudaMallocAsync", bytes);
-  if (bytes >= kBigAlloc && c->big_pool)
-    SPG_CUDA(cudaMallocFromPoolAsync(&p, bytes, c->big_pool, c->stream));
-  else
-    SPG_CUDA(cudaMallocAsync(&p, bytes, c->stream));
-  return static_cast<T*>(p);
+inline cudaError_t pool_alloc(spg_ctx* c, void** p, size_t bytes) {
+  return (bytes >= kBigAlloc && c->big_pool) ? cudaMallocFromPoolAsync(p, bytes, c->big_pool, c->stream)
+                                             : cudaMallocAsync(p, bytes, c->stream);
 }
-
-// As dalloc, but an out-of-memory result returns nullptr instead of failing.
-template <class T>
-T* try_dalloc(spg_ctx* c, size_t n) {
-  if (n == 0) n = 1;
+// Returns every cached large block to the pool and the pools' idle reserve
+// to the device.
+inline void release_cached(spg_ctx* c) {
+  for (auto& kv : c->big_free) cudaFreeAsync(kv.second, c->stream);
+  c->big_free.clear();
+  c->big_cached = 0;
+  SPG_CUDA(cudaStreamSynchronize(c->stream));
+  SPG_CUDA(cudaMemPoolTrimTo(c->pool, 0));
+  if (c->big_pool) SPG_CUDA(cudaMemPoolTrimTo(c->big_pool, 0));
+}
+// Allocation; large requests first try the block cache (a cached block of
+// size in [need, need * 9/8]).  Out of memory: release the caches, retry
+// once; allow_fail then returns nullptr instead of failing.
+inline void* dalloc_bytes(spg_ctx* c, size_t bytes, bool allow_fail) {
   void* p = nullptr;
-  const size_t bytes = n * sizeof(T);
-  const cudaError_t e = (bytes >= kBigAlloc && c->big_pool)
-                            ? cudaMallocFromPoolAsync(&p, bytes, c->big_pool, c->stream)
-                            : cudaMallocAsync(&p, bytes, c->stream);
+  HostTrace ht("cudaMallocAsync", bytes);
+  const bool big = bytes >= kBigAlloc;
+  if (big) {
+    bytes = (bytes + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1);
+    auto it = c->big_free.lower_bound(bytes);
+    if (it != c->big_free.end() && it->first <= bytes + bytes / 8) {
+      p = it->second;
+      c->big_live[p] = it->first;
+      c->big_cached -= it->first;
+      c->big_free.erase(it);
+      return p;
+    }
+  }
+  cudaError_t e = pool_alloc(c, &p, bytes);
   if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    release_cached(c);
+    e = pool_alloc(c, &p, bytes);
+  }
+  if (e == cudaErrorMemoryAllocation && allow_fail) {
     cudaGetLastError();
     return nullptr;
   }
   SPG_CUDA(e);
-  return static_cast<T*>(p);
+  if (big) c->big_live[p] = bytes;
+  return p;
+}
+// Stream-ordered free; large blocks go back to the cache.
+inline void dfree_bytes(spg_ctx* c, void* p) {
+  if (!p) return;
+  auto it = c->big_live.find(p);
+  if (it != c->big_live.end()) {
+    c->big_free.emplace(it->second, p);
+    c->big_cached += it->second;
+    c->big_live.erase(it);
+    return;
+  }
+  SPG_CUDA(cudaFreeAsync(p, c->stream));
+}
+template <class T>
+T* dalloc(spg_ctx* c, size_t n) {
+  return static_cast<T*>(dalloc_bytes(c, std::max<size_t>(n, 1) * sizeof(T), false));
+}
+// As dalloc, but an out-of-memory result returns nullptr instead of failing.
+template <class T>
+T* try_dalloc(spg_ctx* c, size_t n) {
+  return static_cast<T*>(dalloc_bytes(c, std::max<size_t>(n, 1) * sizeof(T), true));
 }
 
 inline size_t pool_attr(cudaMemPool_t p, cudaMemPoolAttr a) {
@@ -134,15 +181,13 @@ inline void mem_snapshot(spg_ctx* c) {
 // Bytes this context can still allocate: free memory at the snapshot plus
 // what its pools had reserved then, minus what they hold in use now.
 inline size_t mem_available(spg_ctx* c) {
-  const size_t used = pool_attr(c->pool, cudaMemPoolAttrUsedMemCurrent) +
-                      pool_attr(c->big_pool, cudaMemPoolAttrUsedMemCurrent);
+  size_t used = pool_attr(c->pool, cudaMemPoolAttrUsedMemCurrent) +
+                pool_attr(c->big_pool, cudaMemPoolAttrUsedMemCurrent);
+  used = used > c->big_cached ? used - c->big_cached : 0;  // cached blocks are ours to reuse
   const size_t have = c->free_snap + c->reserved_snap;
   return have > used ? have - used : 0;
 }
-inline void dfree(spg_ctx* c, void* p) {
-  HostTrace ht("cudaFreeAsync");
-  if (p) SPG_CUDA(cudaFreeAsync(p, c->stream));
-}
+inline void dfree(spg_ctx* c, void* p) { dfree_bytes(c, p); }
 
 // RAII device buffer (freed stream-ordered on the context stream).
 template <class T>
@@ -162,8 +207,12 @@ struct DBuf {
   }
   ~DBuf() { reset(); }
   void reset() {
-    HostTrace ht("cudaFreeAsync", n * sizeof(T));
-    if (p) cudaFreeAsync(p, c->stream);
+    if (p) {
+      try {
+        dfree_bytes(c, p);
+      } catch (...) {  // destructors must not throw
+      }
+    }
     p = nullptr;
   }
   T* release() { T* q = p; p = nullptr; return q; }

@@ -87,7 +87,7 @@ inline int resident_grid(spg_ctx* c, K kern, int threads, size_t smem, int64_t w
 
 template <class SR, class Src, int T, int THREADS>
 void launch_hash(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* rows, int64_t n, int cap, int end_bit,
-                 const int64_t* off, int32_t* sc_cols, typename SR::value_type* sc_vals, int64_t* rownnz) {
+                 const RowOut<typename SR::value_type>& out) {
   using V = typename SR::value_type;
   const size_t fixed = (size_t)T * (sizeof(V) + sizeof(int32_t)) +
                        ((sizeof(typename HashSort<T, THREADS>::Tmp) + 15) & ~size_t(15)) + 64;
@@ -99,20 +99,18 @@ void launch_hash(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* rows
   const size_t smem = fixed + (size_t)cap * per;
   auto kern = hash_rows_kernel<SR, Src, T, THREADS>;
   set_smem(kern, smem);
-  kern<<<resident_grid(c, kern, THREADS, smem, n), THREADS, smem, s>>>(src, rows, n, cap, end_bit, off, sc_cols,
-                                                                       sc_vals, rownnz);
+  kern<<<resident_grid(c, kern, THREADS, smem, n), THREADS, smem, s>>>(src, rows, n, cap, end_bit, out);
   SPG_LAUNCH_CHECK();
   ++c->launches;
 }
 
 template <class SR, class Src, int THREADS, int ITEMS>
 void launch_esc(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* rows, int64_t n, int end_bit,
-                const int64_t* off, int32_t* sc_cols, typename SR::value_type* sc_vals, int64_t* rownnz) {
+                const RowOut<typename SR::value_type>& out) {
   const size_t smem = sizeof(EscSmem<SR, THREADS, ITEMS>);
   auto kern = esc_block_kernel<SR, Src, THREADS, ITEMS>;
   set_smem(kern, smem);
-  kern<<<resident_grid(c, kern, THREADS, smem, n), THREADS, smem, s>>>(src, rows, n, end_bit, off, sc_cols, sc_vals,
-                                                                       rownnz);
+  kern<<<resident_grid(c, kern, THREADS, smem, n), THREADS, smem, s>>>(src, rows, n, end_bit, out);
   SPG_LAUNCH_CHECK();
   ++c->launches;
 }
@@ -122,8 +120,7 @@ void launch_esc(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* rows,
 // 2 CTAs/SM; cfg 2: 32 KB, 512 threads, 3 CTAs/SM.  SPG_DENSE_CFG overrides.
 template <int W, int DT, class SR, class Src>
 void launch_dense_cfg(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* rows, int64_t n, int64_t ncols,
-                      size_t smem_budget, unsigned long long* work, const int64_t* off, int32_t* sc_cols,
-                      typename SR::value_type* sc_vals, int64_t* rownnz) {
+                      size_t smem_budget, unsigned long long* work, const RowOut<typename SR::value_type>& out) {
   using V = typename SR::value_type;
   const int np = (int)((ncols + W - 1) / W);
   const size_t per_seg = SegCache<SR, Src>::bytes_per_seg(np);
@@ -134,7 +131,7 @@ void launch_dense_cfg(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t*
   const size_t smem = fixed + (size_t)cap * per_seg + 64;
   auto kern = dense_panel_kernel<SR, Src, W, DT>;
   set_smem(kern, smem);
-  kern<<<resident_grid(c, kern, DT, smem, n), DT, smem, s>>>(src, rows, n, np, cap, work, off, sc_cols, sc_vals, rownnz);
+  kern<<<resident_grid(c, kern, DT, smem, n), DT, smem, s>>>(src, rows, n, np, cap, work, out);
   SPG_LAUNCH_CHECK();
   ++c->launches;
 }
@@ -155,23 +152,22 @@ inline int dense_panel_width() {
 
 template <class SR, class Src>
 void launch_dense(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* rows, int64_t n, int64_t ncols,
-                  unsigned long long* work, const int64_t* off, int32_t* sc_cols, typename SR::value_type* sc_vals,
-                  int64_t* rownnz) {
+                  unsigned long long* work, const RowOut<typename SR::value_type>& out) {
   using V = typename SR::value_type;
   constexpr int PW = Geom<V>::kPanelW;
   switch (dense_cfg()) {
     case 1:
-      launch_dense_cfg<PW / 2, 512, SR, Src>(c, s, src, rows, n, ncols, 110 * 1024, work, off, sc_cols, sc_vals, rownnz);
+      launch_dense_cfg<PW / 2, 512, SR, Src>(c, s, src, rows, n, ncols, 110 * 1024, work, out);
       break;
     case 2:
-      launch_dense_cfg<PW / 4, 512, SR, Src>(c, s, src, rows, n, ncols, 72 * 1024, work, off, sc_cols, sc_vals, rownnz);
+      launch_dense_cfg<PW / 4, 512, SR, Src>(c, s, src, rows, n, ncols, 72 * 1024, work, out);
       break;
     case 3:
-      launch_dense_cfg<PW / 2, 256, SR, Src>(c, s, src, rows, n, ncols, 74 * 1024, work, off, sc_cols, sc_vals, rownnz);
+      launch_dense_cfg<PW / 2, 256, SR, Src>(c, s, src, rows, n, ncols, 74 * 1024, work, out);
       break;
 
     default:
-      launch_dense_cfg<PW, 1024, SR, Src>(c, s, src, rows, n, ncols, 220 * 1024, work, off, sc_cols, sc_vals, rownnz);
+      launch_dense_cfg<PW, 1024, SR, Src>(c, s, src, rows, n, ncols, 220 * 1024, work, out);
   }
 }
 
@@ -207,7 +203,7 @@ inline bool needs_poff(const MergeSource<SR>&) {
 // of the dense bin for a MulSource.
 template <class SR, class Src>
 void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, spg_mult_stats* st,
-              const spg_dcsr* r_for_panels = nullptr) {
+              const spg_dcsr* r_for_panels = nullptr, bool* two_pass_out = nullptr) {
   using V = typename SR::value_type;
   const int64_t m = src_in.nrows;
   PhaseTimer tm(c, st != nullptr);
@@ -280,34 +276,47 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
   int end_bit = 0;
   while ((int64_t{1} << end_bit) < ncols_out) ++end_bit;
 
-  // Output strategy.  Single pass: every row writes into a scratch slot of
-  // U_i entries, then a compaction copies the exact rows into C.  When the
-  // scratch would not fit the budget (very large C), two passes: a counting
-  // pass (no stores) gives the exact rowptr, then the same kernels write
-  // straight into C at rowptr (no scratch, no compaction, C allocated once).
+  // Output strategy.
+  //  * sum U_i entries fit the budget: each row writes into its own U_i slot
+  //    of the scratch (direct placement at the U prefix), then a streaming
+  //    compaction copies the exact rows into C;
+  //  * otherwise exact-claim mode: each row (dense rows: each panel chunk)
+  //    claims exactly its nnz in a scratch of `budget` bytes, then the
+  //    compaction gathers the rows into C in row order;
+  //  * if even the claims overflow (C too large to sit in HBM twice), that
+  //    pass has still produced the exact rowptr: C is allocated once and the
+  //    same kernels run again writing straight into it.
   size_t budget = c->scratch_budget;
   if (budget == 0) budget = (size_t)(mem_available(c) * 0.45);
   const size_t per_entry = sizeof(int32_t) + sizeof(V);
-  bool two_pass = (size_t)scratch_total * per_entry > budget;
+  int64_t cap = std::min<int64_t>(scratch_total, (int64_t)(budget / per_entry));
   DBuf<int32_t> sc_cols;
   DBuf<V> sc_vals;
-  if (!two_pass) {  // the estimate can be stale (other allocators): an OOM here means two passes
-    int32_t* pc = try_dalloc<int32_t>(c, (size_t)scratch_total);
-    V* pv = pc ? try_dalloc<V>(c, (size_t)scratch_total) : nullptr;
+  while (cap > 0) {  // the estimate can be stale (other allocators): shrink on OOM
+    int32_t* pc = try_dalloc<int32_t>(c, (size_t)cap);
+    V* pv = pc ? try_dalloc<V>(c, (size_t)cap) : nullptr;
     if (pv) {
-      sc_cols = DBuf<int32_t>::adopt(c, pc, (size_t)scratch_total);
-      sc_vals = DBuf<V>::adopt(c, pv, (size_t)scratch_total);
-    } else {
-      if (pc) dfree(c, pc);
-      two_pass = true;
-      mem_snapshot(c);
+      sc_cols = DBuf<int32_t>::adopt(c, pc, (size_t)cap);
+      sc_vals = DBuf<V>::adopt(c, pv, (size_t)cap);
+      break;
     }
+    if (pc) dfree(c, pc);
+    mem_snapshot(c);
+    cap = cap < (int64_t{1} << 20) ? 0 : cap / 2;
+  }
+  const int npc = std::max(np, 1);
+  const bool slotted = cap > 0 && cap == scratch_total;  // U_i slots: no claims needed
+  DBuf<int64_t> rowstart, chunks;
+  DBuf<unsigned long long> bump(c, 1);
+  if (cap > 0 && !slotted) {
+    rowstart = DBuf<int64_t>(c, (size_t)m);
+    if (hcounts[kBinDense] > 0) chunks = DBuf<int64_t>(c, (size_t)hcounts[kBinDense] * npc * 2);
+    SPG_CUDA(cudaMemsetAsync(bump.p, 0, sizeof(unsigned long long), c->stream));
   }
   tm.mark(1);
 
   DBuf<int64_t> lists(c, m);
   DBuf<unsigned long long> cursor(c, kNumBins);
-  float ms_numeric = 0.f, ms_compact = 0.f;
   unsigned long long base[kNumBins];
   {
     unsigned long long acc = 0;
@@ -346,65 +355,93 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
     ++c->launches;
   }
   DBuf<unsigned long long> work(c, 1);
+  float ms_numeric = 0.f, ms_compact = 0.f;
 
-  // One numeric pass over all bins; `offs` = per-row output offsets, outputs
-  // null for a counting pass.
-  auto numeric = [&](const int64_t* offs, int32_t* ocols, V* ovals) {
+  // One numeric pass over all bins with output placement `o`.
+  auto numeric = [&](const RowOut<V>& o) {
     SPG_CUDA(cudaMemsetAsync(work.p, 0, sizeof(unsigned long long), c->stream));
     const int64_t* lb = lists.p;
     StreamFork fk(c, 3);
-    if (nd > 0) launch_dense<SR, Src>(c, fk[0], src, dense_rows, nd, ncols_out, work.p, offs, ocols, ovals, rownnz.p);
+    if (nd > 0) launch_dense<SR, Src>(c, fk[0], src, dense_rows, nd, ncols_out, work.p, o);
     if (hcounts[kBinHashMax] > 0)
       launch_hash<SR, Src, Geom<V>::kMaxT, 1024>(c, fk[1], src, lb + base[kBinHashMax], hcounts[kBinHashMax],
-                                                 V_hash_cap<V>(Geom<V>::kMaxT), end_bit, offs, ocols, ovals,
-                                                 rownnz.p);
+                                                 V_hash_cap<V>(Geom<V>::kMaxT), end_bit, o);
     if (hcounts[kBinHash8K] > 0)
-      launch_hash<SR, Src, 8192, 512>(c, fk[1], src, lb + base[kBinHash8K], hcounts[kBinHash8K], 1024, end_bit, offs,
-                                      ocols, ovals, rownnz.p);
+      launch_hash<SR, Src, 8192, 512>(c, fk[1], src, lb + base[kBinHash8K], hcounts[kBinHash8K], 1024, end_bit, o);
     if (hcounts[kBinHash4K] > 0)
-      launch_hash<SR, Src, 4096, 256>(c, fk[2], src, lb + base[kBinHash4K], hcounts[kBinHash4K], 512, end_bit, offs,
-                                      ocols, ovals, rownnz.p);
+      launch_hash<SR, Src, 4096, 256>(c, fk[2], src, lb + base[kBinHash4K], hcounts[kBinHash4K], 512, end_bit, o);
+    if (hcounts[kBinHash2K] > 0)
+      launch_hash<SR, Src, 2048, 128>(c, fk[2], src, lb + base[kBinHash2K], hcounts[kBinHash2K], 256, end_bit, o);
     if (hcounts[kBinEsc512] > 0)
-      launch_esc<SR, Src, 128, 4>(c, fk[2], src, lb + base[kBinEsc512], hcounts[kBinEsc512], end_bit, offs, ocols,
-                                  ovals, rownnz.p);
+      launch_esc<SR, Src, 128, 4>(c, fk[2], src, lb + base[kBinEsc512], hcounts[kBinEsc512], end_bit, o);
     if (hcounts[kBinWarpEsc] > 0) {
       esc_warp_kernel<SR, Src><<<grid_for(c, hcounts[kBinWarpEsc], 8), 256, 0, fk[2]>>>(
-          src, lb + base[kBinWarpEsc], hcounts[kBinWarpEsc], offs, ocols, ovals, rownnz.p);
+          src, lb + base[kBinWarpEsc], hcounts[kBinWarpEsc], o);
       SPG_LAUNCH_CHECK();
       ++c->launches;
     }
     fk.join();
   };
 
-  if (!two_pass) {
-    numeric(off.p, sc_cols.p, sc_vals.p);
-    tm.mark(2);
-    ms_numeric = tm.between(1, 2);
-    exclusive_scan(c, rownnz.p, out->ptr, m + 1);
-    const int64_t nnz = d2h_scalar(c, out->ptr + m);
-    out->nnz = nnz;
-    out->idx = dalloc<int32_t>(c, (size_t)nnz);
-    out->vals = dalloc<V>(c, (size_t)nnz);
-    compact_rows_kernel<V><<<grid_for(c, m, 8), 256, 0, c->stream>>>(m, off.p, out->ptr, sc_cols.p, sc_vals.p,
-                                                                     out->idx, static_cast<V*>(out->vals));
+  RowOut<V> first;
+  first.rownnz = rownnz.p;
+  if (cap > 0) {
+    first.cols = sc_cols.p;
+    first.vals = sc_vals.p;
+    if (slotted) {
+      first.off = off.p;
+    } else {
+      first.bump = bump.p;
+      first.cap = cap;
+      first.rowstart = rowstart.p;
+      first.chunks = chunks.p;
+    }
+  }
+  numeric(first);
+  exclusive_scan(c, rownnz.p, out->ptr, m + 1);
+  const int64_t nnz = d2h_scalar(c, out->ptr + m);
+  const unsigned long long claimed = cap > 0 && !slotted ? d2h_scalar(c, bump.p) : 0ull;
+  const bool fits = slotted || (cap > 0 && (int64_t)claimed <= cap);
+  tm.mark(2);
+  ms_numeric = tm.between(1, 2);
+  if (!fits) {  // second pass straight into C (the scratch is released first)
+    sc_cols.reset();
+    sc_vals.reset();
+  }
+  out->nnz = nnz;
+  out->idx = dalloc<int32_t>(c, (size_t)nnz);
+  out->vals = dalloc<V>(c, (size_t)nnz);
+  if (fits) {
+    compact_rows_kernel<V><<<grid_for(c, m, 8), 256, 0, c->stream>>>(m, slotted ? off.p : rowstart.p, out->ptr,
+                                                                     sc_cols.p, sc_vals.p, out->idx,
+                                                                     static_cast<V*>(out->vals));
     SPG_LAUNCH_CHECK();
     ++c->launches;
+    if (nd > 0 && !slotted) {
+      compact_chunks_kernel<V><<<grid_for(c, nd, 1, 8), 256, 0, c->stream>>>(
+          dense_rows, nd, npc, chunks.p, out->ptr, sc_cols.p, sc_vals.p, out->idx, static_cast<V*>(out->vals));
+      SPG_LAUNCH_CHECK();
+      ++c->launches;
+    }
     sc_cols.reset();
     sc_vals.reset();
     tm.mark(3);
     ms_compact = tm.between(2, 3);
   } else {
-    numeric(off.p, nullptr, nullptr);  // counting pass
-    exclusive_scan(c, rownnz.p, out->ptr, m + 1);
-    const int64_t nnz = d2h_scalar(c, out->ptr + m);
-    out->nnz = nnz;
-    out->idx = dalloc<int32_t>(c, (size_t)nnz);
-    out->vals = dalloc<V>(c, (size_t)nnz);
-    numeric(out->ptr, out->idx, static_cast<V*>(out->vals));  // writes straight into C
-    tm.mark(2);
-    ms_numeric = tm.between(1, 2);
+    RowOut<V> direct;
+    direct.cols = out->idx;
+    direct.vals = static_cast<V*>(out->vals);
+    direct.off = out->ptr;
+    direct.rownnz = rownnz.p;
+    numeric(direct);
     tm.mark(3);
+    ms_numeric += tm.between(2, 3);
   }
+  if (two_pass_out) *two_pass_out = !fits;
+  if (HostTrace::limit_ms() >= 0)
+    std::fprintf(stderr, "[spg-host] rows=%lld U=%lld cap=%lld nnz=%lld claimed=%llu budget=%zu mode=%d\n",
+                 (long long)m, (long long)scratch_total, (long long)cap, (long long)nnz, claimed, budget,
+                 !fits ? 2 : slotted ? 0 : 1);
   if (st) {
     tm.mark(3);
     st->products = products;
@@ -415,6 +452,7 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
     st->ms_total = tm.between(0, 3);
     st->ms_analyse = st->ms_total - ms_numeric - ms_compact;
     st->kernels = (int64_t)(c->launches - launches0);
+    st->output_mode = !fits ? 2 : slotted ? 0 : 1;
   }
 }
 

@@ -107,6 +107,19 @@ def view_owned(ptr, n: int, dt) -> np.ndarray:
     return raw[: n * dt.itemsize].view(dt)
 
 
+def pinned_copy(a: np.ndarray) -> np.ndarray:
+    """Copy of `a` in page-locked host memory from the library's pinned
+    cache (uploads from it run at full PCIe speed; no cudaHostRegister, whose
+    page locking the host may cap)."""
+    a = np.ascontiguousarray(a)
+    p = lib.spg_host_alloc(max(a.nbytes, 1))
+    if not p:
+        raise MemoryError(f"spg_host_alloc({a.nbytes}) failed")
+    out = view_owned(C.c_void_p(p), a.size, a.dtype).reshape(a.shape)
+    np.copyto(out, a)
+    return out
+
+
 def take_hcsr(sr, h: HCsr, is_csc: bool):
     """Wrap a library-allocated spg_hcsr as numpy arrays (zero copy)."""
     nseg = h.ncols if is_csc else h.nrows

@@ -7,6 +7,7 @@ import oracle_bind as ob
 from helpers import RTOL, assert_same, to_mat, unpack
 from paper_2504_06408_b200 import (DeviceCsr, errors, esc_multiply, generators, local_multiply,
                                    matrix_checksum, merge_partials)
+from paper_2504_06408_b200._lib import lib
 from paper_2504_06408_b200.formats import CscMatrix, CsrMatrix, coo_to_csr
 
 pytestmark = pytest.mark.gpu
@@ -93,7 +94,7 @@ def test_every_bin_against_oracle(ctx, sr):
     assert_same(got, want, sr)
     bins = st["rows_per_bin"]
     assert bins[0] == 2 and bins[1] >= 1 and bins[6] >= 1, bins
-    assert sum(bins[2:6]) >= 3
+    assert sum(bins[2:6]) >= 3 and bins[5] >= 1
 
 
 @pytest.mark.parametrize("sr", [1, 2, 4])
@@ -114,16 +115,25 @@ def test_rmat14_against_reference_checksum(golden, ctx, sr):
 
 
 @pytest.mark.parametrize("sr", [0, 2, 4, 5])
-def test_two_pass_mode_matches_single_pass(ctx, sr):
+def test_output_modes_agree(ctx, sr):
+    """The three output strategies (U-slot scratch, exact claims, two passes)
+    produce the same C; the scratch budget selects the strategy."""
     m = coo_to_csr(generators.generate_rmat(sr, 13, 16.0, 5))
     d = DeviceCsr.upload(ctx, m)
-    full = local_multiply(d, d)
-    ctx.set_scratch_budget(1 << 20)  # 1 MB: forces the count-then-write mode
-    try:
-        small = local_multiply(d, d)
-    finally:
-        ctx.set_scratch_budget(0)
-    assert_same(small.download(), full.download(), sr, rtol=RTOL)
+    st = {}
+    full = local_multiply(d, d, stats=st)
+    assert st["output_mode"] == 0
+    per = 4 + int(lib.spg_value_size(sr))
+    want = full.download()
+    for budget, mode in ((int(st["nnz_out"] * per * 1.02), 1), (1 << 20, 2)):
+        ctx.set_scratch_budget(budget)
+        try:
+            st2 = {}
+            got = local_multiply(d, d, stats=st2)
+        finally:
+            ctx.set_scratch_budget(0)
+        assert st2["output_mode"] == mode
+        assert_same(got.download(), want, sr, rtol=RTOL)
 
 
 @pytest.mark.parametrize("sr", [0, 1, 2, 4, 5])

@@ -87,6 +87,26 @@ def test_er_and_stencil_generators():
         assert set(np.unique(s.values)) == {-1.0, 26.0}
 
 
+@pytest.mark.parametrize("grid", [(1, 2), (2, 2), (2, 4)])
+def test_block_generators_equal_blocks_of_the_full_matrix(grid):
+    """Each rank generates only its block (bench configs 4/5): the union of
+    the blocks is exactly the full generator's matrix."""
+    from paper_2504_06408_b200.summa import block_range
+    pr, pc = grid
+    full = {"er": generators.generate_er(5, 900, 12, 7, value_mode=1), "st": generators.generate_stencil27(0, 7)}
+    for name, m in full.items():
+        n = m.nrows
+        for i in range(pr):
+            for j in range(pc):
+                rr, cr = block_range(n, pr, i), block_range(n, pc, j)
+                b = (generators.generate_er_block(5, n, 12, 7, rr, cr, value_mode=1) if name == "er"
+                     else generators.generate_stencil27_block(0, 7, rr, cr))
+                sel = (m.rows >= rr[0]) & (m.rows < rr[1]) & (m.cols >= cr[0]) & (m.cols < cr[1])
+                assert (b.nrows, b.ncols) == (rr[1] - rr[0], cr[1] - cr[0])
+                assert np.array_equal(b.rows, m.rows[sel] - rr[0]) and np.array_equal(b.cols, m.cols[sel] - cr[0])
+                assert b.values.tobytes() == m.values[sel].tobytes()
+
+
 @pytest.mark.skipif(ob.ref is None, reason="reference harness not built")
 def test_block_and_round_ranges_match_reference():
     for n in (0, 1, 5, 7, 64, 1001):
