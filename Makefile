@@ -24,12 +24,22 @@ $(BUILD)/%.cpp.o: $(SRC)/%.cpp $(HDRS)
 	$(NVCC) $(NVFLAGS) -x c++ -c $< -o $@
 
 $(LIB): $(OBJS)
+	@mkdir -p $(dir $@)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lnccl -lrt -lpthread
 
 oracle:
 	$(MAKE) -C oracle
 
+# A/B tuning builds: make variant VNAME=x VFLAGS="-DSPG_SEG_MODE=0" -> variants/x/libspgemm_b200.so
+# (loaded only when SPG_LIB_PATH points at it)
+VNAME ?= v
+VFLAGS ?=
+variant:
+	$(MAKE) BUILD=build_$(VNAME) LIB=variants/$(VNAME)/libspgemm_b200.so NVFLAGS="$(NVFLAGS) $(VFLAGS)" \
+	    variants/$(VNAME)/libspgemm_b200.so
+	@mkdir -p variants/$(VNAME)
+
 clean:
 	rm -rf $(BUILD) $(LIB)
 
-.PHONY: all oracle clean
+.PHONY: all oracle clean variant

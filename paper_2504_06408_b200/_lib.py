@@ -12,7 +12,7 @@ import os
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libspgemm_b200.so")
+LIB_PATH = os.environ.get("SPG_LIB_PATH") or os.path.join(_HERE, "libspgemm_b200.so")  # override: A/B builds
 
 
 class HCsr(C.Structure):

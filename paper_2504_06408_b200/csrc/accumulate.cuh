@@ -718,7 +718,17 @@ struct SegCache {
 
 // Warp `wid` of NW enumerates its equal share of the cached segments' items
 // (panel p); f(col, value) per item, two items per lane in flight.
-template <class SR, class Src, int NW, class F>
+// SPG_SEG_MODE (compile time, default off: measured no gain on R-MAT): when the warp's share averages
+// >= kSegmentMinAvg items per segment, walk segments whole-warp instead.
+#ifndef SPG_SEG_MODE
+#define SPG_SEG_MODE 0
+#endif
+constexpr bool kSegmentMode = SPG_SEG_MODE != 0;
+#ifndef SPG_SEG_MIN_AVG
+#define SPG_SEG_MIN_AVG 48
+#endif
+constexpr int kSegmentMinAvg = SPG_SEG_MIN_AVG;
+template <class SR, class Src, int NW, int IPL = 2, class F>
 __device__ __forceinline__ void balanced_items(const Src& src, const SegCache<SR, Src>& c, int n, int p, F&& f) {
   using V = typename SR::value_type;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -730,6 +740,43 @@ __device__ __forceinline__ void balanced_items(const Src& src, const SegCache<SR
     const int mid = (s + hs) >> 1;
     if (c.pre[mid] <= lo_q) s = mid;
     else hs = mid;
+  }
+  if constexpr (kSegmentMode) {
+    // Long slices: the whole warp walks one segment at a time (no per-item
+    // segment search), four items per lane in flight.
+    int e = s, he = n;  // largest e with pre[e] < hi_q
+    while (he - e > 1) {
+      const int mid = (e + he) >> 1;
+      if (c.pre[mid] < hi_q) e = mid;
+      else he = mid;
+    }
+    if ((hi_q - lo_q) >= kSegmentMinAvg * (e - s + 1)) {
+      for (int t = s; t <= e; ++t) {
+        int64_t bb;
+        int ln, sd;
+        V m;
+        c.get(t, p, bb, ln, sd, m);
+        const int st = c.pre[t];
+        const int beg = st > lo_q ? st : lo_q;
+        const int end = (st + ln) < hi_q ? (st + ln) : hi_q;
+        const int L = end - beg;
+        bb += beg - st;
+        for (int q = lane; q < L; q += 128) {
+          int32_t cc[4];
+          V xx[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (q + 32 * u < L) {
+              cc[u] = src.col(sd, bb + q + 32 * u);
+              xx[u] = src.val(sd, bb + q + 32 * u);
+            }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (q + 32 * u < L) f(cc[u], src.item(m, xx[u]));
+        }
+      }
+      return;
+    }
   }
   for (int s0 = s; s0 < n && c.pre[s0] < hi_q; s0 += 32) {
     const int t = s0 + lane;
@@ -753,42 +800,37 @@ __device__ __forceinline__ void balanced_items(const Src& src, const SegCache<SR
     }
     const int total = __shfl_sync(kFull, incl, 31);
     const int excl = incl - L;
-    for (int q0 = 0; q0 < total; q0 += 64) {
-      const int qa = q0 + lane, qb = q0 + 32 + lane;
-      int pa = 0, pb = 0;
+    for (int q0 = 0; q0 < total; q0 += 32 * IPL) {
+      int pos[IPL];
+#pragma unroll
+      for (int u = 0; u < IPL; ++u) pos[u] = 0;
 #pragma unroll
       for (int step = 16; step >= 1; step >>= 1) {
-        const int va = __shfl_sync(kFull, incl, pa + step - 1);
-        const int vb = __shfl_sync(kFull, incl, pb + step - 1);
-        if (va <= qa) pa += step;
-        if (vb <= qb) pb += step;
+#pragma unroll
+        for (int u = 0; u < IPL; ++u) {
+          const int v = __shfl_sync(kFull, incl, pos[u] + step - 1);
+          if (v <= q0 + 32 * u + lane) pos[u] += step;
+        }
       }
-      const long long ba = __shfl_sync(kFull, (long long)bb, pa);
-      const long long b2 = __shfl_sync(kFull, (long long)bb, pb);
-      const int ea = __shfl_sync(kFull, excl, pa);
-      const int eb = __shfl_sync(kFull, excl, pb);
-      const V ma = shfl_v(m, pa);
-      const V mb = shfl_v(m, pb);
-      int sa = 0, s2 = 0;
-      if constexpr (Src::kMultiSrc) {
-        sa = __shfl_sync(kFull, sd, pa);
-        s2 = __shfl_sync(kFull, sd, pb);
+      int32_t cc[IPL];
+      V xx[IPL], mm[IPL];
+#pragma unroll
+      for (int u = 0; u < IPL; ++u) {
+        const int q = q0 + 32 * u + lane;
+        const long long bu = __shfl_sync(kFull, (long long)bb, pos[u]);
+        const int eu = __shfl_sync(kFull, excl, pos[u]);
+        mm[u] = shfl_v(m, pos[u]);
+        int su = 0;
+        if constexpr (Src::kMultiSrc) su = __shfl_sync(kFull, sd, pos[u]);
+        if (q < total) {
+          const int64_t w = bu + (q - eu);
+          cc[u] = src.col(su, w);
+          xx[u] = src.val(su, w);
+        }
       }
-      int32_t ca = 0, cb = 0;
-      V xa{}, xb{};
-      const bool oka = qa < total, okb = qb < total;
-      if (oka) {
-        const int64_t u = ba + (qa - ea);
-        ca = src.col(sa, u);
-        xa = src.val(sa, u);
-      }
-      if (okb) {
-        const int64_t u = b2 + (qb - eb);
-        cb = src.col(s2, u);
-        xb = src.val(s2, u);
-      }
-      if (oka) f(ca, src.item(ma, xa));
-      if (okb) f(cb, src.item(mb, xb));
+#pragma unroll
+      for (int u = 0; u < IPL; ++u)
+        if (q0 + 32 * u + lane < total) f(cc[u], src.item(mm[u], xx[u]));
     }
   }
 }
@@ -935,6 +977,10 @@ __device__ __forceinline__ int bitmap_emit(typename SR::value_type* acc, uint32_
 // it goes, so no panel ever needs a separate clear.  Rows with more
 // segments than the cache holds are processed in segment batches per panel.
 // ---------------------------------------------------------------------------
+#ifndef SPG_DENSE_IPL
+#define SPG_DENSE_IPL 2
+#endif
+constexpr int kDenseIPL = SPG_DENSE_IPL;  // items per lane in flight in the dense product loop
 template <class SR, class Src, int W, int THREADS>
 __global__ void __launch_bounds__(THREADS) dense_panel_kernel(Src src, const int64_t* __restrict__ rows,
                                                               int64_t nrows_bin, int npanels, int cap,
@@ -982,7 +1028,7 @@ __global__ void __launch_bounds__(THREADS) dense_panel_kernel(Src src, const int
           __syncthreads();
         }
         cache.template prefix<THREADS, Count>(n, p, scan_tmp);
-        balanced_items<SR, Src, NW>(src, cache, n, p, [&](int32_t c, const V& v) {
+        balanced_items<SR, Src, NW, kDenseIPL>(src, cache, n, p, [&](int32_t c, const V& v) {
           if (SR::is_zero(v)) return;  // add(x, zero) == x: nothing to fold
           const int cc = c - lo;
           const V old = atomic_accumulate<SR, true>(&acc[cc], v);
@@ -1037,11 +1083,8 @@ __device__ __forceinline__ uint32_t hash_slot(uint32_t col, int log2t) {
 // ---------------------------------------------------------------------------
 template <int T, int THREADS>
 struct HashSort {
-  static constexpr int ITEMS = T / 2 / THREADS;  // occupied slots <= T/2 (load factor 1/2)
-  using Sort = cub::BlockRadixSort<uint32_t, THREADS, ITEMS, uint16_t, 4>;
   using Scan = cub::BlockScan<int, THREADS>;
   union Tmp {
-    typename Sort::TempStorage sort;
     typename Scan::TempStorage scan;
   };
 };
@@ -1054,19 +1097,26 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
   using HS = HashSort<T, THREADS>;
   __shared__ long long s_base;
   constexpr int SPT = T / THREADS;
-  constexpr int ITEMS = HS::ITEMS;
   constexpr int NW = THREADS / 32;
+  constexpr int NB = T / 2, NBT = NB / THREADS, kBucketMax = 32;
+  static_assert(NB % THREADS == 0, "bucket count must divide by the CTA size");
   constexpr int LOG2T = (T == 512) ? 9 : (T == 1024) ? 10 : (T == 2048) ? 11 : (T == 4096) ? 12
                       : (T == 8192) ? 13 : (T == 16384) ? 14 : 15;
   static_assert((1 << LOG2T) == T, "T must be a power of two");
-  static_assert(T <= 65536 * 2, "slot ids must fit 16 bits");
+  static_assert(T <= 65536, "slot ids must fit 16 bits");
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  // layout: values [T] | keys [T] (later: bucket starts [T/2] + bucketed keys [T/2])
+  //         | staging: keys [T/2] + (slot | rank << 16) [T/2] | cub temp | segment cache
   V* tvals = reinterpret_cast<V*>(smem_raw);
   int32_t* tkeys = reinterpret_cast<int32_t*>(smem_raw + sizeof(V) * T);
-  typename HS::Tmp* tmp = reinterpret_cast<typename HS::Tmp*>(smem_raw + (sizeof(V) + sizeof(int32_t)) * T);
-  uint32_t* sorted_keys = reinterpret_cast<uint32_t*>(tkeys);  // after compaction, keys are dead
+  uint32_t* stg_key = reinterpret_cast<uint32_t*>(tkeys + T);
+  uint32_t* stg_slot = stg_key + T / 2;
+  typename HS::Tmp* tmp = reinterpret_cast<typename HS::Tmp*>(stg_slot + T / 2);
+  int* bstart = tkeys;                                        // after staging
+  uint32_t* bkeys = reinterpret_cast<uint32_t*>(tkeys) + NB;  // after staging
   SegCache<SR, Src> cache;
   cache.carve(reinterpret_cast<unsigned char*>(tmp) + ((sizeof(typename HS::Tmp) + 15) & ~size_t(15)), cap, 1);
+  const int shift = end_bit > LOG2T - 1 ? end_bit - (LOG2T - 1) : 0;
   for (int64_t r = blockIdx.x; r < nrows_bin; r += gridDim.x) {
     const int64_t i = rows[r];
     for (int e = threadIdx.x; e < T; e += THREADS) {
@@ -1095,18 +1145,11 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
       });
       __syncthreads();
     }
-    // compaction of occupied, non-zero slots into blocked registers
-    int my_slots[SPT];
+    // occupied, non-zero slots of this thread's range -> staging (in order)
+    const int e0 = threadIdx.x * SPT;
     int cnt = 0;
-#pragma unroll
-    for (int q = 0; q < SPT; ++q) {
-      const int e = threadIdx.x * SPT + q;
-      my_slots[q] = -1;
-      if (tkeys[e] != kEmptyKey && !SR::is_zero(tvals[e])) {
-        my_slots[q] = e;
-        ++cnt;
-      }
-    }
+#pragma unroll 4
+    for (int q = 0; q < SPT; ++q) cnt += (tkeys[e0 + q] != kEmptyKey && !SR::is_zero(tvals[e0 + q])) ? 1 : 0;
     int first, total;
     typename HS::Scan(tmp->scan).ExclusiveSum(cnt, first, total);
     if (threadIdx.x == 0) {
@@ -1117,110 +1160,73 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
       __syncthreads();
       continue;
     }
-    uint32_t my_keys[SPT];
-#pragma unroll
-    for (int q = 0; q < SPT; ++q) my_keys[q] = my_slots[q] >= 0 ? (uint32_t)tkeys[my_slots[q]] : 0u;
+#pragma unroll 4
+    for (int q = 0; q < SPT; ++q) {
+      const int e = e0 + q;
+      const int32_t k = tkeys[e];
+      if (k != kEmptyKey && !SR::is_zero(tvals[e])) {
+        stg_key[first] = (uint32_t)k;
+        stg_slot[first] = (uint32_t)e;
+        ++first;
+      }
+    }
+    __syncthreads();  // the key table is free from here on
+    const int64_t o = s_base;
+    // Monotone bucketing by the high column bits: NB = T/2 buckets (>= the
+    // entries), counts by shared atomics (the arrival rank rides in bits
+    // 16..31 of the staged slot), starts by one block scan, in-bucket order
+    // by a rank count; each entry is stored straight at its sorted position.
+    // A row whose columns crowd one bucket (> kBucketMax) is radix-sorted.
+    for (int b = threadIdx.x; b < NB; b += THREADS) bstart[b] = 0;
     __syncthreads();
-    // Monotone bucketing by the high column bits (the keys array is dead
-    // now): NB = T/2 buckets (>= occupied slots), counts by shared atomics,
-    // starts by one block scan, in-bucket order by a rank count, output
-    // written straight to its sorted position.  A row whose columns crowd
-    // one bucket (> kBucketMax entries) takes the radix sort below instead.
-    {
-      constexpr int NB = T / 2, NBT = NB / THREADS, kBucketMax = 32;
-      static_assert(NB % THREADS == 0, "bucket count must divide by the CTA size");
-      const int shift = end_bit > LOG2T - 1 ? end_bit - (LOG2T - 1) : 0;
-      int* bstart = tkeys;                                            // NB counters, then starts
-      uint32_t* bkeys = reinterpret_cast<uint32_t*>(tkeys) + NB;      // keys grouped by bucket
-      for (int b = threadIdx.x; b < NB; b += THREADS) bstart[b] = 0;
-      __syncthreads();
-      // the in-bucket arrival rank rides in bits 16..30 of the slot id
+    for (int e = threadIdx.x; e < total; e += THREADS)
+      stg_slot[e] |= (uint32_t)min(atomicAdd(&bstart[stg_key[e] >> shift], 1), 0xffff) << 16;
+    __syncthreads();
+    int sum = 0, mx = 0;
 #pragma unroll
-      for (int q = 0; q < SPT; ++q)
-        if (my_slots[q] >= 0) my_slots[q] |= min(atomicAdd(&bstart[my_keys[q] >> shift], 1), 0x7fff) << 16;
-      __syncthreads();
-      int sum = 0, mx = 0;
+    for (int b = 0; b < NBT; ++b) {
+      const int n = bstart[threadIdx.x * NBT + b];
+      sum += n;
+      mx = max(mx, n);
+    }
+    if (!__syncthreads_or(mx > kBucketMax)) {
+      int run;
+      typename HS::Scan(tmp->scan).ExclusiveSum(sum, run);
 #pragma unroll
       for (int b = 0; b < NBT; ++b) {
         const int n = bstart[threadIdx.x * NBT + b];
-        sum += n;
-        mx = max(mx, n);
+        bstart[threadIdx.x * NBT + b] = run;
+        run += n;
       }
-      if (!__syncthreads_or(mx > kBucketMax)) {
-        int run;
-        typename HS::Scan(tmp->scan).ExclusiveSum(sum, run);
-#pragma unroll
-        for (int b = 0; b < NBT; ++b) {
-          const int n = bstart[threadIdx.x * NBT + b];
-          bstart[threadIdx.x * NBT + b] = run;
-          run += n;
+      __syncthreads();
+      for (int e = threadIdx.x; e < total; e += THREADS)
+        bkeys[bstart[stg_key[e] >> shift] + (stg_slot[e] >> 16)] = stg_key[e];
+      __syncthreads();
+      if (o >= 0)
+        for (int e = threadIdx.x; e < total; e += THREADS) {
+          const uint32_t key = stg_key[e];
+          const int b = (int)(key >> shift);
+          const int s1 = b + 1 < NB ? bstart[b + 1] : total;
+          int pos = bstart[b];
+          for (int j = pos; j < s1; ++j) pos += bkeys[j] < key;
+          out.cols[o + pos] = (int32_t)key;
+          out.vals[o + pos] = tvals[stg_slot[e] & 0xffff];
         }
-        __syncthreads();
-#pragma unroll
-        for (int q = 0; q < SPT; ++q)
-          if (my_slots[q] >= 0) bkeys[bstart[my_keys[q] >> shift] + (my_slots[q] >> 16)] = my_keys[q];
-        __syncthreads();
-#pragma unroll
-        for (int q = 0; q < SPT; ++q)
-          if (my_slots[q] >= 0) {  // final position replaces the arrival rank
-            const uint32_t key = my_keys[q];
-            const int b = (int)(key >> shift);
-            const int s1 = b + 1 < NB ? bstart[b + 1] : total;
-            int pos = bstart[b];
-            for (int j = pos; j < s1; ++j) pos += bkeys[j] < key;
-            my_slots[q] = (my_slots[q] & 0xffff) | (pos << 16);
-          }
-        __syncthreads();
-        // sorted (key, slot) staging, then coalesced stores of the row
-        uint32_t* skeys = reinterpret_cast<uint32_t*>(bstart);
-        uint16_t* sslot = reinterpret_cast<uint16_t*>(bkeys);
-#pragma unroll
-        for (int q = 0; q < SPT; ++q)
-          if (my_slots[q] >= 0) {
-            skeys[my_slots[q] >> 16] = my_keys[q];
-            sslot[my_slots[q] >> 16] = (uint16_t)(my_slots[q] & 0xffff);
-          }
-        __syncthreads();
-        const int64_t o = s_base;
-        if (o >= 0)
-          for (int e = threadIdx.x; e < total; e += THREADS) {
-            out.cols[o + e] = (int32_t)skeys[e];
-            out.vals[o + e] = tvals[sslot[e]];
-          }
-        __syncthreads();
-        continue;
-      }
+      __syncthreads();
+      continue;
     }
-    // stage (key, slot) in smem, then blocked radix sort
-    uint16_t* stage_slot = reinterpret_cast<uint16_t*>(sorted_keys + T / 2);
-    int w = first;
-#pragma unroll
-    for (int q = 0; q < SPT; ++q)
-      if (my_slots[q] >= 0) {
-        sorted_keys[w] = my_keys[q];
-        stage_slot[w] = (uint16_t)(my_slots[q] & 0xffff);
-        ++w;
-      }
+    // skewed row: bitonic sort of (key << 32 | slot) in the free key table
+    uint64_t* buf = reinterpret_cast<uint64_t*>(tkeys);
     __syncthreads();
-    uint32_t k[ITEMS];
-    uint16_t sl[ITEMS];
-#pragma unroll
-    for (int q = 0; q < ITEMS; ++q) {
-      const int e = threadIdx.x * ITEMS + q;
-      k[q] = e < total ? sorted_keys[e] : (1u << end_bit);
-      sl[q] = e < total ? stage_slot[e] : 0;
-    }
-    __syncthreads();
-    typename HS::Sort(tmp->sort).Sort(k, sl, 0, end_bit + 1);
-    const int64_t o = s_base;
-#pragma unroll
-    for (int q = 0; q < ITEMS; ++q) {
-      const int e = threadIdx.x * ITEMS + q;
-      if (e < total && o >= 0) {
-        out.cols[o + e] = (int32_t)k[q];
-        out.vals[o + e] = tvals[sl[q]];
+    for (int e = threadIdx.x; e < total; e += THREADS)
+      buf[e] = ((uint64_t)stg_key[e] << 32) | (stg_slot[e] & 0xffffu);
+    block_bitonic_sort<THREADS>(buf, total);
+    if (o >= 0)
+      for (int e = threadIdx.x; e < total; e += THREADS) {
+        const uint64_t x = buf[e];
+        out.cols[o + e] = (int32_t)(x >> 32);
+        out.vals[o + e] = tvals[(uint32_t)x & 0xffffu];
       }
-    }
     __syncthreads();
   }
 }

@@ -89,7 +89,7 @@ template <class SR, class Src, int T, int THREADS>
 void launch_hash(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* rows, int64_t n, int cap, int end_bit,
                  const RowOut<typename SR::value_type>& out) {
   using V = typename SR::value_type;
-  const size_t fixed = (size_t)T * (sizeof(V) + sizeof(int32_t)) +
+  const size_t fixed = (size_t)T * (sizeof(V) + sizeof(int32_t) + sizeof(uint32_t)) +
                        ((sizeof(typename HashSort<T, THREADS>::Tmp) + 15) & ~size_t(15)) + 64;
   const size_t per = SegCache<SR, Src>::bytes_per_seg(1);
   const size_t limit = 220 * 1024;
@@ -147,7 +147,7 @@ inline int dense_cfg() {
 template <class V>
 inline int dense_panel_width() {
   const int cfg = dense_cfg();
-  return Geom<V>::kPanelW >> (cfg == 1 || cfg == 3 ? 1 : cfg == 2 ? 2 : 0);
+  return Geom<V>::kPanelW >> (cfg == 1 || cfg == 3 || cfg == 4 || cfg == 5 ? 1 : cfg == 2 ? 2 : 0);
 }
 
 template <class SR, class Src>
@@ -165,6 +165,12 @@ void launch_dense(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* row
     case 3:
       launch_dense_cfg<PW / 2, 256, SR, Src>(c, s, src, rows, n, ncols, 74 * 1024, work, out);
       break;
+    case 4:
+      launch_dense_cfg<PW / 2, 256, SR, Src>(c, s, src, rows, n, ncols, 110 * 1024, work, out);
+      break;
+    case 5:
+      launch_dense_cfg<PW / 2, 128, SR, Src>(c, s, src, rows, n, ncols, 110 * 1024, work, out);
+      break;
 
     default:
       launch_dense_cfg<PW, 1024, SR, Src>(c, s, src, rows, n, ncols, 220 * 1024, work, out);
@@ -174,8 +180,8 @@ void launch_dense(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* row
 // segment-cache capacity that fits next to a T-slot hash table
 template <class V>
 inline int V_hash_cap(int T) {
-  const size_t table = (size_t)T * (sizeof(V) + 4);
-  const size_t room = table < 170 * 1024 ? 170 * 1024 - table : 0;
+  const size_t table = (size_t)T * (sizeof(V) + 8);  // values + keys + staging
+  const size_t room = table < 200 * 1024 ? 200 * 1024 - table : 0;
   const size_t per = 8 + 4 + sizeof(V) + 4 + 4;
   return (int)std::max<size_t>(64, std::min<size_t>(2048, room / per)) & ~3;
 }
@@ -367,9 +373,9 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
       launch_hash<SR, Src, Geom<V>::kMaxT, 1024>(c, fk[1], src, lb + base[kBinHashMax], hcounts[kBinHashMax],
                                                  V_hash_cap<V>(Geom<V>::kMaxT), end_bit, o);
     if (hcounts[kBinHash8K] > 0)
-      launch_hash<SR, Src, 8192, 512>(c, fk[1], src, lb + base[kBinHash8K], hcounts[kBinHash8K], 1024, end_bit, o);
+      launch_hash<SR, Src, 8192, 512>(c, fk[1], src, lb + base[kBinHash8K], hcounts[kBinHash8K], 256, end_bit, o);
     if (hcounts[kBinHash4K] > 0)
-      launch_hash<SR, Src, 4096, 256>(c, fk[2], src, lb + base[kBinHash4K], hcounts[kBinHash4K], 512, end_bit, o);
+      launch_hash<SR, Src, 4096, 256>(c, fk[2], src, lb + base[kBinHash4K], hcounts[kBinHash4K], 256, end_bit, o);
     if (hcounts[kBinHash2K] > 0)
       launch_hash<SR, Src, 2048, 128>(c, fk[2], src, lb + base[kBinHash2K], hcounts[kBinHash2K], 256, end_bit, o);
     if (hcounts[kBinEsc512] > 0)
