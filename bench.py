@@ -335,7 +335,13 @@ def run_summa(args):
     dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=600))
     job = [uuid.uuid4().hex[:12] if rank == 0 else None]
     dist.broadcast_object_list(job, src=0)
-    pr, pc = (int(x) for x in args.grid.split("x")) if args.grid else grid_for(world)
+    wl = workload(args)
+    if args.grid:
+        pr, pc = (int(x) for x in args.grid.split("x"))
+    elif wl["gen"] == "stencil27":  # banded: 1 x N keeps every rank's block column equally loaded
+        pr, pc = 1, world
+    else:
+        pr, pc = grid_for(world)
     if pr * pc != world:
         raise SystemExit(f"--grid {args.grid} does not hold {world} ranks")
     i, j = rank // pc, rank % pc
@@ -345,7 +351,6 @@ def run_summa(args):
     thr_col = args.threshold if args.threshold >= 0 else measured_threshold(pr)  # column scope: fanout pr
 
     t_gen = time.time()
-    wl = workload(args)
     sr, n = wl["sr"], wl["n"]
     from paper_2504_06408_b200.summa import block_from_piece, block_range
     rr, cr = block_range(n, pr, i), block_range(n, pc, j)

@@ -716,6 +716,39 @@ struct SegCache {
   }
 };
 
+// Position of the k-th (0-based) set bit of x (k < popc(x)); popc bisection.
+__device__ __forceinline__ int nth_set_bit(uint32_t x, int k) {
+  int pos = 0;
+  int c = __popc(x & 0xffffu);
+  if (k >= c) { k -= c; pos += 16; x >>= 16; }
+  c = __popc(x & 0xffu);
+  if (k >= c) { k -= c; pos += 8; x >>= 8; }
+  c = __popc(x & 0xfu);
+  if (k >= c) { k -= c; pos += 4; x >>= 4; }
+  c = __popc(x & 0x3u);
+  if (k >= c) { k -= c; pos += 2; x >>= 2; }
+  c = (int)(x & 1u);
+  if (k >= c) pos += 1;
+  return pos;
+}
+
+// Flattened enumeration helper: lane t of the warp holds a run of L_t items
+// starting at excl_t (exclusive prefix over lanes).  For the 32 items
+// [qb, qb + 32) returns, for this lane's item qb + lane, the lane whose run
+// holds it — from two ballots, one OR-reduction and popcounts (no
+// dependent shuffle search).  Valid for qb + lane < total.
+__device__ __forceinline__ int run_owner(int L, int excl, int qb, unsigned nonempty) {
+  const int lane = threadIdx.x & 31;
+  const int incl = excl + L;
+  const unsigned holder = __ballot_sync(kFull, L > 0 && excl <= qb && qb < incl);
+  const int d = excl - qb;
+  const unsigned starts = __reduce_or_sync(kFull, (L > 0 && d > 0 && d < 32) ? (1u << d) : 0u);
+  if (!holder) return 0;
+  const int f = __ffs(holder) - 1;
+  const int rank = __popc(nonempty & ((1u << f) - 1u)) + __popc(starts & ((2u << lane) - 1u));
+  return nth_set_bit(nonempty, rank);
+}
+
 // Warp `wid` of NW enumerates its equal share of the cached segments' items
 // (panel p); f(col, value) per item, two items per lane in flight.
 // SPG_SEG_MODE (compile time, default off: measured no gain on R-MAT): when the warp's share averages
@@ -800,18 +833,11 @@ __device__ __forceinline__ void balanced_items(const Src& src, const SegCache<SR
     }
     const int total = __shfl_sync(kFull, incl, 31);
     const int excl = incl - L;
+    const unsigned nonempty = __ballot_sync(kFull, L > 0);
     for (int q0 = 0; q0 < total; q0 += 32 * IPL) {
       int pos[IPL];
 #pragma unroll
-      for (int u = 0; u < IPL; ++u) pos[u] = 0;
-#pragma unroll
-      for (int step = 16; step >= 1; step >>= 1) {
-#pragma unroll
-        for (int u = 0; u < IPL; ++u) {
-          const int v = __shfl_sync(kFull, incl, pos[u] + step - 1);
-          if (v <= q0 + 32 * u + lane) pos[u] += step;
-        }
-      }
+      for (int u = 0; u < IPL; ++u) pos[u] = run_owner(L, excl, q0 + 32 * u, nonempty);
       int32_t cc[IPL];
       V xx[IPL], mm[IPL];
 #pragma unroll
@@ -847,21 +873,6 @@ __device__ __forceinline__ void balanced_items(const Src& src, const SegCache<SR
 // the fold can cancel back to zero() (fp64 +), which a pre-pass handles.
 // Returns the number of entries written.
 // ---------------------------------------------------------------------------
-// Position of the k-th (0-based) set bit of x (k < popc(x)); popc bisection.
-__device__ __forceinline__ int nth_set_bit(uint32_t x, int k) {
-  int pos = 0;
-  int c = __popc(x & 0xffffu);
-  if (k >= c) { k -= c; pos += 16; x >>= 16; }
-  c = __popc(x & 0xffu);
-  if (k >= c) { k -= c; pos += 8; x >>= 8; }
-  c = __popc(x & 0xfu);
-  if (k >= c) { k -= c; pos += 4; x >>= 4; }
-  c = __popc(x & 0x3u);
-  if (k >= c) { k -= c; pos += 2; x >>= 2; }
-  c = (int)(x & 1u);
-  if (k >= c) pos += 1;
-  return pos;
-}
 
 template <class SR>
 struct AddCanCancel {
@@ -936,14 +947,10 @@ __device__ __forceinline__ int bitmap_emit(typename SR::value_type* acc, uint32_
     }
     const int total = __shfl_sync(kFull, incl, 31);
     const int excl = incl - c;
+    const unsigned nonempty = __ballot_sync(kFull, c > 0);
     for (int q0 = 0; q0 < total; q0 += 32) {
       const int q = q0 + lane;
-      int own = 0;
-#pragma unroll
-      for (int step = 16; step >= 1; step >>= 1) {
-        const int v = __shfl_sync(kFull, incl, own + step - 1);
-        if (v <= q) own += step;
-      }
+      const int own = run_owner(c, excl, q0, nonempty);
       const uint32_t xo = __shfl_sync(kFull, x, own);
       const int eo = __shfl_sync(kFull, excl, own);
       if (q < total) {
@@ -981,8 +988,8 @@ __device__ __forceinline__ int bitmap_emit(typename SR::value_type* acc, uint32_
 #define SPG_DENSE_IPL 2
 #endif
 constexpr int kDenseIPL = SPG_DENSE_IPL;  // items per lane in flight in the dense product loop
-template <class SR, class Src, int W, int THREADS>
-__global__ void __launch_bounds__(THREADS) dense_panel_kernel(Src src, const int64_t* __restrict__ rows,
+template <class SR, class Src, int W, int THREADS, int MINB = 1>
+__global__ void __launch_bounds__(THREADS, MINB) dense_panel_kernel(Src src, const int64_t* __restrict__ rows,
                                                               int64_t nrows_bin, int npanels, int cap,
                                                               unsigned long long* __restrict__ work,
                                                               RowOut<typename SR::value_type> out) {

@@ -118,7 +118,7 @@ void launch_esc(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* rows,
 // Dense-panel geometry: (panel width, CTA size, smem budget per CTA).
 // cfg 0: 128 KB panel, 1024 threads, 1 CTA/SM; cfg 1: 64 KB, 512 threads,
 // 2 CTAs/SM; cfg 2: 32 KB, 512 threads, 3 CTAs/SM.  SPG_DENSE_CFG overrides.
-template <int W, int DT, class SR, class Src>
+template <int W, int DT, class SR, class Src, int MINB = 1>
 void launch_dense_cfg(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* rows, int64_t n, int64_t ncols,
                       size_t smem_budget, unsigned long long* work, const RowOut<typename SR::value_type>& out) {
   using V = typename SR::value_type;
@@ -129,7 +129,7 @@ void launch_dense_cfg(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t*
   const int cap = (int)std::min<size_t>(8192, room / per_seg) & ~3;  // keeps 16-byte values aligned
   if (cap < 32) fail(SPG_ERR_INTERNAL, "dense panel: no room for the segment cache");
   const size_t smem = fixed + (size_t)cap * per_seg + 64;
-  auto kern = dense_panel_kernel<SR, Src, W, DT>;
+  auto kern = dense_panel_kernel<SR, Src, W, DT, MINB>;
   set_smem(kern, smem);
   kern<<<resident_grid(c, kern, DT, smem, n), DT, smem, s>>>(src, rows, n, np, cap, work, out);
   SPG_LAUNCH_CHECK();
@@ -147,7 +147,7 @@ inline int dense_cfg() {
 template <class V>
 inline int dense_panel_width() {
   const int cfg = dense_cfg();
-  return Geom<V>::kPanelW >> (cfg == 1 || cfg == 3 || cfg == 4 || cfg == 5 ? 1 : cfg == 2 ? 2 : 0);
+  return Geom<V>::kPanelW >> (cfg == 1 || cfg >= 3 ? 1 : cfg == 2 ? 2 : 0);
 }
 
 template <class SR, class Src>
@@ -170,6 +170,9 @@ void launch_dense(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* row
       break;
     case 5:
       launch_dense_cfg<PW / 2, 128, SR, Src>(c, s, src, rows, n, ncols, 110 * 1024, work, out);
+      break;
+    case 6:  // 3 CTAs/SM: register cap 42, small segment cache
+      launch_dense_cfg<PW / 2, 512, SR, Src, 3>(c, s, src, rows, n, ncols, 74 * 1024, work, out);
       break;
 
     default:

@@ -155,11 +155,16 @@ extern "C" int spg_summa25_multiply(spg_comm* comm, spg_ctx* c, int sr, int64_t 
     const auto t_start = Clock::now();
 
     // prepare (summa.hpp:278-287)
-    spg_dcsr pa{}, pb{};
+    spg_dcsr pa{}, pb_own{};
+    // C = A (x) A (the same host block passed twice) is prepared once
+    const bool same = (a_csc && b_csc && a_csc->ptr == b_csc->ptr && a_csc->idx == b_csc->idx &&
+                       a_csc->vals == b_csc->vals) ||
+                      (a_dcsc && b_dcsc && a_dcsc->jc == b_dcsc->jc && a_dcsc->cp == b_dcsc->cp &&
+                       a_dcsc->rowids == b_dcsc->rowids && a_dcsc->vals == b_dcsc->vals);
     {
       const auto t0 = Clock::now();
       prepare_block(c, sr, a_csc, a_dcsc, &pa);
-      prepare_block(c, sr, b_csc, b_dcsc, &pb);
+      if (!same) prepare_block(c, sr, b_csc, b_dcsc, &pb_own);
       SPG_CUDA(cudaStreamSynchronize(c->stream));
       led.ms[0] += ms_since(t0);
     }
@@ -167,7 +172,8 @@ extern "C" int spg_summa25_multiply(spg_comm* comm, spg_ctx* c, int sr, int64_t 
       spg_ctx* c;
       spg_dcsr* m;
       ~Owned() { free_dcsr(c, m); }
-    } own_a{c, &pa}, own_b{c, &pb};
+    } own_a{c, &pa}, own_b{c, &pb_own};
+    const spg_dcsr& pb = same ? pa : pb_own;
 
     std::vector<spg_stage> stages(pr + pc + 2);
     const int ns = spg_summa_schedule(inner, pr, pc, stages.data(), (int)stages.size());
