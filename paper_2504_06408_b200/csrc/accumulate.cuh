@@ -732,23 +732,6 @@ __device__ __forceinline__ int nth_set_bit(uint32_t x, int k) {
   return pos;
 }
 
-// Flattened enumeration helper: lane t of the warp holds a run of L_t items
-// starting at excl_t (exclusive prefix over lanes).  For the 32 items
-// [qb, qb + 32) returns, for this lane's item qb + lane, the lane whose run
-// holds it — from two ballots, one OR-reduction and popcounts (no
-// dependent shuffle search).  Valid for qb + lane < total.
-__device__ __forceinline__ int run_owner(int L, int excl, int qb, unsigned nonempty) {
-  const int lane = threadIdx.x & 31;
-  const int incl = excl + L;
-  const unsigned holder = __ballot_sync(kFull, L > 0 && excl <= qb && qb < incl);
-  const int d = excl - qb;
-  const unsigned starts = __reduce_or_sync(kFull, (L > 0 && d > 0 && d < 32) ? (1u << d) : 0u);
-  if (!holder) return 0;
-  const int f = __ffs(holder) - 1;
-  const int rank = __popc(nonempty & ((1u << f) - 1u)) + __popc(starts & ((2u << lane) - 1u));
-  return nth_set_bit(nonempty, rank);
-}
-
 // Warp `wid` of NW enumerates its equal share of the cached segments' items
 // (panel p); f(col, value) per item, two items per lane in flight.
 // SPG_SEG_MODE (compile time, default off: measured no gain on R-MAT): when the warp's share averages
@@ -833,11 +816,18 @@ __device__ __forceinline__ void balanced_items(const Src& src, const SegCache<SR
     }
     const int total = __shfl_sync(kFull, incl, 31);
     const int excl = incl - L;
-    const unsigned nonempty = __ballot_sync(kFull, L > 0);
     for (int q0 = 0; q0 < total; q0 += 32 * IPL) {
       int pos[IPL];
 #pragma unroll
-      for (int u = 0; u < IPL; ++u) pos[u] = run_owner(L, excl, q0 + 32 * u, nonempty);
+      for (int u = 0; u < IPL; ++u) pos[u] = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+#pragma unroll
+        for (int u = 0; u < IPL; ++u) {
+          const int v = __shfl_sync(kFull, incl, pos[u] + step - 1);
+          if (v <= q0 + 32 * u + lane) pos[u] += step;
+        }
+      }
       int32_t cc[IPL];
       V xx[IPL], mm[IPL];
 #pragma unroll
@@ -947,10 +937,14 @@ __device__ __forceinline__ int bitmap_emit(typename SR::value_type* acc, uint32_
     }
     const int total = __shfl_sync(kFull, incl, 31);
     const int excl = incl - c;
-    const unsigned nonempty = __ballot_sync(kFull, c > 0);
     for (int q0 = 0; q0 < total; q0 += 32) {
       const int q = q0 + lane;
-      const int own = run_owner(c, excl, q0, nonempty);
+      int own = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const int v = __shfl_sync(kFull, incl, own + step - 1);
+        if (v <= q) own += step;
+      }
       const uint32_t xo = __shfl_sync(kFull, x, own);
       const int eo = __shfl_sync(kFull, excl, own);
       if (q < total) {
