@@ -157,7 +157,7 @@ void launch_dense(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* row
   constexpr int PW = Geom<V>::kPanelW;
   switch (dense_cfg()) {
     case 1:
-      launch_dense_cfg<PW / 2, 512, SR, Src>(c, s, src, rows, n, ncols, 110 * 1024, work, out);
+      launch_dense_cfg<PW / 2, 512, SR, Src, 2>(c, s, src, rows, n, ncols, 110 * 1024, work, out);
       break;
     case 2:
       launch_dense_cfg<PW / 4, 512, SR, Src>(c, s, src, rows, n, ncols, 72 * 1024, work, out);
@@ -237,7 +237,12 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
   // K1 analyse
   DBuf<int64_t> prods(c, m), ub(c, m + 1), off(c, m + 1), rownnz(c, m + 1);
   DBuf<uint8_t> bins(c, m);
-  analyse_rows_kernel<SR, Src><<<grid_for(c, m, 8), 256, 0, c->stream>>>(src, ncols_out, prods.p, ub.p, bins.p);
+  static const int64_t dense_min = [] {  // SPG_DENSE_MIN: products above which a row goes dense
+    const char* e = std::getenv("SPG_DENSE_MIN");
+    return e ? (int64_t)std::atoll(e) : kDenseMinRow;
+  }();
+  analyse_rows_kernel<SR, Src><<<grid_for(c, m, 8), 256, 0, c->stream>>>(src, ncols_out, dense_min, prods.p, ub.p,
+                                                                        bins.p);
   SPG_LAUNCH_CHECK();
   ++c->launches;
   SPG_CUDA(cudaMemsetAsync(ub.p + m, 0, sizeof(int64_t), c->stream));

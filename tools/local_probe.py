@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--value-mode", type=int, default=0)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--permute", action="store_true")
+    ap.add_argument("--frange", type=float, nargs=2, default=None,
+                    help="keep only rows of the left operand whose product count F is in (lo, hi]")
     args = ap.parse_args()
     from paper_2504_06408_b200 import Context, DeviceCsr, generators, local_multiply
     from paper_2504_06408_b200.semiring import as_id
@@ -42,11 +44,26 @@ def main():
         coo = generators.permute_symmetric(coo, 1)
     a = generators.coo_to_csr_fast(coo)
     print(f"gen {time.time() - t0:.1f}s n={a.nrows} nnz={a.nnz}", file=sys.stderr)
+    import numpy as np
+    from paper_2504_06408_b200.formats import CsrMatrix
+    left = a
+    if args.frange:
+        rl = np.diff(a.rowptr)
+        F = np.zeros(a.nrows, np.int64)
+        np.add.at(F, np.repeat(np.arange(a.nrows), rl), rl[a.colids])
+        keep = np.nonzero((F > args.frange[0]) & (F <= args.frange[1]))[0]
+        lens = rl[keep]
+        ptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        sel = np.concatenate([np.arange(a.rowptr[r], a.rowptr[r + 1]) for r in keep]) if keep.size else np.zeros(0, np.int64)
+        left = CsrMatrix(a.sr, keep.size, a.ncols, ptr, a.colids[sel], a.values[sel])
+        print(f"rows with F in ({args.frange[0]:.0f}, {args.frange[1]:.0f}]: {keep.size}, products {F[keep].sum()}",
+              file=sys.stderr)
     ctx = Context(0)
     d = DeviceCsr.upload(ctx, a)
+    dl = DeviceCsr.upload(ctx, left) if left is not a else d
     for r in range(args.reps):
         st = {}
-        c = local_multiply(d, d, stats=st)
+        c = local_multiply(dl, d, stats=st)
         ctx.sync()
         print(json.dumps({"rep": r, **st}))
         c.free()
