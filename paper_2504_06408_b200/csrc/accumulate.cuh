@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(256) analyse_rows_kernel(Src src, int64_t ncol
       else if (u <= Geom<V>::kMaxT / 2) b = kBinHashMax;
       else b = kBinDense;
       prods[i] = f;
-      ubound[i] = (b == kBinEmpty) ? 0 : u;
+      ubound[i] = (b == kBinEmpty) ? 0 : ((u + 3) & ~int64_t(3));  // 16-byte aligned scratch slots
       bins[i] = b;
     }
   }
@@ -1256,9 +1256,69 @@ __global__ void __launch_bounds__(256) compact_chunks_kernel(const int64_t* __re
   }
 }
 
-// Other rows: row i sits at off[i] of the scratch (off[i] < 0: skip).
+// Cooperative copy (threads tid of nt) of n 32-bit words from a 16-byte
+// aligned source to any destination offset: aligned 16-byte stores, each
+// output quad composed from two aligned source quads (the source may be read
+// up to 3 words past n: scratch buffers carry slack).
+__device__ __forceinline__ void copy_words(uint32_t* __restrict__ dst, int64_t d, const uint32_t* __restrict__ src,
+                                           int64_t s, int64_t n, int tid, int nt) {
+  const int64_t head = std::min<int64_t>((4 - (d & 3)) & 3, n);
+  if (tid < head) dst[d + tid] = src[s + tid];
+  const int64_t rest = n - head;
+  if (rest <= 0) return;
+  const int64_t nq = rest >> 2;
+  const int64_t j0 = s + head;  // first source word of the aligned destination part
+  const int sh = (int)(j0 & 3);
+  const uint4* sq = reinterpret_cast<const uint4*>(src + (j0 - sh));
+  uint4* dq = reinterpret_cast<uint4*>(dst + d + head);
+  auto compose = [sh](const uint4& a, const uint4& b) {
+    if (sh == 0) return a;
+    if (sh == 1) return make_uint4(a.y, a.z, a.w, b.x);
+    if (sh == 2) return make_uint4(a.z, a.w, b.x, b.y);
+    return make_uint4(a.w, b.x, b.y, b.z);
+  };
+  constexpr int U = 4;  // quads in flight per thread
+  int64_t k = tid;
+  for (; k + (int64_t)nt * (U - 1) < nq; k += (int64_t)nt * U) {
+    uint4 a[U], b[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      a[u] = __ldg(sq + k + (int64_t)nt * u);
+      b[u] = sh ? __ldg(sq + k + (int64_t)nt * u + 1) : a[u];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) dq[k + (int64_t)nt * u] = compose(a[u], b[u]);
+  }
+  for (; k < nq; k += nt) dq[k] = compose(__ldg(sq + k), sh ? __ldg(sq + k + 1) : make_uint4(0, 0, 0, 0));
+  const int64_t t0 = head + (nq << 2);
+  if (tid < n - t0) dst[d + t0 + tid] = src[s + t0 + tid];
+}
+
+// U-slot mode, dense rows (the long outputs): one CTA per row, 16-byte copies.
 template <class V>
-__global__ void __launch_bounds__(256) compact_rows_kernel(int64_t nrows, const int64_t* __restrict__ off,
+__global__ void __launch_bounds__(256) compact_long_rows_kernel(const int64_t* __restrict__ rows, int64_t nrows_bin,
+                                                                const int64_t* __restrict__ off,
+                                                                const int64_t* __restrict__ rowptr,
+                                                                const int32_t* __restrict__ sc_cols,
+                                                                const V* __restrict__ sc_vals,
+                                                                int32_t* __restrict__ cols, V* __restrict__ vals) {
+  static_assert(sizeof(V) % 4 == 0, "word copies need 4-byte multiples");
+  constexpr int WPE = (int)(sizeof(V) / 4);
+  for (int64_t r = blockIdx.x; r < nrows_bin; r += gridDim.x) {
+    const int64_t i = rows[r];
+    const int64_t d = rowptr[i], n = rowptr[i + 1] - d, s = off[i];
+    copy_words(reinterpret_cast<uint32_t*>(cols), d, reinterpret_cast<const uint32_t*>(sc_cols), s, n, threadIdx.x,
+               blockDim.x);
+    copy_words(reinterpret_cast<uint32_t*>(vals), d * WPE, reinterpret_cast<const uint32_t*>(sc_vals), s * WPE,
+               n * WPE, threadIdx.x, blockDim.x);
+  }
+}
+
+// Other rows: row i sits at off[i] of the scratch (off[i] < 0: skip; rows
+// whose bin is dense are skipped when `skip` is given).
+template <class V>
+__global__ void __launch_bounds__(256) compact_rows_kernel(int64_t nrows, const uint8_t* __restrict__ skip,
+                                                           const int64_t* __restrict__ off,
                                                            const int64_t* __restrict__ rowptr,
                                                            const int32_t* __restrict__ sc_cols,
                                                            const V* __restrict__ sc_vals, int32_t* __restrict__ cols,
@@ -1272,6 +1332,7 @@ __global__ void __launch_bounds__(256) compact_rows_kernel(int64_t nrows, const 
     if (n == 0) continue;
     const int64_t s = off[i];
     if (s < 0) continue;
+    if (skip && skip[i] == kBinDense) continue;  // copied by compact_long_rows_kernel
     int64_t e = lane;
     for (; e + 96 < n; e += 128) {
       const int32_t c0 = sc_cols[s + e], c1 = sc_cols[s + e + 32], c2 = sc_cols[s + e + 64],

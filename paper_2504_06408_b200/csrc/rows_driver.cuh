@@ -307,8 +307,8 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
   DBuf<int32_t> sc_cols;
   DBuf<V> sc_vals;
   while (cap > 0) {  // the estimate can be stale (other allocators): shrink on OOM
-    int32_t* pc = try_dalloc<int32_t>(c, (size_t)cap);
-    V* pv = pc ? try_dalloc<V>(c, (size_t)cap) : nullptr;
+    int32_t* pc = try_dalloc<int32_t>(c, (size_t)cap + 16);  // slack: vector reads may pass a row end
+    V* pv = pc ? try_dalloc<V>(c, (size_t)cap + 16) : nullptr;
     if (pv) {
       sc_cols = DBuf<int32_t>::adopt(c, pc, (size_t)cap);
       sc_vals = DBuf<V>::adopt(c, pv, (size_t)cap);
@@ -426,11 +426,21 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
   out->idx = dalloc<int32_t>(c, (size_t)nnz);
   out->vals = dalloc<V>(c, (size_t)nnz);
   if (fits) {
-    compact_rows_kernel<V><<<grid_for(c, m, 8), 256, 0, c->stream>>>(m, slotted ? off.p : rowstart.p, out->ptr,
-                                                                     sc_cols.p, sc_vals.p, out->idx,
-                                                                     static_cast<V*>(out->vals));
+    constexpr bool kWords = sizeof(V) % 4 == 0;
+    const bool long_rows = kWords && slotted && nd > 0;  // dense rows: CTA per row, 16-byte copies
+    compact_rows_kernel<V><<<grid_for(c, m, 8), 256, 0, c->stream>>>(
+        m, long_rows ? bins.p : nullptr, slotted ? off.p : rowstart.p, out->ptr, sc_cols.p, sc_vals.p, out->idx,
+        static_cast<V*>(out->vals));
     SPG_LAUNCH_CHECK();
     ++c->launches;
+    if constexpr (kWords) {
+      if (long_rows) {
+        compact_long_rows_kernel<V><<<grid_for(c, nd, 1, 8), 256, 0, c->stream>>>(
+            dense_rows, nd, off.p, out->ptr, sc_cols.p, sc_vals.p, out->idx, static_cast<V*>(out->vals));
+        SPG_LAUNCH_CHECK();
+        ++c->launches;
+      }
+    }
     if (nd > 0 && !slotted) {
       compact_chunks_kernel<V><<<grid_for(c, nd, 1, 8), 256, 0, c->stream>>>(
           dense_rows, nd, npc, chunks.p, out->ptr, sc_cols.p, sc_vals.p, out->idx, static_cast<V*>(out->vals));
