@@ -869,6 +869,10 @@ struct AddCanCancel {
   static constexpr bool value = SR::id == 0;  // arithmetic (+, x): a + (-a) == 0
 };
 
+#ifndef SPG_LANE_EMIT
+#define SPG_LANE_EMIT 0
+#endif
+constexpr bool kLaneEmit = SPG_LANE_EMIT != 0;  // lane-sequential emit instead of the flattened one
 template <class SR, int W, int THREADS>
 __device__ __forceinline__ int bitmap_emit(typename SR::value_type* acc, uint32_t* bm, int col_base,
                                            const RowOut<typename SR::value_type>& out, int64_t row, int64_t slot,
@@ -937,6 +941,22 @@ __device__ __forceinline__ int bitmap_emit(typename SR::value_type* acc, uint32_
     }
     const int total = __shfl_sync(kFull, incl, 31);
     const int excl = incl - c;
+    if constexpr (kLaneEmit) {
+      // each lane writes its own word's entries (no per-entry search)
+      int k = excl;
+      for (uint32_t y = x; y; y &= y - 1) {
+        const int cc = (w << 5) + __ffs(y) - 1;
+        if (store) {
+          out.cols[pos + k] = col_base + cc;
+          out.vals[pos + k] = acc[cc];
+        }
+        acc[cc] = SR::zero();
+        ++k;
+      }
+      if (x) bm[w] = 0u;
+      pos += total;
+      continue;
+    }
     for (int q0 = 0; q0 < total; q0 += 32) {
       const int q = q0 + lane;
       int own = 0;
@@ -1029,15 +1049,30 @@ __global__ void __launch_bounds__(THREADS, MINB) dense_panel_kernel(Src src, con
           __syncthreads();
         }
         cache.template prefix<THREADS, Count>(n, p, scan_tmp);
+#ifdef SPG_ABL_NO_ATOMIC  // ablation build: loads and products only
+        balanced_items<SR, Src, NW, kDenseIPL>(src, cache, n, p, [&](int32_t c, const V& v) {
+          if (bits_equal(v, SR::one()) && c == -7) acc[0] = v;
+        });
+#else
         balanced_items<SR, Src, NW, kDenseIPL>(src, cache, n, p, [&](int32_t c, const V& v) {
           if (SR::is_zero(v)) return;  // add(x, zero) == x: nothing to fold
           const int cc = c - lo;
           const V old = atomic_accumulate<SR, true>(&acc[cc], v);
           if (is_zero_bits<SR>(old)) atomicOr(&bm[cc >> 5], 1u << (cc & 31));  // first touch
         });
+#endif
         __syncthreads();
       }
+#ifdef SPG_ABL_NO_EMIT  // ablation build: clear instead of emitting
+      for (int e = threadIdx.x; e < W / 32; e += THREADS)
+        if (bm[e]) {
+          for (uint32_t y = bm[e]; y; y &= y - 1) acc[(e << 5) + __ffs(y) - 1] = SR::zero();
+          bm[e] = 0u;
+        }
+      __syncthreads();
+#else
       written += bitmap_emit<SR, W, THREADS>(acc, bm, lo, out, i, r, p, npanels, written, wsum, &s_base);
+#endif
     }
     if (threadIdx.x == 0) out.rownnz[i] = written;
   }
