@@ -873,7 +873,24 @@ struct AddCanCancel {
 #define SPG_LANE_EMIT 0
 #endif
 constexpr bool kLaneEmit = SPG_LANE_EMIT != 0;  // lane-sequential emit instead of the flattened one
-template <class SR, int W, int THREADS>
+// Barrier over a warp group: BAR == 0 is __syncthreads, else named barrier
+// BAR over NT threads (warp-specialised kernels).
+template <int BAR, int NT>
+__device__ __forceinline__ void group_sync() {
+  if constexpr (BAR == 0) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NT) : "memory");
+  }
+}
+__device__ __forceinline__ void named_sync(int bar, int nt) {
+  asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nt) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int bar, int nt) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(bar), "r"(nt) : "memory");
+}
+
+template <class SR, int W, int THREADS, int BAR = 0, int WARP0 = 0>
 __device__ __forceinline__ int bitmap_emit(typename SR::value_type* acc, uint32_t* bm, int col_base,
                                            const RowOut<typename SR::value_type>& out, int64_t row, int64_t slot,
                                            int panel, int npanels, int64_t written, int* wsum, long long* s_base) {
@@ -883,7 +900,7 @@ __device__ __forceinline__ int bitmap_emit(typename SR::value_type* acc, uint32_
   constexpr int WPW = WORDS / NW;  // words per warp
   constexpr int ITERS = (WPW + 31) / 32;
   static_assert(WORDS % NW == 0 && (WPW < 32 || WPW % 32 == 0), "bitmap words must split evenly over the warps");
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, wid = (threadIdx.x >> 5) - WARP0;
   const int w0 = wid * WPW;
   if constexpr (AddCanCancel<SR>::value) {
     // drop touched entries whose fold cancelled to zero (restoring exact zero() bits)
@@ -910,7 +927,7 @@ __device__ __forceinline__ int bitmap_emit(typename SR::value_type* acc, uint32_
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
   if (lane == 0) wsum[wid] = cnt;
-  __syncthreads();
+  group_sync<BAR, THREADS>();
   if (wid == 0) {
     const int v = lane < NW ? wsum[lane] : 0;
     int incl = v;
@@ -925,7 +942,7 @@ __device__ __forceinline__ int bitmap_emit(typename SR::value_type* acc, uint32_
       *s_base = out.claim_chunk(row, slot, panel, npanels, written, incl);
     }
   }
-  __syncthreads();
+  group_sync<BAR, THREADS>();
   const bool store = *s_base >= 0;
   int64_t pos = *s_base + wsum[NW + wid];
   for (int it = 0; it < ITERS; ++it) {
@@ -981,7 +998,7 @@ __device__ __forceinline__ int bitmap_emit(typename SR::value_type* acc, uint32_
     pos += total;
   }
   const int total = wsum[2 * NW];
-  __syncthreads();
+  group_sync<BAR, THREADS>();
   return total;
 }
 
@@ -1075,6 +1092,140 @@ __global__ void __launch_bounds__(THREADS, MINB) dense_panel_kernel(Src src, con
 #endif
     }
     if (threadIdx.x == 0) out.rownnz[i] = written;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5' bin 6, warp-specialised: PW product warps fold panel p into one of two
+// accumulators while EW emit warps write out panel p-1 from the other, so
+// the ordered emission overlaps the next panel's gathers and atomics.
+// Hand-off per accumulator buffer b through named barriers:
+//   FULL(b) = 1 + b : product warps arrive after folding, emit warps sync;
+//   FREE(b) = 3 + b : emit warps arrive after emitting, product warps sync.
+// Barrier 5 = product warps only (segment-cache reload, prefix scan),
+// barrier 6 = emit warps only (inside bitmap_emit).
+// ---------------------------------------------------------------------------
+template <class SR, class Src, int W, int PW, int EW>
+__global__ void __launch_bounds__((PW + EW) * 32, 1) dense_panel_ws_kernel(Src src, const int64_t* __restrict__ rows,
+                                                                          int64_t nrows_bin, int npanels, int cap,
+                                                                          unsigned long long* __restrict__ work,
+                                                                          RowOut<typename SR::value_type> out) {
+  using V = typename SR::value_type;
+  constexpr int NT = (PW + EW) * 32, PT = PW * 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* acc = reinterpret_cast<V*>(smem_raw);                               // [2][W]
+  uint32_t* bm = reinterpret_cast<uint32_t*>(smem_raw + 2 * sizeof(V) * W);  // [2][W/32]
+  SegCache<SR, Src> cache;
+  cache.carve(smem_raw + 2 * sizeof(V) * W + 2 * sizeof(uint32_t) * (W / 32), cap, npanels);
+  __shared__ long long s_row, s_base;
+  __shared__ int wsum[2 * EW + 1];
+  __shared__ int psum[PW + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool producer = warp < PW;
+
+  for (int e = threadIdx.x; e < 2 * W; e += NT) acc[e] = SR::zero();
+  for (int e = threadIdx.x; e < 2 * (W / 32); e += NT) bm[e] = 0u;
+  __syncthreads();
+  if (!producer) {  // both buffers start free
+    named_arrive(3, NT);
+    named_arrive(4, NT);
+  }
+  unsigned gp = 0;  // panels handed off so far (selects the buffer)
+  for (;;) {
+    if (threadIdx.x == 0) {
+      const unsigned long long r = atomicAdd(work, 1ull);
+      s_row = r < (unsigned long long)nrows_bin ? (long long)r : -1;
+    }
+    __syncthreads();  // previous row fully emitted; s_row visible
+    const long long r = s_row;
+    if (r < 0) break;
+    const int64_t i = rows[r];
+    const int64_t sb = src.seg_begin(i), se = src.seg_end(i);
+    const int64_t nseg = se - sb;
+    const bool single = nseg <= cap;
+    if (single) {
+      cache.load(src, i, sb, (int)nseg, threadIdx.x, NT);
+      __syncthreads();
+    }
+    if (producer) {
+      for (int p = 0; p < npanels; ++p, ++gp) {
+        const int b = gp & 1;
+        named_sync(3 + b, NT);  // buffer b emitted and cleared
+        V* a = acc + b * W;
+        uint32_t* m = bm + b * (W / 32);
+        const int lo = p * W;
+        for (int64_t c0 = 0; c0 < nseg; c0 += cap) {
+          const int n = (int)(nseg - c0 < (int64_t)cap ? nseg - c0 : (int64_t)cap);
+          if (!single) {
+            named_sync(5, PT);  // previous batch's items consumed
+            cache.load(src, i, sb + c0, n, threadIdx.x, PT);
+            named_sync(5, PT);
+          }
+          // pre[0..n] = prefix of the panel-p slice lengths (product warps)
+          {
+            const int ipt = (n + PT - 1) / PT;
+            const int t0 = threadIdx.x * ipt;
+            int local = 0;
+            for (int q = 0; q < ipt; ++q)
+              if (t0 + q < n) local += cache.len(t0 + q, p);
+            int incl = local;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+              const int x = __shfl_up_sync(kFull, incl, d);
+              if (lane >= d) incl += x;
+            }
+            if (lane == 31) psum[warp] = incl;
+            named_sync(5, PT);
+            if (warp == 0) {
+              const int v = lane < PW ? psum[lane] : 0;
+              int wi = v;
+#pragma unroll
+              for (int d = 1; d < 32; d <<= 1) {
+                const int x = __shfl_up_sync(kFull, wi, d);
+                if (lane >= d) wi += x;
+              }
+              if (lane < PW) psum[lane] = wi - v;
+              if (lane == 31) psum[PW] = wi;
+            }
+            named_sync(5, PT);
+            int first = psum[warp] + incl - local;
+            for (int q = 0; q < ipt; ++q)
+              if (t0 + q < n) {
+                cache.pre[t0 + q] = first;
+                first += cache.len(t0 + q, p);
+              }
+            if (threadIdx.x == 0) cache.pre[n] = psum[PW];
+            named_sync(5, PT);
+          }
+          balanced_items<SR, Src, PW, kDenseIPL>(src, cache, n, p, [&](int32_t c, const V& v) {
+            if (SR::is_zero(v)) return;
+            const int cc = c - lo;
+            const V old = atomic_accumulate<SR, true>(&a[cc], v);
+            if (is_zero_bits<SR>(old)) atomicOr(&m[cc >> 5], 1u << (cc & 31));
+          });
+          if (!single) named_sync(5, PT);
+        }
+        __threadfence_block();
+        named_arrive(1 + b, NT);  // panel p ready for emission
+      }
+    } else {
+      int64_t written = 0;
+      for (int p = 0; p < npanels; ++p, ++gp) {
+        const int b = gp & 1;
+        named_sync(1 + b, NT);  // panel p folded
+        written += bitmap_emit<SR, W, EW * 32, 6, PW>(acc + b * W, bm + b * (W / 32), p * W, out, i, r, p, npanels,
+                                                       written, wsum, &s_base);
+        named_arrive(3 + b, NT);  // buffer b free again
+      }
+      if (threadIdx.x == PT) {
+        out.rownnz[i] = written;
+        if (out.bump) out.rowstart[i] = -2;
+      }
+    }
+  }
+  if (producer) {  // consume the last two FREE hand-offs
+    named_sync(3, NT);
+    named_sync(4, NT);
   }
 }
 

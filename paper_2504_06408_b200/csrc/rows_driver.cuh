@@ -136,6 +136,27 @@ void launch_dense_cfg(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t*
   ++c->launches;
 }
 
+// Warp-specialised dense kernel: two W-column accumulators, PW product warps,
+// EW emit warps, one CTA per SM.
+template <int W, int PW, int EW, class SR, class Src>
+void launch_dense_ws(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* rows, int64_t n, int64_t ncols,
+                     size_t smem_budget, unsigned long long* work, const RowOut<typename SR::value_type>& out) {
+  using V = typename SR::value_type;
+  const int np = (int)((ncols + W - 1) / W);
+  const size_t per_seg = SegCache<SR, Src>::bytes_per_seg(np);
+  const size_t fixed = 2 * (sizeof(V) * W + sizeof(uint32_t) * (W / 32));
+  const size_t room = smem_budget > fixed + 64 ? smem_budget - fixed - 64 : 0;
+  const int cap = (int)std::min<size_t>(8192, room / per_seg) & ~3;
+  if (cap < 32) fail(SPG_ERR_INTERNAL, "dense panel: no room for the segment cache");
+  const size_t smem = fixed + (size_t)cap * per_seg + 64;
+  auto kern = dense_panel_ws_kernel<SR, Src, W, PW, EW>;
+  set_smem(kern, smem);
+  kern<<<resident_grid(c, kern, (PW + EW) * 32, smem, n), (PW + EW) * 32, smem, s>>>(src, rows, n, np, cap, work,
+                                                                                     out);
+  SPG_LAUNCH_CHECK();
+  ++c->launches;
+}
+
 inline int dense_cfg() {
   static int cfg = [] {
     const char* e = std::getenv("SPG_DENSE_CFG");
@@ -170,6 +191,12 @@ void launch_dense(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* row
       break;
     case 5:
       launch_dense_cfg<PW / 2, 128, SR, Src>(c, s, src, rows, n, ncols, 110 * 1024, work, out);
+      break;
+    case 7:  // warp-specialised: 24 product + 8 emit warps, double-buffered 64 KB panels
+      launch_dense_ws<PW / 2, 24, 8, SR, Src>(c, s, src, rows, n, ncols, 220 * 1024, work, out);
+      break;
+    case 8:
+      launch_dense_ws<PW / 2, 28, 4, SR, Src>(c, s, src, rows, n, ncols, 220 * 1024, work, out);
       break;
     case 6:  // 3 CTAs/SM: register cap 42, small segment cache
       launch_dense_cfg<PW / 2, 512, SR, Src, 3>(c, s, src, rows, n, ncols, 74 * 1024, work, out);
