@@ -275,7 +275,7 @@ __device__ __forceinline__ void warp_items(const Src& src, int64_t i, int64_t s0
 // K1: per-row analysis and binning policy
 // ---------------------------------------------------------------------------
 template <class SR, class Src>
-__global__ void __launch_bounds__(256) analyse_rows_kernel(Src src, int64_t ncols_out, int64_t dense_min,
+__global__ void __launch_bounds__(256) analyse_rows_kernel(Src src, int64_t ncols_out, int64_t dense_min, int esc1k,
                                                            int64_t* __restrict__ prods,
                                                            int64_t* __restrict__ ubound,
                                                            uint8_t* __restrict__ bins) {
@@ -298,8 +298,9 @@ __global__ void __launch_bounds__(256) analyse_rows_kernel(Src src, int64_t ncol
       if (f == 0) b = kBinEmpty;
       else if (f <= 32) b = kBinWarpEsc;
       else if (f <= 512 && nseg <= 512) b = kBinEsc512;
+      else if (esc1k && f <= 1024 && nseg <= 1024) b = kBinHash2K;  // bin 5 = block-ESC 1K in this mode
       else if (f > dense_min && dense_ok) b = kBinDense;
-      else if (u <= 1024) b = kBinHash2K;
+      else if (!esc1k && u <= 1024) b = kBinHash2K;
       else if (u <= 2048) b = kBinHash4K;
       else if (u <= 4096) b = kBinHash8K;
       else if (u <= Geom<V>::kMaxT / 2) b = kBinHashMax;

@@ -268,8 +268,12 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
     const char* e = std::getenv("SPG_DENSE_MIN");
     return e ? (int64_t)std::atoll(e) : kDenseMinRow;
   }();
-  analyse_rows_kernel<SR, Src><<<grid_for(c, m, 8), 256, 0, c->stream>>>(src, ncols_out, dense_min, prods.p, ub.p,
-                                                                        bins.p);
+  static const int esc1k = [] {  // SPG_ESC1K=1: rows with F <= 1024 are sorted (block-ESC) instead of hashed
+    const char* e = std::getenv("SPG_ESC1K");
+    return e ? std::atoi(e) : 0;
+  }();
+  analyse_rows_kernel<SR, Src><<<grid_for(c, m, 8), 256, 0, c->stream>>>(src, ncols_out, dense_min, esc1k, prods.p,
+                                                                        ub.p, bins.p);
   SPG_LAUNCH_CHECK();
   ++c->launches;
   SPG_CUDA(cudaMemsetAsync(ub.p + m, 0, sizeof(int64_t), c->stream));
@@ -411,8 +415,12 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
       launch_hash<SR, Src, 8192, 512>(c, fk[1], src, lb + base[kBinHash8K], hcounts[kBinHash8K], 256, end_bit, o);
     if (hcounts[kBinHash4K] > 0)
       launch_hash<SR, Src, 4096, 256>(c, fk[2], src, lb + base[kBinHash4K], hcounts[kBinHash4K], 256, end_bit, o);
-    if (hcounts[kBinHash2K] > 0)
-      launch_hash<SR, Src, 2048, 128>(c, fk[2], src, lb + base[kBinHash2K], hcounts[kBinHash2K], 256, end_bit, o);
+    if (hcounts[kBinHash2K] > 0) {
+      if (esc1k)
+        launch_esc<SR, Src, 256, 4>(c, fk[2], src, lb + base[kBinHash2K], hcounts[kBinHash2K], end_bit, o);
+      else
+        launch_hash<SR, Src, 2048, 128>(c, fk[2], src, lb + base[kBinHash2K], hcounts[kBinHash2K], 256, end_bit, o);
+    }
     if (hcounts[kBinEsc512] > 0)
       launch_esc<SR, Src, 128, 4>(c, fk[2], src, lb + base[kBinEsc512], hcounts[kBinEsc512], end_bit, o);
     if (hcounts[kBinWarpEsc] > 0) {

@@ -4,7 +4,7 @@ import numpy as np
 import pytest
 
 import oracle_bind as ob
-from helpers import RTOL, assert_same, to_mat, unpack
+from helpers import RTOL, assert_same, ptr_idx_vals, to_mat, unpack
 from paper_2504_06408_b200 import (DeviceCsr, errors, esc_multiply, generators, local_multiply,
                                    matrix_checksum, merge_partials)
 from paper_2504_06408_b200._lib import lib
@@ -207,3 +207,27 @@ def test_merge_dense_panels_against_oracle(ctx, sr):
     assert np.array_equal(out.colptr, want.ptr) and np.array_equal(out.rowids, want.idx)
     assert out.values.tobytes() == want.vals.tobytes()
     assert st["rows_per_bin"][6] == nrows
+
+
+@pytest.mark.parametrize("N", [7, 24])
+def test_config4_stencil27_fp64_against_oracle(ctx, N):
+    """BASELINE config 4 family (3D 27-point Laplacian, fp64): totals equal the
+    closed forms and C equals the oracle within the fp64
+    tolerance (integer-valued, so in fact exactly)."""
+    a = coo_to_csr(generators.generate_stencil27(0, N))
+    st = {}
+    got = esc_multiply(a, a, ctx=ctx, stats=st)
+    assert st["products"] == (9 * N - 10) ** 3 and got.nnz == (5 * N - 6) ** 3
+    want = ob.orc_multiply(to_mat(a), to_mat(a))
+    assert_same(got, want, 0, rtol=RTOL)
+    assert np.array_equal(np.asarray(ptr_idx_vals(got)[2]), np.asarray(ptr_idx_vals(want)[2]))  # integer-valued: exact
+
+
+@pytest.mark.parametrize("n,d", [(4096, 16), (1 << 14, 64)])
+def test_config5_er_maxtimes_struct_against_oracle(ctx, n, d):
+    """BASELINE config 5 family (ER rows, max-times on the {weight, tag}
+    struct, value_mode 1): bit-exact against the oracle."""
+    a = coo_to_csr(generators.generate_er(5, n, d, 1, value_mode=1))
+    got = esc_multiply(a, a, ctx=ctx)
+    want = ob.orc_multiply(to_mat(a), to_mat(a))
+    assert_same(got, want, 5)
