@@ -51,7 +51,7 @@
 
 namespace spg {
 
-constexpr int kNumBins = 8;
+constexpr int kNumBins = 9;
 constexpr int32_t kEmptyKey = -1;
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -64,6 +64,7 @@ enum Bin : uint8_t {
   kBinHash2K = 5,    // U <= 1024: 2K-slot hash, 128 threads (many CTAs per SM)
   kBinDense = 6,     // long rows: dense column panels
   kBinHashMax = 7,   // wide outputs: largest smem hash
+  kBinBitRank = 8,   // F <= kBitRankMax, narrow C: presence bitmap + ranked accumulator
 };
 
 // ---------------------------------------------------------------------------
@@ -276,6 +277,7 @@ __device__ __forceinline__ void warp_items(const Src& src, int64_t i, int64_t s0
 // ---------------------------------------------------------------------------
 template <class SR, class Src>
 __global__ void __launch_bounds__(256) analyse_rows_kernel(Src src, int64_t ncols_out, int64_t dense_min, int esc1k,
+                                                           int64_t bitrank_max, int64_t bitrank_segs,
                                                            int64_t* __restrict__ prods,
                                                            int64_t* __restrict__ ubound,
                                                            uint8_t* __restrict__ bins) {
@@ -299,6 +301,7 @@ __global__ void __launch_bounds__(256) analyse_rows_kernel(Src src, int64_t ncol
       else if (f <= 32) b = kBinWarpEsc;
       else if (f <= 512 && nseg <= 512) b = kBinEsc512;
       else if (esc1k && f <= 1024 && nseg <= 1024) b = kBinHash2K;  // bin 5 = block-ESC 1K in this mode
+      else if (bitrank_max > 0 && f <= bitrank_max && nseg <= bitrank_segs) b = kBinBitRank;
       else if (f > dense_min && dense_ok) b = kBinDense;
       else if (!esc1k && u <= 1024) b = kBinHash2K;
       else if (u <= 2048) b = kBinHash4K;
@@ -1227,6 +1230,91 @@ __global__ void __launch_bounds__((PW + EW) * 32, 1) dense_panel_ws_kernel(Src s
   if (producer) {  // consume the last two FREE hand-offs
     named_sync(3, NT);
     named_sync(4, NT);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4' bin 8: bit-rank accumulator for mid-size rows of a narrow C (ncols up
+// to a few 100K).  Pass 1 sets a presence bit per product column over the
+// WHOLE row (ncols/8 bytes of smem, no column panels); a block scan of the
+// word popcounts gives every present column its rank = its output position;
+// pass 2 folds each product into acc[rank] with native smem atomics; the
+// output is the bitmap expanded in order plus acc[0..nnz) copied straight
+// out — sorted without sorting, no probing, no per-panel phases.
+// Not used for semirings whose fold can cancel to zero (fp64 +).
+// ---------------------------------------------------------------------------
+template <class SR, class Src, int THREADS, int NMAX>
+__global__ void __launch_bounds__(THREADS) bitrank_rows_kernel(Src src, const int64_t* __restrict__ rows,
+                                                               int64_t nrows_bin, int cap, int words,
+                                                               RowOut<typename SR::value_type> out) {
+  using V = typename SR::value_type;
+  constexpr int NW = THREADS / 32;
+  using Scan = cub::BlockScan<int, THREADS>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  static_assert(NMAX <= 65536, "ranks are stored in 16 bits");
+  V* acc = reinterpret_cast<V*>(smem_raw);                                        // [NMAX]
+  uint32_t* bm = reinterpret_cast<uint32_t*>(smem_raw + sizeof(V) * NMAX);        // [words]
+  uint16_t* wpre = reinterpret_cast<uint16_t*>(bm + ((words + 7) & ~7));          // [words]
+  SegCache<SR, Src> cache;
+  cache.carve(reinterpret_cast<unsigned char*>(wpre + ((words + 7) & ~7)), cap, 1);
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ long long s_base;
+  const int wpt = (words + THREADS - 1) / THREADS;
+  const int w0 = threadIdx.x * wpt;
+  for (int e = threadIdx.x; e < words; e += THREADS) bm[e] = 0u;
+  __syncthreads();
+  for (int64_t r = blockIdx.x; r < nrows_bin; r += gridDim.x) {
+    const int64_t i = rows[r];
+    const int64_t sb = src.seg_begin(i);
+    const int n = (int)(src.seg_end(i) - sb);  // <= cap by binning
+    cache.load(src, i, sb, n, threadIdx.x, THREADS);
+    __syncthreads();
+    cache.template prefix<THREADS, Scan>(n, 0, scan_tmp);
+    // pass 1: presence
+    balanced_items<SR, Src, NW>(src, cache, n, 0, [&](int32_t c, const V& v) {
+      if (!SR::is_zero(v)) atomicOr(&bm[c >> 5], 1u << (c & 31));
+    });
+    __syncthreads();
+    // ranks: exclusive prefix of the word popcounts
+    int local = 0;
+    for (int q = 0; q < wpt; ++q)
+      if (w0 + q < words) local += __popc(bm[w0 + q]);
+    int first, total;
+    Scan(scan_tmp).ExclusiveSum(local, first, total);
+    for (int q = 0; q < wpt; ++q)
+      if (w0 + q < words) {
+        wpre[w0 + q] = (uint16_t)first;
+        first += __popc(bm[w0 + q]);
+      }
+    for (int e = threadIdx.x; e < total; e += THREADS) acc[e] = SR::zero();
+    if (threadIdx.x == 0) {
+      s_base = out.claim_row(i, total);
+      out.rownnz[i] = total;
+    }
+    __syncthreads();
+    // pass 2: fold into acc[rank]
+    balanced_items<SR, Src, NW>(src, cache, n, 0, [&](int32_t c, const V& v) {
+      if (SR::is_zero(v)) return;
+      const int w = c >> 5;
+      const int rank = wpre[w] + __popc(bm[w] & ((1u << (c & 31)) - 1u));
+      atomic_accumulate<SR, true>(&acc[rank], v);
+    });
+    __syncthreads();
+    // emit: columns from the bitmap (in order), values straight from acc
+    const int64_t o = s_base;
+    if (o >= 0) {
+      for (int q = 0; q < wpt; ++q) {
+        const int w = w0 + q;
+        if (w >= words) break;
+        int k = wpre[w];
+        for (uint32_t y = bm[w]; y; y &= y - 1) out.cols[o + k++] = (w << 5) + __ffs(y) - 1;
+      }
+      for (int e = threadIdx.x; e < total; e += THREADS) out.vals[o + e] = acc[e];
+    }
+    __syncthreads();
+    for (int q = 0; q < wpt; ++q)
+      if (w0 + q < words) bm[w0 + q] = 0u;
+    __syncthreads();
   }
 }
 
