@@ -188,6 +188,7 @@ struct Geom {
 constexpr int kDenseMaxPanels = 16;   // beyond this many panels prefer hashing
 constexpr int kDenseMinPerPanel = 1024;
 constexpr int64_t kDenseMinRow = 4096;  // rows with more products go dense (when panels are few)
+constexpr int64_t kBitRankMinF = 2048;  // bit-rank bin floor (smaller rows: hash bins, more rows per SM)
 
 template <class V>
 __host__ __device__ inline int npanels_for(int64_t ncols, int w = Geom<V>::kPanelW) {
@@ -278,6 +279,7 @@ __device__ __forceinline__ void warp_items(const Src& src, int64_t i, int64_t s0
 template <class SR, class Src>
 __global__ void __launch_bounds__(256) analyse_rows_kernel(Src src, int64_t ncols_out, int64_t dense_min, int esc1k,
                                                            int64_t bitrank_max, int64_t bitrank_segs,
+                                                           int64_t bitrank_span, int32_t* __restrict__ colmin,
                                                            int64_t* __restrict__ prods,
                                                            int64_t* __restrict__ ubound,
                                                            uint8_t* __restrict__ bins) {
@@ -292,6 +294,28 @@ __global__ void __launch_bounds__(256) analyse_rows_kernel(Src src, int64_t ncol
     for (int64_t s = sb + lane; s < se; s += 32) f += src.seg_len(i, s);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) f += __shfl_xor_sync(kFull, f, o);
+    // column window of the row (bit-rank candidates only): min first / max last column over its segments
+    int64_t span = INT64_MAX;
+    if (bitrank_max > 0 && f > kBitRankMinF && f <= bitrank_max && se - sb <= bitrank_segs) {
+      int32_t cmin = INT32_MAX, cmax = -1;
+      for (int64_t s = sb + lane; s < se; s += 32) {
+        int64_t bb;
+        int len, sd;
+        V m;
+        src.seg(i, s, -1, bb, len, sd, m);
+        if (len > 0) {
+          cmin = min(cmin, src.col(sd, bb));
+          cmax = max(cmax, src.col(sd, bb + len - 1));
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        cmin = min(cmin, __shfl_xor_sync(kFull, cmin, o));
+        cmax = max(cmax, __shfl_xor_sync(kFull, cmax, o));
+      }
+      span = cmax >= cmin ? (int64_t)cmax - cmin + 1 : 0;
+      if (lane == 0) colmin[i] = cmin;
+    }
     if (lane == 0) {
       const int64_t u = f < ncols_out ? f : ncols_out;
       const int64_t nseg = se - sb;
@@ -301,7 +325,7 @@ __global__ void __launch_bounds__(256) analyse_rows_kernel(Src src, int64_t ncol
       else if (f <= 32) b = kBinWarpEsc;
       else if (f <= 512 && nseg <= 512) b = kBinEsc512;
       else if (esc1k && f <= 1024 && nseg <= 1024) b = kBinHash2K;  // bin 5 = block-ESC 1K in this mode
-      else if (bitrank_max > 0 && f <= bitrank_max && nseg <= bitrank_segs) b = kBinBitRank;
+      else if (bitrank_max > 0 && f <= bitrank_max && nseg <= bitrank_segs && span <= bitrank_span) b = kBinBitRank;
       else if (f > dense_min && dense_ok) b = kBinDense;
       else if (!esc1k && u <= 1024) b = kBinHash2K;
       else if (u <= 2048) b = kBinHash4K;
@@ -1234,57 +1258,81 @@ __global__ void __launch_bounds__((PW + EW) * 32, 1) dense_panel_ws_kernel(Src s
 }
 
 // ---------------------------------------------------------------------------
-// K4' bin 8: bit-rank accumulator for mid-size rows of a narrow C (ncols up
-// to a few 100K).  Pass 1 sets a presence bit per product column over the
-// WHOLE row (ncols/8 bytes of smem, no column panels); a block scan of the
-// word popcounts gives every present column its rank = its output position;
-// pass 2 folds each product into acc[rank] with native smem atomics; the
-// output is the bitmap expanded in order plus acc[0..nnz) copied straight
-// out — sorted without sorting, no probing, no per-panel phases.
+// K4' bin 8: bit-rank accumulator for mid-size rows whose output columns lie
+// in a window [colmin, colmin + span) of at most 32*WMAX columns.  Pass 1
+// sets a presence bit per product column (plus a summary bit per non-empty
+// word); the non-empty words, listed in order from the summary, get their
+// word ranks by one block scan, so every present column's rank is its output
+// position; pass 2 folds each product into acc[rank] with native smem
+// atomics; the output is the bitmap expanded in order plus acc[0..nnz)
+// copied straight out — sorted without sorting, no probing, no column
+// panels, and per-row work proportional to the non-empty words only.
 // Not used for semirings whose fold can cancel to zero (fp64 +).
 // ---------------------------------------------------------------------------
-template <class SR, class Src, int THREADS, int NMAX>
+template <class SR, class Src, int THREADS, int NMAX, int WMAX>
 __global__ void __launch_bounds__(THREADS) bitrank_rows_kernel(Src src, const int64_t* __restrict__ rows,
-                                                               int64_t nrows_bin, int cap, int words,
+                                                               int64_t nrows_bin, int cap,
+                                                               const int32_t* __restrict__ colmin,
                                                                RowOut<typename SR::value_type> out) {
   using V = typename SR::value_type;
   constexpr int NW = THREADS / 32;
+  constexpr int SW = WMAX / 32;                        // summary words
+  static_assert(NMAX <= 65535 && WMAX <= 65536 && SW <= THREADS, "bit-rank geometry");
+  constexpr int LPT = (NMAX + THREADS - 1) / THREADS;  // listed words per thread (<= NMAX words are non-empty)
   using Scan = cub::BlockScan<int, THREADS>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  static_assert(NMAX <= 65536, "ranks are stored in 16 bits");
-  V* acc = reinterpret_cast<V*>(smem_raw);                                        // [NMAX]
-  uint32_t* bm = reinterpret_cast<uint32_t*>(smem_raw + sizeof(V) * NMAX);        // [words]
-  uint16_t* wpre = reinterpret_cast<uint16_t*>(bm + ((words + 7) & ~7));          // [words]
+  V* acc = reinterpret_cast<V*>(smem_raw);                               // [NMAX]
+  uint32_t* bm = reinterpret_cast<uint32_t*>(acc + NMAX);                // [WMAX] presence
+  uint32_t* sm = bm + WMAX;                                              // [SW] non-empty words
+  uint16_t* wrank = reinterpret_cast<uint16_t*>(sm + SW);                // [WMAX] rank of a word's first entry
+  uint16_t* list = wrank + WMAX;                                         // [NMAX] non-empty words in order
   SegCache<SR, Src> cache;
-  cache.carve(reinterpret_cast<unsigned char*>(wpre + ((words + 7) & ~7)), cap, 1);
+  cache.carve(reinterpret_cast<unsigned char*>(list + ((NMAX + 7) & ~7)), cap, 1);
   __shared__ typename Scan::TempStorage scan_tmp;
   __shared__ long long s_base;
-  const int wpt = (words + THREADS - 1) / THREADS;
-  const int w0 = threadIdx.x * wpt;
-  for (int e = threadIdx.x; e < words; e += THREADS) bm[e] = 0u;
+  __shared__ int s_nw;
+  for (int e = threadIdx.x; e < WMAX; e += THREADS) bm[e] = 0u;
+  for (int e = threadIdx.x; e < SW; e += THREADS) sm[e] = 0u;
   __syncthreads();
   for (int64_t r = blockIdx.x; r < nrows_bin; r += gridDim.x) {
     const int64_t i = rows[r];
+    const int32_t lo = colmin[i];
     const int64_t sb = src.seg_begin(i);
     const int n = (int)(src.seg_end(i) - sb);  // <= cap by binning
     cache.load(src, i, sb, n, threadIdx.x, THREADS);
     __syncthreads();
     cache.template prefix<THREADS, Scan>(n, 0, scan_tmp);
-    // pass 1: presence
+    // pass 1: presence (+ summary bit on a word's first touch)
     balanced_items<SR, Src, NW>(src, cache, n, 0, [&](int32_t c, const V& v) {
-      if (!SR::is_zero(v)) atomicOr(&bm[c >> 5], 1u << (c & 31));
+      if (SR::is_zero(v)) return;
+      const int cc = c - lo, w = cc >> 5;
+      if (atomicOr(&bm[w], 1u << (cc & 31)) == 0u) atomicOr(&sm[w >> 5], 1u << (w & 31));
     });
     __syncthreads();
-    // ranks: exclusive prefix of the word popcounts
+    // list the non-empty words in order (summary word t -> thread t)
+    {
+      const uint32_t x = threadIdx.x < SW ? sm[threadIdx.x] : 0u;
+      int first, nw;
+      Scan(scan_tmp).ExclusiveSum(__popc(x), first, nw);
+      for (uint32_t y = x; y; y &= y - 1) list[first++] = (uint16_t)((threadIdx.x << 5) + __ffs(y) - 1);
+      if (threadIdx.x == 0) s_nw = nw;
+    }
+    __syncthreads();
+    const int nw = s_nw;
+    // word ranks: block scan of the popcounts over the listed words (blocked)
     int local = 0;
-    for (int q = 0; q < wpt; ++q)
-      if (w0 + q < words) local += __popc(bm[w0 + q]);
+    const int k0 = threadIdx.x * LPT;
+#pragma unroll
+    for (int q = 0; q < LPT; ++q)
+      if (k0 + q < nw) local += __popc(bm[list[k0 + q]]);
     int first, total;
     Scan(scan_tmp).ExclusiveSum(local, first, total);
-    for (int q = 0; q < wpt; ++q)
-      if (w0 + q < words) {
-        wpre[w0 + q] = (uint16_t)first;
-        first += __popc(bm[w0 + q]);
+#pragma unroll
+    for (int q = 0; q < LPT; ++q)
+      if (k0 + q < nw) {
+        const int w = list[k0 + q];
+        wrank[w] = (uint16_t)first;
+        first += __popc(bm[w]);
       }
     for (int e = threadIdx.x; e < total; e += THREADS) acc[e] = SR::zero();
     if (threadIdx.x == 0) {
@@ -1295,25 +1343,27 @@ __global__ void __launch_bounds__(THREADS) bitrank_rows_kernel(Src src, const in
     // pass 2: fold into acc[rank]
     balanced_items<SR, Src, NW>(src, cache, n, 0, [&](int32_t c, const V& v) {
       if (SR::is_zero(v)) return;
-      const int w = c >> 5;
-      const int rank = wpre[w] + __popc(bm[w] & ((1u << (c & 31)) - 1u));
-      atomic_accumulate<SR, true>(&acc[rank], v);
+      const int cc = c - lo, w = cc >> 5;
+      atomic_accumulate<SR, true>(&acc[wrank[w] + __popc(bm[w] & ((1u << (cc & 31)) - 1u))], v);
     });
     __syncthreads();
-    // emit: columns from the bitmap (in order), values straight from acc
+    // emit: columns expanded from the listed words, values straight from acc
     const int64_t o = s_base;
     if (o >= 0) {
-      for (int q = 0; q < wpt; ++q) {
-        const int w = w0 + q;
-        if (w >= words) break;
-        int k = wpre[w];
-        for (uint32_t y = bm[w]; y; y &= y - 1) out.cols[o + k++] = (w << 5) + __ffs(y) - 1;
-      }
+#pragma unroll
+      for (int q = 0; q < LPT; ++q)
+        if (k0 + q < nw) {
+          const int w = list[k0 + q];
+          int k = wrank[w];
+          for (uint32_t y = bm[w]; y; y &= y - 1) out.cols[o + k++] = lo + (w << 5) + __ffs(y) - 1;
+        }
       for (int e = threadIdx.x; e < total; e += THREADS) out.vals[o + e] = acc[e];
     }
     __syncthreads();
-    for (int q = 0; q < wpt; ++q)
-      if (w0 + q < words) bm[w0 + q] = 0u;
+#pragma unroll
+    for (int q = 0; q < LPT; ++q)
+      if (k0 + q < nw) bm[list[k0 + q]] = 0u;
+    if (threadIdx.x < SW) sm[threadIdx.x] = 0u;
     __syncthreads();
   }
 }

@@ -235,7 +235,7 @@ inline bool needs_poff(const MergeSource<SR>&) {
 }
 
 #ifndef SPG_BITRANK_N
-#define SPG_BITRANK_N 4096  // bit-rank bin: rows with F <= this many products
+#define SPG_BITRANK_N 0  // bit-rank bin: rows with F <= this many products (0: 8192, 4096 for values > 4 B)
 #endif
 
 // Runs the pipeline for rows [0, src.nrows) with output width ncols_out.
@@ -276,20 +276,21 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
     const char* e = std::getenv("SPG_ESC1K");
     return e ? std::atoi(e) : 0;
   }();
-  // bit-rank bin (bin 8): rows with F <= kBitRankN of a C narrow enough for a whole-row presence bitmap
+  // bit-rank bin (bin 8): rows with 512 < F <= kBitRankN whose output columns fit a window of 32*kBitRankW
   static const int bitrank_on = [] {
     const char* e = std::getenv("SPG_BITRANK");
     return e ? std::atoi(e) : 1;
   }();
-  constexpr int kBitRankN = SPG_BITRANK_N, kBitRankSegs = 512, kBitRankThreads = 512;
-  const int br_words = (int)((ncols_out + 31) / 32);
-  const size_t br_smem = sizeof(V) * kBitRankN + (sizeof(uint32_t) + sizeof(uint16_t)) * (size_t)((br_words + 7) & ~7) +
+  constexpr int kBitRankN = SPG_BITRANK_N > 0 ? SPG_BITRANK_N : (sizeof(V) <= 4 ? 8192 : 4096);
+  constexpr int kBitRankW = 8192, kBitRankSegs = 256, kBitRankThreads = 512;
+  const size_t br_smem = sizeof(V) * kBitRankN + sizeof(uint32_t) * (kBitRankW + kBitRankW / 32) +
+                         sizeof(uint16_t) * (kBitRankW + ((kBitRankN + 7) & ~7)) +
                          (size_t)kBitRankSegs * SegCache<SR, Src>::bytes_per_seg(1) + 64;
-  // worth it when the whole-row bitmap is small next to the rows' work (measured: 2.4-3.4x faster than the
-  // hash bins for ER rows over 64K columns, slower for R-MAT rows over 256K columns)
-  const bool bitrank = bitrank_on && !AddCanCancel<SR>::value && br_smem <= 220 * 1024 && br_words <= kBitRankN / 2;
+  const bool bitrank = bitrank_on && !AddCanCancel<SR>::value && br_smem <= 220 * 1024;
+  DBuf<int32_t> colmin(c, bitrank ? (size_t)m : 1);
   analyse_rows_kernel<SR, Src><<<grid_for(c, m, 8), 256, 0, c->stream>>>(
-      src, ncols_out, dense_min, esc1k, bitrank ? kBitRankN : 0, kBitRankSegs, prods.p, ub.p, bins.p);
+      src, ncols_out, dense_min, esc1k, bitrank ? kBitRankN : 0, kBitRankSegs, 32 * (int64_t)kBitRankW, colmin.p,
+      prods.p, ub.p, bins.p);
   SPG_LAUNCH_CHECK();
   ++c->launches;
   SPG_CUDA(cudaMemsetAsync(ub.p + m, 0, sizeof(int64_t), c->stream));
@@ -440,10 +441,10 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
     if (hcounts[kBinEsc512] > 0)
       launch_esc<SR, Src, 128, 4>(c, fk[2], src, lb + base[kBinEsc512], hcounts[kBinEsc512], end_bit, o);
     if (hcounts[kBinBitRank] > 0) {
-      auto kern = bitrank_rows_kernel<SR, Src, kBitRankThreads, kBitRankN>;
+      auto kern = bitrank_rows_kernel<SR, Src, kBitRankThreads, kBitRankN, kBitRankW>;
       set_smem(kern, br_smem);
       kern<<<resident_grid(c, kern, kBitRankThreads, br_smem, (int64_t)hcounts[kBinBitRank]), kBitRankThreads, br_smem,
-             fk[1]>>>(src, lb + base[kBinBitRank], (int64_t)hcounts[kBinBitRank], kBitRankSegs, br_words, o);
+             fk[1]>>>(src, lb + base[kBinBitRank], (int64_t)hcounts[kBinBitRank], kBitRankSegs, colmin.p, o);
       SPG_LAUNCH_CHECK();
       ++c->launches;
     }
