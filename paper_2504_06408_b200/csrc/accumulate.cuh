@@ -339,6 +339,13 @@ __global__ void __launch_bounds__(256) analyse_rows_kernel(Src src, int64_t ncol
   }
 }
 
+// number of rows (prefix of a list sorted by F descending) with more than t products
+static __global__ void count_above_kernel(const int64_t* __restrict__ rows, int64_t n, const int64_t* __restrict__ f,
+                                          int64_t t, unsigned long long* out) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    if (f[rows[k]] > t) atomicAdd(out, 1ull);
+}
+
 // ---------------------------------------------------------------------------
 // K2: bin histogram + scatter into per-bin row lists
 // ---------------------------------------------------------------------------
@@ -433,6 +440,8 @@ struct RowOut {
   int64_t cap = 0;
   int64_t* rowstart = nullptr;  // claim mode: scratch start of row i (-2: dense row, see chunks)
   int64_t* chunks = nullptr;    // claim mode, dense rows: (start, count) per (dense slot, panel)
+  int64_t slot_base = 0;        // dense slot of the launch's first row (several dense launches share `chunks`)
+  int chunk_stride = 0;         // chunk entries per dense slot (>= the launch's panel count)
   int64_t* rownnz = nullptr;
 
   __device__ __forceinline__ bool writes() const { return cols != nullptr; }
@@ -454,8 +463,9 @@ struct RowOut {
     if (!cols) return -1;
     if (!bump) return off[i] + written;
     const int64_t b = claim(n);
-    chunks[2 * (slot * np + p)] = b;
-    chunks[2 * (slot * np + p) + 1] = n;
+    const int64_t e = (slot + slot_base) * (chunk_stride > 0 ? chunk_stride : np) + p;
+    chunks[2 * e] = b;
+    chunks[2 * e + 1] = n;
     return b;
   }
 };

@@ -372,7 +372,10 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
   DBuf<unsigned long long> bump(c, 1);
   if (cap > 0 && !slotted) {
     rowstart = DBuf<int64_t>(c, (size_t)m);
-    if (hcounts[kBinDense] > 0) chunks = DBuf<int64_t>(c, (size_t)hcounts[kBinDense] * npc * 2);
+    if (hcounts[kBinDense] > 0) {
+      chunks = DBuf<int64_t>(c, (size_t)hcounts[kBinDense] * npc * 2);
+      SPG_CUDA(cudaMemsetAsync(chunks.p, 0, sizeof(int64_t) * hcounts[kBinDense] * npc * 2, c->stream));
+    }
     SPG_CUDA(cudaMemsetAsync(bump.p, 0, sizeof(unsigned long long), c->stream));
   }
   tm.mark(1);
@@ -411,20 +414,60 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
     ++c->launches;
     dense_rows = dense_sorted.p;
   }
+  // Heavy dense rows (F > kHeavyF: hundreds to thousands of segments) run in
+  // a 1-CTA/SM kernel with twice the panel width and a ~1000-segment cache
+  // (no segment batching); measured 2.2x faster for them than the 2-CTA one.
+  constexpr int64_t kHeavyF = 262144;
+  int64_t nh = 0;
+  Src src_heavy = src;
+  DBuf<int32_t> poff_heavy;
+  static const int heavy_on = [] {
+    const char* e = std::getenv("SPG_DENSE_HEAVY");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (heavy_on && nd > 0 && dense_cfg() == 1) {
+    DBuf<unsigned long long> cnt(c, 1);
+    SPG_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), c->stream));
+    count_above_kernel<<<grid_for(c, nd, 256, 2), 256, 0, c->stream>>>(dense_rows, nd, prods.p, kHeavyF, cnt.p);
+    SPG_LAUNCH_CHECK();
+    ++c->launches;
+    nh = (int64_t)d2h_scalar(c, cnt.p);
+    if (nh > 0) {
+      const int W2 = Geom<V>::kPanelW;
+      const int np2 = npanels_for<V>(ncols_out, W2);
+      if (np2 > 1 && needs_poff(src)) {
+        const spg_dcsr& R = *r_for_panels;
+        poff_heavy = DBuf<int32_t>(c, (size_t)R.nrows * (np2 + 1));
+        panel_offsets_kernel<<<grid_for(c, R.nrows, 8), 256, 0, c->stream>>>(R.nrows, R.ptr, R.idx, np2, W2,
+                                                                            poff_heavy.p);
+        SPG_LAUNCH_CHECK();
+        ++c->launches;
+      }
+      set_panels(src_heavy, poff_heavy.p, np2, W2);
+    }
+  }
   if (hcounts[kBinEmpty] > 0) {
     zero_empty_rows_kernel<<<grid_for(c, m, 256, 4), 256, 0, c->stream>>>(bins.p, m, rownnz.p);
     SPG_LAUNCH_CHECK();
     ++c->launches;
   }
-  DBuf<unsigned long long> work(c, 1);
+  DBuf<unsigned long long> work(c, 2);
   float ms_numeric = 0.f, ms_compact = 0.f;
 
   // One numeric pass over all bins with output placement `o`.
   auto numeric = [&](const RowOut<V>& o) {
-    SPG_CUDA(cudaMemsetAsync(work.p, 0, sizeof(unsigned long long), c->stream));
+    SPG_CUDA(cudaMemsetAsync(work.p, 0, 2 * sizeof(unsigned long long), c->stream));
     const int64_t* lb = lists.p;
     StreamFork fk(c, 3);
-    if (nd > 0) launch_dense<SR, Src>(c, fk[0], src, dense_rows, nd, ncols_out, work.p, o);
+    if (nh > 0) {
+      constexpr int PW = Geom<V>::kPanelW;
+      launch_dense_cfg<PW, 1024, SR, Src>(c, fk[0], src_heavy, dense_rows, nh, ncols_out, 220 * 1024, work.p + 1, o);
+    }
+    if (nd > nh) {
+      RowOut<V> rest = o;
+      rest.slot_base = nh;
+      launch_dense<SR, Src>(c, fk[0], src, dense_rows + nh, nd - nh, ncols_out, work.p, rest);
+    }
     if (hcounts[kBinHashMax] > 0)
       launch_hash<SR, Src, Geom<V>::kMaxT, 1024>(c, fk[1], src, lb + base[kBinHashMax], hcounts[kBinHashMax],
                                                  V_hash_cap<V>(Geom<V>::kMaxT), end_bit, o);
@@ -469,6 +512,7 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
       first.cap = cap;
       first.rowstart = rowstart.p;
       first.chunks = chunks.p;
+      first.chunk_stride = npc;
     }
   }
   numeric(first);
