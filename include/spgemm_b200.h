@@ -103,8 +103,9 @@ typedef struct {
 typedef struct {
   int64_t products;        /* F: intermediate products (flops = 2F) */
   int64_t nnz_out;
-  int64_t rows_per_bin[9]; /* 0 empty, 1 warp-ESC, 2 block-ESC, 3/4/5 hash 4K/8K/2K, 6 dense panels,
-                              7 hash max, 8 bit-rank (presence bitmap + ranked accumulator) */
+  int64_t rows_per_bin[10]; /* 0 empty, 1 warp-ESC, 2 block-ESC, 3/4/5 hash 4K/8K/2K, 6 dense panels,
+                               7 hash max, 8 bit-rank (presence bitmap + ranked accumulator),
+                               9 rank panels (bit-rank with accumulator panels in rank space) */
   double ms_analyse;       /* row products + binning + offsets */
   double ms_numeric;       /* accumulate kernels */
   double ms_compact;       /* output scan + compaction */

@@ -51,7 +51,7 @@
 
 namespace spg {
 
-constexpr int kNumBins = 9;
+constexpr int kNumBins = 10;
 constexpr int32_t kEmptyKey = -1;
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -65,6 +65,7 @@ enum Bin : uint8_t {
   kBinDense = 6,     // long rows: dense column panels
   kBinHashMax = 7,   // wide outputs: largest smem hash
   kBinBitRank = 8,   // F <= kBitRankMax, narrow C: presence bitmap + ranked accumulator
+  kBinRankPanels = 9,  // longer rows in a bounded column window: bitmap ranks, accumulator panels in rank space
 };
 
 // ---------------------------------------------------------------------------
@@ -279,7 +280,9 @@ __device__ __forceinline__ void warp_items(const Src& src, int64_t i, int64_t s0
 template <class SR, class Src>
 __global__ void __launch_bounds__(256) analyse_rows_kernel(Src src, int64_t ncols_out, int64_t dense_min, int esc1k,
                                                            int64_t bitrank_max, int64_t bitrank_segs,
-                                                           int64_t bitrank_span, int32_t* __restrict__ colmin,
+                                                           int64_t bitrank_span, int64_t rankpanel_segs,
+                                                           int64_t rankpanel_maxf,
+                                                           int32_t* __restrict__ colmin,
                                                            int64_t* __restrict__ prods,
                                                            int64_t* __restrict__ ubound,
                                                            uint8_t* __restrict__ bins) {
@@ -296,7 +299,9 @@ __global__ void __launch_bounds__(256) analyse_rows_kernel(Src src, int64_t ncol
     for (int o = 16; o > 0; o >>= 1) f += __shfl_xor_sync(kFull, f, o);
     // column window of the row (bit-rank candidates only): min first / max last column over its segments
     int64_t span = INT64_MAX;
-    if (bitrank_max > 0 && f > kBitRankMinF && f <= bitrank_max && se - sb <= bitrank_segs) {
+    if (bitrank_max > 0 && f > kBitRankMinF &&
+        ((f <= bitrank_max && se - sb <= bitrank_segs) ||
+         (rankpanel_segs > 0 && f <= rankpanel_maxf && se - sb <= rankpanel_segs))) {
       int32_t cmin = INT32_MAX, cmax = -1;
       for (int64_t s = sb + lane; s < se; s += 32) {
         int64_t bb;
@@ -326,6 +331,9 @@ __global__ void __launch_bounds__(256) analyse_rows_kernel(Src src, int64_t ncol
       else if (f <= 512 && nseg <= 512) b = kBinEsc512;
       else if (esc1k && f <= 1024 && nseg <= 1024) b = kBinHash2K;  // bin 5 = block-ESC 1K in this mode
       else if (bitrank_max > 0 && f <= bitrank_max && nseg <= bitrank_segs && span <= bitrank_span) b = kBinBitRank;
+      else if (rankpanel_segs > 0 && f > bitrank_max && f <= rankpanel_maxf && nseg <= rankpanel_segs &&
+               span <= bitrank_span)
+        b = kBinRankPanels;
       else if (f > dense_min && dense_ok) b = kBinDense;
       else if (!esc1k && u <= 1024) b = kBinHash2K;
       else if (u <= 2048) b = kBinHash4K;
@@ -1370,6 +1378,159 @@ __global__ void __launch_bounds__(THREADS) bitrank_rows_kernel(Src src, const in
       for (int e = threadIdx.x; e < total; e += THREADS) out.vals[o + e] = acc[e];
     }
     __syncthreads();
+#pragma unroll
+    for (int q = 0; q < LPT; ++q)
+      if (k0 + q < nw) bm[list[k0 + q]] = 0u;
+    if (threadIdx.x < SW) sm[threadIdx.x] = 0u;
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5'' bin 9: rank panels.  Long rows whose output columns fit a window of
+// 32*WMAX columns: pass 1 marks presence over the whole window, a block scan
+// of the non-empty words' popcounts ranks every output column (= its output
+// position), all output columns are written at once, and the values are
+// folded panel by panel in RANK space — panel k holds ranks [k*NMAX,
+// (k+1)*NMAX), i.e. a column range found from the ranks, so every
+// accumulator slot is an output and a row needs ceil(nnz/NMAX) panels
+// instead of ncols/W.  Segment slices per panel come from binary searches
+// in the (sorted) right-operand rows.  Emission is a contiguous copy.
+// ---------------------------------------------------------------------------
+template <class SR, class Src, int THREADS, int NMAX, int WMAX>
+__global__ void __launch_bounds__(THREADS, 1) rankpanel_rows_kernel(Src src, const int64_t* __restrict__ rows,
+                                                                    int64_t nrows_bin, int cap,
+                                                                    const int32_t* __restrict__ colmin,
+                                                                    RowOut<typename SR::value_type> out) {
+  using V = typename SR::value_type;
+  constexpr int NW = THREADS / 32;
+  constexpr int SW = WMAX / 32;
+  constexpr int LPT = (WMAX + THREADS - 1) / THREADS;  // listed words per thread
+  static_assert(WMAX <= 65536 && SW <= THREADS, "rank-panel geometry");
+  using Scan = cub::BlockScan<int, THREADS>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* acc = reinterpret_cast<V*>(smem_raw);                  // [NMAX]
+  uint32_t* bm = reinterpret_cast<uint32_t*>(acc + NMAX);   // [WMAX]
+  uint32_t* sm = bm + WMAX;                                 // [SW]
+  int* wrank = reinterpret_cast<int*>(sm + SW);             // [WMAX]
+  uint16_t* list = reinterpret_cast<uint16_t*>(wrank + WMAX);  // [WMAX]
+  int64_t* b0 = reinterpret_cast<int64_t*>(list + WMAX);    // [cap] whole-segment starts
+  int* len0 = reinterpret_cast<int*>(b0 + cap);             // [cap]
+  SegCache<SR, Src> cache;
+  cache.carve(reinterpret_cast<unsigned char*>(len0 + ((cap + 3) & ~3)), cap, 1);
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ long long s_base;
+  __shared__ int s_nw, s_clo, s_chi;
+  for (int e = threadIdx.x; e < WMAX; e += THREADS) bm[e] = 0u;
+  for (int e = threadIdx.x; e < SW; e += THREADS) sm[e] = 0u;
+  __syncthreads();
+  for (int64_t r = blockIdx.x; r < nrows_bin; r += gridDim.x) {
+    const int64_t i = rows[r];
+    const int32_t lo = colmin[i];
+    const int64_t sb = src.seg_begin(i);
+    const int n = (int)(src.seg_end(i) - sb);  // <= cap by binning
+    cache.load(src, i, sb, n, threadIdx.x, THREADS);
+    __syncthreads();
+    for (int t = threadIdx.x; t < n; t += THREADS) {
+      b0[t] = cache.b[t];
+      len0[t] = cache.po[t];
+    }
+    cache.template prefix<THREADS, Scan>(n, 0, scan_tmp);
+    // pass 1: presence over the window (+ summary bit on a word's first touch)
+    balanced_items<SR, Src, NW>(src, cache, n, 0, [&](int32_t c, const V& v) {
+      if (SR::is_zero(v)) return;
+      const int cc = c - lo, w = cc >> 5;
+      if (atomicOr(&bm[w], 1u << (cc & 31)) == 0u) atomicOr(&sm[w >> 5], 1u << (w & 31));
+    });
+    __syncthreads();
+    {
+      const uint32_t x = threadIdx.x < SW ? sm[threadIdx.x] : 0u;
+      int first, nw;
+      Scan(scan_tmp).ExclusiveSum(__popc(x), first, nw);
+      for (uint32_t y = x; y; y &= y - 1) list[first++] = (uint16_t)((threadIdx.x << 5) + __ffs(y) - 1);
+      if (threadIdx.x == 0) s_nw = nw;
+    }
+    __syncthreads();
+    const int nw = s_nw;
+    const int k0 = threadIdx.x * LPT;
+    int local = 0;
+#pragma unroll
+    for (int q = 0; q < LPT; ++q)
+      if (k0 + q < nw) local += __popc(bm[list[k0 + q]]);
+    int first, total;
+    Scan(scan_tmp).ExclusiveSum(local, first, total);
+#pragma unroll
+    for (int q = 0; q < LPT; ++q)
+      if (k0 + q < nw) {
+        const int w = list[k0 + q];
+        wrank[w] = first;
+        first += __popc(bm[w]);
+      }
+    if (threadIdx.x == 0) {
+      s_base = out.claim_row(i, total);
+      out.rownnz[i] = total;
+    }
+    __syncthreads();
+    const int64_t o = s_base;
+    // all output columns of the row
+    if (o >= 0) {
+#pragma unroll
+      for (int q = 0; q < LPT; ++q)
+        if (k0 + q < nw) {
+          const int w = list[k0 + q];
+          int k = wrank[w];
+          for (uint32_t y = bm[w]; y; y &= y - 1) out.cols[o + k++] = lo + (w << 5) + __ffs(y) - 1;
+        }
+    }
+    const int npan = (total + NMAX - 1) / NMAX;
+    for (int pk = 0; pk < npan; ++pk) {
+      const int R0 = pk * NMAX, R1 = min(total, R0 + NMAX);
+      if (npan > 1) {
+        // window columns of ranks R0 and R1-1
+#pragma unroll
+        for (int q = 0; q < LPT; ++q)
+          if (k0 + q < nw) {
+            const int w = list[k0 + q];
+            const int a = wrank[w], c = __popc(bm[w]);
+            if (a <= R0 && R0 < a + c) s_clo = (w << 5) + nth_set_bit(bm[w], R0 - a);
+            if (a <= R1 - 1 && R1 - 1 < a + c) s_chi = (w << 5) + nth_set_bit(bm[w], R1 - 1 - a);
+          }
+        __syncthreads();
+        const int clo = lo + s_clo, chi = lo + s_chi;
+        // each segment's slice with columns in [clo, chi] (binary searches in the sorted R row)
+        for (int t = threadIdx.x; t < n; t += THREADS) {
+          const int64_t bb = b0[t];
+          const int sd = cache.sid[t];
+          int a = 0, z = len0[t];  // first position with col >= clo
+          while (a < z) {
+            const int mid = (a + z) >> 1;
+            if (src.col(sd, bb + mid) < clo) a = mid + 1;
+            else z = mid;
+          }
+          int e = a, y = len0[t];  // first position with col > chi
+          while (e < y) {
+            const int mid = (e + y) >> 1;
+            if (src.col(sd, bb + mid) <= chi) e = mid + 1;
+            else y = mid;
+          }
+          cache.b[t] = bb + a;
+          cache.po[t] = e - a;
+        }
+        __syncthreads();
+        cache.template prefix<THREADS, Scan>(n, 0, scan_tmp);
+      }
+      for (int e = threadIdx.x; e < R1 - R0; e += THREADS) acc[e] = SR::zero();
+      __syncthreads();
+      balanced_items<SR, Src, NW>(src, cache, n, 0, [&](int32_t c, const V& v) {
+        if (SR::is_zero(v)) return;
+        const int cc = c - lo, w = cc >> 5;
+        atomic_accumulate<SR, true>(&acc[wrank[w] + __popc(bm[w] & ((1u << (cc & 31)) - 1u)) - R0], v);
+      });
+      __syncthreads();
+      if (o >= 0)
+        for (int e = threadIdx.x; e < R1 - R0; e += THREADS) out.vals[o + R0 + e] = acc[e];
+      __syncthreads();
+    }
 #pragma unroll
     for (int q = 0; q < LPT; ++q)
       if (k0 + q < nw) bm[list[k0 + q]] = 0u;

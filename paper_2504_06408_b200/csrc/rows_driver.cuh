@@ -287,10 +287,25 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
                          sizeof(uint16_t) * (kBitRankW + ((kBitRankN + 7) & ~7)) +
                          (size_t)kBitRankSegs * SegCache<SR, Src>::bytes_per_seg(1) + 64;
   const bool bitrank = bitrank_on && !AddCanCancel<SR>::value && br_smem <= 220 * 1024;
+  // rank-panel bin (bin 9): longer rows in the same window, accumulator panels in rank space
+  static const int rankpanel_on = [] {
+    const char* e = std::getenv("SPG_RANKPANEL");
+    return e ? std::atoi(e) : 1;
+  }();
+  constexpr int kRpN = 65536 / (int)sizeof(V), kRpSegs = 1024, kRpThreads = 1024;
+  const size_t rp_smem = sizeof(V) * kRpN + sizeof(uint32_t) * (kBitRankW + kBitRankW / 32) +
+                         sizeof(int) * kBitRankW + sizeof(uint16_t) * kBitRankW +
+                         (sizeof(int64_t) + sizeof(int)) * kRpSegs +
+                         (size_t)kRpSegs * SegCache<SR, Src>::bytes_per_seg(1) + 64;
+  const bool rankpanel = bitrank && rankpanel_on && rp_smem <= 220 * 1024;
+  static const int64_t rp_maxf = [] {  // rank-panel rows: F up to this many products
+    const char* e = std::getenv("SPG_RP_MAXF");
+    return e ? (int64_t)std::atoll(e) : (int64_t)16384;
+  }();
   DBuf<int32_t> colmin(c, bitrank ? (size_t)m : 1);
   analyse_rows_kernel<SR, Src><<<grid_for(c, m, 8), 256, 0, c->stream>>>(
-      src, ncols_out, dense_min, esc1k, bitrank ? kBitRankN : 0, kBitRankSegs, 32 * (int64_t)kBitRankW, colmin.p,
-      prods.p, ub.p, bins.p);
+      src, ncols_out, dense_min, esc1k, bitrank ? kBitRankN : 0, kBitRankSegs, 32 * (int64_t)kBitRankW,
+      rankpanel ? kRpSegs : 0, rp_maxf, colmin.p, prods.p, ub.p, bins.p);
   SPG_LAUNCH_CHECK();
   ++c->launches;
   SPG_CUDA(cudaMemsetAsync(ub.p + m, 0, sizeof(int64_t), c->stream));
@@ -491,6 +506,14 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
       SPG_LAUNCH_CHECK();
       ++c->launches;
     }
+    if (hcounts[kBinRankPanels] > 0) {
+      auto kern = rankpanel_rows_kernel<SR, Src, kRpThreads, kRpN, kBitRankW>;
+      set_smem(kern, rp_smem);
+      kern<<<resident_grid(c, kern, kRpThreads, rp_smem, (int64_t)hcounts[kBinRankPanels]), kRpThreads, rp_smem,
+             fk[0]>>>(src, lb + base[kBinRankPanels], (int64_t)hcounts[kBinRankPanels], kRpSegs, colmin.p, o);
+      SPG_LAUNCH_CHECK();
+      ++c->launches;
+    }
     if (hcounts[kBinWarpEsc] > 0) {
       esc_warp_kernel<SR, Src><<<grid_for(c, hcounts[kBinWarpEsc], 8), 256, 0, fk[2]>>>(
           src, lb + base[kBinWarpEsc], hcounts[kBinWarpEsc], o);
@@ -574,7 +597,7 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
     tm.mark(3);
     st->products = products;
     st->nnz_out = out->nnz;
-    for (int b = 0; b < 9; ++b) st->rows_per_bin[b] = b < kNumBins ? (int64_t)hcounts[b] : 0;
+    for (int b = 0; b < 10; ++b) st->rows_per_bin[b] = b < kNumBins ? (int64_t)hcounts[b] : 0;
     st->ms_numeric = ms_numeric;
     st->ms_compact = ms_compact;
     st->ms_total = tm.between(0, 3);
