@@ -231,3 +231,26 @@ def test_config5_er_maxtimes_struct_against_oracle(ctx, n, d):
     got = esc_multiply(a, a, ctx=ctx)
     want = ob.orc_multiply(to_mat(a), to_mat(a))
     assert_same(got, want, 5)
+
+
+@pytest.mark.parametrize("sr", [1, 2, 4])
+def test_bitrank_and_rank_panel_bins_against_oracle(ctx, sr):
+    """Rows sized for the bit-rank bin (2048 < F <= 8192) and the rank-panel
+    bin (8192 < F <= 16384, more outputs than one accumulator panel for
+    8-byte values) over a 200K-column output: bit-exact vs the oracle."""
+    rng = np.random.default_rng(7 + sr)
+    ncols, nb = 200_000, 64
+    lens = np.full(nb, 1000)
+    bptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    bcols = np.concatenate([np.sort(rng.choice(ncols, 1000, replace=False)) for _ in range(nb)]).astype(np.int64)
+    from golden.make_golden import exact_values
+    b = CsrMatrix(sr, nb, ncols, bptr, bcols, exact_values(sr, rng, bcols.size))
+    rows = [np.sort(rng.choice(nb, k, replace=False)) for k in (3, 6, 12, 15, 16)]
+    aptr = np.concatenate([[0], np.cumsum([len(x) for x in rows])]).astype(np.int64)
+    acols = np.concatenate(rows).astype(np.int64)
+    a = CsrMatrix(sr, len(rows), nb, aptr, acols, exact_values(sr, rng, acols.size))
+    st = {}
+    got = esc_multiply(a, b, ctx=ctx, stats=st)
+    assert_same(got, ob.orc_multiply(to_mat(a), to_mat(b)), sr)
+    bins = st["rows_per_bin"]
+    assert bins[8] + bins[9] >= 3, bins
