@@ -191,7 +191,7 @@ def test_merge_dense_panels_against_oracle(ctx, sr):
     nrows, ncols, K = 6, 200_000, 3
     parts = []
     for _ in range(K):
-        rs = [np.sort(rng.choice(ncols, int(rng.integers(2000, 5000)), replace=False)) for _ in range(nrows)]
+        rs = [np.sort(rng.choice(ncols, int(rng.integers(6000, 9000)), replace=False)) for _ in range(nrows)]
         ptr = np.concatenate([[0], np.cumsum([len(x) for x in rs])]).astype(np.int64)
         idx = np.concatenate(rs).astype(np.int64)
         parts.append(CsrMatrix(sr, nrows, ncols, ptr, idx, exact_values(sr, rng, idx.size)))
