@@ -790,7 +790,7 @@ constexpr bool kSegmentMode = SPG_SEG_MODE != 0;
 #define SPG_SEG_MIN_AVG 48
 #endif
 constexpr int kSegmentMinAvg = SPG_SEG_MIN_AVG;
-template <class SR, class Src, int NW, int IPL = 2, class F>
+template <class SR, class Src, int NW, int IPL = 2, bool kColsOnly = false, class F>
 __device__ __forceinline__ void balanced_items(const Src& src, const SegCache<SR, Src>& c, int n, int p, F&& f) {
   using V = typename SR::value_type;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -887,12 +887,15 @@ __device__ __forceinline__ void balanced_items(const Src& src, const SegCache<SR
         if (q < total) {
           const int64_t w = bu + (q - eu);
           cc[u] = src.col(su, w);
-          xx[u] = src.val(su, w);
+          if constexpr (!kColsOnly) xx[u] = src.val(su, w);
         }
       }
 #pragma unroll
       for (int u = 0; u < IPL; ++u)
-        if (q0 + 32 * u + lane < total) f(cc[u], src.item(mm[u], xx[u]));
+        if (q0 + 32 * u + lane < total) {
+          if constexpr (kColsOnly) f(cc[u], mm[u]);  // value not loaded
+          else f(cc[u], src.item(mm[u], xx[u]));
+        }
     }
   }
 }
@@ -1353,10 +1356,6 @@ __global__ void __launch_bounds__(THREADS) bitrank_rows_kernel(Src src, const in
         first += __popc(bm[w]);
       }
     for (int e = threadIdx.x; e < total; e += THREADS) acc[e] = SR::zero();
-    if (threadIdx.x == 0) {
-      s_base = out.claim_row(i, total);
-      out.rownnz[i] = total;
-    }
     __syncthreads();
     // pass 2: fold into acc[rank]
     balanced_items<SR, Src, NW>(src, cache, n, 0, [&](int32_t c, const V& v) {
@@ -1364,6 +1363,11 @@ __global__ void __launch_bounds__(THREADS) bitrank_rows_kernel(Src src, const in
       const int cc = c - lo, w = cc >> 5;
       atomic_accumulate<SR, true>(&acc[wrank[w] + __popc(bm[w] & ((1u << (cc & 31)) - 1u))], v);
     });
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_base = out.claim_row(i, total);
+      out.rownnz[i] = total;
+    }
     __syncthreads();
     // emit: columns expanded from the listed words, values straight from acc
     const int64_t o = s_base;

@@ -254,3 +254,26 @@ def test_bitrank_and_rank_panel_bins_against_oracle(ctx, sr):
     assert_same(got, ob.orc_multiply(to_mat(a), to_mat(b)), sr)
     bins = st["rows_per_bin"]
     assert bins[8] + bins[9] >= 3, bins
+
+
+def test_bitrank_drops_columns_whose_products_are_all_zero(ctx):
+    """Tropical (min, saturating +): products that saturate to INT32_MAX are
+    the semiring zero and must vanish from C (local_spgemm.hpp:57-58) — the
+    bit-rank bin marks presence from columns alone and must redo such rows."""
+    rng = np.random.default_rng(11)
+    ncols, nb = 100_000, 8
+    bptr = np.arange(0, 1000 * nb + 1, 1000, dtype=np.int64)
+    bcols = np.concatenate([np.sort(rng.choice(ncols, 1000, replace=False)) for _ in range(nb)]).astype(np.int64)
+    big = (1 << 30) + 5
+    bvals = rng.integers(1, 100, bcols.size).astype(np.int32)
+    bvals[: 2000] = big                      # B rows 0-1: saturate against a big A entry
+    b = CsrMatrix(4, nb, ncols, bptr, bcols, bvals)
+    acols = np.arange(nb, dtype=np.int64)
+    avals = np.full(nb, 3, dtype=np.int32)
+    avals[:2] = big                          # row 0 x B rows 0-1: all products saturate
+    a = CsrMatrix(4, 1, nb, np.array([0, nb], dtype=np.int64), acols, avals)
+    st = {}
+    got = esc_multiply(a, b, ctx=ctx, stats=st)
+    want = ob.orc_multiply(to_mat(a), to_mat(b))
+    assert_same(got, want, 4)
+    assert st["rows_per_bin"][8] == 1
