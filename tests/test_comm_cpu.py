@@ -50,7 +50,7 @@ def _worker(rank, world, pr, pc, job, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,pr,pc", [(2, 1, 2), (4, 2, 2)])
+@pytest.mark.parametrize("world,pr,pc", [(2, 1, 2), (4, 2, 2), (8, 2, 4)])
 def test_fabric_multiprocess(world, pr, pc):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

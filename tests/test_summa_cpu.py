@@ -1,5 +1,5 @@
 """CPU (no GPU): the SUMMA data flow of summa25_multiply across real
-processes (gloo, world size 2 and 4) — block distribution (local_block /
+processes (gloo, world size 2, 4 and 8) — block distribution (local_block /
 block_range, dist_matrix.hpp:23-111), the stage schedule (spg_summa_schedule:
 the reference's q stages on square grids, the common refinement on
 rectangular ones, summa.hpp:248-330), panel slicing at a_off / b_off, the
@@ -90,7 +90,7 @@ def _worker(rank, world, pr, pc, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,pr,pc", [(2, 1, 2), (2, 2, 1), (4, 2, 2)])
+@pytest.mark.parametrize("world,pr,pc", [(2, 1, 2), (2, 2, 1), (4, 2, 2), (8, 2, 4)])
 def test_summa_dataflow_multiprocess(world, pr, pc):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
