@@ -194,7 +194,7 @@ def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    a = make_input(args.scale, args.ef, args.seed)
+    a = make_input(args.scale, args.ef, args.seed, permute=args.permute)  # same relabelled A as our arm
     times = []
     res = None
     for i in range(args.warmup + args.steps):
@@ -207,8 +207,8 @@ def run_reference_arm(args):
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "Gflop/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.median(times)) * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
-            "data": "synthetic", "config": {"workload": f"rmat{args.scale}_ef{int(args.ef)}_tropical_i32_AxA",
-                                            "sample": res["sample"]},
+            "data": "synthetic", "config": {"workload": f"rmat{args.scale}_ef{int(args.ef)}_tropical_i32_AxA (BASELINE config 2)",
+                                            "permuted": bool(args.permute), "sample": res["sample"]},
             "cpu_baseline": {"value": val, "unit": "Gflop/s", "cores": res["cores"], "kind": res["kind"],
                              "sample": res["sample"]},
             "e2e": {"value": val, "unit": "Gflop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
