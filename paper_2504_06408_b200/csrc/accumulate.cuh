@@ -1068,6 +1068,10 @@ __device__ __forceinline__ int bitmap_emit(typename SR::value_type* acc, uint32_
 #define SPG_DENSE_IPL 2
 #endif
 constexpr int kDenseIPL = SPG_DENSE_IPL;  // items per lane in flight in the dense product loop
+#ifndef SPG_PREALL
+#define SPG_PREALL 1
+#endif
+constexpr bool kPreAll = SPG_PREALL != 0;
 template <class SR, class Src, int W, int THREADS, int MINB = 1>
 __global__ void __launch_bounds__(THREADS, MINB) dense_panel_kernel(Src src, const int64_t* __restrict__ rows,
                                                               int64_t nrows_bin, int npanels, int cap,
@@ -1081,6 +1085,10 @@ __global__ void __launch_bounds__(THREADS, MINB) dense_panel_kernel(Src src, con
   uint32_t* bm = reinterpret_cast<uint32_t*>(smem_raw + sizeof(V) * W);
   SegCache<SR, Src> cache;
   cache.carve(smem_raw + sizeof(V) * W + sizeof(uint32_t) * (W / 32), cap, npanels);
+  // kPreAll: every panel's segment prefix is computed once per row (one warp
+  // per panel) instead of a block scan + barrier per panel
+  int* pre_all = kPreAll ? cache.pre + ((cap + 1 + 3) & ~3) : nullptr;  // [npanels][cap + 1]
+  int* const pre0 = cache.pre;
   __shared__ typename Count::TempStorage scan_tmp;
   __shared__ long long s_row, s_base;
   __shared__ int wsum[2 * NW + 1];
@@ -1103,6 +1111,26 @@ __global__ void __launch_bounds__(THREADS, MINB) dense_panel_kernel(Src src, con
     if (single) {
       cache.load(src, i, sb, (int)nseg, threadIdx.x, THREADS);
       __syncthreads();
+      if constexpr (kPreAll) {
+        const int lane = threadIdx.x & 31, n = (int)nseg;
+        for (int p = threadIdx.x >> 5; p < npanels; p += NW) {
+          int* pp = pre_all + (size_t)p * (cap + 1);
+          int run = 0;
+          for (int t0 = 0; t0 < n; t0 += 32) {
+            const int ln = t0 + lane < n ? cache.len(t0 + lane, p) : 0;
+            int incl = ln;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+              const int x = __shfl_up_sync(kFull, incl, d);
+              if (lane >= d) incl += x;
+            }
+            if (t0 + lane < n) pp[t0 + lane] = run + incl - ln;
+            run += __shfl_sync(kFull, incl, 31);
+          }
+          if (lane == 0) pp[n] = run;
+        }
+        __syncthreads();
+      }
     }
     int64_t written = 0;
     if (threadIdx.x == 0 && out.bump) out.rowstart[i] = -2;  // chunked: see out.chunks
@@ -1114,7 +1142,12 @@ __global__ void __launch_bounds__(THREADS, MINB) dense_panel_kernel(Src src, con
           cache.load(src, i, sb + c0, n, threadIdx.x, THREADS);
           __syncthreads();
         }
-        cache.template prefix<THREADS, Count>(n, p, scan_tmp);
+        if (kPreAll && single) {
+          cache.pre = pre_all + (size_t)p * (cap + 1);
+        } else {
+          cache.pre = pre0;
+          cache.template prefix<THREADS, Count>(n, p, scan_tmp);
+        }
 #ifdef SPG_ABL_NO_ATOMIC  // ablation build: loads and products only
         balanced_items<SR, Src, NW, kDenseIPL>(src, cache, n, p, [&](int32_t c, const V& v) {
           if (bits_equal(v, SR::one()) && c == -7) acc[0] = v;

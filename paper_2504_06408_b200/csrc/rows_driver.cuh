@@ -123,8 +123,8 @@ void launch_dense_cfg(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t*
                       size_t smem_budget, unsigned long long* work, const RowOut<typename SR::value_type>& out) {
   using V = typename SR::value_type;
   const int np = (int)((ncols + W - 1) / W);
-  const size_t per_seg = SegCache<SR, Src>::bytes_per_seg(np);
-  const size_t fixed = sizeof(V) * W + sizeof(uint32_t) * (W / 32);
+  const size_t per_seg = SegCache<SR, Src>::bytes_per_seg(np) + (kPreAll ? sizeof(int) * np : 0);
+  const size_t fixed = sizeof(V) * W + sizeof(uint32_t) * (W / 32) + (kPreAll ? sizeof(int) * (np + 4) : 0);
   const size_t room = smem_budget > fixed + 64 ? smem_budget - fixed - 64 : 0;
   const int cap = (int)std::min<size_t>(8192, room / per_seg) & ~3;  // keeps 16-byte values aligned
   if (cap < 32) fail(SPG_ERR_INTERNAL, "dense panel: no room for the segment cache");
@@ -297,7 +297,7 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
                          sizeof(int) * kBitRankW + sizeof(uint16_t) * kBitRankW +
                          (sizeof(int64_t) + sizeof(int)) * kRpSegs +
                          (size_t)kRpSegs * SegCache<SR, Src>::bytes_per_seg(1) + 64;
-  const bool rankpanel = bitrank && rankpanel_on && rp_smem <= 220 * 1024;
+  const bool rankpanel = bitrank && rankpanel_on && rp_smem <= 220 * 1024 && sizeof(V) == 4;  // measured gain: 4-byte values
   static const int64_t rp_maxf = [] {  // rank-panel rows: F up to this many products
     const char* e = std::getenv("SPG_RP_MAXF");
     return e ? (int64_t)std::atoll(e) : (int64_t)16384;
