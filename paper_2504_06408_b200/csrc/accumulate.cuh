@@ -1076,7 +1076,7 @@ template <class SR, class Src, int W, int THREADS, int MINB = 1>
 __global__ void __launch_bounds__(THREADS, MINB) dense_panel_kernel(Src src, const int64_t* __restrict__ rows,
                                                               int64_t nrows_bin, int npanels, int cap,
                                                               unsigned long long* __restrict__ work,
-                                                              RowOut<typename SR::value_type> out) {
+                                                              RowOut<typename SR::value_type> out, bool preall) {
   using V = typename SR::value_type;
   constexpr int NW = THREADS / 32;
   using Count = cub::BlockScan<int, THREADS>;
@@ -1087,7 +1087,7 @@ __global__ void __launch_bounds__(THREADS, MINB) dense_panel_kernel(Src src, con
   cache.carve(smem_raw + sizeof(V) * W + sizeof(uint32_t) * (W / 32), cap, npanels);
   // kPreAll: every panel's segment prefix is computed once per row (one warp
   // per panel) instead of a block scan + barrier per panel
-  int* pre_all = kPreAll ? cache.pre + ((cap + 1 + 3) & ~3) : nullptr;  // [npanels][cap + 1]
+  int* pre_all = preall ? cache.pre + ((cap + 1 + 3) & ~3) : nullptr;  // [npanels][cap + 1]
   int* const pre0 = cache.pre;
   __shared__ typename Count::TempStorage scan_tmp;
   __shared__ long long s_row, s_base;
@@ -1111,7 +1111,7 @@ __global__ void __launch_bounds__(THREADS, MINB) dense_panel_kernel(Src src, con
     if (single) {
       cache.load(src, i, sb, (int)nseg, threadIdx.x, THREADS);
       __syncthreads();
-      if constexpr (kPreAll) {
+      if (preall) {
         const int lane = threadIdx.x & 31, n = (int)nseg;
         for (int p = threadIdx.x >> 5; p < npanels; p += NW) {
           int* pp = pre_all + (size_t)p * (cap + 1);
@@ -1142,7 +1142,7 @@ __global__ void __launch_bounds__(THREADS, MINB) dense_panel_kernel(Src src, con
           cache.load(src, i, sb + c0, n, threadIdx.x, THREADS);
           __syncthreads();
         }
-        if (kPreAll && single) {
+        if (preall && single) {
           cache.pre = pre_all + (size_t)p * (cap + 1);
         } else {
           cache.pre = pre0;

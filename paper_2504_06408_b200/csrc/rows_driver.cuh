@@ -123,15 +123,16 @@ void launch_dense_cfg(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t*
                       size_t smem_budget, unsigned long long* work, const RowOut<typename SR::value_type>& out) {
   using V = typename SR::value_type;
   const int np = (int)((ncols + W - 1) / W);
-  const size_t per_seg = SegCache<SR, Src>::bytes_per_seg(np) + (kPreAll ? sizeof(int) * np : 0);
-  const size_t fixed = sizeof(V) * W + sizeof(uint32_t) * (W / 32) + (kPreAll ? sizeof(int) * (np + 4) : 0);
+  const bool preall = kPreAll && np <= 32;  // per-row prefixes of every panel (small panel counts)
+  const size_t per_seg = SegCache<SR, Src>::bytes_per_seg(np) + (preall ? sizeof(int) * np : 0);
+  const size_t fixed = sizeof(V) * W + sizeof(uint32_t) * (W / 32) + (preall ? sizeof(int) * (np + 4) : 0);
   const size_t room = smem_budget > fixed + 64 ? smem_budget - fixed - 64 : 0;
   const int cap = (int)std::min<size_t>(8192, room / per_seg) & ~3;  // keeps 16-byte values aligned
   if (cap < 32) fail(SPG_ERR_INTERNAL, "dense panel: no room for the segment cache");
   const size_t smem = fixed + (size_t)cap * per_seg + 64;
   auto kern = dense_panel_kernel<SR, Src, W, DT, MINB>;
   set_smem(kern, smem);
-  kern<<<resident_grid(c, kern, DT, smem, n), DT, smem, s>>>(src, rows, n, np, cap, work, out);
+  kern<<<resident_grid(c, kern, DT, smem, n), DT, smem, s>>>(src, rows, n, np, cap, work, out, preall);
   SPG_LAUNCH_CHECK();
   ++c->launches;
 }
