@@ -51,3 +51,20 @@ def test_summa_rectangular_grids(grid):
     for fuse in (1, 0):
         out = run_worker(pr * pc, "--sr", 4, "--scale", 10, "--grid", grid, "--fuse", fuse, "--mode", 2)
         assert "blocks_ok=True checksum_ok=True" in out
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(os.environ.get("SPG_FULLSIZE") != "1", reason="full-size BASELINE configs: set SPG_FULLSIZE=1")
+@pytest.mark.parametrize("config", [2, 4, 5, 3])
+def test_fullsize_config_against_streaming_oracle(config):
+    """BASELINE configs at full size on all GPUs vs the oracle's streaming
+    checksum of the full C (tests/fullsize_worker.py)."""
+    n = ngpus()
+    nproc = 8 if n >= 8 else 4 if n >= 4 else 2 if n >= 2 else 1
+    if config in (3, 5) and nproc < 4:
+        pytest.skip("needs 4 GPUs (C does not fit fewer)")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nproc-per-node", str(nproc),
+           os.path.join(ROOT, "tests", "fullsize_worker.py"), "--config", str(config)]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=3000, cwd=ROOT,
+                       env=dict(os.environ, MASTER_ADDR="127.0.0.1"))
+    assert p.returncode == 0 and '"match": true' in p.stdout, p.stdout[-3000:] + p.stderr[-3000:]
