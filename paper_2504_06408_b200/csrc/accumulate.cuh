@@ -790,7 +790,10 @@ constexpr bool kSegmentMode = SPG_SEG_MODE != 0;
 #define SPG_SEG_MIN_AVG 48
 #endif
 constexpr int kSegmentMinAvg = SPG_SEG_MIN_AVG;
-template <class SR, class Src, int NW, int IPL = 2, bool kColsOnly = false, class F>
+// kNarrowSearch: bound each batch's shuffle search to the segments [f, l]
+// it touches (measured: a gain for the long segments of dense rows, a loss
+// for short ones — used by the dense kernel only).
+template <class SR, class Src, int NW, int IPL = 2, bool kColsOnly = false, bool kNarrowSearch = false, class F>
 __device__ __forceinline__ void balanced_items(const Src& src, const SegCache<SR, Src>& c, int n, int p, F&& f) {
   using V = typename SR::value_type;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -864,14 +867,35 @@ __device__ __forceinline__ void balanced_items(const Src& src, const SegCache<SR
     const int excl = incl - L;
     for (int q0 = 0; q0 < total; q0 += 32 * IPL) {
       int pos[IPL];
+      if constexpr (kNarrowSearch) {
+        // the batch's items lie in segments [f, l]: search only that range
+        // (one segment: no shuffle at all; two: one step)
+        const int qlast = min(q0 + 32 * IPL - 1, total - 1);
+        const int f = __popc(__ballot_sync(kFull, incl <= q0));
+        const int l = __popc(__ballot_sync(kFull, incl <= qlast));
 #pragma unroll
-      for (int u = 0; u < IPL; ++u) pos[u] = 0;
+        for (int u = 0; u < IPL; ++u) pos[u] = f;
+        const int span = l - f;
+        if (span > 0) {
+          for (int step = 1 << (31 - __clz(span)); step >= 1; step >>= 1) {
 #pragma unroll
-      for (int step = 16; step >= 1; step >>= 1) {
+            for (int u = 0; u < IPL; ++u) {
+              const int at = pos[u] + step - 1;
+              const int v = __shfl_sync(kFull, incl, at < 31 ? at : 31);
+              if (at < l && v <= q0 + 32 * u + lane) pos[u] += step;
+            }
+          }
+        }
+      } else {
 #pragma unroll
-        for (int u = 0; u < IPL; ++u) {
-          const int v = __shfl_sync(kFull, incl, pos[u] + step - 1);
-          if (v <= q0 + 32 * u + lane) pos[u] += step;
+        for (int u = 0; u < IPL; ++u) pos[u] = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+#pragma unroll
+          for (int u = 0; u < IPL; ++u) {
+            const int v = __shfl_sync(kFull, incl, pos[u] + step - 1);
+            if (v <= q0 + 32 * u + lane) pos[u] += step;
+          }
         }
       }
       int32_t cc[IPL];
@@ -1153,7 +1177,7 @@ __global__ void __launch_bounds__(THREADS, MINB) dense_panel_kernel(Src src, con
           if (bits_equal(v, SR::one()) && c == -7) acc[0] = v;
         });
 #else
-        balanced_items<SR, Src, NW, kDenseIPL>(src, cache, n, p, [&](int32_t c, const V& v) {
+        balanced_items<SR, Src, NW, kDenseIPL, false, true>(src, cache, n, p, [&](int32_t c, const V& v) {
           if (SR::is_zero(v)) return;  // add(x, zero) == x: nothing to fold
           const int cc = c - lo;
           const V old = atomic_accumulate<SR, true>(&acc[cc], v);
