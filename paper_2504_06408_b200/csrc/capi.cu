@@ -3,12 +3,14 @@
 // points and the host-array drop-ins.  Every function converts C++
 // exceptions into an SPG_ERR_* status + last-error message.
 #include <algorithm>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "comm.h"
@@ -171,10 +173,61 @@ void host_release(void* p) {
   if (!pinned().put(p)) std::free(p);
 }
 
-__global__ void widen_into_kernel(const int32_t* __restrict__ in, int64_t* __restrict__ out, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = in[i];
-}
+
+
+// Persistent host worker pool: parallel_for(n, fn) runs fn(lo, hi) over n
+// items split across the workers and the caller, and returns when all are done.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool* p = new HostPool();  // intentionally leaked (process lifetime)
+    return *p;
+  }
+  void parallel_for(int64_t n, const std::function<void(int64_t, int64_t)>& fn) {
+    const int parts = (int)workers_.size() + 1;
+    std::unique_lock<std::mutex> lk(mu_);
+    job_ = &fn;
+    n_ = n;
+    parts_ = parts;
+    pending_ = parts - 1;
+    ++gen_;
+    cv_.notify_all();
+    lk.unlock();
+    fn(0, n / parts);  // the caller takes part 0
+    lk.lock();
+    done_.wait(lk, [&] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  HostPool() {
+    const int t = (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency())) - 1;
+    for (int k = 0; k < t; ++k) workers_.emplace_back([this, k] { run(k + 1); });
+    for (auto& w : workers_) w.detach();
+  }
+  void run(int part) {
+    uint64_t seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait(lk, [&] { return gen_ != seen; });
+      seen = gen_;
+      const auto* fn = job_;
+      const int64_t n = n_;
+      const int parts = parts_;
+      lk.unlock();
+      (*fn)(n * part / parts, n * (part + 1) / parts);
+      lk.lock();
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int64_t, int64_t)>* job_ = nullptr;
+  int64_t n_ = 0;
+  int parts_ = 1, pending_ = 0;
+  uint64_t gen_ = 0;
+};
 
 void download(spg_ctx* c, int vs, const spg_dcsr* d, int is_csc, spg_hcsr* h) {
   const int64_t nseg = is_csc ? d->ncols : d->nrows;
@@ -186,19 +239,60 @@ void download(spg_ctx* c, int vs, const spg_dcsr* d, int is_csc, spg_hcsr* h) {
   h->vals = pinned().get((size_t)vs * std::max<int64_t>(d->nnz, 1));
   SPG_CUDA(cudaMemcpyAsync(h->ptr, d->ptr, sizeof(int64_t) * (nseg + 1), cudaMemcpyDeviceToHost, c->stream));
   if (d->nnz > 0) {
-    // values first (overlaps the widening kernel), then indices widened to
-    // the reference's int64 on device in chunks
-    SPG_CUDA(cudaMemcpyAsync(h->vals, d->vals, (size_t)vs * d->nnz, cudaMemcpyDeviceToHost, c->stream));
-    const int64_t chunk = int64_t(1) << 28;
-    DBuf<int64_t> wide(c, (size_t)std::min<int64_t>(chunk, d->nnz));
-    for (int64_t o = 0; o < d->nnz; o += chunk) {
-      const int64_t n = std::min<int64_t>(chunk, d->nnz - o);
-      widen_into_kernel<<<std::min<int64_t>((n + 255) / 256, (int64_t)c->sm_count * 16), 256, 0, c->stream>>>(
-          d->idx + o, wide.p, n);
-      SPG_LAUNCH_CHECK();
-      ++c->launches;
-      SPG_CUDA(cudaMemcpyAsync(h->idx + o, wide.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, c->stream));
+    // int32 indices cross PCIe in chunks through two pinned staging buffers
+    // and are widened to the reference's int64 by host threads while the
+    // next chunk (and finally the values) is in flight: 4 + V bytes per
+    // entry on the bus instead of 8 + V
+    const int64_t chunk = std::min<int64_t>(int64_t(1) << 25, d->nnz);
+    int32_t* stage[2] = {static_cast<int32_t*>(pinned().get(sizeof(int32_t) * chunk)),
+                         static_cast<int32_t*>(pinned().get(sizeof(int32_t) * chunk))};
+    cudaEvent_t ev[2];
+    for (auto& e : ev) SPG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    auto widen = [&](int k) {
+      const int64_t o = (int64_t)k * chunk, n = std::min<int64_t>(chunk, d->nnz - o);
+      {
+        HostTrace ht("download: wait chunk", (size_t)k);
+        SPG_CUDA(cudaEventSynchronize(ev[k & 1]));
+      }
+      const int32_t* in = stage[k & 1];
+      int64_t* out = h->idx + o;
+      HostTrace ht("download: widen chunk", (size_t)k);
+      HostPool::get().parallel_for(n, [&](int64_t lo, int64_t hi) {
+        for (int64_t e = lo; e < hi; ++e) out[e] = in[e];
+      });
+    };
+    const int nch = (int)((d->nnz + chunk - 1) / chunk);
+    // values on a side stream, concurrently with the index pipeline
+    cudaStream_t side = nullptr;
+    cudaEvent_t ready = nullptr;
+    SPG_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    SPG_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    SPG_CUDA(cudaEventRecord(ready, c->stream));
+    SPG_CUDA(cudaStreamWaitEvent(side, ready, 0));
+    SPG_CUDA(cudaMemcpyAsync(h->vals, d->vals, (size_t)vs * d->nnz, cudaMemcpyDeviceToHost, side));
+    try {
+      for (int k = 0; k < nch; ++k) {
+        const int64_t o = (int64_t)k * chunk, n = std::min<int64_t>(chunk, d->nnz - o);
+        SPG_CUDA(cudaMemcpyAsync(stage[k & 1], d->idx + o, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
+        SPG_CUDA(cudaEventRecord(ev[k & 1], c->stream));
+        if (k > 0) widen(k - 1);
+      }
+      widen(nch - 1);
+      SPG_CUDA(cudaStreamSynchronize(side));
+    } catch (...) {
+      cudaStreamSynchronize(side);
+      cudaStreamDestroy(side);
+      cudaEventDestroy(ready);
+      for (auto& e : ev) cudaEventDestroy(e);
+      host_release(stage[0]);
+      host_release(stage[1]);
+      throw;
     }
+    cudaStreamDestroy(side);
+    cudaEventDestroy(ready);
+    for (auto& e : ev) cudaEventDestroy(e);
+    host_release(stage[0]);
+    host_release(stage[1]);
   }
   HostTrace ht("download sync", (size_t)d->nnz);
   SPG_CUDA(cudaStreamSynchronize(c->stream));
