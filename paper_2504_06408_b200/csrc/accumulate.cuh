@@ -278,7 +278,7 @@ __device__ __forceinline__ void warp_items(const Src& src, int64_t i, int64_t s0
 // K1: per-row analysis and binning policy
 // ---------------------------------------------------------------------------
 template <class SR, class Src>
-__global__ void __launch_bounds__(256) analyse_rows_kernel(Src src, int64_t ncols_out, int64_t dense_min, int esc1k,
+__global__ void __launch_bounds__(256) analyse_rows_kernel(Src src, int64_t ncols_out, int64_t dense_min,
                                                            int64_t bitrank_max, int64_t bitrank_segs,
                                                            int64_t bitrank_span, int64_t rankpanel_segs,
                                                            int64_t rankpanel_maxf,
@@ -329,13 +329,12 @@ __global__ void __launch_bounds__(256) analyse_rows_kernel(Src src, int64_t ncol
       if (f == 0) b = kBinEmpty;
       else if (f <= 32) b = kBinWarpEsc;
       else if (f <= 512 && nseg <= 512) b = kBinEsc512;
-      else if (esc1k && f <= 1024 && nseg <= 1024) b = kBinHash2K;  // bin 5 = block-ESC 1K in this mode
       else if (bitrank_max > 0 && f <= bitrank_max && nseg <= bitrank_segs && span <= bitrank_span) b = kBinBitRank;
       else if (rankpanel_segs > 0 && f > bitrank_max && f <= rankpanel_maxf && nseg <= rankpanel_segs &&
                span <= bitrank_span)
         b = kBinRankPanels;
       else if (f > dense_min && dense_ok) b = kBinDense;
-      else if (!esc1k && u <= 1024) b = kBinHash2K;
+      else if (u <= 1024) b = kBinHash2K;
       else if (u <= 2048) b = kBinHash4K;
       else if (u <= 4096) b = kBinHash8K;
       else if (u <= Geom<V>::kMaxT / 2) b = kBinHashMax;
@@ -780,16 +779,6 @@ __device__ __forceinline__ int nth_set_bit(uint32_t x, int k) {
 
 // Warp `wid` of NW enumerates its equal share of the cached segments' items
 // (panel p); f(col, value) per item, two items per lane in flight.
-// SPG_SEG_MODE (compile time, default off: measured no gain on R-MAT): when the warp's share averages
-// >= kSegmentMinAvg items per segment, walk segments whole-warp instead.
-#ifndef SPG_SEG_MODE
-#define SPG_SEG_MODE 0
-#endif
-constexpr bool kSegmentMode = SPG_SEG_MODE != 0;
-#ifndef SPG_SEG_MIN_AVG
-#define SPG_SEG_MIN_AVG 48
-#endif
-constexpr int kSegmentMinAvg = SPG_SEG_MIN_AVG;
 // kNarrowSearch: bound each batch's shuffle search to the segments [f, l]
 // it touches (measured: a gain for the long segments of dense rows, a loss
 // for short ones — used by the dense kernel only).
@@ -805,43 +794,6 @@ __device__ __forceinline__ void balanced_items(const Src& src, const SegCache<SR
     const int mid = (s + hs) >> 1;
     if (c.pre[mid] <= lo_q) s = mid;
     else hs = mid;
-  }
-  if constexpr (kSegmentMode) {
-    // Long slices: the whole warp walks one segment at a time (no per-item
-    // segment search), four items per lane in flight.
-    int e = s, he = n;  // largest e with pre[e] < hi_q
-    while (he - e > 1) {
-      const int mid = (e + he) >> 1;
-      if (c.pre[mid] < hi_q) e = mid;
-      else he = mid;
-    }
-    if ((hi_q - lo_q) >= kSegmentMinAvg * (e - s + 1)) {
-      for (int t = s; t <= e; ++t) {
-        int64_t bb;
-        int ln, sd;
-        V m;
-        c.get(t, p, bb, ln, sd, m);
-        const int st = c.pre[t];
-        const int beg = st > lo_q ? st : lo_q;
-        const int end = (st + ln) < hi_q ? (st + ln) : hi_q;
-        const int L = end - beg;
-        bb += beg - st;
-        for (int q = lane; q < L; q += 128) {
-          int32_t cc[4];
-          V xx[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (q + 32 * u < L) {
-              cc[u] = src.col(sd, bb + q + 32 * u);
-              xx[u] = src.val(sd, bb + q + 32 * u);
-            }
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (q + 32 * u < L) f(cc[u], src.item(m, xx[u]));
-        }
-      }
-      return;
-    }
   }
   for (int s0 = s; s0 < n && c.pre[s0] < hi_q; s0 += 32) {
     const int t = s0 + lane;
@@ -942,10 +894,6 @@ struct AddCanCancel {
   static constexpr bool value = SR::id == 0;  // arithmetic (+, x): a + (-a) == 0
 };
 
-#ifndef SPG_LANE_EMIT
-#define SPG_LANE_EMIT 0
-#endif
-constexpr bool kLaneEmit = SPG_LANE_EMIT != 0;  // lane-sequential emit instead of the flattened one
 // Barrier over a warp group: BAR == 0 is __syncthreads, else named barrier
 // BAR over NT threads (warp-specialised kernels).
 template <int BAR, int NT>
@@ -1031,22 +979,6 @@ __device__ __forceinline__ int bitmap_emit(typename SR::value_type* acc, uint32_
     }
     const int total = __shfl_sync(kFull, incl, 31);
     const int excl = incl - c;
-    if constexpr (kLaneEmit) {
-      // each lane writes its own word's entries (no per-entry search)
-      int k = excl;
-      for (uint32_t y = x; y; y &= y - 1) {
-        const int cc = (w << 5) + __ffs(y) - 1;
-        if (store) {
-          out.cols[pos + k] = col_base + cc;
-          out.vals[pos + k] = acc[cc];
-        }
-        acc[cc] = SR::zero();
-        ++k;
-      }
-      if (x) bm[w] = 0u;
-      pos += total;
-      continue;
-    }
     for (int q0 = 0; q0 < total; q0 += 32) {
       const int q = q0 + lane;
       int own = 0;

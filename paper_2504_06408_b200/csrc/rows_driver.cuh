@@ -169,7 +169,7 @@ inline int dense_cfg() {
 template <class V>
 inline int dense_panel_width() {
   const int cfg = dense_cfg();
-  return Geom<V>::kPanelW >> (cfg == 1 || cfg >= 3 ? 1 : cfg == 2 ? 2 : 0);
+  return Geom<V>::kPanelW >> (cfg == 1 || cfg == 7 ? 1 : 0);
 }
 
 template <class SR, class Src>
@@ -178,32 +178,13 @@ void launch_dense(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* row
   using V = typename SR::value_type;
   constexpr int PW = Geom<V>::kPanelW;
   switch (dense_cfg()) {
-    case 1:
+    case 1:  // default: 64 KB panel, 512 threads, 2 CTAs/SM
       launch_dense_cfg<PW / 2, 512, SR, Src, 2>(c, s, src, rows, n, ncols, 110 * 1024, work, out);
       break;
-    case 2:
-      launch_dense_cfg<PW / 4, 512, SR, Src>(c, s, src, rows, n, ncols, 72 * 1024, work, out);
-      break;
-    case 3:
-      launch_dense_cfg<PW / 2, 256, SR, Src>(c, s, src, rows, n, ncols, 74 * 1024, work, out);
-      break;
-    case 4:
-      launch_dense_cfg<PW / 2, 256, SR, Src>(c, s, src, rows, n, ncols, 110 * 1024, work, out);
-      break;
-    case 5:
-      launch_dense_cfg<PW / 2, 128, SR, Src>(c, s, src, rows, n, ncols, 110 * 1024, work, out);
-      break;
-    case 7:  // warp-specialised: 24 product + 8 emit warps, double-buffered 64 KB panels
+    case 7:  // warp-specialised: 24 product + 8 emit warps, double-buffered 64 KB panels (measured slower)
       launch_dense_ws<PW / 2, 24, 8, SR, Src>(c, s, src, rows, n, ncols, 220 * 1024, work, out);
       break;
-    case 8:
-      launch_dense_ws<PW / 2, 28, 4, SR, Src>(c, s, src, rows, n, ncols, 220 * 1024, work, out);
-      break;
-    case 6:  // 3 CTAs/SM: register cap 42, small segment cache
-      launch_dense_cfg<PW / 2, 512, SR, Src, 3>(c, s, src, rows, n, ncols, 74 * 1024, work, out);
-      break;
-
-    default:
+    default:  // 0: 128 KB panel, 1024 threads, 1 CTA/SM
       launch_dense_cfg<PW, 1024, SR, Src>(c, s, src, rows, n, ncols, 220 * 1024, work, out);
   }
 }
@@ -273,10 +254,6 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
     const char* e = std::getenv("SPG_DENSE_MIN");
     return e ? (int64_t)std::atoll(e) : kDenseMinRow;
   }();
-  static const int esc1k = [] {  // SPG_ESC1K=1: rows with F <= 1024 are sorted (block-ESC) instead of hashed
-    const char* e = std::getenv("SPG_ESC1K");
-    return e ? std::atoi(e) : 0;
-  }();
   // bit-rank bin (bin 8): rows with 512 < F <= kBitRankN whose output columns fit a window of 32*kBitRankW
   static const int bitrank_on = [] {
     const char* e = std::getenv("SPG_BITRANK");
@@ -305,7 +282,7 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
   }();
   DBuf<int32_t> colmin(c, bitrank ? (size_t)m : 1);
   analyse_rows_kernel<SR, Src><<<grid_for(c, m, 8), 256, 0, c->stream>>>(
-      src, ncols_out, dense_min, esc1k, bitrank ? kBitRankN : 0, kBitRankSegs, 32 * (int64_t)kBitRankW,
+      src, ncols_out, dense_min, bitrank ? kBitRankN : 0, kBitRankSegs, 32 * (int64_t)kBitRankW,
       rankpanel ? kRpSegs : 0, rp_maxf, colmin.p, prods.p, ub.p, bins.p);
   SPG_LAUNCH_CHECK();
   ++c->launches;
@@ -491,12 +468,8 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
       launch_hash<SR, Src, 8192, 512>(c, fk[1], src, lb + base[kBinHash8K], hcounts[kBinHash8K], 256, end_bit, o);
     if (hcounts[kBinHash4K] > 0)
       launch_hash<SR, Src, 4096, 256>(c, fk[2], src, lb + base[kBinHash4K], hcounts[kBinHash4K], 256, end_bit, o);
-    if (hcounts[kBinHash2K] > 0) {
-      if (esc1k)
-        launch_esc<SR, Src, 256, 4>(c, fk[2], src, lb + base[kBinHash2K], hcounts[kBinHash2K], end_bit, o);
-      else
-        launch_hash<SR, Src, 2048, 128>(c, fk[2], src, lb + base[kBinHash2K], hcounts[kBinHash2K], 256, end_bit, o);
-    }
+    if (hcounts[kBinHash2K] > 0)
+      launch_hash<SR, Src, 2048, 128>(c, fk[2], src, lb + base[kBinHash2K], hcounts[kBinHash2K], 256, end_bit, o);
     if (hcounts[kBinEsc512] > 0)
       launch_esc<SR, Src, 128, 4>(c, fk[2], src, lb + base[kBinEsc512], hcounts[kBinEsc512], end_bit, o);
     if (hcounts[kBinBitRank] > 0) {
