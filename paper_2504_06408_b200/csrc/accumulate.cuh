@@ -1391,7 +1391,7 @@ __global__ void __launch_bounds__(THREADS) bitrank_rows_kernel(Src src, const in
 // in the (sorted) right-operand rows.  Emission is a contiguous copy.
 // ---------------------------------------------------------------------------
 template <class SR, class Src, int THREADS, int NMAX, int WMAX>
-__global__ void __launch_bounds__(THREADS, 1) rankpanel_rows_kernel(Src src, const int64_t* __restrict__ rows,
+__global__ void __launch_bounds__(THREADS, THREADS <= 512 ? 2 : 1) rankpanel_rows_kernel(Src src, const int64_t* __restrict__ rows,
                                                                     int64_t nrows_bin, int cap,
                                                                     const int32_t* __restrict__ colmin,
                                                                     RowOut<typename SR::value_type> out) {
@@ -1405,8 +1405,8 @@ __global__ void __launch_bounds__(THREADS, 1) rankpanel_rows_kernel(Src src, con
   V* acc = reinterpret_cast<V*>(smem_raw);                  // [NMAX]
   uint32_t* bm = reinterpret_cast<uint32_t*>(acc + NMAX);   // [WMAX]
   uint32_t* sm = bm + WMAX;                                 // [SW]
-  int* wrank = reinterpret_cast<int*>(sm + SW);             // [WMAX]
-  uint16_t* list = reinterpret_cast<uint16_t*>(wrank + WMAX);  // [WMAX]
+  uint16_t* wrank = reinterpret_cast<uint16_t*>(sm + SW);   // [WMAX] (ranks < F <= 65535 by binning)
+  uint16_t* list = wrank + WMAX;                            // [WMAX]
   int64_t* b0 = reinterpret_cast<int64_t*>(list + WMAX);    // [cap] whole-segment starts
   int* len0 = reinterpret_cast<int*>(b0 + cap);             // [cap]
   SegCache<SR, Src> cache;
@@ -1456,7 +1456,7 @@ __global__ void __launch_bounds__(THREADS, 1) rankpanel_rows_kernel(Src src, con
     for (int q = 0; q < LPT; ++q)
       if (k0 + q < nw) {
         const int w = list[k0 + q];
-        wrank[w] = first;
+        wrank[w] = (uint16_t)first;
         first += __popc(bm[w]);
       }
     if (threadIdx.x == 0) {

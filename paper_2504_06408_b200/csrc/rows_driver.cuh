@@ -272,13 +272,12 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
   }();
   constexpr int kRpN = 65536 / (int)sizeof(V), kRpSegs = 1024, kRpThreads = 1024;
   const size_t rp_smem = sizeof(V) * kRpN + sizeof(uint32_t) * (kBitRankW + kBitRankW / 32) +
-                         sizeof(int) * kBitRankW + sizeof(uint16_t) * kBitRankW +
-                         (sizeof(int64_t) + sizeof(int)) * kRpSegs +
+                         2 * sizeof(uint16_t) * kBitRankW + (sizeof(int64_t) + sizeof(int)) * kRpSegs +
                          (size_t)kRpSegs * SegCache<SR, Src>::bytes_per_seg(1) + 64;
   const bool rankpanel = bitrank && rankpanel_on && rp_smem <= 220 * 1024 && sizeof(V) == 4;  // measured gain: 4-byte values
   static const int64_t rp_maxf = [] {  // rank-panel rows: F up to this many products
     const char* e = std::getenv("SPG_RP_MAXF");
-    return e ? (int64_t)std::atoll(e) : (int64_t)16384;
+    return std::min<int64_t>(e ? (int64_t)std::atoll(e) : (int64_t)16384, 65535);  // 16-bit ranks
   }();
   DBuf<int32_t> colmin(c, bitrank ? (size_t)m : 1);
   analyse_rows_kernel<SR, Src><<<grid_for(c, m, 8), 256, 0, c->stream>>>(
