@@ -1288,7 +1288,8 @@ __global__ void __launch_bounds__(THREADS) bitrank_rows_kernel(Src src, const in
   constexpr int NW = THREADS / 32;
   constexpr int SW = WMAX / 32;                        // summary words
   static_assert(NMAX <= 65535 && WMAX <= 65536 && SW <= THREADS, "bit-rank geometry");
-  constexpr int LPT = (NMAX + THREADS - 1) / THREADS;  // listed words per thread (<= NMAX words are non-empty)
+  constexpr int LPT0 = (NMAX + THREADS - 1) / THREADS;
+  constexpr int LPT = LPT0 >= 16 ? (LPT0 | 1) : LPT0;  // listed words per thread (odd when long: fewer bank conflicts)
   using Scan = cub::BlockScan<int, THREADS>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* acc = reinterpret_cast<V*>(smem_raw);                               // [NMAX]
@@ -1398,7 +1399,8 @@ __global__ void __launch_bounds__(THREADS, THREADS <= 512 ? 2 : 1) rankpanel_row
   using V = typename SR::value_type;
   constexpr int NW = THREADS / 32;
   constexpr int SW = WMAX / 32;
-  constexpr int LPT = (WMAX + THREADS - 1) / THREADS;  // listed words per thread
+  constexpr int LPT0 = (WMAX + THREADS - 1) / THREADS;
+  constexpr int LPT = LPT0 >= 16 ? (LPT0 | 1) : LPT0;  // listed words per thread (odd when long: fewer bank conflicts)
   static_assert(WMAX <= 65536 && SW <= THREADS, "rank-panel geometry");
   using Scan = cub::BlockScan<int, THREADS>;
   extern __shared__ __align__(16) unsigned char smem_raw[];

@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--value-mode", type=int, default=0)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--permute", action="store_true")
+    ap.add_argument("--block", type=int, nargs=4, default=None, metavar=("PR", "PC", "I", "J"),
+                    help="multiply block row I of A by block column J of A (the local work of grid rank (I, J))")
     ap.add_argument("--frange", type=float, nargs=2, default=None,
                     help="keep only rows of the left operand whose product count F is in (lo, hi]")
     args = ap.parse_args()
@@ -58,9 +60,25 @@ def main():
         left = CsrMatrix(a.sr, keep.size, a.ncols, ptr, a.colids[sel], a.values[sel])
         print(f"rows with F in ({args.frange[0]:.0f}, {args.frange[1]:.0f}]: {keep.size}, products {F[keep].sum()}",
               file=sys.stderr)
+    right = a
+    if args.block:
+        from paper_2504_06408_b200.summa import block_range
+        pr, pc, bi, bj = args.block
+        r0, r1 = block_range(a.nrows, pr, bi)
+        c0, c1 = block_range(a.ncols, pc, bj)
+        rows_ = np.arange(r0, r1)
+        lens = np.diff(a.rowptr)[r0:r1]
+        left = CsrMatrix(a.sr, r1 - r0, a.ncols, np.concatenate([[0], np.cumsum(lens)]).astype(np.int64),
+                         a.colids[a.rowptr[r0]:a.rowptr[r1]], a.values[a.rowptr[r0]:a.rowptr[r1]])
+        keep = (a.colids >= c0) & (a.colids < c1)
+        rr = np.repeat(np.arange(a.nrows), np.diff(a.rowptr))[keep]
+        ptr = np.concatenate([[0], np.cumsum(np.bincount(rr, minlength=a.nrows))]).astype(np.int64)
+        right = CsrMatrix(a.sr, a.nrows, c1 - c0, ptr, a.colids[keep] - c0, a.values[keep])
+        print(f"block ({bi},{bj}) of {pr}x{pc}: left {left.nrows}x{left.ncols} nnz {left.nnz}, right nnz {right.nnz}",
+              file=sys.stderr)
     ctx = Context(0)
-    d = DeviceCsr.upload(ctx, a)
-    dl = DeviceCsr.upload(ctx, left) if left is not a else d
+    d = DeviceCsr.upload(ctx, right)
+    dl = DeviceCsr.upload(ctx, left) if left is not a else DeviceCsr.upload(ctx, a)
     for r in range(args.reps):
         st = {}
         c = local_multiply(dl, d, stats=st)
