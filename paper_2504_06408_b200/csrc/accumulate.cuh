@@ -1362,10 +1362,9 @@ __global__ void __launch_bounds__(THREADS) bitrank_rows_kernel(Src src, const in
     // emit: columns expanded from the listed words, values straight from acc
     const int64_t o = s_base;
     if (o >= 0) {
-#pragma unroll
-      for (int q = 0; q < LPT; ++q)
-        if (k0 + q < nw) {
-          const int w = list[k0 + q];
+      // striped over the listed words: neighbouring lanes write neighbouring output runs
+      for (int kw = threadIdx.x; kw < nw; kw += THREADS) {
+          const int w = list[kw];
           int k = wrank[w];
           for (uint32_t y = bm[w]; y; y &= y - 1) out.cols[o + k++] = lo + (w << 5) + __ffs(y) - 1;
         }
@@ -1469,10 +1468,9 @@ __global__ void __launch_bounds__(THREADS, THREADS <= 512 ? 2 : 1) rankpanel_row
     const int64_t o = s_base;
     // all output columns of the row
     if (o >= 0) {
-#pragma unroll
-      for (int q = 0; q < LPT; ++q)
-        if (k0 + q < nw) {
-          const int w = list[k0 + q];
+      // striped over the listed words: neighbouring lanes write neighbouring output runs
+      for (int kw = threadIdx.x; kw < nw; kw += THREADS) {
+          const int w = list[kw];
           int k = wrank[w];
           for (uint32_t y = bm[w]; y; y &= y - 1) out.cols[o + k++] = lo + (w << 5) + __ffs(y) - 1;
         }
