@@ -297,6 +297,9 @@ def run_single(args):
         "config": {"workload": f"rmat{args.scale}_ef{int(args.ef)}_tropical_i32_AxA (BASELINE config 2)",
                    "grid": "1x1", "permuted": bool(args.permute), "products": F, "nnz_A": a.nnz, "nnz_C": nnz_c,
                    "time_to_C_ms": ms, "steps_ms": [round(float(x), 3) for x in times],
+                   "phases_ms_untimed_warmup_call": {k: round(st[k], 3) for k in ("ms_analyse", "ms_numeric",
+                                                                                    "ms_compact")},
+                   "rows_per_bin": st["rows_per_bin"], "output_mode": st["output_mode"],
                    "l2": "flushed between steps (512 MB write)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
