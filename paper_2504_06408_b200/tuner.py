@@ -138,3 +138,49 @@ def save_model(path: str, curves: Dict[str, Curve], extra: dict | None = None):
         doc.update(extra)
     with open(path, "w") as f:
         json.dump(doc, f, indent=1)
+
+
+INFINITE_THRESHOLD = (1 << 64) - 1  # kInfiniteThreshold: every payload on the host path
+
+
+def crossover_warning(host, device, lo: int = 1, hi: int = 1 << 30) -> Optional[str]:
+    """crossover_warning (tuner.hpp:43-53): text when the measured curves have
+    no host/device crossover in range (hybrid routing then degenerates)."""
+    if find_crossover(host, device, lo, hi) is not None:
+        return None
+    return ("latency model has no host/device crossover in its sampled range; "
+            "hybrid routing will degenerate to a single path")
+
+
+def sweep_thresholds(comm, ctx, a_block, n: int, thresholds: Sequence[int], allsum, allmax,
+                     two_round: bool = True) -> List[dict]:
+    """sweep_thresholds (tuner.hpp:64-99): runs C = A (x) A once per threshold
+    under hybrid routing on this rank's block (every rank calls it with the
+    same thresholds) and tabulates the host-handled broadcast percentage, the
+    MEASURED broadcast time (the reference reports its simulated cost) and the
+    local-multiply time, both max over ranks, plus the checksum of C.  Every
+    run must produce the identical product: diverging checksums raise
+    InternalError.  `allsum(int) -> int` / `allmax(float) -> float` reduce a
+    value over all ranks (e.g. torch.distributed)."""
+    from . import errors
+    from .summa import HYBRID, checksum_part, checksum_seed, summa25_multiply
+
+    rows: List[dict] = []
+    for t in thresholds:
+        c, led = summa25_multiply(comm, ctx, a_block, a_block, n, n, n, two_round=two_round, mode=HYBRID,
+                                  threshold=int(t), threshold_col=int(t))
+        part = checksum_part(c, a_block.rows[0], a_block.cols[0])
+        c.free()
+        lo, hi = allsum(part & 0xFFFFFFFF), allsum(part >> 32)
+        checksum = (checksum_seed(n, n) + lo + (hi << 32)) % (1 << 64)
+        host, dev = allsum(led["host_bcasts"]), allsum(led["device_bcasts"])
+        if rows and checksum != rows[0]["result_checksum"]:
+            raise errors.InternalError("threshold sweep runs produced different products; routing must "
+                                       "not affect results")
+        rows.append({"threshold_bytes": int(t),
+                     "pct_host_bcasts": 0.0 if host + dev == 0 else 100.0 * host / (host + dev),
+                     "comm_seconds": allmax(led["ms"]["broadcast"]) / 1e3,
+                     "wall_local_seconds": allmax(led["ms"]["local_multiply"]) / 1e3,
+                     "time_to_c_seconds": allmax(led["ms_total"]) / 1e3,
+                     "result_checksum": checksum})
+    return rows

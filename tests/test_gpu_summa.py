@@ -68,3 +68,20 @@ def test_fullsize_config_against_streaming_oracle(config):
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=3000, cwd=ROOT,
                        env=dict(os.environ, MASTER_ADDR="127.0.0.1"))
     assert p.returncode == 0 and '"match": true' in p.stdout, p.stdout[-3000:] + p.stderr[-3000:]
+
+
+def test_threshold_sweep_same_product_every_threshold():
+    """sweep_thresholds (tuner.hpp:64-99): every threshold of the ladder, from
+    all-device to all-host, yields the identical C (checksums compared)."""
+    n = ngpus()
+    nproc = 4 if n >= 4 else 2 if n >= 2 else 1
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nproc-per-node", str(nproc),
+           os.path.join(ROOT, "tools", "threshold_sweep.py"), "--scale", "11", "--reps", "1"]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
+                       env=dict(os.environ, MASTER_ADDR="127.0.0.1"))
+    assert p.returncode == 0 and '"same_product_every_threshold": true' in p.stdout, p.stdout[-2000:] + p.stderr[-3000:]
+    if nproc > 1:
+        import json
+        doc = json.loads(p.stdout.strip().splitlines()[-1])
+        pct = [r["pct_host_bcasts"] for r in doc["rows"]]
+        assert pct[0] == 0.0 and pct[-1] == 100.0  # threshold 0: all device; infinity: all host

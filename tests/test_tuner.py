@@ -55,3 +55,12 @@ def test_model_json_round_trip(tmp_path):
     doc = json.load(open(p))
     assert set(doc["curves"]) == {"host_bcast", "device_bcast", "copy_h2d", "copy_d2h"}
     assert doc["curves"]["host_bcast"][3] == [8.0, 30e-6 + 8 / (12 * GIB)]
+
+
+def test_crossover_warning():
+    """crossover_warning (tuner.hpp:43-53): None when the curves cross, the
+    reference's text when one path wins everywhere."""
+    host = [(1.0, 1e-6), (1e9, 1.0)]
+    assert tuner.crossover_warning(host, [(1.0, 1e-5), (1e9, 0.05)]) is None
+    msg = tuner.crossover_warning(host, [(1.0, 1e-7), (1e9, 0.05)])
+    assert msg and "no host/device crossover" in msg
