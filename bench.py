@@ -55,7 +55,8 @@ class Clocks:
     def __init__(self, gpu: int):
         self.gpu = gpu
         self.proc = None
-        self.path = tempfile.mktemp(suffix=".csv")
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
 
     def __enter__(self):
         try:
@@ -70,8 +71,10 @@ class Clocks:
         t0 = time.time()
         while self.proc is not None and time.time() - t0 < 10.0:
             self.f.flush()
-            if os.path.getsize(self.path) > 0 and open(self.path).read().count("\n") >= 2:
-                break
+            if os.path.getsize(self.path) > 0:
+                with open(self.path) as fh:
+                    if fh.read().count("\n") >= 2:
+                        break
             time.sleep(0.05)
         return self
 
