@@ -1635,11 +1635,15 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
       });
       __syncthreads();
     }
-    // occupied, non-zero slots of this thread's range -> staging (in order)
-    const int e0 = threadIdx.x * SPT;
+    // occupied, non-zero slots -> staging.  Slots are taken striped (slot
+    // t + q*THREADS: conflict-free shared loads); staging order is free, the
+    // bucketing below sorts by column.
     int cnt = 0;
 #pragma unroll 4
-    for (int q = 0; q < SPT; ++q) cnt += (tkeys[e0 + q] != kEmptyKey && !SR::is_zero(tvals[e0 + q])) ? 1 : 0;
+    for (int q = 0; q < SPT; ++q) {
+      const int e = threadIdx.x + q * THREADS;
+      cnt += (tkeys[e] != kEmptyKey && !SR::is_zero(tvals[e])) ? 1 : 0;
+    }
     int first, total;
     typename HS::Scan(tmp->scan).ExclusiveSum(cnt, first, total);
     if (threadIdx.x == 0) {
@@ -1652,7 +1656,7 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
     }
 #pragma unroll 4
     for (int q = 0; q < SPT; ++q) {
-      const int e = e0 + q;
+      const int e = threadIdx.x + q * THREADS;
       const int32_t k = tkeys[e];
       if (k != kEmptyKey && !SR::is_zero(tvals[e])) {
         stg_key[first] = (uint32_t)k;
