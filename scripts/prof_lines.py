@@ -19,8 +19,13 @@ for line in raw:
             st = int(d["Warp Stall Sampling (All Samples)"]); ie = int(d["Instructions Executed"])
         except ValueError:
             continue
-        rows.append((st, ie, fname, int(r[0]), r[1].strip()[:90]))
+        try:
+            xs = int(d.get("L1 Wavefronts Shared Excessive", "0") or 0)
+        except ValueError:
+            xs = 0
+        rows.append((st, ie, fname, int(r[0]), r[1].strip()[:90], xs))
 tot_s = sum(x[0] for x in rows) or 1; tot_i = sum(x[1] for x in rows) or 1
+tot_x = sum(x[5] for x in rows) or 1
 rows.sort(reverse=True)
-for st, ie, f, ln, src in rows[:top]:
-    print(f"{st / tot_s * 100:5.1f}% stall {ie / tot_i * 100:5.1f}% inst  {f}:{ln}  {src}")
+for st, ie, f, ln, src, xs in rows[:top]:
+    print(f"{st / tot_s * 100:5.1f}% stall {ie / tot_i * 100:5.1f}% inst {xs / tot_x * 100:5.1f}% smem-excess  {f}:{ln}  {src}")
