@@ -283,6 +283,14 @@ SPG_API int spg_summa25_multiply(spg_comm* comm, spg_ctx* ctx, int sr, int64_t a
                                  const spg_hdcsc* b_dcsc, const spg_summa_opts* opts,
                                  spg_dcsr* c_csc, spg_ledger* ledger);
 
+/* gather (dist_matrix.hpp gather): every rank's CSC block of C
+ * (block-local indices, rows offset row_off, columns offset col_off) to world
+ * rank `root`, assembled there ON THE GPU into the full nrows x ncols CSC
+ * matrix (blocks over NCCL send/recv; columns merged in block-row order).
+ * Collective over all ranks; non-root ranks get an empty `out`. */
+SPG_API int spg_gather(spg_comm* comm, spg_ctx* ctx, int sr, const spg_dcsr* block_csc, int64_t row_off,
+                       int64_t col_off, int64_t nrows, int64_t ncols, int root, spg_dcsr* out_csc);
+
 #ifdef __cplusplus
 }
 #endif

@@ -140,6 +140,38 @@ void comm_abort(spg_comm* c, const std::string& why) {
 }
 
 void comm_barrier(spg_comm* c) { barrier_wait(c, c->hdr->world_bar, c->world); }
+int comm_world_rank(const spg_comm* c) { return c->rank; }
+int comm_world_size(const spg_comm* c) { return c->world; }
+
+void comm_allgather_i64(spg_comm* c, const int64_t* mine, int n, int64_t* all, cudaStream_t stream) {
+  if (!c->world_comm) fail(SPG_ERR_ARG, "allgather needs a GPU communicator");
+  int64_t* d = nullptr;
+  SPG_CUDA(cudaMallocAsync(&d, sizeof(int64_t) * n * (c->world + 1), stream));
+  SPG_CUDA(cudaMemcpyAsync(d, mine, sizeof(int64_t) * n, cudaMemcpyHostToDevice, stream));
+  nccl_check(ncclAllGather(d, d + n, n, ncclInt64, c->world_comm, stream), "ncclAllGather");
+  SPG_CUDA(cudaMemcpyAsync(all, d + n, sizeof(int64_t) * n * c->world, cudaMemcpyDeviceToHost, stream));
+  SPG_CUDA(cudaFreeAsync(d, stream));
+  SPG_CUDA(cudaStreamSynchronize(stream));
+}
+
+void comm_gather_bytes(spg_comm* c, int root, const void* send, uint64_t bytes, void* const* recv,
+                       const uint64_t* recv_bytes, cudaStream_t stream) {
+  if (!c->world_comm) fail(SPG_ERR_ARG, "gather needs a GPU communicator");
+  if (root < 0 || root >= c->world) fail(SPG_ERR_PROTOCOL, "gather root outside the world");
+  nccl_check(ncclGroupStart(), "ncclGroupStart");
+  if (c->rank != root) {
+    if (bytes) nccl_check(ncclSend(send, bytes, ncclUint8, root, c->world_comm, stream), "ncclSend");
+  } else {
+    for (int r = 0; r < c->world; ++r)
+      if (r != root && recv_bytes[r])
+        nccl_check(ncclRecv(recv[r], recv_bytes[r], ncclUint8, r, c->world_comm, stream), "ncclRecv");
+  }
+  nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+  SPG_CUDA(cudaStreamSynchronize(stream));
+  ncclResult_t async_err = ncclSuccess;
+  nccl_check(ncclCommGetAsyncError(c->world_comm, &async_err), "ncclCommGetAsyncError");
+  nccl_check(async_err, "gather (async)");
+}
 
 // Rank::exchange_sizes (fabric.hpp:335-338): root publishes, all read.
 void comm_exchange_sizes(spg_comm* c, int scope, int root, int64_t triple[3]) {

@@ -48,6 +48,14 @@ void comm_exchange_sizes(spg_comm* c, int scope, int root, int64_t triple[3]);
 int comm_bcast(spg_comm* c, int scope, int root, void* buf, uint64_t bytes, int mode, uint64_t threshold,
                cudaStream_t stream, bool device_buffer);
 void comm_barrier(spg_comm* c);
+int comm_world_rank(const spg_comm* c);
+int comm_world_size(const spg_comm* c);
+// every rank contributes n int64 (host), every rank receives world*n (host), over NCCL
+void comm_allgather_i64(spg_comm* c, const int64_t* mine, int n, int64_t* all, cudaStream_t stream);
+// device buffers to world rank `root` over NCCL (send on non-roots; the root receives
+// recv[r] of recv_bytes[r] from every other rank r)
+void comm_gather_bytes(spg_comm* c, int root, const void* send, uint64_t bytes, void* const* recv,
+                       const uint64_t* recv_bytes, cudaStream_t stream);
 void comm_abort(spg_comm* c, const std::string& why);
 CommCounters& comm_counters(spg_comm* c);
 

@@ -338,3 +338,145 @@ extern "C" int spg_summa25_multiply(spg_comm* comm, spg_ctx* c, int sr, int64_t 
     if (ledger) *ledger = led;
   });
 }
+
+// ---------------------------------------------------------------------------
+// gather (dist_matrix.hpp: gather): every rank's CSC block of C
+// to one rank, assembled on that rank's GPU into the full CSC matrix.  Blocks
+// travel packed (wire format) over NCCL send/recv; the root merges each
+// column's pieces in block-row order (row ranges are disjoint and
+// increasing, so no sort is needed).
+// ---------------------------------------------------------------------------
+namespace spg {
+namespace {
+
+constexpr int kMaxGatherParts = 32;
+struct GatherParts {
+  const int64_t* ptr[kMaxGatherParts];
+  const int32_t* idx[kMaxGatherParts];
+  const unsigned char* vals[kMaxGatherParts];
+  int64_t r0[kMaxGatherParts], c0[kMaxGatherParts], nc[kMaxGatherParts];
+  int n;  // parts sorted by (c0, r0)
+};
+
+__device__ __forceinline__ void parts_of_col(const GatherParts& g, int64_t c, int& first, int& last) {
+  first = last = -1;
+  for (int k = 0; k < g.n; ++k)
+    if (c >= g.c0[k] && c < g.c0[k] + g.nc[k]) {
+      if (first < 0) first = k;
+      last = k;
+    }
+}
+
+__global__ void gather_count_kernel(GatherParts g, int64_t ncols, int64_t* cnt) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ncols; c += (int64_t)gridDim.x * blockDim.x) {
+    int f, l;
+    parts_of_col(g, c, f, l);
+    int64_t n = 0;
+    for (int k = f; k >= 0 && k <= l; ++k) {
+      const int64_t lc = c - g.c0[k];
+      n += g.ptr[k][lc + 1] - g.ptr[k][lc];
+    }
+    cnt[c] = n;
+  }
+}
+
+__global__ void gather_fill_kernel(GatherParts g, int64_t ncols, int vs, const int64_t* __restrict__ colptr,
+                                   int32_t* __restrict__ idx, unsigned char* __restrict__ vals) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = warp; c < ncols; c += nwarps) {
+    int f, l;
+    parts_of_col(g, c, f, l);
+    int64_t d = colptr[c];
+    for (int k = f; k >= 0 && k <= l; ++k) {
+      const int64_t lc = c - g.c0[k];
+      const int64_t b = g.ptr[k][lc], n = g.ptr[k][lc + 1] - b;
+      for (int64_t e = lane; e < n; e += 32) {
+        idx[d + e] = (int32_t)(g.idx[k][b + e] + g.r0[k]);
+        for (int q = 0; q < vs; ++q) vals[(d + e) * vs + q] = g.vals[k][(b + e) * vs + q];
+      }
+      d += n;
+    }
+  }
+}
+
+}  // namespace
+}  // namespace spg
+
+extern "C" int spg_gather(spg_comm* comm, spg_ctx* c, int sr, const spg_dcsr* blk, int64_t row_off, int64_t col_off,
+                          int64_t nrows, int64_t ncols, int root, spg_dcsr* out) {
+  return guarded_summa(c, comm, [&] {
+    if (!comm || !c || !blk || !out) fail(SPG_ERR_ARG, "null argument");
+    SPG_CUDA(cudaSetDevice(c->device));
+    const int vs = ops_for(sr)->value_size;
+    const int world = comm_world_size(comm), me = comm_world_rank(comm);
+    if (world > kMaxGatherParts) fail(SPG_ERR_GRID, "gather supports up to 32 ranks");
+    // my block, packed (CSC: ptr over its columns)
+    const size_t bytes = panel_bytes(blk->ncols, blk->nnz, vs);
+    DBuf<char> mine(c, bytes);
+    spg_dcsr v = panel_view(mine.p, blk->ncols, blk->nrows, blk->nnz);
+    SPG_CUDA(cudaMemcpyAsync(v.ptr, blk->ptr, sizeof(int64_t) * (blk->ncols + 1), cudaMemcpyDeviceToDevice, c->stream));
+    if (blk->nnz) {
+      SPG_CUDA(cudaMemcpyAsync(v.idx, blk->idx, sizeof(int32_t) * blk->nnz, cudaMemcpyDeviceToDevice, c->stream));
+      SPG_CUDA(cudaMemcpyAsync(v.vals, blk->vals, (size_t)vs * blk->nnz, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    const int64_t meta[6] = {blk->nnz, row_off, col_off, blk->nrows, blk->ncols, (int64_t)bytes};
+    std::vector<int64_t> all((size_t)world * 6);
+    comm_allgather_i64(comm, meta, 6, all.data(), c->stream);
+    std::vector<DBuf<char>> bufs(world);
+    std::vector<void*> recv(world, nullptr);
+    std::vector<uint64_t> rbytes(world, 0);
+    if (me == root)
+      for (int r = 0; r < world; ++r) {
+        rbytes[r] = (uint64_t)all[r * 6 + 5];
+        if (r != root) {
+          bufs[r] = DBuf<char>(c, rbytes[r]);
+          recv[r] = bufs[r].p;
+        } else {
+          recv[r] = mine.p;
+        }
+      }
+    comm_gather_bytes(comm, root, mine.p, bytes, recv.data(), rbytes.data(), c->stream);
+    out->nrows = nrows;
+    out->ncols = ncols;
+    out->nnz = 0;
+    out->ptr = nullptr;
+    out->idx = nullptr;
+    out->vals = nullptr;
+    if (me != root) return;
+    std::vector<int> order(world);
+    for (int r = 0; r < world; ++r) order[r] = r;
+    std::sort(order.begin(), order.end(), [&](int a, int b) {
+      return std::make_pair(all[a * 6 + 2], all[a * 6 + 1]) < std::make_pair(all[b * 6 + 2], all[b * 6 + 1]);
+    });
+    GatherParts g{};
+    g.n = world;
+    for (int k = 0; k < world; ++k) {
+      const int r = order[k];
+      const spg_dcsr pv = panel_view(recv[r], all[r * 6 + 4], all[r * 6 + 3], all[r * 6 + 0]);
+      g.ptr[k] = pv.ptr;
+      g.idx[k] = pv.idx;
+      g.vals[k] = static_cast<const unsigned char*>(pv.vals);
+      g.r0[k] = all[r * 6 + 1];
+      g.c0[k] = all[r * 6 + 2];
+      g.nc[k] = all[r * 6 + 4];
+    }
+    DBuf<int64_t> cnt(c, ncols + 1);
+    SPG_CUDA(cudaMemsetAsync(cnt.p + ncols, 0, sizeof(int64_t), c->stream));
+    gather_count_kernel<<<(int)std::min<int64_t>((ncols + 255) / 256, (int64_t)c->sm_count * 16), 256, 0, c->stream>>>(
+        g, ncols, cnt.p);
+    SPG_LAUNCH_CHECK();
+    ++c->launches;
+    out->ptr = dalloc<int64_t>(c, ncols + 1);
+    exclusive_scan_i64(c, cnt.p, out->ptr, ncols + 1);
+    out->nnz = d2h_scalar(c, out->ptr + ncols);
+    out->idx = dalloc<int32_t>(c, (size_t)std::max<int64_t>(out->nnz, 1));
+    out->vals = dalloc<unsigned char>(c, (size_t)vs * std::max<int64_t>(out->nnz, 1));
+    gather_fill_kernel<<<(int)std::min<int64_t>((ncols + 7) / 8, (int64_t)c->sm_count * 16), 256, 0, c->stream>>>(
+        g, ncols, vs, out->ptr, out->idx, static_cast<unsigned char*>(out->vals));
+    SPG_LAUNCH_CHECK();
+    ++c->launches;
+    SPG_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}

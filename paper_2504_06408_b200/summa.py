@@ -160,6 +160,19 @@ def summa25_multiply(comm: Comm, ctx: Context, a_block: LocalBlock, b_block: Loc
     return DeviceCsr(ctx, sr, out, is_csc=True), led.as_dict()
 
 
+def gather(comm: Comm, ctx: Context, c_block: DeviceCsr, rows: tuple, cols: tuple, nrows: int, ncols: int,
+           root: int = 0):
+    """gather (dist_matrix.hpp): this rank's CSC block of C
+    (global extents rows/cols) to world rank `root`, assembled on its GPU.
+    Collective; returns the full CSC DeviceCsr on the root, None elsewhere."""
+    out = DCsr()
+    check(lib.spg_gather(comm.handle, ctx.handle, int(c_block.sr), C.byref(c_block.d), int(rows[0]), int(cols[0]),
+                         int(nrows), int(ncols), int(root), C.byref(out)), ctx.handle)
+    if comm.rank != root:
+        return None
+    return DeviceCsr(ctx, c_block.sr, out, is_csc=True)
+
+
 def checksum_part(c: DeviceCsr, row_off: int, col_off: int) -> int:
     """This block's share of matrix_checksum of the distributed matrix."""
     out = C.c_uint64()

@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--staging", type=int, default=1 << 16)
     ap.add_argument("--fuse", type=int, default=1)
     ap.add_argument("--grid", default="", help="PRxPC (default: the BASELINE grid for the world size)")
+    ap.add_argument("--gather", type=int, default=0, help="also gather C on rank 0 (GPU assembly) and compare")
     args = ap.parse_args()
 
     import torch.distributed as dist
@@ -38,7 +39,7 @@ def main():
     import oracle_bind as ob
     from paper_2504_06408_b200 import Context, generators
     from paper_2504_06408_b200.formats import coo_to_csr
-    from paper_2504_06408_b200.summa import Comm, checksum_part, checksum_seed, grid_for, local_block, \
+    from paper_2504_06408_b200.summa import Comm, checksum_part, checksum_seed, gather, grid_for, local_block, \
         summa25_multiply
 
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -57,6 +58,7 @@ def main():
     c, led = summa25_multiply(comm, ctx, blk, blk, n, n, n, two_round=bool(args.two_round), mode=args.mode,
                               threshold=args.threshold, fuse_stages=bool(args.fuse))
     part = checksum_part(c, blk.rows[0], blk.cols[0])
+    full = gather(comm, ctx, c, blk.rows, blk.cols, n, n, root=0) if args.gather else None
     got = c.download()  # CSC of the C block
 
     a = coo_to_csr(m)
@@ -86,6 +88,19 @@ def main():
             total = (total + int(p[0]) + (int(p[1]) << 32)) % (1 << 64)
         want = ob.orc_checksum(want_full)
         allok = all(int(p[2]) for p in parts)
+        if full is not None:  # gathered full C (CSC) against the oracle's full C
+            g = full.download()
+            rr_all = np.repeat(np.arange(n), np.diff(want_full.ptr))
+            order_all = np.lexsort((rr_all, want_full.idx))
+            wcolptr = np.concatenate([[0], np.cumsum(np.bincount(want_full.idx, minlength=n))])
+            gok = np.array_equal(g.colptr, wcolptr) and np.array_equal(g.rowids, rr_all[order_all])
+            if args.sr == 0:
+                x, y = g.values, want_full.vals[order_all]
+                gok = gok and bool(np.all(np.abs(x - y) <= 1e-12 * np.maximum(np.abs(x), np.abs(y)) + 1e-300))
+            else:
+                gok = gok and g.values.tobytes() == want_full.vals[order_all].tobytes()
+            print(f"[summa_worker] gather_ok={gok}", flush=True)
+            allok = allok and gok
         cs_ok = total == want or args.sr == 0  # fp64 values hash bitwise
         print(f"[summa_worker] grid {pr}x{pc} sr={args.sr} s{args.scale} two_round={args.two_round} "
               f"mode={args.mode} fuse={args.fuse}: blocks_ok={allok} checksum_ok={cs_ok} ledger0={led}", flush=True)

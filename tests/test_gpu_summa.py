@@ -85,3 +85,13 @@ def test_threshold_sweep_same_product_every_threshold():
         doc = json.loads(p.stdout.strip().splitlines()[-1])
         pct = [r["pct_host_bcasts"] for r in doc["rows"]]
         assert pct[0] == 0.0 and pct[-1] == 100.0  # threshold 0: all device; infinity: all host
+
+
+@pytest.mark.parametrize("sr", [4, 0, 5])
+def test_gather_full_c_on_root(sr):
+    """gather: the blocks of C assembled on rank 0's GPU equal
+    the oracle's full C (tropical / max-times bit-exact, fp64 within 1e-12)."""
+    n = ngpus()
+    nproc = 8 if n >= 8 else 4 if n >= 4 else 2 if n >= 2 else 1
+    out = run_worker(nproc, "--sr", sr, "--scale", 10, "--gather", 1)
+    assert "gather_ok=True" in out and "blocks_ok=True" in out
