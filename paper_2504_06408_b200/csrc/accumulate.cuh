@@ -189,7 +189,10 @@ struct Geom {
 constexpr int kDenseMaxPanels = 16;   // beyond this many panels prefer hashing
 constexpr int kDenseMinPerPanel = 1024;
 constexpr int64_t kDenseMinRow = 4096;  // rows with more products go dense (when panels are few)
-constexpr int64_t kBitRankMinF = 2048;  // bit-rank bin floor (smaller rows: hash bins, more rows per SM)
+#ifndef SPG_BITRANK_MINF
+#define SPG_BITRANK_MINF 2048
+#endif
+constexpr int64_t kBitRankMinF = SPG_BITRANK_MINF;  // bit-rank bin floor (smaller rows: hash bins, more rows per SM)
 
 template <class V>
 __host__ __device__ inline int npanels_for(int64_t ncols, int w = Geom<V>::kPanelW) {
