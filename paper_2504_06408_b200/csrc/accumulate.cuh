@@ -452,6 +452,11 @@ struct RowOut {
   int64_t* chunks = nullptr;    // claim mode, dense rows: (start, count) per (dense slot, panel)
   int64_t slot_base = 0;        // dense slot of the launch's first row (several dense launches share `chunks`)
   int chunk_stride = 0;         // chunk entries per dense slot (>= the launch's panel count)
+  // U-slot mode, dense rows: per-(panel, warp) chunks inside the row's slot
+  // ((start within the slot, count) per chunk; a row's chunks in (panel,
+  // warp) order are its sorted output) — warps claim without a block scan
+  int32_t* wchunks = nullptr;
+  int wstride = 0;              // chunks per dense slot = panels x warps
   int64_t* rownnz = nullptr;
 
   __device__ __forceinline__ bool writes() const { return cols != nullptr; }
@@ -1010,6 +1015,93 @@ __device__ __forceinline__ int bitmap_emit(typename SR::value_type* acc, uint32_
   return total;
 }
 
+// Per-warp emission for U-slot mode: each warp counts the entries of its own
+// column slice, claims that many slots of the row's scratch slot with one
+// shared atomicAdd, records the chunk (start, count) and writes its entries
+// in column order — no block-wide count/scan/offset barriers.  The chunks in
+// (panel, warp) order are the row's sorted output; the compaction
+// concatenates them.
+template <class SR, int W, int THREADS>
+__device__ __forceinline__ void bitmap_emit_warp(typename SR::value_type* acc, uint32_t* bm, int col_base,
+                                                 const RowOut<typename SR::value_type>& out, int64_t row,
+                                                 int64_t slot, int panel, int* s_fill) {
+  using V = typename SR::value_type;
+  constexpr int NW = THREADS / 32;
+  constexpr int WORDS = W / 32;
+  constexpr int WPW = WORDS / NW;
+  constexpr int ITERS = (WPW + 31) / 32;
+  static_assert(WORDS % NW == 0 && (WPW < 32 || WPW % 32 == 0), "bitmap words must split evenly over the warps");
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int w0 = wid * WPW;
+  if constexpr (AddCanCancel<SR>::value) {
+    for (int it = 0; it < ITERS; ++it) {
+      const int wl = it * 32 + lane;
+      if (wl >= WPW) break;
+      const int w = w0 + wl;
+      uint32_t x = bm[w];
+      for (uint32_t y = x; y; y &= y - 1) {
+        const int bit = __ffs(y) - 1;
+        if (SR::is_zero(acc[(w << 5) + bit])) {
+          acc[(w << 5) + bit] = SR::zero();
+          x &= ~(1u << bit);
+        }
+      }
+      bm[w] = x;
+    }
+    __syncwarp();
+  }
+  int cnt = 0;
+  for (int it = 0; it < ITERS; ++it) {
+    const int wl = it * 32 + lane;
+    cnt += wl < WPW ? __popc(bm[w0 + wl]) : 0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
+  int base = 0;
+  if (lane == 0) {
+    base = cnt ? atomicAdd(s_fill, cnt) : 0;
+    int32_t* ch = out.wchunks + 2 * ((slot + out.slot_base) * out.wstride + (int64_t)panel * NW + wid);
+    ch[0] = base;
+    ch[1] = cnt;
+  }
+  base = __shfl_sync(kFull, base, 0);
+  int64_t pos = out.off[row] + base;
+  for (int it = 0; it < ITERS; ++it) {
+    const int wl = it * 32 + lane;
+    const int w = w0 + wl;
+    const uint32_t x = wl < WPW ? bm[w] : 0u;
+    const int c = __popc(x);
+    int incl = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int t = __shfl_up_sync(kFull, incl, d);
+      if (lane >= d) incl += t;
+    }
+    const int total = __shfl_sync(kFull, incl, 31);
+    const int excl = incl - c;
+    for (int q0 = 0; q0 < total; q0 += 32) {
+      const int q = q0 + lane;
+      int own = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const int v = __shfl_sync(kFull, incl, own + step - 1);
+        if (v <= q) own += step;
+      }
+      const uint32_t xo = __shfl_sync(kFull, x, own);
+      const int eo = __shfl_sync(kFull, excl, own);
+      if (q < total) {
+        const int bit = nth_set_bit(xo, q - eo);
+        const int cc = ((w0 + it * 32 + own) << 5) + bit;
+        out.cols[pos + q] = col_base + cc;
+        out.vals[pos + q] = acc[cc];
+        acc[cc] = SR::zero();
+      }
+    }
+    if (x) bm[w] = 0u;
+    pos += total;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K5 bin 6: dense accumulator over column panels in shared memory.
 //
@@ -1051,6 +1143,8 @@ __global__ void __launch_bounds__(THREADS, MINB) dense_panel_kernel(Src src, con
   __shared__ typename Count::TempStorage scan_tmp;
   __shared__ long long s_row, s_base;
   __shared__ int wsum[2 * NW + 1];
+  __shared__ int s_fill;  // per-warp emission: entries of the current row claimed so far
+  const bool warp_emit = out.wchunks != nullptr;
 
   for (int e = threadIdx.x; e < W; e += THREADS) acc[e] = SR::zero();
   for (int e = threadIdx.x; e < W / 32; e += THREADS) bm[e] = 0u;
@@ -1059,6 +1153,7 @@ __global__ void __launch_bounds__(THREADS, MINB) dense_panel_kernel(Src src, con
     if (threadIdx.x == 0) {
       const unsigned long long r = atomicAdd(work, 1ull);
       s_row = r < (unsigned long long)nrows_bin ? (long long)r : -1;
+      s_fill = 0;
     }
     __syncthreads();
     const long long r = s_row;
@@ -1129,10 +1224,15 @@ __global__ void __launch_bounds__(THREADS, MINB) dense_panel_kernel(Src src, con
         }
       __syncthreads();
 #else
-      written += bitmap_emit<SR, W, THREADS>(acc, bm, lo, out, i, r, p, npanels, written, wsum, &s_base);
+      if (warp_emit) {
+        bitmap_emit_warp<SR, W, THREADS>(acc, bm, lo, out, i, r, p, &s_fill);
+        __syncthreads();  // slices cleared before the next panel's atomics
+      } else {
+        written += bitmap_emit<SR, W, THREADS>(acc, bm, lo, out, i, r, p, npanels, written, wsum, &s_base);
+      }
 #endif
     }
-    if (threadIdx.x == 0) out.rownnz[i] = written;
+    if (threadIdx.x == 0) out.rownnz[i] = warp_emit ? s_fill : written;
   }
 }
 
@@ -1731,6 +1831,62 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
 // ---------------------------------------------------------------------------
 // K7: compaction scratch -> exact CSR (warp per row, 4-way unrolled)
 // ---------------------------------------------------------------------------
+// U-slot mode, dense rows with per-warp chunks: CTA per row; one block scan
+// over the row's chunk counts gives each chunk its place in C, then each
+// warp copies its chunks (coalesced within a chunk).
+template <class V, int THREADS>
+__global__ void __launch_bounds__(THREADS) compact_wchunks_kernel(const int64_t* __restrict__ rows, int64_t nrows_bin,
+                                                                  const int32_t* __restrict__ wchunks, int wstride,
+                                                                  const int64_t* __restrict__ off,
+                                                                  const int64_t* __restrict__ rowptr,
+                                                                  const int32_t* __restrict__ sc_cols,
+                                                                  const V* __restrict__ sc_vals,
+                                                                  int32_t* __restrict__ cols, V* __restrict__ vals) {
+  using Scan = cub::BlockScan<int, THREADS>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int spos[THREADS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t r = blockIdx.x; r < nrows_bin; r += gridDim.x) {
+    const int64_t i = rows[r];
+    const int32_t* ch = wchunks + 2 * (r * wstride);
+    const int64_t s0 = off[i];
+    int64_t d0 = rowptr[i];
+    for (int t0 = 0; t0 < wstride; t0 += THREADS) {
+      const int k = t0 + threadIdx.x;
+      const int cnt = k < wstride ? ch[2 * k + 1] : 0;
+      int pos, total;
+      Scan(tmp).ExclusiveSum(cnt, pos, total);
+      spos[threadIdx.x] = pos;
+      __syncthreads();
+      for (int kk = warp; kk < THREADS && t0 + kk < wstride; kk += THREADS / 32) {
+        const int n = ch[2 * (t0 + kk) + 1];
+        const int64_t s = s0 + ch[2 * (t0 + kk)], d = d0 + spos[kk];
+        int e = lane;
+        for (; e + 96 < n; e += 128) {  // four entries per lane in flight
+          int32_t cc[4];
+          V vv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            cc[u] = sc_cols[s + e + 32 * u];
+            vv[u] = sc_vals[s + e + 32 * u];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            cols[d + e + 32 * u] = cc[u];
+            vals[d + e + 32 * u] = vv[u];
+          }
+        }
+        for (; e < n; e += 32) {
+          cols[d + e] = sc_cols[s + e];
+          vals[d + e] = sc_vals[s + e];
+        }
+      }
+      d0 += total;
+      __syncthreads();
+    }
+  }
+}
+
 // Dense rows: concatenate their per-panel chunks (CTA per row).
 template <class V>
 __global__ void __launch_bounds__(256) compact_chunks_kernel(const int64_t* __restrict__ rows, int64_t nrows_bin,

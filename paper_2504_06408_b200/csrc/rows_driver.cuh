@@ -360,6 +360,14 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
   }
   const int npc = std::max(np, 1);
   const bool slotted = cap > 0 && cap == scratch_total;  // U_i slots: no claims needed
+  // U-slot mode: dense rows emit per-warp chunks (no block scan per panel)
+  static const int warp_emit_on = [] {
+    const char* e = std::getenv("SPG_WARP_EMIT");
+    return e ? std::atoi(e) : 1;
+  }();
+  const bool warp_emit = warp_emit_on && slotted && hcounts[kBinDense] > 0 && dense_cfg() == 1;
+  const int wstride = npc * (512 / 32);  // panels x warps of the 2-CTA kernel (= the heavy kernel's)
+  DBuf<int32_t> wchunks(c, warp_emit ? (size_t)hcounts[kBinDense] * wstride * 2 : 1);
   DBuf<int64_t> rowstart, chunks;
   DBuf<unsigned long long> bump(c, 1);
   if (cap > 0 && !slotted) {
@@ -503,6 +511,10 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
     first.vals = sc_vals.p;
     if (slotted) {
       first.off = off.p;
+      if (warp_emit) {
+        first.wchunks = wchunks.p;
+        first.wstride = wstride;
+      }
     } else {
       first.bump = bump.p;
       first.cap = cap;
@@ -527,12 +539,19 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
   out->vals = dalloc<V>(c, (size_t)nnz);
   if (fits) {
     constexpr bool kWords = sizeof(V) % 4 == 0;
-    const bool long_rows = kWords && slotted && nd > 0;  // dense rows: CTA per row, 16-byte copies
+    const bool long_rows = kWords && slotted && nd > 0 && !warp_emit;  // dense rows: CTA per row, 16-byte copies
     compact_rows_kernel<V><<<grid_for(c, m, 8), 256, 0, c->stream>>>(
-        m, long_rows ? bins.p : nullptr, slotted ? off.p : rowstart.p, out->ptr, sc_cols.p, sc_vals.p, out->idx,
-        static_cast<V*>(out->vals));
+        m, (long_rows || warp_emit) ? bins.p : nullptr, slotted ? off.p : rowstart.p, out->ptr, sc_cols.p, sc_vals.p,
+        out->idx, static_cast<V*>(out->vals));
     SPG_LAUNCH_CHECK();
     ++c->launches;
+    if (warp_emit) {
+      compact_wchunks_kernel<V, 256><<<grid_for(c, nd, 1, 8), 256, 0, c->stream>>>(
+          dense_rows, nd, wchunks.p, wstride, off.p, out->ptr, sc_cols.p, sc_vals.p, out->idx,
+          static_cast<V*>(out->vals));
+      SPG_LAUNCH_CHECK();
+      ++c->launches;
+    }
     if constexpr (kWords) {
       if (long_rows) {
         compact_long_rows_kernel<V><<<grid_for(c, nd, 1, 8), 256, 0, c->stream>>>(
