@@ -459,9 +459,14 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
     SPG_CUDA(cudaMemsetAsync(work.p, 0, 2 * sizeof(unsigned long long), c->stream));
     const int64_t* lb = lists.p;
     StreamFork fk(c, 3);
+    static const int plan = [] {  // SPG_STREAM_PLAN (default 1): heavy rows and rank panels on their own streams
+      const char* e = std::getenv("SPG_STREAM_PLAN");
+      return e ? std::atoi(e) : 1;
+    }();
     if (nh > 0) {
       constexpr int PW = Geom<V>::kPanelW;
-      launch_dense_cfg<PW, 1024, SR, Src>(c, fk[0], src_heavy, dense_rows, nh, ncols_out, 220 * 1024, work.p + 1, o);
+      launch_dense_cfg<PW, 1024, SR, Src>(c, plan == 1 ? fk[1] : fk[0], src_heavy, dense_rows, nh, ncols_out,
+                                          220 * 1024, work.p + 1, o);
     }
     if (nd > nh) {
       RowOut<V> rest = o;
@@ -491,7 +496,8 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
       auto kern = rankpanel_rows_kernel<SR, Src, kRpThreads, kRpN, kBitRankW>;
       set_smem(kern, rp_smem);
       kern<<<resident_grid(c, kern, kRpThreads, rp_smem, (int64_t)hcounts[kBinRankPanels]), kRpThreads, rp_smem,
-             fk[0]>>>(src, lb + base[kBinRankPanels], (int64_t)hcounts[kBinRankPanels], kRpSegs, colmin.p, o);
+             plan == 1 ? fk[2] : fk[0]>>>(src, lb + base[kBinRankPanels], (int64_t)hcounts[kBinRankPanels], kRpSegs,
+                                          colmin.p, o);
       SPG_LAUNCH_CHECK();
       ++c->launches;
     }
