@@ -140,6 +140,16 @@ void comm_abort(spg_comm* c, const std::string& why) {
 }
 
 void comm_barrier(spg_comm* c) { barrier_wait(c, c->hdr->world_bar, c->world); }
+
+void comm_bcast_wait(spg_comm* c, cudaStream_t stream) {
+  SPG_CUDA(cudaStreamSynchronize(stream));
+  for (ncclComm_t comm : {c->row_comm, c->col_comm}) {
+    if (!comm) continue;
+    ncclResult_t async_err = ncclSuccess;
+    nccl_check(ncclCommGetAsyncError(comm, &async_err), "ncclCommGetAsyncError");
+    nccl_check(async_err, "ncclBroadcast (async)");
+  }
+}
 int comm_world_rank(const spg_comm* c) { return c->rank; }
 int comm_world_size(const spg_comm* c) { return c->world; }
 
@@ -188,7 +198,7 @@ void comm_exchange_sizes(spg_comm* c, int scope, int root, int64_t triple[3]) {
 }
 
 int comm_bcast(spg_comm* c, int scope, int root, void* buf, uint64_t bytes, int mode, uint64_t threshold,
-               cudaStream_t stream, bool device_buffer) {
+               cudaStream_t stream, bool device_buffer, bool wait) {
   const int n = comm_scope_size(c, scope);
   if (root < 0 || root >= n)
     fail(SPG_ERR_PROTOCOL, "broadcast root " + std::to_string(root) + " is outside the scope");
@@ -212,10 +222,12 @@ int comm_bcast(spg_comm* c, int scope, int root, void* buf, uint64_t bytes, int 
   if (path == SPG_PATH_DEVICE) {
     ncclComm_t comm = scope == SPG_SCOPE_ROW ? c->row_comm : c->col_comm;
     nccl_check(ncclBroadcast(buf, buf, bytes, ncclUint8, root, comm, stream), "ncclBroadcast");
-    SPG_CUDA(cudaStreamSynchronize(stream));
-    ncclResult_t async_err = ncclSuccess;
-    nccl_check(ncclCommGetAsyncError(comm, &async_err), "ncclCommGetAsyncError");
-    nccl_check(async_err, "ncclBroadcast (async)");
+    if (wait) {
+      SPG_CUDA(cudaStreamSynchronize(stream));
+      ncclResult_t async_err = ncclSuccess;
+      nccl_check(ncclCommGetAsyncError(comm, &async_err), "ncclCommGetAsyncError");
+      nccl_check(async_err, "ncclBroadcast (async)");
+    }
   } else {
     // Root D2H into pinned shm staging, receivers H2D; two half-slots
     // pipeline consecutive chunks (root fills chunk i+1 while peers drain i).

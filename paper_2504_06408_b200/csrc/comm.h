@@ -46,7 +46,9 @@ int comm_pc(const spg_comm* c);
 void comm_exchange_sizes(spg_comm* c, int scope, int root, int64_t triple[3]);
 // returns SPG_PATH_*; `stream` orders the transfer after prior device work
 int comm_bcast(spg_comm* c, int scope, int root, void* buf, uint64_t bytes, int mode, uint64_t threshold,
-               cudaStream_t stream, bool device_buffer);
+               cudaStream_t stream, bool device_buffer, bool wait = true);
+// after device broadcasts issued with wait = false: drain the stream, check NCCL errors
+void comm_bcast_wait(spg_comm* c, cudaStream_t stream);
 void comm_barrier(spg_comm* c);
 int comm_world_rank(const spg_comm* c);
 int comm_world_size(const spg_comm* c);

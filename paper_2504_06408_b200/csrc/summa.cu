@@ -76,6 +76,51 @@ void pack_cols(spg_ctx* c, const spg_dcsr& m, int64_t b, int64_t e, int vs, Pane
 }
 
 // broadcast_panel (summa.hpp:212-235): size triple always, payload if nnz > 0.
+// Root side of broadcast_panel: slice + pack (done for all stages up front in
+// fused mode, so its host syncs never wait behind in-flight broadcasts).
+void pack_panel(spg_ctx* c, spg_comm* comm, int scope, int root, bool by_rows, const spg_dcsr& prepared, int64_t b,
+                int64_t e, int vs, Panel& p) {
+  if (comm_scope_index(comm, scope) != root) return;
+  if (by_rows) pack_rows(c, prepared, b, e, vs, p);
+  else pack_cols(c, prepared, b, e, vs, p);
+}
+
+// Size triple + payload of an already packed panel (wait = false: device
+// broadcasts stay in flight; the caller drains them once).
+void send_panel(spg_ctx* c, spg_comm* comm, int scope, int root, int vs, const spg_summa_opts& o, Panel& p,
+                spg_ledger& led, bool wait) {
+  const bool me = comm_scope_index(comm, scope) == root;
+  int64_t triple[3] = {0, 0, 0};
+  if (me) {
+    triple[0] = p.view.nrows;
+    triple[1] = p.view.ncols;
+    triple[2] = p.view.nnz;
+  }
+  const auto t0 = Clock::now();
+  comm_exchange_sizes(comm, scope, root, triple);
+  ++led.size_exchanges;
+  if (triple[2] == 0) {
+    led.ms[1] += ms_since(t0);
+    return;  // summa.hpp:226: empty panels are not broadcast
+  }
+  p.present = true;
+  if (!me) {
+    p.bytes = panel_bytes(triple[0], triple[2], vs);
+    p.buf = DBuf<char>(c, p.bytes);
+    p.view = panel_view(p.buf.p, triple[0], triple[1], triple[2]);
+  }
+  const uint64_t thr = (scope == SPG_SCOPE_COL && o.threshold_col) ? o.threshold_col : o.threshold;
+  const int path = comm_bcast(comm, scope, root, p.buf.p, p.bytes, o.comm_mode, thr, c->stream, true, wait);
+  if (path == SPG_PATH_HOST) {
+    ++led.host_bcasts;
+    led.bytes_host_path += p.bytes;
+  } else {
+    ++led.device_bcasts;
+    led.bytes_device_path += p.bytes;
+  }
+  led.ms[1] += ms_since(t0);
+}
+
 void broadcast_panel(spg_ctx* c, spg_comm* comm, int scope, int root, bool by_rows, const spg_dcsr& prepared,
                      int64_t b, int64_t e, int vs, const spg_summa_opts& o, Panel& p, spg_ledger& led) {
   const bool me = comm_scope_index(comm, scope) == root;
@@ -199,7 +244,45 @@ extern "C" int spg_summa25_multiply(spg_comm* comm, spg_ctx* c, int sr, int64_t 
     };
     const int64_t block_rows = are - arb, block_cols = bce - bcb;
     try {
-      for (int r = 0; r < rounds; ++r) {
+      if (opts->fuse_stages) {
+        // Fused: pack every panel this rank roots first, then exchange sizes and
+        // issue all broadcasts back to back (device ones stay in flight), then
+        // drain once — the per-stage host syncs no longer serialise them.
+        struct Pending {
+          int s, r;
+          int64_t rows;
+          Panel a, b;
+        };
+        std::vector<Pending> pend;
+        for (int r = 0; r < rounds; ++r)
+          for (int s = 0; s < ns; ++s) {
+            const spg_stage& st = stages[s];
+            int64_t hb, he;
+            spg_round_range(st.hi - st.lo, rounds, r, &hb, &he);
+            pend.push_back({s, r, he - hb, Panel{}, Panel{}});
+            Pending& q = pend.back();
+            pack_panel(c, comm, SPG_SCOPE_ROW, st.a_col_block, true, pa, st.a_off + hb, st.a_off + he, vs, q.a);
+            pack_panel(c, comm, SPG_SCOPE_COL, st.b_row_block, false, pb, st.b_off + hb, st.b_off + he, vs, q.b);
+          }
+        for (auto& q : pend) {
+          const spg_stage& st = stages[q.s];
+          send_panel(c, comm, SPG_SCOPE_ROW, st.a_col_block, vs, *opts, q.a, led, false);
+          send_panel(c, comm, SPG_SCOPE_COL, st.b_row_block, vs, *opts, q.b, led, false);
+        }
+        {
+          const auto t0 = Clock::now();
+          comm_bcast_wait(comm, c->stream);
+          led.ms[1] += ms_since(t0);
+        }
+        uint64_t total = 0;
+        for (auto& q : pend) {
+          total += (q.a.present ? q.a.bytes : 0) + (q.b.present ? q.b.bytes : 0);
+          if (!(q.a.present && q.b.present)) ++led.skipped_stages;
+          kept.push_back({q.s, q.r, std::move(q.a), std::move(q.b), q.rows, block_cols});
+        }
+        if (total > led.peak_bcast_buffer_bytes) led.peak_bcast_buffer_bytes = total;
+      }
+      for (int r = 0; r < (opts->fuse_stages ? 0 : rounds); ++r) {
         for (int s = 0; s < ns; ++s) {
           const spg_stage& st = stages[s];
           int64_t hb, he;
