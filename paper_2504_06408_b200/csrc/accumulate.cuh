@@ -1399,9 +1399,10 @@ __global__ void __launch_bounds__(THREADS) bitrank_rows_kernel(Src src, const in
   uint32_t* bm = reinterpret_cast<uint32_t*>(acc + NMAX);                // [WMAX] presence
   uint32_t* sm = bm + WMAX;                                              // [SW] non-empty words
   uint16_t* wrank = reinterpret_cast<uint16_t*>(sm + SW);                // [WMAX] rank of a word's first entry
-  uint16_t* list = wrank + WMAX;                                         // [NMAX] non-empty words in order
+  constexpr int LMAX = NMAX < WMAX ? NMAX : WMAX;                        // non-empty words <= both
+  uint16_t* list = wrank + WMAX;                                         // [LMAX] non-empty words in order
   SegCache<SR, Src> cache;
-  cache.carve(reinterpret_cast<unsigned char*>(list + ((NMAX + 7) & ~7)), cap, 1);
+  cache.carve(reinterpret_cast<unsigned char*>(list + ((LMAX + 7) & ~7)), cap, 1);
   __shared__ typename Scan::TempStorage scan_tmp;
   __shared__ long long s_base;
   __shared__ int s_nw;

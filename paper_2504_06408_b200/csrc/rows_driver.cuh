@@ -261,9 +261,18 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
   }();
   constexpr int kBitRankN = SPG_BITRANK_N > 0 ? SPG_BITRANK_N : (sizeof(V) <= 4 ? 8192 : 4096);
   constexpr int kBitRankW = 8192, kBitRankSegs = 256, kBitRankThreads = 512;
-  const size_t br_smem = sizeof(V) * kBitRankN + sizeof(uint32_t) * (kBitRankW + kBitRankW / 32) +
+  // narrow outputs (<= 131072 columns, e.g. SUMMA blocks): a half-size window fits 3 CTAs per SM
+  constexpr int kBitRankW2 = 4096;
+  const bool br_narrow = ncols_out <= 32 * (int64_t)kBitRankW2;
+  auto br_bytes = [&](int w) {
+    return sizeof(V) * kBitRankN + sizeof(uint32_t) * (w + w / 32) +
+           sizeof(uint16_t) * (w + ((std::min(kBitRankN, w) + 7) & ~7)) +
+           (size_t)kBitRankSegs * SegCache<SR, Src>::bytes_per_seg(1) + 64;
+  };
+  const size_t br_smem_wide = sizeof(V) * kBitRankN + sizeof(uint32_t) * (kBitRankW + kBitRankW / 32) +
                          sizeof(uint16_t) * (kBitRankW + ((kBitRankN + 7) & ~7)) +
                          (size_t)kBitRankSegs * SegCache<SR, Src>::bytes_per_seg(1) + 64;
+  const size_t br_smem = br_narrow ? br_bytes(kBitRankW2) : br_smem_wide;
   const bool bitrank = bitrank_on && !AddCanCancel<SR>::value && br_smem <= 220 * 1024;
   // rank-panel bin (bin 9): longer rows in the same window, accumulator panels in rank space
   static const int rankpanel_on = [] {
@@ -281,7 +290,7 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
   }();
   DBuf<int32_t> colmin(c, bitrank ? (size_t)m : 1);
   analyse_rows_kernel<SR, Src><<<grid_for(c, m, 8), 256, 0, c->stream>>>(
-      src, ncols_out, dense_min, bitrank ? kBitRankN : 0, kBitRankSegs, 32 * (int64_t)kBitRankW,
+      src, ncols_out, dense_min, bitrank ? kBitRankN : 0, kBitRankSegs, 32 * (int64_t)kBitRankW,  // window (both)
       rankpanel ? kRpSegs : 0, rp_maxf, colmin.p, prods.p, ub.p, bins.p);
   SPG_LAUNCH_CHECK();
   ++c->launches;
@@ -485,10 +494,17 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
     if (hcounts[kBinEsc512] > 0)
       launch_esc<SR, Src, 128, 4>(c, fk[2], src, lb + base[kBinEsc512], hcounts[kBinEsc512], end_bit, o);
     if (hcounts[kBinBitRank] > 0) {
-      auto kern = bitrank_rows_kernel<SR, Src, kBitRankThreads, kBitRankN, kBitRankW>;
-      set_smem(kern, br_smem);
-      kern<<<resident_grid(c, kern, kBitRankThreads, br_smem, (int64_t)hcounts[kBinBitRank]), kBitRankThreads, br_smem,
-             fk[1]>>>(src, lb + base[kBinBitRank], (int64_t)hcounts[kBinBitRank], kBitRankSegs, colmin.p, o);
+      if (br_narrow) {  // ncols <= 32*W2: every window fits the half-size bitmap
+        auto kern = bitrank_rows_kernel<SR, Src, kBitRankThreads, kBitRankN, kBitRankW2>;
+        set_smem(kern, br_smem);
+        kern<<<resident_grid(c, kern, kBitRankThreads, br_smem, (int64_t)hcounts[kBinBitRank]), kBitRankThreads,
+               br_smem, fk[1]>>>(src, lb + base[kBinBitRank], (int64_t)hcounts[kBinBitRank], kBitRankSegs, colmin.p, o);
+      } else {
+        auto kern = bitrank_rows_kernel<SR, Src, kBitRankThreads, kBitRankN, kBitRankW>;
+        set_smem(kern, br_smem);
+        kern<<<resident_grid(c, kern, kBitRankThreads, br_smem, (int64_t)hcounts[kBinBitRank]), kBitRankThreads,
+               br_smem, fk[1]>>>(src, lb + base[kBinBitRank], (int64_t)hcounts[kBinBitRank], kBitRankSegs, colmin.p, o);
+      }
       SPG_LAUNCH_CHECK();
       ++c->launches;
     }
