@@ -261,9 +261,9 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
   }();
   constexpr int kBitRankN = SPG_BITRANK_N > 0 ? SPG_BITRANK_N : (sizeof(V) <= 4 ? 8192 : 4096);
   constexpr int kBitRankW = 8192, kBitRankSegs = 256, kBitRankThreads = 512;
-  // narrow outputs (<= 131072 columns, e.g. SUMMA blocks): a half-size window fits 3 CTAs per SM
+  // narrow outputs (<= 131072 columns): a half-size window when the full one would leave a single CTA per
+  // SM (wide values; measured 8.1 -> 7.4 ms on ER max-times, no gain for 4-byte values at 2 CTAs/SM)
   constexpr int kBitRankW2 = 4096;
-  const bool br_narrow = ncols_out <= 32 * (int64_t)kBitRankW2;
   auto br_bytes = [&](int w) {
     return sizeof(V) * kBitRankN + sizeof(uint32_t) * (w + w / 32) +
            sizeof(uint16_t) * (w + ((std::min(kBitRankN, w) + 7) & ~7)) +
@@ -272,6 +272,7 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
   const size_t br_smem_wide = sizeof(V) * kBitRankN + sizeof(uint32_t) * (kBitRankW + kBitRankW / 32) +
                          sizeof(uint16_t) * (kBitRankW + ((kBitRankN + 7) & ~7)) +
                          (size_t)kBitRankSegs * SegCache<SR, Src>::bytes_per_seg(1) + 64;
+  const bool br_narrow = ncols_out <= 32 * (int64_t)kBitRankW2 && br_smem_wide > 110 * 1024;
   const size_t br_smem = br_narrow ? br_bytes(kBitRankW2) : br_smem_wide;
   const bool bitrank = bitrank_on && !AddCanCancel<SR>::value && br_smem <= 220 * 1024;
   // rank-panel bin (bin 9): longer rows in the same window, accumulator panels in rank space
