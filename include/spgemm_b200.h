@@ -60,7 +60,8 @@ enum {
   SPG_ERR_CUDA = 10,                 /* CUDA runtime failure */
   SPG_ERR_OOM = 11,                  /* device or host allocation failure */
   SPG_ERR_NCCL = 12,                 /* NCCL failure (surfaces as ProtocolError) */
-  SPG_ERR_ARG = 13                   /* invalid argument (null pointer, bad id) */
+  SPG_ERR_ARG = 13,                  /* invalid argument (null pointer, bad id) */
+  SPG_ERR_UNSUPPORTED_FORMAT = 14    /* UnsupportedFormatError */
 };
 
 /* communication paths / modes (comm.hpp:14-55) */
@@ -208,6 +209,13 @@ SPG_API int spg_generate_er_block(int sr, int64_t n, int d, uint64_t seed, int v
 SPG_API int spg_generate_stencil27_block(int sr, int64_t N, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
                                          int64_t* nrows, int64_t* nnz, int64_t** rows, int64_t** cols,
                                          void** vals);
+/* read_matrix_market<SR>(path) (matrix_market.hpp:43-141): ASCII coordinate
+ * file (real / integer / pattern, general / symmetric) -> normalised COO
+ * (normalize_coo, formats.hpp:105-133).  MalformedInputError "path:line: what"
+ * for structural errors, UnsupportedFormatError for other headers.  Host
+ * arrays freed with spg_free. */
+SPG_API int spg_read_matrix_market(int sr, const char* path, int64_t* nrows, int64_t* ncols, int64_t* nnz,
+                                   int64_t** rows, int64_t** cols, void** vals);
 /* normalised COO (row-major, unique) -> CSR / CSC host arrays, no copies of
  * the reference's fold semantics needed (input already unique). */
 SPG_API int spg_coo_to_csr(int sr, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rows,

@@ -65,12 +65,20 @@ inline void throw_status(int st, const char* msg) {
     case SPG_ERR_UNSUPPORTED_SEMIRING: throw UnsupportedSemiringError(m);
     case SPG_ERR_PROTOCOL: case SPG_ERR_NCCL: throw ProtocolError(m);
     case SPG_ERR_MALFORMED: throw MalformedInputError(m);
+    case SPG_ERR_UNSUPPORTED_FORMAT: throw UnsupportedFormatError(m);
     case SPG_ERR_INVALID_RANGE: throw InvalidRangeError(m);
     case SPG_ERR_INTERNAL: throw InternalError(m);
     case SPG_ERR_ABORTED: throw AbortedError(m);
     case SPG_ERR_DEADLOCK: throw DeadlockError(m);
     default: throw DeviceError(m);
   }
+}
+
+// Throws for a failed C-ABI status, reading the message only AFTER the call
+// returned (the message pointer is invalidated by the call that sets it, so
+// it must not be an argument evaluated alongside that call).
+inline void throw_last(int st) {
+  if (st != SPG_OK) throw_status(st, spg_last_error(nullptr));
 }
 
 // -------------------------------------------------------------- semirings
@@ -152,7 +160,7 @@ inline void take_idx(std::vector<index_t>& dst, index_t* src, index_t n) {
 // ------------------------------------------------------------------ context
 class Context {
  public:
-  explicit Context(int device = 0) { throw_status(spg_ctx_create(device, &c_), spg_last_error(nullptr)); }
+  explicit Context(int device = 0) { throw_last(spg_ctx_create(device, &c_)); }
   ~Context() { spg_ctx_destroy(c_); }
   Context(const Context&) = delete;
   Context& operator=(const Context&) = delete;
@@ -241,10 +249,28 @@ CooMatrix<SR> generate_rmat(int scale, double edge_factor, std::uint64_t seed) {
   int64_t n = 0, nnz = 0;
   int64_t *rows = nullptr, *cols = nullptr;
   void* vals = nullptr;
-  throw_status(spg_generate_rmat(SR::id, scale, edge_factor, seed, &n, &nnz, &rows, &cols, &vals),
-               spg_last_error(nullptr));
+  throw_last(spg_generate_rmat(SR::id, scale, edge_factor, seed, &n, &nnz, &rows, &cols, &vals));
   CooMatrix<SR> out;
   out.nrows = out.ncols = n;
+  out.tuples.resize((size_t)nnz);
+  const auto* v = static_cast<const typename SR::value_type*>(vals);
+  for (int64_t k = 0; k < nnz; ++k) out.tuples[k] = {rows[k], cols[k], v[k]};
+  spg_free(rows);
+  spg_free(cols);
+  spg_free(vals);
+  return out;
+}
+
+// read_matrix_market<SR>(path) (matrix_market.hpp:43-141): normalised COO.
+template <class SR>
+CooMatrix<SR> read_matrix_market(const std::string& path) {
+  int64_t m = 0, n = 0, nnz = 0;
+  int64_t *rows = nullptr, *cols = nullptr;
+  void* vals = nullptr;
+  throw_last(spg_read_matrix_market(SR::id, path.c_str(), &m, &n, &nnz, &rows, &cols, &vals));
+  CooMatrix<SR> out;
+  out.nrows = m;
+  out.ncols = n;
   out.tuples.resize((size_t)nnz);
   const auto* v = static_cast<const typename SR::value_type*>(vals);
   for (int64_t k = 0; k < nnz; ++k) out.tuples[k] = {rows[k], cols[k], v[k]};
@@ -260,8 +286,8 @@ class Comm {
  public:
   Comm(const std::string& job, int world, int rank, int pr, int pc, int device,
        std::uint64_t staging_bytes = 64ull << 20) {
-    throw_status(spg_comm_create(job.c_str(), world, rank, pr, pc, device, staging_bytes, &c_),
-                 spg_comm_last_error(nullptr));
+    const int st = spg_comm_create(job.c_str(), world, rank, pr, pc, device, staging_bytes, &c_);
+    if (st != SPG_OK) throw_status(st, spg_comm_last_error(nullptr));
   }
   ~Comm() { spg_comm_destroy(c_); }
   Comm(const Comm&) = delete;

@@ -28,6 +28,7 @@
 #include "spsumma/dist_matrix.hpp"
 #include "spsumma/formats.hpp"
 #include "spsumma/local_spgemm.hpp"
+#include "spsumma/matrix_market.hpp"
 #include "spsumma/rmat.hpp"
 #include "spsumma/semiring.hpp"
 #include "spsumma/serialize.hpp"
@@ -163,6 +164,9 @@ int guarded(F&& f) {
   } catch (const InternalError& e) {
     g_err = e.what();
     return 7;
+  } catch (const UnsupportedFormatError& e) {
+    g_err = e.what();
+    return 14;
   } catch (const std::exception& e) {
     g_err = e.what();
     return 9;
@@ -304,6 +308,17 @@ int ref_generate_rmat(int sr, int scale, double edge_factor, uint64_t seed, ref_
     return with_ref_sr(sr, [&](auto t) {
       using SR = typename decltype(t)::type;
       from_coo(generate_rmat<SR>(scale, edge_factor, seed), out);
+      return 0;
+    });
+  });
+}
+
+// read_matrix_market<SR>(path), matrix_market.hpp:43-141.
+int ref_read_matrix_market(int sr, const char* path, ref_coo* out) {
+  return guarded([&] {
+    return with_ref_sr(sr, [&](auto t) {
+      using SR = typename decltype(t)::type;
+      from_coo(read_matrix_market<SR>(path), out);
       return 0;
     });
   });

@@ -117,6 +117,8 @@ _SIGS = [
                                         C.c_int64, C.c_int64, _i64p, _P(_i64p), _P(_i64p), _P(C.c_void_p)]),
     ("spg_generate_stencil27_block", C.c_int, [C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                                                _i64p, _i64p, _P(_i64p), _P(_i64p), _P(C.c_void_p)]),
+    ("spg_read_matrix_market", C.c_int, [C.c_int, C.c_char_p, _i64p, _i64p, _i64p, _P(_i64p), _P(_i64p),
+                                         _P(C.c_void_p)]),
     ("spg_host_alloc", C.c_void_p, [C.c_uint64]),
     ("spg_coo_to_csr", C.c_int, [C.c_int, C.c_int64, C.c_int64, C.c_int64, _i64p, _i64p, C.c_void_p,
                                  C.c_int, _P(HCsr)]),

@@ -29,6 +29,7 @@ void gen_rmat(int, int, double, uint64_t, int64_t*, int64_t*, int64_t**, int64_t
 void gen_er(int, int64_t, int, uint64_t, int, int64_t, int64_t, int64_t, int64_t, int64_t*, int64_t**, int64_t**,
             void**);
 void gen_stencil27(int, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t*, int64_t*, int64_t**, int64_t**, void**);
+void read_matrix_market(int, const char*, int64_t*, int64_t*, int64_t*, int64_t**, int64_t**, void**);
 
 thread_local std::string g_last_error;
 
@@ -716,6 +717,14 @@ int spg_generate_stencil27_block(int sr, int64_t N, int64_t r0, int64_t r1, int6
   return guarded(nullptr, [&] {
     need(nrows && nnz && rows && cols && vals, "null argument");
     gen_stencil27(sr, N, r0, r1, c0, c1, nrows, nnz, rows, cols, vals);
+  });
+}
+
+int spg_read_matrix_market(int sr, const char* path, int64_t* nrows, int64_t* ncols, int64_t* nnz, int64_t** rows,
+                           int64_t** cols, void** vals) {
+  return guarded(nullptr, [&] {
+    need(path && nrows && ncols && nnz && rows && cols && vals, "null argument");
+    read_matrix_market(sr, path, nrows, ncols, nnz, rows, cols, vals);
   });
 }
 

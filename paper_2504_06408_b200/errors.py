@@ -61,7 +61,7 @@ _BY_STATUS = {
     1: ShapeError, 2: GridError, 3: UnsupportedSemiringError, 4: ProtocolError,
     5: MalformedInputError, 6: InvalidRangeError, 7: InternalError, 8: AbortedError,
     9: DeadlockError, 10: CudaError, 11: OutOfMemoryError, 12: ProtocolError,
-    13: ValueError,
+    13: ValueError, 14: UnsupportedFormatError,
 }
 
 

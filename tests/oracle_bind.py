@@ -53,6 +53,7 @@ if ref is not None:
     ref.ref_last_error.restype = C.c_char_p
     ref.ref_free.argtypes = [C.c_void_p]
     ref.ref_generate_rmat.argtypes = [C.c_int, C.c_int, C.c_double, C.c_uint64, _P(Coo)]
+    ref.ref_read_matrix_market.argtypes = [C.c_int, C.c_char_p, _P(Coo)]
     ref.ref_random_coo.argtypes = [C.c_int, C.c_uint64, C.c_int64, C.c_int64, C.c_double, C.c_int, _P(Coo)]
     ref.ref_esc_multiply.argtypes = [C.c_int, _P(Csr), _P(Csr), C.c_uint64, _P(Csr)]
     ref.ref_naive_multiply.argtypes = [C.c_int, _P(Csr), _P(Csr), _P(Csr)]
@@ -183,6 +184,15 @@ def ref_generate_rmat(sr, scale, ef, seed):
     out = Coo()
     _ok(ref.ref_generate_rmat(sr, scale, ef, seed, C.byref(out)))
     return _take_coo(sr, out)
+
+
+def ref_read_matrix_market(sr, path):
+    """(status, message, (nrows, ncols, rows, cols, vals) or None)."""
+    out = Coo()
+    rc = ref.ref_read_matrix_market(sr, os.fsencode(path), C.byref(out))
+    if rc != 0:
+        return rc, ref.ref_last_error().decode(), None
+    return 0, "", _take_coo(sr, out)
 
 
 def ref_random_coo(sr, seed, nrows, ncols, density, exact=True):

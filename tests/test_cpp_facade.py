@@ -13,14 +13,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BIN = os.path.join(ROOT, "build", "facade_main")
 
 
-def build_facade():
-    os.makedirs(os.path.dirname(BIN), exist_ok=True)
+def build_facade(src="facade_main.cpp", exe=BIN):
+    os.makedirs(os.path.dirname(exe), exist_ok=True)
     lib_dir = os.path.join(ROOT, "paper_2504_06408_b200")
     cmd = ["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"),
-           os.path.join(ROOT, "tests", "cpp", "facade_main.cpp"), "-o", BIN, "-L", lib_dir, "-lspgemm_b200",
+           os.path.join(ROOT, "tests", "cpp", src), "-o", exe, "-L", lib_dir, "-lspgemm_b200",
            f"-Wl,-rpath,{lib_dir}"]
     subprocess.run(cmd, check=True, capture_output=True, text=True)
-    return BIN
+    return exe
 
 
 def test_facade_compiles_and_links():
@@ -40,3 +40,20 @@ def test_facade_matches_oracle():
     assert int(kv["checksum"]) == ob.orc_checksum(want)
     assert int(kv["merge_nnz"]) == want.nnz
     assert kv["shape_error"] == "1"
+
+
+def test_facade_read_matrix_market(tmp_path):
+    """read_matrix_market<SR> through the C++ facade (no GPU): tuples and the
+    exception classes of matrix_market.hpp."""
+    exe = build_facade("facade_mm.cpp", os.path.join(ROOT, "build", "facade_mm"))
+    good = tmp_path / "g.mtx"
+    good.write_text("%%MatrixMarket matrix coordinate real symmetric\n3 3 3\n1 1 2.5\n3 1 -1\n3 1 4\n")
+    out = subprocess.run([exe, str(good)], check=True, capture_output=True, text=True).stdout.split("\n")
+    assert out[:4] == ["3 3 3", "0 0 2.5", "0 2 3", "2 0 3"]
+    bad = tmp_path / "b.mtx"
+    bad.write_text("%%MatrixMarket matrix array real general\n1 1\n1\n")
+    out = subprocess.run([exe, str(bad)], check=True, capture_output=True, text=True).stdout
+    assert out.startswith("error UnsupportedFormatError ") and "unsupported format 'array'" in out
+    bad.write_text("%%MatrixMarket matrix coordinate real general\n3 3 2\n1 1 1\n")
+    out = subprocess.run([exe, str(bad)], check=True, capture_output=True, text=True).stdout
+    assert out.strip() == f"error MalformedInputError {bad}:3: file ends after 1 of 2 entries"
