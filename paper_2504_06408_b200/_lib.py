@@ -152,6 +152,13 @@ def _load():
         raise ImportError(
             f"{LIB_PATH} is missing: build it with `make -j` (or __graft_entry__.build()); "
             "there is no CPU fallback for the SpGEMM path")
+    # torch first: its bundled libnccl.so.2 then satisfies this library's
+    # NCCL dependency (loading the system NCCL first would leave torch's CUDA
+    # library with unresolved newer NCCL symbols when it is imported later)
+    try:
+        import torch  # noqa: F401
+    except ImportError:
+        pass
     lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
     for name, res, args in _SIGS:
         try:
