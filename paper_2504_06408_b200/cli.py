@@ -256,10 +256,11 @@ def cmd_multiply(args) -> int:
         raise errors.ShapeError(f"multiply squares its input; got {a.nrows}x{a.ncols}")
     i, j = job.rank // job.pc, job.rank % job.pc
     blk = local_block(a, job.pr, job.pc, i, j)
-    _run(job, a, blk, mode, thr, thr_col)  # warm-up, excluded from the report
+    _run(job, a, blk, mode, thr, thr_col)  # warm-up, excluded from the report (its C is released)
     its = []
     c = None
     for _ in range(args.iters):
+        c = None  # release the previous C first: its memory is reused, not mapped afresh
         c, led = _run(job, a, blk, mode, thr, thr_col)
         its.append(led)
     full = gather(job.comm, job.ctx, c, blk.rows, blk.cols, a.nrows, a.ncols, root=0)
