@@ -1996,6 +1996,9 @@ __global__ void __launch_bounds__(256) compact_long_rows_kernel(const int64_t* _
   }
 }
 
+#ifndef SPG_ROWS_VEC
+#define SPG_ROWS_VEC 512  // rows with at least this many entries copy with 16-byte accesses (0: never)
+#endif
 // Other rows: row i sits at off[i] of the scratch (off[i] < 0: skip; rows
 // whose bin is dense are skipped when `skip` is given).
 template <class V>
@@ -2015,6 +2018,15 @@ __global__ void __launch_bounds__(256) compact_rows_kernel(int64_t nrows, const 
     const int64_t s = off[i];
     if (s < 0) continue;
     if (skip && skip[i] == kBinDense) continue;  // copied by compact_long_rows_kernel
+    if constexpr (SPG_ROWS_VEC > 0 && sizeof(V) % 4 == 0) {
+      if (n >= SPG_ROWS_VEC) {  // long row: 16-byte loads and stores
+        constexpr int WPE = (int)(sizeof(V) / 4);
+        copy_words(reinterpret_cast<uint32_t*>(cols), d, reinterpret_cast<const uint32_t*>(sc_cols), s, n, lane, 32);
+        copy_words(reinterpret_cast<uint32_t*>(vals), d * WPE, reinterpret_cast<const uint32_t*>(sc_vals), s * WPE,
+                   n * WPE, lane, 32);
+        continue;
+      }
+    }
     int64_t e = lane;
     for (; e + 96 < n; e += 128) {
       const int32_t c0 = sc_cols[s + e], c1 = sc_cols[s + e + 32], c2 = sc_cols[s + e + 64],
