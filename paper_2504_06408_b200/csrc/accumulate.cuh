@@ -1837,8 +1837,11 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
 // and counts staged in smem with it), then each warp copies two chunks per
 // step with both chunks' loads in flight before the stores (coalesced within
 // a chunk; chunks average ~150 entries).
+#ifndef SPG_COMPACT_MINB
+#define SPG_COMPACT_MINB 4  // min resident CTAs/SM for the compaction kernels, values <= 4 B (64 regs; 1 -> 4 saves 0.3 ms, 6 spills; wider values spill)
+#endif
 template <class V, int THREADS>
-__global__ void __launch_bounds__(THREADS) compact_wchunks_kernel(const int64_t* __restrict__ rows, int64_t nrows_bin,
+__global__ void __launch_bounds__(THREADS, sizeof(V) <= 4 ? SPG_COMPACT_MINB : 1) compact_wchunks_kernel(const int64_t* __restrict__ rows, int64_t nrows_bin,
                                                                   const int32_t* __restrict__ wchunks, int wstride,
                                                                   const int64_t* __restrict__ off,
                                                                   const int64_t* __restrict__ rowptr,
@@ -2002,7 +2005,7 @@ __global__ void __launch_bounds__(256) compact_long_rows_kernel(const int64_t* _
 // Other rows: row i sits at off[i] of the scratch (off[i] < 0: skip; rows
 // whose bin is dense are skipped when `skip` is given).
 template <class V>
-__global__ void __launch_bounds__(256) compact_rows_kernel(int64_t nrows, const uint8_t* __restrict__ skip,
+__global__ void __launch_bounds__(256, sizeof(V) <= 4 ? SPG_COMPACT_MINB : 1) compact_rows_kernel(int64_t nrows, const uint8_t* __restrict__ skip,
                                                            const int64_t* __restrict__ off,
                                                            const int64_t* __restrict__ rowptr,
                                                            const int32_t* __restrict__ sc_cols,
