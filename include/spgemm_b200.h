@@ -104,16 +104,18 @@ typedef struct {
 typedef struct {
   int64_t products;        /* F: intermediate products (flops = 2F) */
   int64_t nnz_out;
-  int64_t rows_per_bin[10]; /* 0 empty, 1 warp-ESC, 2 block-ESC, 3/4/5 hash 4K/8K/2K, 6 dense panels,
+  int64_t rows_per_bin[11]; /* 0 empty, 1 warp-ESC, 2 block-ESC, 3/4/5 hash 4K/8K/2K, 6 dense panels,
                                7 hash max, 8 bit-rank (presence bitmap + ranked accumulator),
-                               9 rank panels (bit-rank with accumulator panels in rank space) */
+                               9 rank panels (bit-rank with accumulator panels in rank space),
+                               10 bitmap-rank (symbolic bitmap + ranked fold, written straight into C) */
   double ms_analyse;       /* row products + binning + offsets */
   double ms_numeric;       /* accumulate kernels */
   double ms_compact;       /* output scan + compaction */
   double ms_total;
   int64_t kernels;         /* kernels launched by the call */
   int64_t output_mode;     /* 0: U-slot scratch + compaction, 1: exact claims + compaction,
-                              2: two passes (count, then write into C) */
+                              2: two passes (count, then write into C),
+                              3: bitmap-rank (long rows straight into C, short rows compacted) */
 } spg_mult_stats;
 
 /* ---------------------------------------------------------------- misc */
@@ -134,11 +136,21 @@ SPG_API uint64_t spg_ctx_kernel_launches(const spg_ctx* ctx);
 /* bytes of device scratch the single-pass numeric may use (0 = auto: 45% of free
  * HBM); above it the multiply switches to the exact two-pass mode */
 SPG_API int spg_ctx_set_scratch_budget(spg_ctx* ctx, uint64_t bytes);
+/* Local-multiply pipeline: SPG_PIPE_AUTO (default) sends rows with more than
+   2048 products through the bitmap-rank kernels (symbolic bitmap pass, exact
+   rowptr, values folded in rank space straight into C) whenever the output
+   width fits a shared-memory bitmap; SPG_PIPE_BINS forces the per-bin
+   accumulators (hash / dense panels / bit-rank) with scratch + compaction. */
+#define SPG_PIPE_AUTO 0
+#define SPG_PIPE_BINS 1
+SPG_API int spg_ctx_set_pipeline(spg_ctx* ctx, int mode);
 
 /* ---------------------------------------------------- device matrices */
 SPG_API int spg_dcsr_alloc(spg_ctx* ctx, int sr, int64_t nrows, int64_t ncols, int64_t nseg,
                            int64_t nnz, spg_dcsr* out);
 SPG_API int spg_dcsr_free(spg_ctx* ctx, spg_dcsr* m);
+/* stream-ordered device -> host copy of `bytes` (synchronous on return) */
+SPG_API int spg_copy_to_host(spg_ctx* ctx, void* dst, const void* src, uint64_t bytes);
 /* H2D of a host CSR (or CSC) with int64 -> int32 index narrowing on device */
 SPG_API int spg_upload(spg_ctx* ctx, int sr, const spg_hcsr* h, int is_csc, spg_dcsr* out);
 /* D2H into library-allocated host arrays (pinned, recycled by the library:

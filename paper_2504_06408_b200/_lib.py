@@ -38,7 +38,7 @@ class DCsr(C.Structure):
 
 class MultStats(C.Structure):
     _fields_ = [("products", C.c_int64), ("nnz_out", C.c_int64),
-                ("rows_per_bin", C.c_int64 * 10), ("ms_analyse", C.c_double),
+                ("rows_per_bin", C.c_int64 * 11), ("ms_analyse", C.c_double),
                 ("ms_numeric", C.c_double), ("ms_compact", C.c_double),
                 ("ms_total", C.c_double), ("kernels", C.c_int64), ("output_mode", C.c_int64)]
 
@@ -92,8 +92,10 @@ _SIGS = [
     ("spg_ctx_sync", C.c_int, [C.c_void_p]),
     ("spg_ctx_kernel_launches", C.c_uint64, [C.c_void_p]),
     ("spg_ctx_set_scratch_budget", C.c_int, [C.c_void_p, C.c_uint64]),
+    ("spg_ctx_set_pipeline", C.c_int, [C.c_void_p, C.c_int]),
     ("spg_dcsr_alloc", C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64, _P(DCsr)]),
     ("spg_dcsr_free", C.c_int, [C.c_void_p, _P(DCsr)]),
+    ("spg_copy_to_host", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64]),
     ("spg_upload", C.c_int, [C.c_void_p, C.c_int, _P(HCsr), C.c_int, _P(DCsr)]),
     ("spg_download", C.c_int, [C.c_void_p, C.c_int, _P(DCsr), C.c_int, _P(HCsr)]),
     ("spg_hcsr_free", None, [_P(HCsr)]),

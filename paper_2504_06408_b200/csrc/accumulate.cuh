@@ -51,7 +51,7 @@
 
 namespace spg {
 
-constexpr int kNumBins = 10;
+constexpr int kNumBins = 11;
 constexpr int32_t kEmptyKey = -1;
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -66,6 +66,7 @@ enum Bin : uint8_t {
   kBinHashMax = 7,   // wide outputs: largest smem hash
   kBinBitRank = 8,   // F <= kBitRankMax, narrow C: presence bitmap + ranked accumulator
   kBinRankPanels = 9,  // longer rows in a bounded column window: bitmap ranks, accumulator panels in rank space
+  kBinBitmap = 10,     // bitmap-rank pipeline (bitmap_rank.cuh): symbolic bitmap pass, then ranks, output direct into C
 };
 
 // ---------------------------------------------------------------------------
@@ -284,7 +285,7 @@ template <class SR, class Src>
 __global__ void __launch_bounds__(256) analyse_rows_kernel(Src src, int64_t ncols_out, int64_t dense_min,
                                                            int64_t bitrank_max, int64_t bitrank_segs,
                                                            int64_t bitrank_span, int64_t rankpanel_segs,
-                                                           int64_t rankpanel_maxf,
+                                                           int64_t rankpanel_maxf, int64_t bitmap_min,
                                                            int32_t* __restrict__ colmin,
                                                            int64_t* __restrict__ prods,
                                                            int64_t* __restrict__ ubound,
@@ -330,6 +331,7 @@ __global__ void __launch_bounds__(256) analyse_rows_kernel(Src src, int64_t ncol
       uint8_t b;
       const bool dense_ok = np <= kDenseMaxPanels || f >= (int64_t)kDenseMinPerPanel * np;
       if (f == 0) b = kBinEmpty;
+      else if (bitmap_min > 0 && f > bitmap_min) b = kBinBitmap;
       else if (f <= 32) b = kBinWarpEsc;
       else if (f <= 512 && nseg <= 512) b = kBinEsc512;
       else if (bitrank_max > 0 && f <= bitrank_max && nseg <= bitrank_segs && span <= bitrank_span) b = kBinBitRank;
@@ -343,7 +345,7 @@ __global__ void __launch_bounds__(256) analyse_rows_kernel(Src src, int64_t ncol
       else if (u <= Geom<V>::kMaxT / 2) b = kBinHashMax;
       else b = kBinDense;
       prods[i] = f;
-      ubound[i] = (b == kBinEmpty) ? 0 : ((u + 3) & ~int64_t(3));  // 16-byte aligned scratch slots
+      ubound[i] = (b == kBinEmpty || b == kBinBitmap) ? 0 : ((u + 3) & ~int64_t(3));  // 16-byte aligned scratch slots
       bins[i] = b;
     }
   }
@@ -2020,7 +2022,7 @@ __global__ void __launch_bounds__(256, sizeof(V) <= 4 ? SPG_COMPACT_MINB : 1) co
     if (n == 0) continue;
     const int64_t s = off[i];
     if (s < 0) continue;
-    if (skip && skip[i] == kBinDense) continue;  // copied by compact_long_rows_kernel
+    if (skip && (skip[i] == kBinDense || skip[i] == kBinBitmap)) continue;  // copied by compact_long_rows_kernel
     if constexpr (SPG_ROWS_VEC > 0 && sizeof(V) % 4 == 0) {
       if (n >= SPG_ROWS_VEC) {  // long row: 16-byte loads and stores
         constexpr int WPE = (int)(sizeof(V) / 4);

@@ -426,6 +426,13 @@ int spg_ctx_set_scratch_budget(spg_ctx* c, uint64_t bytes) {
   return guarded(c, [&] { c->scratch_budget = bytes; });
 }
 
+int spg_ctx_set_pipeline(spg_ctx* c, int mode) {
+  return guarded(c, [&] {
+    need(c && (mode == SPG_PIPE_AUTO || mode == SPG_PIPE_BINS), "pipeline: unknown mode");
+    c->pipeline = mode;
+  });
+}
+
 int spg_dcsr_alloc(spg_ctx* c, int sr, int64_t nrows, int64_t ncols, int64_t nseg, int64_t nnz, spg_dcsr* out) {
   return guarded(c, [&] {
     need(c && out, "null argument");
@@ -445,6 +452,15 @@ int spg_dcsr_free(spg_ctx* c, spg_dcsr* m) {
     need(c && m, "null argument");
     use_device(c);
     free_dcsr(c, m);
+  });
+}
+
+int spg_copy_to_host(spg_ctx* c, void* dst, const void* src, uint64_t bytes) {
+  return guarded(c, [&] {
+    need(c && (bytes == 0 || (dst && src)), "null argument");
+    use_device(c);
+    if (bytes) SPG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+    SPG_CUDA(cudaStreamSynchronize(c->stream));
   });
 }
 

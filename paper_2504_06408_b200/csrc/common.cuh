@@ -66,6 +66,7 @@ struct spg_ctx {
   cudaEvent_t fork_ev = nullptr;
   uint64_t launches = 0;  // kernels launched by this context (evidence counter)
   size_t scratch_budget = 0;  // bytes the row-batched numeric pass may use (0 = auto)
+  int pipeline = 0;           // SPG_PIPE_AUTO (bitmap-rank when eligible) or SPG_PIPE_BINS
 };
 
 namespace spg {

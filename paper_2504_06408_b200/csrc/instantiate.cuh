@@ -81,7 +81,7 @@ struct OpsImpl {
                              spg_mult_stats* st) {
     MulSource<SR> src{a->ptr, a->idx, static_cast<const V*>(a->vals),
                       b->ptr, b->idx, static_cast<const V*>(b->vals), a->nrows};
-    run_rows<SR>(c, src, b->ncols, out, st, b);
+    if (!run_rows_br<SR>(c, src, b, b->ncols, out, st)) run_rows<SR>(c, src, b->ncols, out, st, b);
   }
 
   static void merge(spg_ctx* c, int nparts, const spg_dcsr* parts, int64_t rows, int64_t cols,

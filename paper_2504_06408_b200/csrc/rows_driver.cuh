@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "accumulate.cuh"
+#include "bitmap_rank.cuh"
 
 namespace spg {
 
@@ -74,7 +75,8 @@ struct StreamFork {
 
 template <class K>
 inline void set_smem(K kern, size_t smem) {
-  if (smem > 48 * 1024) SPG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // static + dynamic above 48 KB needs the opt-in (set unconditionally: cheap, idempotent)
+  if (smem > 16 * 1024) SPG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
 }
 
 template <class K>
@@ -292,7 +294,7 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
   DBuf<int32_t> colmin(c, bitrank ? (size_t)m : 1);
   analyse_rows_kernel<SR, Src><<<grid_for(c, m, 8), 256, 0, c->stream>>>(
       src, ncols_out, dense_min, bitrank ? kBitRankN : 0, kBitRankSegs, 32 * (int64_t)kBitRankW,  // window (both)
-      rankpanel ? kRpSegs : 0, rp_maxf, colmin.p, prods.p, ub.p, bins.p);
+      rankpanel ? kRpSegs : 0, rp_maxf, 0, colmin.p, prods.p, ub.p, bins.p);
   SPG_LAUNCH_CHECK();
   ++c->launches;
   SPG_CUDA(cudaMemsetAsync(ub.p + m, 0, sizeof(int64_t), c->stream));
@@ -612,7 +614,7 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
     tm.mark(3);
     st->products = products;
     st->nnz_out = out->nnz;
-    for (int b = 0; b < 10; ++b) st->rows_per_bin[b] = b < kNumBins ? (int64_t)hcounts[b] : 0;
+    for (int b = 0; b < kNumBins; ++b) st->rows_per_bin[b] = (int64_t)hcounts[b];
     st->ms_numeric = ms_numeric;
     st->ms_compact = ms_compact;
     st->ms_total = tm.between(0, 3);
@@ -620,6 +622,286 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
     st->kernels = (int64_t)(c->launches - launches0);
     st->output_mode = !fits ? 2 : slotted ? 0 : 1;
   }
+}
+
+
+// ---------------------------------------------------------------------------
+// Bitmap-rank driver (bitmap_rank.cuh) for a local multiply whose output
+// width fits a shared-memory bitmap: rows with F > SPG_BR_MINF products take
+// the symbolic-bitmap / rank path and write straight into C; the short rows
+// run the hash / ESC kernels into U-slot scratch and only they are compacted.
+// Returns false (nothing changed) when the call is not eligible or the
+// bitmaps do not fit the memory budget; the caller then runs run_rows.
+// ---------------------------------------------------------------------------
+template <class SR>
+bool run_rows_br(spg_ctx* c, const MulSource<SR>& src, const spg_dcsr* r, int64_t ncols_out, spg_dcsr* out,
+                 spg_mult_stats* st) {
+  using V = typename SR::value_type;
+  using Src = MulSource<SR>;
+  static const int br_on = [] {
+    const char* e = std::getenv("SPG_BR");
+    return e ? std::atoi(e) : 1;
+  }();
+  static const int64_t br_minf = [] {  // rows with more products take the bitmap path (<= 4096: see below)
+    const char* e = std::getenv("SPG_BR_MINF");
+    return std::min<int64_t>(e ? (int64_t)std::atoll(e) : 2048, 4096);
+  }();
+  const int64_t m = src.nrows;
+  if (!br_on || c->pipeline == SPG_PIPE_BINS || m == 0 || ncols_out <= 0 || ncols_out > kBrMaxCols)
+    return false;
+  const int64_t nnz_r = r->nnz;
+  if (nnz_r >= (int64_t{1} << 31) - 64) return false;  // 32-bit entry offsets
+  const int nwords = br_words(ncols_out);
+  PhaseTimer tm(c, st != nullptr);
+  const uint64_t launches0 = c->launches;
+  tm.mark(0);
+
+  // K1 analyse: F <= br_minf (<= 4096) rows go to the ESC / hash bins only
+  DBuf<int64_t> prods(c, m), ub(c, m + 1), off(c, m + 1), rownnz(c, m + 1);
+  DBuf<uint8_t> bins(c, m);
+  DBuf<int32_t> colmin(c, 1);
+  analyse_rows_kernel<SR, Src><<<grid_for(c, m, 8), 256, 0, c->stream>>>(
+      src, ncols_out, INT64_MAX, 0, 0, 0, 0, 0, br_minf, colmin.p, prods.p, ub.p, bins.p);
+  SPG_LAUNCH_CHECK();
+  ++c->launches;
+  SPG_CUDA(cudaMemsetAsync(ub.p + m, 0, sizeof(int64_t), c->stream));
+  SPG_CUDA(cudaMemsetAsync(rownnz.p + m, 0, sizeof(int64_t), c->stream));
+  exclusive_scan(c, ub.p, off.p, m + 1);
+  DBuf<unsigned long long> counts(c, kNumBins + 1);
+  SPG_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(unsigned long long) * (kNumBins + 1), c->stream));
+  bin_count_kernel<<<grid_for(c, m, 1024, 2), 1024, 0, c->stream>>>(bins.p, m, counts.p);
+  SPG_LAUNCH_CHECK();
+  ++c->launches;
+  unsigned long long hcounts[kNumBins];
+  int64_t scratch_total = 0;
+  SPG_CUDA(cudaMemcpyAsync(hcounts, counts.p, sizeof(hcounts), cudaMemcpyDeviceToHost, c->stream));
+  SPG_CUDA(cudaMemcpyAsync(&scratch_total, off.p + m, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  SPG_CUDA(cudaStreamSynchronize(c->stream));
+  const int64_t nb = (int64_t)hcounts[kBinBitmap];
+
+  // memory: U-slot scratch of the short rows + one bitmap per long row
+  size_t budget = c->scratch_budget;
+  if (budget == 0) budget = (size_t)(mem_available(c) * 0.45);
+  const size_t bm_bytes = (size_t)nb * nwords * sizeof(uint32_t);
+  const size_t sc_bytes = (size_t)scratch_total * (sizeof(int32_t) + sizeof(V));
+  if (bm_bytes + sc_bytes > budget) return false;
+  uint32_t* gbm_p = nb > 0 ? try_dalloc<uint32_t>(c, (size_t)nb * nwords) : nullptr;
+  if (nb > 0 && !gbm_p) return false;
+  DBuf<uint32_t> gbm = DBuf<uint32_t>::adopt(c, gbm_p, (size_t)nb * nwords);
+  DBuf<int32_t> sc_cols(c, (size_t)scratch_total + 16);
+  DBuf<V> sc_vals(c, (size_t)scratch_total + 16);
+
+  int64_t products = 0;
+  if (st) {
+    size_t bytes = 0;
+    DBuf<int64_t> fsum(c, 1);
+    SPG_CUDA(cub::DeviceReduce::Sum(nullptr, bytes, prods.p, fsum.p, m, c->stream));
+    ensure_cub_tmp(c, bytes);
+    SPG_CUDA(cub::DeviceReduce::Sum(c->cub_tmp, bytes, prods.p, fsum.p, m, c->stream));
+    ++c->launches;
+    products = d2h_scalar(c, fsum.p);
+  }
+  int end_bit = 0;
+  while ((int64_t{1} << end_bit) < ncols_out) ++end_bit;
+
+  // K2 bin lists; the bitmap bin sorted by F descending (largest rows first)
+  DBuf<int64_t> lists(c, m);
+  DBuf<unsigned long long> cursor(c, kNumBins);
+  unsigned long long base[kNumBins];
+  {
+    unsigned long long acc = 0;
+    for (int b = 0; b < kNumBins; ++b) {
+      base[b] = acc;
+      if (b > 0) acc += hcounts[b];
+    }
+  }
+  SPG_CUDA(cudaMemcpyAsync(cursor.p, base, sizeof(base), cudaMemcpyHostToDevice, c->stream));
+  bin_scatter_kernel<<<grid_for(c, m, 1024, 2), 1024, 0, c->stream>>>(bins.p, m, cursor.p, lists.p);
+  SPG_LAUNCH_CHECK();
+  ++c->launches;
+  const int64_t* brows = lists.p + base[kBinBitmap];
+  DBuf<int64_t> bsorted, bk1, bk2;
+  if (nb > 1) {
+    bk1 = DBuf<int64_t>(c, nb);
+    bk2 = DBuf<int64_t>(c, nb);
+    bsorted = DBuf<int64_t>(c, nb);
+    gather_keys_kernel<<<grid_for(c, nb, 256, 4), 256, 0, c->stream>>>(brows, nb, prods.p, bk1.p);
+    SPG_LAUNCH_CHECK();
+    ++c->launches;
+    size_t bytes = 0;
+    SPG_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, bk1.p, bk2.p, brows, bsorted.p, (int)nb, 0,
+                                                        64, c->stream));
+    ensure_cub_tmp(c, bytes);
+    SPG_CUDA(cub::DeviceRadixSort::SortPairsDescending(c->cub_tmp, bytes, bk1.p, bk2.p, brows, bsorted.p, (int)nb,
+                                                        0, 64, c->stream));
+    ++c->launches;
+    brows = bsorted.p;
+  }
+  if (hcounts[kBinEmpty] > 0) {
+    zero_empty_rows_kernel<<<grid_for(c, m, 256, 4), 256, 0, c->stream>>>(bins.p, m, rownnz.p);
+    SPG_LAUNCH_CHECK();
+    ++c->launches;
+  }
+  DBuf<unsigned long long> work(c, 2);
+  SPG_CUDA(cudaMemsetAsync(work.p, 0, 2 * sizeof(unsigned long long), c->stream));
+  tm.mark(1);
+
+  constexpr int kSymThreads = 512, kNumThreads = 512;
+  // numeric geometry: 2 CTAs/SM when the bitmap is <= 32 KB, else 1; the rest
+  // of the CTA's shared memory is the rank window's accumulator
+  auto num_kern = br_numeric_kernel<SR, Src, kNumThreads, 2>;
+  int capv = 0;
+  {
+    cudaFuncAttributes fa{};
+    SPG_CUDA(cudaFuncGetAttributes(&fa, num_kern));
+    const size_t per_sm = 232448 - 2048;  // usable shared memory per SM, 1 KB reserved per CTA
+    const size_t num_budget = (nwords <= 8192 ? per_sm / 2 : per_sm) - fa.sharedSizeBytes - 256;
+    const BrNumLayout<V> l0{nwords + 8, 0};
+    const size_t fixed = l0.bytes(kNumThreads);
+    capv = fixed < num_budget ? (int)std::min<size_t>(65535, (num_budget - fixed) / sizeof(V)) & ~7 : 0;
+    if (capv < 1024) fail(SPG_ERR_INTERNAL, "bitmap-rank: no shared memory left for the accumulator");
+  }
+  const int wstride = (int)((ncols_out + capv - 1) / capv) + 1;
+  DBuf<int32_t> wcol(c, (size_t)std::max<int64_t>(nb, 1) * wstride), nwin(c, (size_t)nb + 1);
+  {  // symbolic (long rows) || numeric of the short rows into their slots
+    StreamFork fk(c, 3);
+    if (nb > 0) {
+      const size_t smem = sizeof(uint32_t) * (size_t)nwords + BrSegs<V>::bytes(kSymThreads) + 64;
+      auto kern = br_symbolic_kernel<SR, Src, kSymThreads, 3>;
+      set_smem(kern, smem);
+      kern<<<resident_grid(c, kern, kSymThreads, smem, nb), kSymThreads, smem, fk[0]>>>(
+          src, brows, nb, nwords, capv, wstride, work.p, gbm.p, wcol.p, nwin.p, rownnz.p);
+      SPG_LAUNCH_CHECK();
+      ++c->launches;
+    }
+    RowOut<V> o;
+    o.cols = sc_cols.p;
+    o.vals = sc_vals.p;
+    o.off = off.p;
+    o.rownnz = rownnz.p;
+    const int64_t* lb = lists.p;
+    if (hcounts[kBinHash8K] > 0)
+      launch_hash<SR, Src, 8192, 512>(c, fk[1], src, lb + base[kBinHash8K], hcounts[kBinHash8K], 256, end_bit, o);
+    if (hcounts[kBinHash4K] > 0)
+      launch_hash<SR, Src, 4096, 256>(c, fk[1], src, lb + base[kBinHash4K], hcounts[kBinHash4K], 256, end_bit, o);
+    if (hcounts[kBinHash2K] > 0)
+      launch_hash<SR, Src, 2048, 128>(c, fk[2], src, lb + base[kBinHash2K], hcounts[kBinHash2K], 256, end_bit, o);
+    if (hcounts[kBinEsc512] > 0)
+      launch_esc<SR, Src, 128, 4>(c, fk[2], src, lb + base[kBinEsc512], hcounts[kBinEsc512], end_bit, o);
+    if (hcounts[kBinWarpEsc] > 0) {
+      esc_warp_kernel<SR, Src><<<grid_for(c, hcounts[kBinWarpEsc], 8), 256, 0, fk[2]>>>(
+          src, lb + base[kBinWarpEsc], hcounts[kBinWarpEsc], o);
+      SPG_LAUNCH_CHECK();
+      ++c->launches;
+    }
+    for (int b : {(int)kBinDense, (int)kBinHashMax, (int)kBinBitRank, (int)kBinRankPanels})
+      if (hcounts[b] > 0) fail(SPG_ERR_INTERNAL, "bitmap-rank driver: unexpected bin");
+    fk.join();
+  }
+  out->ptr = dalloc<int64_t>(c, m + 1);
+  exclusive_scan(c, rownnz.p, out->ptr, m + 1);
+  // (row, window) work items
+  DBuf<int64_t> winoff(c, (size_t)nb + 1);
+  DBuf<int2> items;
+  int64_t nitems = 0;
+  if (nb > 0) {
+    DBuf<int64_t> nwin64(c, (size_t)nb + 1);
+    widen_kernel<<<grid_for(c, nb + 1, 256, 4), 256, 0, c->stream>>>(nwin.p, nb, nwin64.p);
+    SPG_LAUNCH_CHECK();
+    exclusive_scan(c, nwin64.p, winoff.p, nb + 1);
+    c->launches += 1;
+  }
+  int64_t hv[2] = {0, 0};
+  SPG_CUDA(cudaMemcpyAsync(&hv[0], out->ptr + m, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  if (nb > 0) SPG_CUDA(cudaMemcpyAsync(&hv[1], winoff.p + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  SPG_CUDA(cudaStreamSynchronize(c->stream));
+  const int64_t nnz = hv[0];
+  nitems = hv[1];
+  DBuf<BrPack<V>> pack;
+  if constexpr (sizeof(V) <= 8) {
+    if (nitems > 0 && nnz_r > 0) {
+      pack = DBuf<BrPack<V>>(c, (size_t)nnz_r);
+      br_pack_kernel<V><<<grid_for(c, nnz_r, 256, 8), 256, 0, c->stream>>>(nnz_r, src.ridx, src.rval, pack.p);
+      SPG_LAUNCH_CHECK();
+      ++c->launches;
+    }
+  }
+  if (nitems > 0) {
+    items = DBuf<int2>(c, (size_t)nitems);
+    br_expand_items_kernel<<<grid_for(c, nb, 256, 4), 256, 0, c->stream>>>(nb, nwin.p, winoff.p, items.p);
+    SPG_LAUNCH_CHECK();
+    ++c->launches;
+  }
+  tm.mark(2);
+  const float ms_sym = tm.between(1, 2);
+  out->nrows = m;
+  out->ncols = ncols_out;
+  out->nnz = nnz;
+  out->idx = dalloc<int32_t>(c, (size_t)nnz);
+  out->vals = dalloc<V>(c, (size_t)nnz);
+  DBuf<unsigned long long> zeros(c, 1);
+  DBuf<unsigned long long> rowzero(c, (size_t)m);
+  SPG_CUDA(cudaMemsetAsync(zeros.p, 0, sizeof(unsigned long long), c->stream));
+  SPG_CUDA(cudaMemsetAsync(rowzero.p, 0, sizeof(unsigned long long) * (size_t)m, c->stream));
+  {  // numeric (long rows, straight into C) || compaction of the short rows
+    StreamFork fk(c, 2);
+    if (nitems > 0) {
+      const size_t smem = BrNumLayout<V>{nwords + 8, capv}.bytes(kNumThreads);
+      auto kern = num_kern;
+      set_smem(kern, smem);
+      kern<<<resident_grid(c, kern, kNumThreads, smem, nitems), kNumThreads, smem, fk[0]>>>(
+          src, pack.p, items.p, nitems, brows, ncols_out, nwords, capv, wstride, wcol.p, work.p + 1, gbm.p, out->ptr,
+          out->idx, static_cast<V*>(out->vals), zeros.p, rowzero.p);
+      SPG_LAUNCH_CHECK();
+      ++c->launches;
+    }
+    if (scratch_total > 0) {
+      compact_rows_kernel<V><<<grid_for(c, m, 8), 256, 0, fk[1]>>>(m, bins.p, off.p, out->ptr, sc_cols.p, sc_vals.p,
+                                                                 out->idx, static_cast<V*>(out->vals));
+      SPG_LAUNCH_CHECK();
+      ++c->launches;
+    }
+    fk.join();
+  }
+  tm.mark(3);
+  const float ms_num = tm.between(2, 3);
+  gbm.reset();
+  sc_cols.reset();
+  sc_vals.reset();
+  if (nb > 0 && d2h_scalar(c, zeros.p) > 0) {  // entries that folded to zero(): drop them
+    DBuf<int64_t> kept(c, (size_t)m + 1), nptr(c, (size_t)m + 1);
+    br_kept_counts_kernel<<<grid_for(c, m, 256, 4), 256, 0, c->stream>>>(m, out->ptr, rowzero.p, kept.p);
+    SPG_LAUNCH_CHECK();
+    SPG_CUDA(cudaMemsetAsync(kept.p + m, 0, sizeof(int64_t), c->stream));
+    exclusive_scan(c, kept.p, nptr.p, m + 1);
+    const int64_t nn = d2h_scalar(c, nptr.p + m);
+    int32_t* ni = dalloc<int32_t>(c, (size_t)nn);
+    V* nv = dalloc<V>(c, (size_t)nn);
+    drop_zero_entries_kernel<SR><<<grid_for(c, m, 8), 256, 0, c->stream>>>(
+        m, out->ptr, out->idx, static_cast<const V*>(out->vals), nptr.p, ni, nv);
+    SPG_LAUNCH_CHECK();
+    c->launches += 2;
+    dfree(c, out->idx);
+    dfree(c, out->vals);
+    dfree(c, out->ptr);
+    out->ptr = nptr.release();
+    out->idx = ni;
+    out->vals = nv;
+    out->nnz = nn;
+  }
+  if (st) {
+    tm.mark(3);
+    st->products = products;
+    st->nnz_out = out->nnz;
+    for (int b = 0; b < kNumBins; ++b) st->rows_per_bin[b] = (int64_t)hcounts[b];
+    st->ms_numeric = ms_sym + ms_num;
+    st->ms_compact = 0.0;
+    st->ms_total = tm.between(0, 3);
+    st->ms_analyse = st->ms_total - st->ms_numeric;
+    st->kernels = (int64_t)(c->launches - launches0);
+    st->output_mode = 3;
+  }
+  return true;
 }
 
 }  // namespace spg

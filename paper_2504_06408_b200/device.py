@@ -35,6 +35,13 @@ class Context:
     def set_scratch_budget(self, nbytes: int):
         check(lib.spg_ctx_set_scratch_budget(self.handle, int(nbytes)), self.handle)
 
+    PIPE_AUTO, PIPE_BINS = 0, 1
+
+    def set_pipeline(self, mode: int):
+        """PIPE_AUTO: bitmap-rank kernels for long rows when the output width
+        fits; PIPE_BINS: the per-bin accumulators with scratch + compaction."""
+        check(lib.spg_ctx_set_pipeline(self.handle, int(mode)), self.handle)
+
     def close(self):
         if self.handle:
             lib.spg_ctx_destroy(self.handle)
@@ -167,6 +174,14 @@ class DeviceCsr:
         check(lib.spg_download(self.ctx.handle, int(self.sr), C.byref(self.d), int(self.is_csc), C.byref(h)),
               self.ctx.handle)
         return take_hcsr(self.sr, h, self.is_csc)
+
+    def rowptr_host(self) -> np.ndarray:
+        """The device row (CSC: column) pointers copied to the host."""
+        nseg = self.ncols if self.is_csc else self.nrows
+        out = np.empty(nseg + 1, dtype=np.int64)
+        check(lib.spg_copy_to_host(self.ctx.handle, out.ctypes.data_as(C.c_void_p),
+                                   C.c_void_p(self.d.ptr), out.nbytes), self.ctx.handle)
+        return out
 
     def checksum(self) -> int:
         out = C.c_uint64()

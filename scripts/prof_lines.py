@@ -26,6 +26,7 @@ for line in raw:
         rows.append((st, ie, fname, int(r[0]), r[1].strip()[:90], xs))
 tot_s = sum(x[0] for x in rows) or 1; tot_i = sum(x[1] for x in rows) or 1
 tot_x = sum(x[5] for x in rows) or 1
-rows.sort(reverse=True)
+key = 1 if len(sys.argv) > 3 and sys.argv[3] == "inst" else 0
+rows.sort(key=lambda x: x[key], reverse=True)
 for st, ie, f, ln, src, xs in rows[:top]:
     print(f"{st / tot_s * 100:5.1f}% stall {ie / tot_i * 100:5.1f}% inst {xs / tot_x * 100:5.1f}% smem-excess  {f}:{ln}  {src}")

@@ -23,3 +23,14 @@ def golden():
 def ctx():
     from paper_2504_06408_b200 import default_context
     return default_context(0)
+
+
+@pytest.fixture
+def bins_ctx(ctx):
+    """The context with the per-bin accumulators forced (no bitmap-rank path):
+    tests that target a specific bin (hash, dense panels, bit-rank) use it."""
+    ctx.set_pipeline(ctx.PIPE_BINS)
+    try:
+        yield ctx
+    finally:
+        ctx.set_pipeline(ctx.PIPE_AUTO)

@@ -67,7 +67,7 @@ def _rand(sr, rng, m, k, dens):
 
 
 @pytest.mark.parametrize("sr", [0, 1, 2, 3, 4, 5])
-def test_every_bin_against_oracle(ctx, sr):
+def test_every_bin_against_oracle(bins_ctx, sr):
     """Rows engineered to land in every accumulator bin: empty, <=32 products
     (warp-ESC), the four hash-table sizes and the dense global accumulator."""
     rng = np.random.default_rng(100 + sr)
@@ -89,7 +89,7 @@ def test_every_bin_against_oracle(ctx, sr):
     acols = np.concatenate(rows).astype(np.int64)
     a = CsrMatrix(sr, len(sizes), 2000, aptr, acols, exact_values(sr, rng, acols.size))
     st = {}
-    got = esc_multiply(a, b, ctx=ctx, stats=st)
+    got = esc_multiply(a, b, ctx=bins_ctx, stats=st)
     want = ob.orc_multiply(to_mat(a), to_mat(b))
     assert_same(got, want, sr)
     bins = st["rows_per_bin"]
@@ -115,23 +115,23 @@ def test_rmat14_against_reference_checksum(golden, ctx, sr):
 
 
 @pytest.mark.parametrize("sr", [0, 2, 4, 5])
-def test_output_modes_agree(ctx, sr):
+def test_output_modes_agree(bins_ctx, sr):
     """The three output strategies (U-slot scratch, exact claims, two passes)
     produce the same C; the scratch budget selects the strategy."""
     m = coo_to_csr(generators.generate_rmat(sr, 13, 16.0, 5))
-    d = DeviceCsr.upload(ctx, m)
+    d = DeviceCsr.upload(bins_ctx, m)
     st = {}
     full = local_multiply(d, d, stats=st)
     assert st["output_mode"] == 0
     per = 4 + int(lib.spg_value_size(sr))
     want = full.download()
     for budget, mode in ((int(st["nnz_out"] * per * 1.02), 1), (1 << 20, 2)):
-        ctx.set_scratch_budget(budget)
+        bins_ctx.set_scratch_budget(budget)
         try:
             st2 = {}
             got = local_multiply(d, d, stats=st2)
         finally:
-            ctx.set_scratch_budget(0)
+            bins_ctx.set_scratch_budget(0)
         assert st2["output_mode"] == mode
         assert_same(got.download(), want, sr, rtol=RTOL)
 
@@ -162,7 +162,7 @@ def test_device_checksum_matches_reference(ctx):
 
 
 @pytest.mark.parametrize("sr", [0, 2, 4, 5])
-def test_wide_output_uses_hash_bins(ctx, sr):
+def test_wide_output_uses_hash_bins(bins_ctx, sr):
     """Outputs wider than 16 dense panels with medium rows go to the hash bins."""
     rng = np.random.default_rng(7 + sr)
     from golden.make_golden import exact_values
@@ -176,13 +176,13 @@ def test_wide_output_uses_hash_bins(ctx, sr):
     acols = np.concatenate(rows).astype(np.int64)
     a = CsrMatrix(sr, len(rows), 400, aptr, acols, exact_values(sr, rng, acols.size))
     st = {}
-    got = esc_multiply(a, b, ctx=ctx, stats=st)
+    got = esc_multiply(a, b, ctx=bins_ctx, stats=st)
     assert_same(got, ob.orc_multiply(to_mat(a), to_mat(b)), sr)
     assert sum(st["rows_per_bin"][i] for i in (3, 4, 7)) >= 2, st["rows_per_bin"]
 
 
 @pytest.mark.parametrize("sr", [1, 2, 4])
-def test_merge_dense_panels_against_oracle(ctx, sr):
+def test_merge_dense_panels_against_oracle(bins_ctx, sr):
     """Merging long partial rows over a wide block takes the dense panel path
     with per-partial binary-searched panel bounds; checked against the oracle
     product [I I I] . vstack(partials)."""
@@ -195,7 +195,7 @@ def test_merge_dense_panels_against_oracle(ctx, sr):
         ptr = np.concatenate([[0], np.cumsum([len(x) for x in rs])]).astype(np.int64)
         idx = np.concatenate(rs).astype(np.int64)
         parts.append(CsrMatrix(sr, nrows, ncols, ptr, idx, exact_values(sr, rng, idx.size)))
-    dparts = [DeviceCsr.upload(ctx, p) for p in parts]
+    dparts = [DeviceCsr.upload(bins_ctx, p) for p in parts]
     st = {}
     out = merge_partials(dparts, ncols, nrows, stats=st).download()  # CSC of C == CSR of C^T
     one = {0: 1.0, 1: 0.0, 2: 1, 4: 0}[sr]
@@ -234,7 +234,7 @@ def test_config5_er_maxtimes_struct_against_oracle(ctx, n, d):
 
 
 @pytest.mark.parametrize("sr", [1, 2, 4])
-def test_bitrank_and_rank_panel_bins_against_oracle(ctx, sr):
+def test_bitrank_and_rank_panel_bins_against_oracle(bins_ctx, sr):
     """Rows sized for the bit-rank bin (2048 < F <= 8192) and the rank-panel
     bin (8192 < F <= 16384) over a 200K-column output: bit-exact vs the
     oracle (the other rows take the hash / dense bins)."""
@@ -250,14 +250,14 @@ def test_bitrank_and_rank_panel_bins_against_oracle(ctx, sr):
     acols = np.concatenate(rows).astype(np.int64)
     a = CsrMatrix(sr, len(rows), nb, aptr, acols, exact_values(sr, rng, acols.size))
     st = {}
-    got = esc_multiply(a, b, ctx=ctx, stats=st)
+    got = esc_multiply(a, b, ctx=bins_ctx, stats=st)
     assert_same(got, ob.orc_multiply(to_mat(a), to_mat(b)), sr)
     bins = st["rows_per_bin"]
     # 4-byte values: bit-rank (F <= 8192) + rank panels (F <= 16384); others: bit-rank only
     assert bins[8] + bins[9] >= (3 if int(lib.spg_value_size(sr)) == 4 else 1), bins
 
 
-def test_bitrank_drops_columns_whose_products_are_all_zero(ctx):
+def test_bitrank_drops_columns_whose_products_are_all_zero(bins_ctx):
     """Tropical (min, saturating +): products that saturate to INT32_MAX are
     the semiring zero and must vanish from C (local_spgemm.hpp:57-58) — the
     bit-rank bin marks presence from columns alone and must redo such rows."""
@@ -274,7 +274,7 @@ def test_bitrank_drops_columns_whose_products_are_all_zero(ctx):
     avals[:2] = big                          # row 0 x B rows 0-1: all products saturate
     a = CsrMatrix(4, 1, nb, np.array([0, nb], dtype=np.int64), acols, avals)
     st = {}
-    got = esc_multiply(a, b, ctx=ctx, stats=st)
+    got = esc_multiply(a, b, ctx=bins_ctx, stats=st)
     want = ob.orc_multiply(to_mat(a), to_mat(b))
     assert_same(got, want, 4)
     assert st["rows_per_bin"][8] == 1
