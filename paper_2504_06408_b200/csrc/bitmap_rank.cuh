@@ -41,13 +41,70 @@
 
 namespace spg {
 
-constexpr int64_t kBrMaxCols = 1 << 19;  // output width whose bitmap fits shared memory (64 KB)
+constexpr int64_t kBrMaxCols = 1 << 19;
+constexpr int kBrMaxPanels = 256;  // fine column panels per row (window boundaries fall on them)
 
-// words per bitmap slot, padded to a multiple of 4096 (16-byte quads for
-// every thread of the 512- and 1024-thread kernels)
+// SPG_BR_PROF builds: per-phase cycle totals (thread 0 of every CTA), printed
+// by the driver — numeric 0 grab, 1 bitmap in, 2 count pass, 3 rank/emit
+// pass, 4 columns out, 5 segment cache, 6 fold, 7 values out; symbolic 8
+// grab, 9 segment cache, 10 walk, 11 tail.
+#ifdef SPG_BR_PROF
+static __device__ unsigned long long br_prof[16];
+#define BR_T(k)                                                        \
+  if (threadIdx.x == 0) {                                              \
+    const long long t_ = clock64();                                    \
+    atomicAdd(&br_prof[(k)], (unsigned long long)(t_ - br_t_last));    \
+    br_t_last = t_;                                                    \
+  }
+#define BR_T_INIT long long br_t_last = clock64();
+#else
+#define BR_T(k)
+#define BR_T_INIT
+#endif  // output width whose bitmap fits shared memory (64 KB)
+
+// words per bitmap slot: a power of two >= 4096 (whole 16-byte quads for every
+// thread, whole fine panels)
 __host__ __device__ inline int br_words(int64_t ncols) {
   const int64_t w = (ncols + 31) / 32;
-  return (int)((w + 4095) / 4096 * 4096);
+  int n = 4096;
+  while (n < w) n <<= 1;
+  return n;
+}
+
+// mbarrier + bulk-copy (TMA) primitives
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred P1;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n @!P1 bra WAIT_%=;\n}" ::"r"(
+          smem_addr(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+// bulk copy of nw bitmap words [wb, wb + nw) of slot `slot` into bm (one
+// thread; completion = the mbarrier's transaction count)
+__device__ __forceinline__ void br_bitmap_copy(uint32_t* bm, const uint32_t* gbm, int64_t slot, int nwords, int wb,
+                                               int nw, unsigned long long* bar) {
+  fence_proxy_async();  // earlier generic accesses of bm precede the async-proxy writes
+  const unsigned bytes = (unsigned)nw * 4u;
+  mbar_expect_tx(bar, bytes);
+  const char* gsrc = reinterpret_cast<const char*>(gbm + (size_t)slot * nwords + wb);
+  for (unsigned o = 0; o < bytes; o += 16384u)
+    bulk_g2s(reinterpret_cast<char*>(bm) + o, gsrc + o, min(16384u, bytes - o), bar);
 }
 
 // Right operand with column and value interleaved (one 8- or 16-byte load per
@@ -86,17 +143,6 @@ struct BrSegs {
   }
 };
 
-// lower_bound over the sorted columns [lo, hi) of a right-operand row
-template <class Src>
-__device__ __forceinline__ int64_t br_lower_bound(const Src& src, int64_t lo, int64_t hi, int32_t x) {
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (src.col(0, mid) < x) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo;
-}
-
 // One segment per thread, fetched early into registers (its global loads
 // then overlap whatever the CTA does before br_seg_build).
 template <class V>
@@ -115,19 +161,39 @@ __device__ __forceinline__ BrSegReg<typename SR::value_type> br_seg_fetch(const 
   }
   return g;
 }
-// Restricts the fetched segments to output columns [clo, chi) when
+// The slice of each segment inside fine panels [p0, p1): the right
+// operand's panel offsets poff[k * (npf + 1) + p] (entries of R row k with
+// column < p * panel width, computed once per call) bound it — no search.
+template <class SR, class Src>
+__device__ __forceinline__ BrSegReg<typename SR::value_type> br_seg_fetch_panels(const Src& src,
+                                                                                const int32_t* __restrict__ poff,
+                                                                                int npf, int p0, int p1, bool restrict_cols,
+                                                                                int64_t i, int64_t s0, int n) {
+  BrSegReg<typename SR::value_type> g;
+  g.m = SR::zero();
+  if ((int)threadIdx.x < n) {
+    const int32_t k = __ldg(src.lidx + s0 + threadIdx.x);
+    g.b = __ldg(src.rptr + k);
+    g.m = src.lval[s0 + threadIdx.x];
+    if (restrict_cols) {
+      const int32_t* po = poff + (int64_t)k * (npf + 1);
+      const int32_t a = __ldg(po + p0), e = __ldg(po + p1);
+      g.b += a;
+      g.len = e - a;
+    } else {
+      g.len = (int)(__ldg(src.rptr + k + 1) - g.b);
+    }
+  }
+  return g;
+}
+
+// Builds the compacted cache from the fetched segments to output columns [clo, chi) when
 // `restrict_cols`, drops the empty ones and builds the compacted cache;
 // returns the number kept.  Block-wide (ends with a barrier).
 template <class SR, class Src, int THREADS, class Scan64>
 __device__ __forceinline__ int br_seg_build(const Src& src, const BrSegs<typename SR::value_type>& cs,
-                                            BrSegReg<typename SR::value_type> g, int32_t clo, int32_t chi,
-                                            bool restrict_cols, typename Scan64::TempStorage& tmp) {
-  if (restrict_cols && g.len > 0) {
-    const int64_t f = br_lower_bound(src, g.b, g.b + g.len, clo);
-    const int64_t e = br_lower_bound(src, f, g.b + g.len, chi);
-    g.b = f;
-    g.len = (int)(e - f);
-  }
+                                            const BrSegReg<typename SR::value_type>& g,
+                                            typename Scan64::TempStorage& tmp, int* s_cnt) {
   const unsigned long long packed = g.len > 0 ? ((1ull << 32) | (unsigned long long)g.len) : 0ull;
   unsigned long long excl, total;
   Scan64(tmp).ExclusiveSum(packed, excl, total);
@@ -138,7 +204,10 @@ __device__ __forceinline__ int br_seg_build(const Src& src, const BrSegs<typenam
     cs.pre[k] = (int)(excl & 0xffffffffull);
     cs.mult[k] = g.m;
   }
-  if (threadIdx.x == 0) cs.pre[nn] = (int)(total & 0xffffffffull);
+  if (threadIdx.x == 0) {
+    cs.pre[nn] = (int)(total & 0xffffffffull);
+    *s_cnt = 0;
+  }
   __syncthreads();
   return nn;
 }
@@ -148,10 +217,11 @@ __device__ __forceinline__ int br_seg_build(const Src& src, const BrSegs<typenam
 // unset when !kVals).
 template <class SR, class Src, int NW, int IPL, bool kVals, bool kPacked, class F>
 __device__ __forceinline__ void br_items(const Src& src, const BrPack<typename SR::value_type>* __restrict__ pack,
-                                         const BrSegs<typename SR::value_type>& cs, int n, F&& f) {
+                                         const BrSegs<typename SR::value_type>& cs, int n, int* s_cnt, F&& f) {
   using V = typename SR::value_type;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int P = cs.pre[n];
+  const int wid = threadIdx.x >> 5;
   const int lo_q = (int)((int64_t)P * wid / NW), hi_q = (int)((int64_t)P * (wid + 1) / NW);
   if (lo_q >= hi_q) return;
   int s = 0, hs = n;  // s = largest t with pre[t] <= q0
@@ -214,15 +284,22 @@ __device__ __forceinline__ void br_items(const Src& src, const BrPack<typename S
 }
 
 #ifndef SPG_BR_IPL
-#define SPG_BR_IPL 4
+#define SPG_BR_IPL 4  // numeric: 32-item steps per warp iteration (loads in flight)
+#endif
+#ifndef SPG_BR_SYM_IPL
+#define SPG_BR_SYM_IPL 2
+#endif
+#ifndef SPG_BR_SYM_MINB
+#define SPG_BR_SYM_MINB 3
 #endif
 
 template <class SR, class Src, int THREADS, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB) br_symbolic_kernel(Src src, const int64_t* __restrict__ rows,
                                                                     int64_t nrows_bin, int nwords, int capv,
-                                                                    int wstride, unsigned long long* __restrict__ work,
+                                                                    int wpp, int npf, int wstride,
+                                                                    unsigned long long* __restrict__ work,
                                                                     uint32_t* __restrict__ gbm,
-                                                                    int32_t* __restrict__ wcol,
+                                                                    int2* __restrict__ wlist,
                                                                     int32_t* __restrict__ nwin_out,
                                                                     int64_t* __restrict__ rownnz) {
   using V = typename SR::value_type;
@@ -239,6 +316,9 @@ __global__ void __launch_bounds__(THREADS, MINB) br_symbolic_kernel(Src src, con
     typename Scan64::TempStorage scan64;
   } tmp;
   __shared__ long long s_row;
+  __shared__ int s_cnt;
+  __shared__ int s_pc[kBrMaxPanels];
+  BR_T_INIT
   uint4* bq = reinterpret_cast<uint4*>(bm);
   const int nq = nwords >> 2;
   for (int q = threadIdx.x; q < nq; q += THREADS) bq[q] = make_uint4(0u, 0u, 0u, 0u);
@@ -251,53 +331,58 @@ __global__ void __launch_bounds__(THREADS, MINB) br_symbolic_kernel(Src src, con
       s_row = r < (unsigned long long)nrows_bin ? (long long)r : -1;
     }
     __syncthreads();
+    BR_T(8);
     const long long r = s_row;
     if (r < 0) break;
     const int64_t i = rows[r];
     const int64_t sb = src.seg_begin(i), nseg = src.seg_end(i) - sb;
     for (int64_t c0 = 0; c0 < nseg; c0 += THREADS) {
       const int n = (int)(nseg - c0 < (int64_t)THREADS ? nseg - c0 : (int64_t)THREADS);
-      const int nn = br_seg_build<SR, Src, THREADS, Scan64>(src, cs, br_seg_fetch<SR>(src, i, sb + c0, n), 0, 0, false,
-                                                             tmp.scan64);
-      br_items<SR, Src, NW, 2, false, false>(src, nullptr, cs, nn, [&](int32_t c, const V&) {
+      const int nn = br_seg_build<SR, Src, THREADS, Scan64>(src, cs, br_seg_fetch<SR>(src, i, sb + c0, n), tmp.scan64,
+                                                             &s_cnt);
+      BR_T(9);
+      br_items<SR, Src, NW, SPG_BR_SYM_IPL, false, false>(src, nullptr, cs, nn, &s_cnt, [&](int32_t c, const V&) {
         atomicOr(&bm[c >> 5], 1u << (c & 31));
       });
       __syncthreads();
+      BR_T(10);
     }
-    // nnz, window start columns (rank k * capv), bitmap out
+    // nnz, outputs per fine panel (wpp words), rank windows = greedy runs of
+    // whole panels holding <= capv outputs, bitmap out
     int cnt = 0;
     for (int k = 0; k < wpt; k += 4) {
       const uint4 x = bq[(w0 + k) >> 2];
       cnt += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
     }
-    int pre, total;
-    Scan(tmp.scan).ExclusiveSum(cnt, pre, total);
-    if (cnt > 0) {
-      int k = pre <= 0 ? 1 : (pre + capv - 1) / capv;
-      if (k == 0) k = 1;
-      int run = pre;
-      for (int q = 0; q < wpt && (int64_t)k * capv < pre + cnt; ++q) {
-        const uint32_t x = bm[w0 + q];
-        const int c = __popc(x);
-        while ((int64_t)k * capv < run + c) {
-          wcol[r * wstride + k] = ((w0 + q) << 5) + nth_set_bit(x, k * capv - run);
-          ++k;
-        }
-        run += c;
-      }
-    }
-    if (threadIdx.x == 0) {
-      wcol[r * wstride] = 0;
-      nwin_out[r] = (total + capv - 1) / capv;
-      rownnz[i] = total;
+    {
+      const int tpp = wpp / wpt;  // threads per panel (a power of two <= 32)
+      int pc = cnt;
+      for (int o = 1; o < tpp; o <<= 1) pc += __shfl_xor_sync(kFull, pc, o);
+      if ((threadIdx.x & (tpp - 1)) == 0 && threadIdx.x / tpp < npf) s_pc[threadIdx.x / tpp] = pc;
     }
     __syncthreads();
+    if (threadIdx.x == 0) {
+      int nwin = 0, run = 0, acc = 0;
+      for (int p = 0; p < npf; ++p) {
+        const int c = s_pc[p];
+        if (p == 0 || acc + c > capv) {
+          wlist[r * wstride + nwin++] = make_int2(p, run);
+          acc = 0;
+        }
+        acc += c;
+        run += c;
+      }
+      wlist[r * wstride + nwin] = make_int2(npf, run);
+      nwin_out[r] = run > 0 ? nwin : 0;
+      rownnz[i] = run;
+    }
     uint4* gq = reinterpret_cast<uint4*>(gbm + (size_t)r * nwords);
     for (int q = threadIdx.x; q < nq; q += THREADS) {
       __stcs(gq + q, bq[q]);  // streamed: keeps the right operand resident in L2
       bq[q] = make_uint4(0u, 0u, 0u, 0u);
     }
     __syncthreads();
+    BR_T(11);
   }
 }
 
@@ -371,7 +456,8 @@ struct BrNumLayout {
 template <class SR, class Src, int THREADS, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB) br_numeric_kernel(
     Src src, const BrPack<typename SR::value_type>* __restrict__ pack, const int2* __restrict__ items, int64_t nitems, const int64_t* __restrict__ rows, int64_t ncols,
-    int nwords, int capv, int wstride, const int32_t* __restrict__ wcol, unsigned long long* __restrict__ work,
+    int nwords, int capv, int wpp, int npf, int wstride, const int2* __restrict__ wlist,
+    const int32_t* __restrict__ poff, unsigned long long* __restrict__ work,
     const uint32_t* __restrict__ gbm, const int64_t* __restrict__ rowptr, int32_t* __restrict__ ccols,
     typename SR::value_type* __restrict__ cvals, unsigned long long* __restrict__ zeros,
     unsigned long long* __restrict__ rowzero) {
@@ -396,10 +482,18 @@ __global__ void __launch_bounds__(THREADS, MINB) br_numeric_kernel(
   } tmp;
   __shared__ long long s_item, s_next;
   __shared__ int s_wsum[NW];
+  __shared__ int s_cnt;
+  __shared__ __align__(8) unsigned long long s_bar;  // bitmap bulk copy completion
+  __shared__ bool s_issued;                          // this item's copy was issued ahead
+  BR_T_INIT
   if (threadIdx.x == 0) {
+    s_issued = false;
     const unsigned long long w = atomicAdd(work, 1ull);
     s_next = w < (unsigned long long)nitems ? (long long)w : -1;
+    mbar_init(&s_bar, 1);
+    fence_mbar_init();
   }
+  unsigned phase = 0;
   for (;;) {
     // work items are grabbed one ahead: the next item's bitmap words are
     // prefetched into L2 while this one is processed
@@ -413,105 +507,92 @@ __global__ void __launch_bounds__(THREADS, MINB) br_numeric_kernel(
       s_next = nx;
     }
     __syncthreads();
+    BR_T(0);
     const long long wi = s_item;
     if (wi < 0) break;
     const int2 it = items[wi];
     const int64_t slot = it.x;
     const int k = it.y;
     const int64_t i = rows[slot];
-    // this item's segments: loads issued now, consumed after the bitmap work
+    const int2 w0 = wlist[slot * wstride + k], w1 = wlist[slot * wstride + k + 1];
+    const int p0 = w0.x, p1 = w1.x;                      // fine panels [p0, p1)
+    const int r0 = w0.y, nr = w1.y - w0.y;               // output ranks [r0, r0 + nr)
+    const int wb = p0 * wpp, nw = (p1 - p0) * wpp;       // bitmap words held
+    // 1. the window's bitmap words: one bulk (TMA) copy into shared memory,
+    //    completing on an mbarrier (issued at the end of the previous item's
+    //    fold when this item was known then; else now)
+    if (threadIdx.x == 0 && !s_issued) br_bitmap_copy(bm, gbm, slot, nwords, wb, nw, &s_bar);
+    // this item's segments (slices of the window's panels): loads issued now
     const int64_t sb = src.seg_begin(i), nseg = src.seg_end(i) - sb;
-    const BrSegReg<V> g0 = br_seg_fetch<SR>(src, i, sb, (int)(nseg < THREADS ? nseg : THREADS));
+    const bool restrict_cols = p0 > 0 || p1 < npf;
+    const BrSegReg<V> g0 =
+        br_seg_fetch_panels<SR>(src, poff, npf, p0, p1, restrict_cols, i, sb, (int)(nseg < THREADS ? nseg : THREADS));
     const int64_t base = rowptr[i];
-    const int nnz = (int)(rowptr[i + 1] - base);
-    const int nwin = (nnz + capv - 1) / capv;
-    const int r0 = k * capv;
-    const int nr = min(capv, nnz - r0);
-    const int32_t clo = wcol[slot * wstride + k];
-    const int32_t chi = k + 1 < nwin ? wcol[slot * wstride + k + 1] : (int32_t)ncols;
-    const int wb = (clo >> 5) & ~3;                       // first word held (quad aligned)
-    const int nw = ((((chi + 31) >> 5) - wb) + 3) & ~3;  // words held
-    {
-      const long long nx = s_next;
-      if (nx >= 0) {  // L2 prefetch of the next item's bitmap words (128 B lines)
-        const int2 jt = items[nx];
-        const int64_t nrow = rows[jt.x];
-        const int64_t nb0 = rowptr[nrow];
-        const int nnz2 = (int)(rowptr[nrow + 1] - nb0);
-        const int nwin2 = (nnz2 + capv - 1) / capv;
-        const int32_t c0 = wcol[(int64_t)jt.x * wstride + jt.y];
-        const int32_t c1 = jt.y + 1 < nwin2 ? wcol[(int64_t)jt.x * wstride + jt.y + 1] : (int32_t)ncols;
-        const char* p0 = reinterpret_cast<const char*>(gbm + (size_t)jt.x * nwords + ((c0 >> 5) & ~31));
-        const int nl = (((c1 + 31) >> 5) - ((c0 >> 5) & ~31) + 31) >> 5;
-        for (int l = threadIdx.x; l < nl; l += THREADS) asm volatile("prefetch.global.L2 [%0];" ::"l"(p0 + 128 * l));
-      }
-    }
-    // 1. the window's bitmap words; bits outside [clo, chi) cleared
-    {
-      const uint4* gq = reinterpret_cast<const uint4*>(gbm + (size_t)slot * nwords + wb);
-      uint4* bq = reinterpret_cast<uint4*>(bm);
-      for (int q = threadIdx.x; q < (nw >> 2); q += THREADS) bq[q] = __ldcs(gq + q);
-    }
-    __syncthreads();
-    // 2. ranks: warp w owns the contiguous words [w*per, (w+1)*per), lanes
-    //    interleaved (conflict-free); pass 1 masks + counts, pass 2 scans per
-    //    32 words, stores the word's first rank and emits its columns in rank
-    //    order into the stage (stored contiguously after a barrier)
+    mbar_wait(&s_bar, phase);
+    phase ^= 1u;
+    BR_T(1);
+    // 2. ranks: lane t of the CTA owns L consecutive words (L a power of two),
+    //    visited in an order rotated by its bank group so the lanes of a warp
+    //    hit distinct banks; pass 1 masks + counts, one scan of the lanes'
+    //    counts, pass 2 stores each word's first rank and emits its columns in
+    //    rank order into the stage (stored contiguously after a barrier)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int per = ((nw + NW * 32 - 1) / (NW * 32)) * 32;
-    const int jw0 = wid * per, jw1 = min(nw, jw0 + per);
-    {
-      int cnt = 0;
-      for (int j = jw0 + lane; j < jw1; j += 32) {
-        const int c0 = (wb + j) << 5;
-        uint32_t x = bm[j];
-        if (c0 < clo || c0 + 32 > chi) {
-          if (c0 < clo) x = clo - c0 >= 32 ? 0u : x & ~((1u << (clo - c0)) - 1u);
-          if (c0 + 32 > chi) x = chi <= c0 ? 0u : x & ((1u << (chi - c0)) - 1u);
-          bm[j] = x;
-        }
-        cnt += __popc(x);
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
-      if (lane == 0) s_wsum[wid] = cnt;
-    }
-    __syncthreads();
-    {
-      int run = 0;
-      for (int w = 0; w < wid; ++w) run += s_wsum[w];
-      for (int j = jw0 + lane; j - lane < jw1; j += 32) {
-        const uint32_t x = j < jw1 ? bm[j] : 0u;
-        const int c = __popc(x);
-        int incl = c;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const int t = __shfl_up_sync(kFull, incl, d);
-          if (lane >= d) incl += t;
-        }
-        int rk = run + incl - c;
-        if (j < jw1) pre16[j] = (uint16_t)rk;
-        const uint32_t cb = (uint32_t)(wb + j) << 5;
-        if constexpr (sizeof(V) >= 4) {
-          for (uint32_t y = x; y; y &= y - 1) stage[rk++] = cb + __ffs(y) - 1;
-        } else {
-          for (uint32_t y = x; y; y &= y - 1) ccols[base + r0 + rk++] = cb + __ffs(y) - 1;
-        }
-        run += __shfl_sync(kFull, incl, 31);
+    int L = 1;
+    while (L * THREADS < nw) L <<= 1;
+    const int jt0 = threadIdx.x * L;
+    const int rot = L >= 32 ? lane & (L - 1) : (lane / (32 / L)) & (L - 1);
+    int tcnt = 0, thi = 0;
+    for (int k = 0; k < L; ++k) {
+      const int j = jt0 + ((k + rot) & (L - 1));
+      if (j < nw) {
+        const int c = __popc(bm[j]);
+        tcnt += c;
+        if (k < L - rot) thi += c;
       }
     }
+    int incl = tcnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int t = __shfl_up_sync(kFull, incl, d);
+      if (lane >= d) incl += t;
+    }
+    if (lane == 31) s_wsum[wid] = incl;
     __syncthreads();
+    BR_T(2);
+    {
+      int start = incl - tcnt;
+      for (int w = 0; w < wid; ++w) start += s_wsum[w];
+      int rk = start + (tcnt - thi);  // rank of the first word visited (word rot of the chunk)
+      for (int k = 0; k < L; ++k) {
+        if (k == L - rot) rk = start;  // wrapped to word 0 of the chunk
+        const int j = jt0 + ((k + rot) & (L - 1));
+        if (j < nw) {
+          const uint32_t x = bm[j];
+          pre16[j] = (uint16_t)rk;
+          const uint32_t cb = (uint32_t)(wb + j) << 5;
+          if constexpr (sizeof(V) >= 4) {
+            for (uint32_t y = x; y; y &= y - 1) stage[rk++] = cb + __ffs(y) - 1;
+          } else {
+            for (uint32_t y = x; y; y &= y - 1) ccols[base + r0 + rk++] = cb + __ffs(y) - 1;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    BR_T(3);
     if constexpr (sizeof(V) >= 4) {
       smem_words_out(reinterpret_cast<uint32_t*>(ccols), base + r0, stage, nr, threadIdx.x, THREADS);
       __syncthreads();
+      BR_T(4);
     }
     for (int e = threadIdx.x; e < nr; e += THREADS) acc[e] = SR::zero();
     // 3. fold the window's products into acc[rank]
     for (int64_t c0 = 0; c0 < nseg; c0 += THREADS) {
       const int n = (int)(nseg - c0 < (int64_t)THREADS ? nseg - c0 : (int64_t)THREADS);
-      const BrSegReg<V> g = c0 == 0 ? g0 : br_seg_fetch<SR>(src, i, sb + c0, n);
-      const int nn = br_seg_build<SR, Src, THREADS, Scan64>(src, cs, g, clo, chi, nwin > 1, tmp.scan64);
-      br_items<SR, Src, NW, (sizeof(V) > 4 ? 2 : SPG_BR_IPL), true, (sizeof(V) <= 8)>(src, pack, cs, nn,
+      const BrSegReg<V> g = c0 == 0 ? g0 : br_seg_fetch_panels<SR>(src, poff, npf, p0, p1, restrict_cols, i, sb + c0, n);
+      const int nn = br_seg_build<SR, Src, THREADS, Scan64>(src, cs, g, tmp.scan64, &s_cnt);
+      BR_T(5);
+      br_items<SR, Src, NW, (sizeof(V) > 4 ? 2 : SPG_BR_IPL), true, (sizeof(V) <= 8)>(src, pack, cs, nn, &s_cnt,
                                                                                       [&](int32_t c, const V& v) {
         if (SR::is_zero(v)) return;  // add(x, zero) == x
         const int j = (c >> 5) - wb;
@@ -519,6 +600,18 @@ __global__ void __launch_bounds__(THREADS, MINB) br_numeric_kernel(
         atomic_accumulate<SR, true>(&acc[rk], v);
       });
       __syncthreads();
+      BR_T(6);
+    }
+    // the fold is done with bm: start the next item's bitmap copy now so it
+    // lands while this item's values go out
+    if (threadIdx.x == 0) {
+      const long long nx = s_next;
+      s_issued = nx >= 0;
+      if (nx >= 0) {
+        const int2 jt = items[nx];
+        const int q0 = wlist[(int64_t)jt.x * wstride + jt.y].x, q1 = wlist[(int64_t)jt.x * wstride + jt.y + 1].x;
+        br_bitmap_copy(bm, gbm, jt.x, nwords, q0 * wpp, (q1 - q0) * wpp, &s_bar);
+      }
     }
     // 4. values out (zero() entries counted for the drop-zeros fix-up)
     int zc = 0;
@@ -530,6 +623,7 @@ __global__ void __launch_bounds__(THREADS, MINB) br_numeric_kernel(
       atomicAdd(zeros, (unsigned long long)zt);
     }
     __syncthreads();
+    BR_T(7);
   }
 }
 

@@ -761,16 +761,32 @@ bool run_rows_br(spg_ctx* c, const MulSource<SR>& src, const spg_dcsr* r, int64_
     capv = fixed < num_budget ? (int)std::min<size_t>(65535, (num_budget - fixed) / sizeof(V)) & ~7 : 0;
     if (capv < 1024) fail(SPG_ERR_INTERNAL, "bitmap-rank: no shared memory left for the accumulator");
   }
-  const int wstride = (int)((ncols_out + capv - 1) / capv) + 1;
-  DBuf<int32_t> wcol(c, (size_t)std::max<int64_t>(nb, 1) * wstride), nwin(c, (size_t)nb + 1);
+  // fine column panels: window boundaries fall on them, so a segment's slice
+  // of a window comes from the right operand's panel offsets (no search)
+  int wf = 1024;  // panel width: ~64 panels per row (<= kBrMaxPanels; a panel never exceeds capv outputs)
+  while ((ncols_out + wf - 1) / wf > kBrMaxPanels) wf *= 2;
+  while (wf * 2 <= capv && (ncols_out + wf - 1) / wf > 64) wf *= 2;
+  if (wf > capv || wf / 32 > 32 * (nwords / kSymThreads)) return false;
+  const int npf = (int)((ncols_out + wf - 1) / wf);
+  const int wpp = wf / 32;
+  const int wstride = npf + 2;
+  DBuf<int2> wlist(c, (size_t)std::max<int64_t>(nb, 1) * wstride);
+  DBuf<int32_t> nwin(c, (size_t)nb + 1);
+  DBuf<int32_t> poff;
+  if (nb > 0) {
+    poff = DBuf<int32_t>(c, (size_t)r->nrows * (npf + 1));
+    panel_offsets_kernel<<<grid_for(c, r->nrows, 8), 256, 0, c->stream>>>(r->nrows, r->ptr, r->idx, npf, wf, poff.p);
+    SPG_LAUNCH_CHECK();
+    ++c->launches;
+  }
   {  // symbolic (long rows) || numeric of the short rows into their slots
     StreamFork fk(c, 3);
     if (nb > 0) {
       const size_t smem = sizeof(uint32_t) * (size_t)nwords + BrSegs<V>::bytes(kSymThreads) + 64;
-      auto kern = br_symbolic_kernel<SR, Src, kSymThreads, 3>;
+      auto kern = br_symbolic_kernel<SR, Src, kSymThreads, SPG_BR_SYM_MINB>;
       set_smem(kern, smem);
       kern<<<resident_grid(c, kern, kSymThreads, smem, nb), kSymThreads, smem, fk[0]>>>(
-          src, brows, nb, nwords, capv, wstride, work.p, gbm.p, wcol.p, nwin.p, rownnz.p);
+          src, brows, nb, nwords, capv, wpp, npf, wstride, work.p, gbm.p, wlist.p, nwin.p, rownnz.p);
       SPG_LAUNCH_CHECK();
       ++c->launches;
     }
@@ -850,7 +866,8 @@ bool run_rows_br(spg_ctx* c, const MulSource<SR>& src, const spg_dcsr* r, int64_
       auto kern = num_kern;
       set_smem(kern, smem);
       kern<<<resident_grid(c, kern, kNumThreads, smem, nitems), kNumThreads, smem, fk[0]>>>(
-          src, pack.p, items.p, nitems, brows, ncols_out, nwords, capv, wstride, wcol.p, work.p + 1, gbm.p, out->ptr,
+          src, pack.p, items.p, nitems, brows, ncols_out, nwords, capv, wpp, npf, wstride, wlist.p, poff.p, work.p + 1,
+          gbm.p, out->ptr,
           out->idx, static_cast<V*>(out->vals), zeros.p, rowzero.p);
       SPG_LAUNCH_CHECK();
       ++c->launches;
@@ -865,6 +882,17 @@ bool run_rows_br(spg_ctx* c, const MulSource<SR>& src, const spg_dcsr* r, int64_
   }
   tm.mark(3);
   const float ms_num = tm.between(2, 3);
+#ifdef SPG_BR_PROF
+  {
+    unsigned long long pr[16];
+    SPG_CUDA(cudaMemcpyFromSymbol(pr, br_prof, sizeof(pr)));
+    const unsigned long long z[16] = {};
+    SPG_CUDA(cudaMemcpyToSymbol(br_prof, z, sizeof(z)));
+    std::fprintf(stderr, "[br-prof] items=%lld rows=%lld cycles(G):", (long long)nitems, (long long)nb);
+    for (int k = 0; k < 12; ++k) std::fprintf(stderr, " %d:%.3f", k, pr[k] * 1e-9);
+    std::fprintf(stderr, "\n");
+  }
+#endif
   gbm.reset();
   sc_cols.reset();
   sc_vals.reset();
