@@ -37,6 +37,8 @@
 #pragma once
 #include <cub/block/block_reduce.cuh>
 
+#include <type_traits>
+
 #include "accumulate.cuh"
 
 namespace spg {
@@ -93,6 +95,17 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
           smem_addr(bar)),
       "r"(phase)
       : "memory");
+}
+
+// number of right-operand values that are not SR::small (fast-multiply check)
+template <class SR>
+__global__ void br_count_not_small_kernel(int64_t n, const typename SR::value_type* __restrict__ v,
+                                          unsigned long long* __restrict__ out) {
+  unsigned long long c = 0;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
+    c += SR::small(v[u]) ? 0 : 1;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
 }
 
 // bulk copy of nw bitmap words [wb, wb + nw) of slot `slot` into bm (one
@@ -193,7 +206,7 @@ __device__ __forceinline__ BrSegReg<typename SR::value_type> br_seg_fetch_panels
 template <class SR, class Src, int THREADS, class Scan64>
 __device__ __forceinline__ int br_seg_build(const Src& src, const BrSegs<typename SR::value_type>& cs,
                                             const BrSegReg<typename SR::value_type>& g,
-                                            typename Scan64::TempStorage& tmp, int* s_cnt) {
+                                            typename Scan64::TempStorage& tmp, int* s_cnt, bool* all_small = nullptr) {
   const unsigned long long packed = g.len > 0 ? ((1ull << 32) | (unsigned long long)g.len) : 0ull;
   unsigned long long excl, total;
   Scan64(tmp).ExclusiveSum(packed, excl, total);
@@ -208,14 +221,20 @@ __device__ __forceinline__ int br_seg_build(const Src& src, const BrSegs<typenam
     cs.pre[nn] = (int)(total & 0xffffffffull);
     *s_cnt = 0;
   }
-  __syncthreads();
+  if constexpr (has_mul_small<SR>::value) {
+    const bool ok = __syncthreads_and(g.len == 0 || SR::small(g.m));
+    if (all_small) *all_small = ok;
+  } else {
+    __syncthreads();
+    if (all_small) *all_small = false;
+  }
   return nn;
 }
 
 // Warp `wid` of NW walks its equal share of the cached segments' items,
 // 32 * IPL at a time; f(col, value) per item (value = mul(left, right), or
 // unset when !kVals).
-template <class SR, class Src, int NW, int IPL, bool kVals, bool kPacked, class F>
+template <class SR, class Src, int NW, int IPL, bool kVals, bool kPacked, bool kFast = false, class F>
 __device__ __forceinline__ void br_items(const Src& src, const BrPack<typename SR::value_type>* __restrict__ pack,
                                          const BrSegs<typename SR::value_type>& cs, int n, int* s_cnt, F&& f) {
   using V = typename SR::value_type;
@@ -277,8 +296,9 @@ __device__ __forceinline__ void br_items(const Src& src, const BrPack<typename S
 #pragma unroll
     for (int k = 0; k < IPL; ++k)
       if (q0 + 32 * k + lane < hi_q) {
-        if constexpr (kVals) f(cc[k], src.item(mm[k], xx[k]));
-        else f(cc[k], V{});
+        if constexpr (kVals && kFast) f(cc[k], SR::mul_small(mm[k], xx[k]), std::true_type{});
+        else if constexpr (kVals) f(cc[k], src.item(mm[k], xx[k]), std::false_type{});
+        else f(cc[k], V{}, std::false_type{});
       }
   }
 }
@@ -341,7 +361,7 @@ __global__ void __launch_bounds__(THREADS, MINB) br_symbolic_kernel(Src src, con
       const int nn = br_seg_build<SR, Src, THREADS, Scan64>(src, cs, br_seg_fetch<SR>(src, i, sb + c0, n), tmp.scan64,
                                                              &s_cnt);
       BR_T(9);
-      br_items<SR, Src, NW, SPG_BR_SYM_IPL, false, false>(src, nullptr, cs, nn, &s_cnt, [&](int32_t c, const V&) {
+      br_items<SR, Src, NW, SPG_BR_SYM_IPL, false, false>(src, nullptr, cs, nn, &s_cnt, [&](int32_t c, const V&, auto) {
         atomicOr(&bm[c >> 5], 1u << (c & 31));
       });
       __syncthreads();
@@ -457,7 +477,7 @@ template <class SR, class Src, int THREADS, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB) br_numeric_kernel(
     Src src, const BrPack<typename SR::value_type>* __restrict__ pack, const int2* __restrict__ items, int64_t nitems, const int64_t* __restrict__ rows, int64_t ncols,
     int nwords, int capv, int wpp, int npf, int wstride, const int2* __restrict__ wlist,
-    const int32_t* __restrict__ poff, unsigned long long* __restrict__ work,
+    const int32_t* __restrict__ poff, bool r_small, unsigned long long* __restrict__ work,
     const uint32_t* __restrict__ gbm, const int64_t* __restrict__ rowptr, int32_t* __restrict__ ccols,
     typename SR::value_type* __restrict__ cvals, unsigned long long* __restrict__ zeros,
     unsigned long long* __restrict__ rowzero) {
@@ -590,15 +610,24 @@ __global__ void __launch_bounds__(THREADS, MINB) br_numeric_kernel(
     for (int64_t c0 = 0; c0 < nseg; c0 += THREADS) {
       const int n = (int)(nseg - c0 < (int64_t)THREADS ? nseg - c0 : (int64_t)THREADS);
       const BrSegReg<V> g = c0 == 0 ? g0 : br_seg_fetch_panels<SR>(src, poff, npf, p0, p1, restrict_cols, i, sb + c0, n);
-      const int nn = br_seg_build<SR, Src, THREADS, Scan64>(src, cs, g, tmp.scan64, &s_cnt);
+      bool small = false;
+      const int nn = br_seg_build<SR, Src, THREADS, Scan64>(src, cs, g, tmp.scan64, &s_cnt, &small);
       BR_T(5);
-      br_items<SR, Src, NW, (sizeof(V) > 4 ? 2 : SPG_BR_IPL), true, (sizeof(V) <= 8)>(src, pack, cs, nn, &s_cnt,
-                                                                                      [&](int32_t c, const V& v) {
-        if (SR::is_zero(v)) return;  // add(x, zero) == x
+      auto fold = [&](int32_t c, const V& v, auto fast) {
+        if constexpr (!decltype(fast)::value) {
+          if (SR::is_zero(v)) return;  // add(x, zero) == x
+        }
         const int j = (c >> 5) - wb;
         const int rk = (int)pre16[j] + __popc(bm[j] & ((1u << (c & 31)) - 1u));
         atomic_accumulate<SR, true>(&acc[rk], v);
-      });
+      };
+      constexpr int IPL = sizeof(V) > 4 ? 2 : SPG_BR_IPL;
+      if constexpr (has_mul_small<SR>::value && sizeof(V) <= 8) {
+        if (small && r_small) br_items<SR, Src, NW, IPL, true, true, true>(src, pack, cs, nn, &s_cnt, fold);
+        else br_items<SR, Src, NW, IPL, true, true, false>(src, pack, cs, nn, &s_cnt, fold);
+      } else {
+        br_items<SR, Src, NW, IPL, true, (sizeof(V) <= 8), false>(src, pack, cs, nn, &s_cnt, fold);
+      }
       __syncthreads();
       BR_T(6);
     }

@@ -833,6 +833,17 @@ bool run_rows_br(spg_ctx* c, const MulSource<SR>& src, const spg_dcsr* r, int64_
   SPG_CUDA(cudaStreamSynchronize(c->stream));
   const int64_t nnz = hv[0];
   nitems = hv[1];
+  bool r_small = false;
+  if constexpr (has_mul_small<SR>::value) {
+    if (nitems > 0) {
+      DBuf<unsigned long long> ns(c, 1);
+      SPG_CUDA(cudaMemsetAsync(ns.p, 0, sizeof(unsigned long long), c->stream));
+      br_count_not_small_kernel<SR><<<grid_for(c, nnz_r, 256, 8), 256, 0, c->stream>>>(nnz_r, src.rval, ns.p);
+      SPG_LAUNCH_CHECK();
+      ++c->launches;
+      r_small = d2h_scalar(c, ns.p) == 0;
+    }
+  }
   DBuf<BrPack<V>> pack;
   if constexpr (sizeof(V) <= 8) {
     if (nitems > 0 && nnz_r > 0) {
@@ -866,7 +877,7 @@ bool run_rows_br(spg_ctx* c, const MulSource<SR>& src, const spg_dcsr* r, int64_
       auto kern = num_kern;
       set_smem(kern, smem);
       kern<<<resident_grid(c, kern, kNumThreads, smem, nitems), kNumThreads, smem, fk[0]>>>(
-          src, pack.p, items.p, nitems, brows, ncols_out, nwords, capv, wpp, npf, wstride, wlist.p, poff.p, work.p + 1,
+          src, pack.p, items.p, nitems, brows, ncols_out, nwords, capv, wpp, npf, wstride, wlist.p, poff.p, r_small, work.p + 1,
           gbm.p, out->ptr,
           out->idx, static_cast<V*>(out->vals), zeros.p, rowzero.p);
       SPG_LAUNCH_CHECK();

@@ -149,6 +149,9 @@ struct TropicalI32 {
     if (y < -2147483648.0) return INT32_MIN;
     return (value_type)llround(y);
   }
+  // fast path (see has_mul_small): |a|, |b| < 2^29 => a + b neither saturates nor hits zero()
+  SPG_HD static bool small(value_type v) { return v > -(1 << 29) && v < (1 << 29); }
+  SPG_HD static value_type mul_small(value_type a, value_type b) { return a + b; }
 #ifdef __CUDACC__
   __device__ __forceinline__ static value_type acc_shared(value_type* p, value_type v) { return atomicMin(p, v); }
   __device__ __forceinline__ static value_type acc_global(value_type* p, value_type v) { return atomicMin(p, v); }
@@ -185,6 +188,22 @@ template <class SR>
 struct has_acc<SR, decltype((void)SR::acc_shared((typename SR::value_type*)nullptr,
                                                  typename SR::value_type{}),
                             void())> {
+  static constexpr bool value = true;
+};
+
+// Optional fast multiply: a semiring may declare `small(v)` and
+// `mul_small(a, b)`, promising mul_small(a, b) == mul(a, b) and
+// !is_zero(mul(a, b)) whenever small(a) && small(b).  The bitmap-rank fold
+// uses it for a batch whose left scalars and right-operand values are all
+// small (checked per call / per batch), dropping the saturation and
+// zero-product tests from the per-product work.
+template <class SR, class = void>
+struct has_mul_small {
+  static constexpr bool value = false;
+};
+template <class SR>
+struct has_mul_small<SR, decltype((void)SR::small(typename SR::value_type{}),
+                                  (void)SR::mul_small(typename SR::value_type{}, typename SR::value_type{}), void())> {
   static constexpr bool value = true;
 };
 
