@@ -236,11 +236,10 @@ __device__ __forceinline__ int br_seg_build(const Src& src, const BrSegs<typenam
 // unset when !kVals).
 template <class SR, class Src, int NW, int IPL, bool kVals, bool kPacked, bool kFast = false, class F>
 __device__ __forceinline__ void br_items(const Src& src, const BrPack<typename SR::value_type>* __restrict__ pack,
-                                         const BrSegs<typename SR::value_type>& cs, int n, int* s_cnt, F&& f) {
+                                         const BrSegs<typename SR::value_type>& cs, int n, int wid, F&& f) {
   using V = typename SR::value_type;
   const int lane = threadIdx.x & 31;
   const int P = cs.pre[n];
-  const int wid = threadIdx.x >> 5;
   const int lo_q = (int)((int64_t)P * wid / NW), hi_q = (int)((int64_t)P * (wid + 1) / NW);
   if (lo_q >= hi_q) return;
   int s = 0, hs = n;  // s = largest t with pre[t] <= q0
@@ -361,7 +360,7 @@ __global__ void __launch_bounds__(THREADS, MINB) br_symbolic_kernel(Src src, con
       const int nn = br_seg_build<SR, Src, THREADS, Scan64>(src, cs, br_seg_fetch<SR>(src, i, sb + c0, n), tmp.scan64,
                                                              &s_cnt);
       BR_T(9);
-      br_items<SR, Src, NW, SPG_BR_SYM_IPL, false, false>(src, nullptr, cs, nn, &s_cnt, [&](int32_t c, const V&, auto) {
+      br_items<SR, Src, NW, SPG_BR_SYM_IPL, false, false>(src, nullptr, cs, nn, (int)(threadIdx.x >> 5), [&](int32_t c, const V&, auto) {
         atomicOr(&bm[c >> 5], 1u << (c & 31));
       });
       __syncthreads();
@@ -623,10 +622,10 @@ __global__ void __launch_bounds__(THREADS, MINB) br_numeric_kernel(
       };
       constexpr int IPL = sizeof(V) > 4 ? 2 : SPG_BR_IPL;
       if constexpr (has_mul_small<SR>::value && sizeof(V) <= 8) {
-        if (small && r_small) br_items<SR, Src, NW, IPL, true, true, true>(src, pack, cs, nn, &s_cnt, fold);
-        else br_items<SR, Src, NW, IPL, true, true, false>(src, pack, cs, nn, &s_cnt, fold);
+        if (small && r_small) br_items<SR, Src, NW, IPL, true, true, true>(src, pack, cs, nn, (int)(threadIdx.x >> 5), fold);
+        else br_items<SR, Src, NW, IPL, true, true, false>(src, pack, cs, nn, (int)(threadIdx.x >> 5), fold);
       } else {
-        br_items<SR, Src, NW, IPL, true, (sizeof(V) <= 8), false>(src, pack, cs, nn, &s_cnt, fold);
+        br_items<SR, Src, NW, IPL, true, (sizeof(V) <= 8), false>(src, pack, cs, nn, (int)(threadIdx.x >> 5), fold);
       }
       __syncthreads();
       BR_T(6);
