@@ -30,6 +30,15 @@ sys.path.insert(0, ROOT)
 
 METRIC = "semiring SpGEMM Gflop/s & time-to-C at 1/2/4/8 B200 vs CPU ref"
 GRIDS = {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}
+# matrix_checksum (checksum.hpp:20-38) of C = A.A from the CPU oracle's streaming
+# restatement (oracle/spg_oracle.cpp, pinned to the reference): the bench
+# checks its own C against these after the timed loop ("parity" in the line).
+# key: (config, scale, edge factor, seed, permuted)
+GOLDEN_CSUM = {
+    (2, 18, 16.0, 1, True): 7149000290918998130,
+    (2, 18, 16.0, 1, False): 10351070082044141371,
+    (3, 22, 16.0, 1, True): 216229255003959338,
+}
 
 
 def log(*a):
@@ -192,26 +201,83 @@ def cpu_reference_gflops(a, sr, target_products, nthreads=None):
             "seconds": sec}
 
 
+def host_info():
+    """nproc, CPU model and host RAM of the box (recorded beside the CPU numbers)."""
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    mem_gb = None
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                mem_gb = round(int(line.split()[1]) / 2**20, 1)
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model, "host_ram_gb": mem_gb}
+
+
+def reference_input(args):
+    """A for the reference arm, built by the REFERENCE itself (oracle/_ref:
+    generate_rmat, rmat.hpp:15-60, and coo_to_csr) plus the same seeded
+    relabelling in numpy — the reference process never loads this repo's
+    library."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_bind as ob
+    _, _, r, c, v = ob.ref_generate_rmat(4, args.scale, args.ef, args.seed)
+    n = 1 << args.scale
+    if args.permute:  # generators.permute_symmetric: entry (i, j) -> (p[i], p[j])
+        perm = np.random.default_rng(args.seed).permutation(n).astype(np.int64)
+        r, c = perm[r], perm[c]
+    m = ob.ref_coo_to_csr(4, n, n, r, c, v)
+
+    class _Csr:  # the fields cpu_reference_gflops reads
+        nrows, ncols = m.nrows, m.ncols
+        rowptr, colids, values = m.ptr, m.idx, m.vals
+        nnz = int(m.ptr[-1])
+    return _Csr
+
+
 def run_reference_arm(args):
-    """`--impl reference`: the reference CPU implementation on the host cores."""
+    """`--impl reference`: the reference CPU implementation on the host cores:
+    its esc_multiply (local_spgemm.hpp:83-156, compiled unmodified into
+    oracle/_ref) over disjoint row slices of the same C = A.A on every host
+    thread, each step a bounded row sample (the full product needs ~24 B per
+    product = ~70 GB of expand-sort-compress tuples)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    a = make_input(args.scale, args.ef, args.seed, permute=args.permute)  # same relabelled A as our arm
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_bind as ob
+    if ob.ref is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libspsumma_ref.so not built"}), flush=True)
+        return
+    a = reference_input(args)
     times = []
     res = None
     for i in range(args.warmup + args.steps):
         res = cpu_reference_gflops(a, 4, args.cpu_products)
         if i >= args.warmup:
             times.append(res["seconds"])
-    val = res["value"]
     gflops = [2.0 * float(res["sample"].split("F=")[1].split(" ")[0]) / t / 1e9 for t in times]
     val = float(np.median(gflops))
+    hi = host_info()
+    F_full = 2934326978 if (args.scale, args.ef) == (18, 16.0) else None
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "Gflop/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.median(times)) * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic", "config": {"workload": f"rmat{args.scale}_ef{int(args.ef)}_tropical_i32_AxA (BASELINE config 2)",
-                                            "permuted": bool(args.permute), "sample": res["sample"]},
+                                            "permuted": bool(args.permute), "sample": res["sample"],
+                                            "input": "generated and compressed by the reference (oracle/_ref)",
+                                            "summa25_multiply_full": "infeasible here: ~24 B x F = "
+                                            + (f"{24 * F_full / 1e9:.0f} GB" if F_full else "24 B x F")
+                                            + " of expand-sort-compress tuples vs host RAM " + str(hi["host_ram_gb"]) + " GB",
+                                            **hi},
             "cpu_baseline": {"value": val, "unit": "Gflop/s", "cores": res["cores"], "kind": res["kind"],
                              "sample": res["sample"]},
             "e2e": {"value": val, "unit": "Gflop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -255,8 +321,14 @@ def run_single(args):
             e1.record(stream)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
-            c.free()
+            if len(times) < args.steps:
+                c.free()
     launches = ctx.kernel_launches() - launches0
+    # parity: the last timed C against the oracle's checksum of the same product
+    csum = c.checksum()
+    c.free()
+    golden = GOLDEN_CSUM.get((2, args.scale, args.ef, args.seed, bool(args.permute)))
+    parity = None if golden is None else bool(csum == golden)
     ms = float(np.mean(times))
     gflops = 2.0 * F / (ms * 1e-3) / 1e9
     peak, peak_kind = peaks()
@@ -281,10 +353,41 @@ def run_single(args):
     e2e_s = float(np.median(e2e_times)) if e2e_times else float("nan")
     unpin()
 
+    # companion measurement on the generator's own vertex order (SURVEY §7:
+    # the relabelled input is reported beside the unpermuted one)
+    unperm = None
+    if args.permute and not args.no_unpermuted:
+        del d
+        a_u = make_input(args.scale, args.ef, args.seed, permute=False)
+        d_u = DeviceCsr.upload(ctx, a_u)
+        for _ in range(2):
+            local_multiply(d_u, d_u).free()
+        t_u = []
+        for k in range(3):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            c_u = local_multiply(d_u, d_u)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            t_u.append(e0.elapsed_time(e1))
+            if k < 2:
+                c_u.free()
+        cs_u = c_u.checksum()
+        c_u.free()
+        g_u = GOLDEN_CSUM.get((2, args.scale, args.ef, args.seed, False))
+        ms_u = float(np.mean(t_u))
+        unperm = {"ms_per_step": ms_u, "value": 2.0 * F / (ms_u * 1e-3) / 1e9, "unit": "Gflop/s",
+                  "roofline_frac": b_alg(a_u.nnz, a_u.nrows, F, nnz_c, vs) / (ms_u * 1e-3) / 1e9 / peak,
+                  "parity": None if g_u is None else bool(cs_u == g_u), "steps": 3, "warmup": 2}
+        del d_u
+
     cpu = None
     if not args.no_cpu_baseline:
         cpu = cpu_reference_gflops(a, sr, args.cpu_products)
         cpu.pop("seconds", None)
+        cpu.update(host_info())
 
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -299,7 +402,10 @@ def run_single(args):
         "vs_baseline": None, "dtype": "int32", "data": "synthetic",
         "config": {"workload": f"rmat{args.scale}_ef{int(args.ef)}_tropical_i32_AxA (BASELINE config 2)",
                    "grid": "1x1", "permuted": bool(args.permute), "products": F, "nnz_A": a.nnz, "nnz_C": nnz_c,
-                   "time_to_C_ms": ms, "steps_ms": [round(float(x), 3) for x in times],
+                   "local_multiply_ms": ms,
+                   "local_multiply_ms_note": "device-resident A, C materialised in HBM; the host round trip is e2e",
+                   "steps_ms": [round(float(x), 3) for x in times],
+                   "unpermuted": unperm,
                    "phases_ms_untimed_warmup_call": {k: round(st[k], 3) for k in ("ms_analyse", "ms_numeric",
                                                                                     "ms_compact")},
                    "rows_per_bin": st["rows_per_bin"], "output_mode": st["output_mode"],
@@ -307,6 +413,9 @@ def run_single(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "note": f"B_alg of the whole local multiply (SURVEY §8d) / its event time; peak {peak_kind}"},
+        "parity": parity,
+        "parity_check": {"checksum_C": csum, "golden": golden,
+                         "how": "matrix_checksum (checksum.hpp:20-38) of the last timed C vs the CPU oracle's"},
         "cpu_baseline": cpu,
         "e2e": (None if args.e2e_steps <= 0 else
                 {"value": 2.0 * F / e2e_s / 1e9, "unit": "Gflop/s", "h2d_bytes_per_step": h2d,
@@ -509,6 +618,7 @@ def main():
     ap.add_argument("--cpu-products", type=float, default=0.0,
                     help="products in the CPU sample (default: 3e7 per host core, at most 1e9)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-unpermuted", action="store_true", help="skip the companion unpermuted N=1 measurement")
     ap.add_argument("--summa", action="store_true", help="use the SUMMA path even on one GPU (1x1 grid)")
     ap.add_argument("--one-round", action="store_true", help="SummaOptions::two_round = false")
     ap.add_argument("--no-fuse", action="store_true", help="per-stage multiplies + merge_partials (reference structure)")

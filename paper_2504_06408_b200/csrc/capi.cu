@@ -178,6 +178,8 @@ void host_release(void* p) {
 
 // Persistent host worker pool: parallel_for(n, fn) runs fn(lo, hi) over n
 // items split across the workers and the caller, and returns when all are done.
+// Calls from several host threads (one context per GPU) are serialised by
+// call_mu_: a job owns the pool until every part has finished.
 class HostPool {
  public:
   static HostPool& get() {
@@ -185,6 +187,7 @@ class HostPool {
     return *p;
   }
   void parallel_for(int64_t n, const std::function<void(int64_t, int64_t)>& fn) {
+    std::lock_guard<std::mutex> call(call_mu_);
     const int parts = (int)workers_.size() + 1;
     std::unique_lock<std::mutex> lk(mu_);
     job_ = &fn;
@@ -222,6 +225,7 @@ class HostPool {
     }
   }
   std::vector<std::thread> workers_;
+  std::mutex call_mu_;  // one parallel_for at a time
   std::mutex mu_;
   std::condition_variable cv_, done_;
   const std::function<void(int64_t, int64_t)>* job_ = nullptr;
@@ -603,7 +607,8 @@ void prepare_block(spg_ctx* c, int sr, const spg_hcsr* csc, const spg_hdcsc* dcs
   const int vs = ops->value_size;
   if (dcsc) {
     // dcsc_decompress checks (formats.hpp:222-242), done on the host arrays
-    if (dcsc->njc < 0 || (dcsc->njc > 0 && (!dcsc->jc || !dcsc->cp)))
+    // cp always has njc + 1 entries (njc == 0 included); jc has njc
+    if (dcsc->njc < 0 || !dcsc->cp || (dcsc->njc > 0 && !dcsc->jc))
       fail(SPG_ERR_MALFORMED, "dcsc_decompress: bad cp offset array");
     if (dcsc->cp[0] != 0 || dcsc->cp[dcsc->njc] != dcsc->nnz)
       fail(SPG_ERR_MALFORMED, "dcsc_decompress: bad cp offset array");

@@ -378,7 +378,10 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
     return e ? std::atoi(e) : 1;
   }();
   const bool warp_emit = warp_emit_on && slotted && hcounts[kBinDense] > 0 && dense_cfg() == 1;
-  const int wstride = npc * (512 / 32);  // panels x warps of the 2-CTA kernel (= the heavy kernel's)
+  // chunks per dense slot: panels x warps of the 2-CTA kernel (W/2 panels, 16
+  // warps) and of the heavy-row kernel (W panels, 32 warps) — they differ when
+  // ncols is not a multiple of W (e.g. ncols <= W/2), so take the larger
+  const int wstride = std::max(npc * (512 / 32), std::max(npanels_for<V>(ncols_out, Geom<V>::kPanelW), 1) * (1024 / 32));
   DBuf<int32_t> wchunks(c, warp_emit ? (size_t)hcounts[kBinDense] * wstride * 2 : 1);
   DBuf<int64_t> rowstart, chunks;
   DBuf<unsigned long long> bump(c, 1);
