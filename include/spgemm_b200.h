@@ -271,7 +271,10 @@ SPG_API int spg_exchange_sizes(spg_comm* comm, int scope, int root, int64_t trip
  * SPG_PATH_HOST or SPG_PATH_DEVICE.  `root` is the scope-local index. */
 SPG_API int spg_bcast(spg_comm* comm, int scope, int root, void* dev_buf, uint64_t bytes,
                       int mode, uint64_t threshold, int* path_out);
-SPG_API int spg_comm_set_device_transport(spg_comm* comm, int transport);
+SPG_API int spg_comm_set_device_transport(spg_comm* comm, int transport); /* SPG_DEV_NCCL (P2P: SPG_ERR_ARG, not implemented) */
+/* 1 when the device path is available (one GPU per rank: NCCL row/column
+   communicators); 0 when ranks share a GPU, which runs the host path only */
+SPG_API int spg_comm_has_device_path(const spg_comm* comm);
 
 typedef struct {
   int two_round;      /* SummaOptions::two_round (summa.hpp:174-177) */

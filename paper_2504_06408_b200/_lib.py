@@ -139,6 +139,7 @@ _SIGS = [
     ("spg_bcast", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_uint64, C.c_int, C.c_uint64,
                             _P(C.c_int)]),
     ("spg_comm_set_device_transport", C.c_int, [C.c_void_p, C.c_int]),
+    ("spg_comm_has_device_path", C.c_int, [C.c_void_p]),
     ("spg_gather", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, _P(DCsr), C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                              C.c_int, _P(DCsr)]),
     ("spg_summa25_multiply", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64,

@@ -46,6 +46,7 @@ struct Header {
   Barrier world_bar;
   Barrier scope_bar[2][kMaxGridSide];
   Slot slot[2][kMaxGridSide];
+  unsigned char dev_uuid[kMaxGridSide * kMaxGridSide][16];  // per rank: its GPU (cudaDeviceProp::uuid)
 };
 
 size_t header_bytes() { return (sizeof(Header) + 4095) & ~size_t(4095); }
@@ -69,6 +70,7 @@ struct spg_comm {
   bool registered = false;
   ncclComm_t world_comm = nullptr, row_comm = nullptr, col_comm = nullptr;
   int transport = SPG_DEV_NCCL;
+  bool shared_gpu = false;  // several ranks on one GPU: no NCCL communicator, host path only
   std::string last_error;
   spg::CommCounters counters;
   bool owner = false;
@@ -208,7 +210,10 @@ int comm_bcast(spg_comm* c, int scope, int root, void* buf, uint64_t bytes, int 
   else if (mode == SPG_COMM_DEVICE_ONLY) path = SPG_PATH_DEVICE;
   else path = bytes >= threshold ? SPG_PATH_DEVICE : SPG_PATH_HOST;
   if (!device_buffer) path = SPG_PATH_HOST;  // host buffers (CPU tests) only travel through shm
-  if (path == SPG_PATH_DEVICE && !c->world_comm) fail(SPG_ERR_ARG, "device path needs a GPU communicator");
+  if (path == SPG_PATH_DEVICE && !c->world_comm)
+    fail(SPG_ERR_ARG, c->shared_gpu ? "device path unavailable: ranks of this job share a GPU (NCCL needs one GPU "
+                                      "per rank); use the host path (SPG_COMM_HOST_ONLY)"
+                                    : "device path needs a GPU communicator");
   if (path == SPG_PATH_HOST) {
     ++c->counters.host_bcasts;
     c->counters.bytes_host += bytes;
@@ -383,6 +388,16 @@ int spg_comm_create(const char* job, int world, int rank, int pr, int pc, int de
       SPG_CUDA(cudaSetDevice(device));
       SPG_CUDA(cudaHostRegister(c->staging, (size_t)(pr + pc) * c->staging_bytes, cudaHostRegisterDefault));
       c->registered = true;
+      // ranks sharing a GPU (e.g. a 2x2 grid exercised on a 1-GPU box) cannot
+      // form an NCCL communicator: they run with the host path only
+      cudaDeviceProp prop{};
+      SPG_CUDA(cudaGetDeviceProperties(&prop, device));
+      std::memcpy(c->hdr->dev_uuid[rank], &prop.uuid, 16);
+      comm_barrier(c);
+      for (int r = 0; r < world; ++r)
+        if (r != rank && std::memcmp(c->hdr->dev_uuid[r], c->hdr->dev_uuid[rank], 16) == 0) c->shared_gpu = true;
+    }
+    if (device >= 0 && !c->shared_gpu) {
       while (c->hdr->uid_ready.load(std::memory_order_acquire) != 1) std::this_thread::sleep_for(std::chrono::milliseconds(1));
       ncclUniqueId id;
       std::memcpy(&id, c->hdr->uid, sizeof(id));
@@ -452,9 +467,13 @@ int spg_bcast(spg_comm* c, int scope, int root, void* buf, uint64_t bytes, int m
 
 int spg_comm_set_device_transport(spg_comm* c, int transport) {
   return cguard(c, [&] {
-    if (transport != SPG_DEV_NCCL && transport != SPG_DEV_P2P) fail(SPG_ERR_ARG, "unknown transport");
+    if (transport == SPG_DEV_P2P)
+      fail(SPG_ERR_ARG, "device transport P2P is not implemented; the device path uses NCCL over NVLink");
+    if (transport != SPG_DEV_NCCL) fail(SPG_ERR_ARG, "unknown transport");
     c->transport = transport;
   });
 }
+
+int spg_comm_has_device_path(const spg_comm* c) { return c && c->world_comm ? 1 : 0; }
 
 }  // extern "C"

@@ -107,6 +107,11 @@ class Comm:
         if rc != 0:
             raise errors.from_status(rc, lib.spg_comm_last_error(self.handle).decode())
 
+    @property
+    def has_device_path(self) -> bool:
+        """False when ranks share a GPU (no NCCL communicator): host path only."""
+        return bool(lib.spg_comm_has_device_path(self.handle))
+
     def barrier(self):
         self._check(lib.spg_comm_barrier(self.handle))
 

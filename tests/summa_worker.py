@@ -32,6 +32,9 @@ def main():
     ap.add_argument("--fuse", type=int, default=1)
     ap.add_argument("--grid", default="", help="PRxPC (default: the BASELINE grid for the world size)")
     ap.add_argument("--gather", type=int, default=0, help="also gather C on rank 0 (GPU assembly) and compare")
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--golden-ledger", default="", help="golden.npz key prefix (summa_<sr>_p<p>_r<two>): compare the "
+                    "distributed ledger counters with the reference's summa25_multiply")
     args = ap.parse_args()
 
     import torch.distributed as dist
@@ -43,18 +46,21 @@ def main():
         summa25_multiply
 
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    import torch
+    local = int(os.environ.get("LOCAL_RANK", rank)) % max(1, torch.cuda.device_count())  # ranks may share a GPU
     dist.init_process_group("gloo")
     job = [uuid.uuid4().hex[:12] if rank == 0 else None]
     dist.broadcast_object_list(job, src=0)
     pr, pc = (int(x) for x in args.grid.split("x")) if args.grid else grid_for(world)
     i, j = rank // pc, rank % pc
 
-    m = generators.generate_rmat(args.sr, args.scale, args.ef, 1)
+    m = generators.generate_rmat(args.sr, args.scale, args.ef, args.seed)
     n = m.nrows
     blk = local_block(m, pr, pc, i, j)
     ctx = Context(local)
     comm = Comm(job[0], world, rank, pr, pc, local, staging_bytes=args.staging)
+    if not comm.has_device_path and args.mode != 0:
+        raise SystemExit("ranks share a GPU: run with --mode 0 (host path)")
     c, led = summa25_multiply(comm, ctx, blk, blk, n, n, n, two_round=bool(args.two_round), mode=args.mode,
                               threshold=args.threshold, fuse_stages=bool(args.fuse))
     part = checksum_part(c, blk.rows[0], blk.cols[0])
@@ -77,9 +83,9 @@ def main():
         ok = ok and bool(np.all(np.abs(x - y) <= 1e-12 * np.maximum(np.abs(x), np.abs(y)) + 1e-300))
     else:
         ok = ok and got.values.tobytes() == bv[order].tobytes()
-    import torch
     t = torch.tensor([part & 0xFFFFFFFF, part >> 32, int(ok), led["local_multiply_calls"],
-                      led["host_bcasts"], led["device_bcasts"]], dtype=torch.int64)
+                      led["host_bcasts"], led["device_bcasts"], led["size_exchanges"], led["skipped_stages"]],
+                     dtype=torch.int64)
     parts = [torch.zeros_like(t) for _ in range(world)]
     dist.all_gather(parts, t)
     if rank == 0:
@@ -102,6 +108,23 @@ def main():
             print(f"[summa_worker] gather_ok={gok}", flush=True)
             allok = allok and gok
         cs_ok = total == want or args.sr == 0  # fp64 values hash bitwise
+        if args.golden_ledger:
+            # the reference charges each collective once (fabric.hpp:220-241); every rank of a
+            # square q x q grid counts the q-rank collectives it joins, and its own multiplies
+            g = np.load(os.path.join(HERE, "golden", "golden.npz"))
+            gl = g[args.golden_ledger + "_ledger"]
+            q = pr
+            bc = sum(int(p[4]) + int(p[5]) for p in parts)
+            sx = sum(int(p[6]) for p in parts)
+            lm = sum(int(p[3]) for p in parts)
+            sk = sum(int(p[7]) for p in parts)
+            led_ok = (pr == pc and bc == q * (gl[0] + gl[1]) and sx == q * gl[4] and sk == gl[6]
+                      and (args.fuse or lm == gl[5]))
+            led_ok = led_ok and total == int(g[args.golden_ledger + "_csum"][0])
+            print(f"[summa_worker] golden ledger {args.golden_ledger}: bcasts {bc}/{q} vs {gl[0] + gl[1]}, "
+                  f"size exchanges {sx}/{q} vs {gl[4]}, multiplies {lm} vs {gl[5]}, skipped {sk} vs {gl[6]}: "
+                  f"ledger_ok={led_ok}", flush=True)
+            allok = allok and led_ok
         print(f"[summa_worker] grid {pr}x{pc} sr={args.sr} s{args.scale} two_round={args.two_round} "
               f"mode={args.mode} fuse={args.fuse}: blocks_ok={allok} checksum_ok={cs_ok} ledger0={led}", flush=True)
         if not (allok and cs_ok):

@@ -42,6 +42,32 @@ def test_summa_host_path_chunked_staging():
     assert "blocks_ok=True checksum_ok=True" in out
 
 
+@pytest.mark.parametrize("grid", ["1x2", "2x2", "2x4", "1x4"])
+@pytest.mark.parametrize("fuse", [1, 0])
+def test_summa_grids_on_one_gpu_host_path(grid, fuse):
+    """Every BASELINE grid shape, its ranks sharing the box's GPU(s) when
+    there are fewer GPUs than ranks (no NCCL then: host-path broadcasts
+    through the pinned shared-memory staging): schedule, panel slicing, size
+    exchanges, broadcasts, fused or per-stage multiplies + merge, checked
+    block by block against the oracle."""
+    pr, pc = (int(x) for x in grid.split("x"))
+    out = run_worker(pr * pc, "--sr", 4, "--scale", 10, "--grid", grid, "--fuse", fuse, "--mode", 0)
+    assert "blocks_ok=True checksum_ok=True" in out
+
+
+@pytest.mark.parametrize("sr", [1, 2, 4])
+@pytest.mark.parametrize("two_round", [1, 0])
+def test_summa_2x2_ledger_matches_reference(sr, two_round):
+    """p = 4 (2 x 2) summa25_multiply of the golden R-MAT (scale 9, edge factor
+    8, seed 3) in the reference structure (per-stage multiplies + merge): the
+    distributed counters — broadcasts, size exchanges, local multiplies,
+    skipped stages — and the checksum of C equal the reference's
+    (tests/golden/make_golden.py section 6)."""
+    out = run_worker(4, "--sr", sr, "--scale", 9, "--ef", 8, "--seed", 3, "--grid", "2x2", "--fuse", 0,
+                     "--mode", 0, "--two-round", two_round, "--golden-ledger", f"summa_{sr}_p4_r{two_round}")
+    assert "ledger_ok=True" in out and "blocks_ok=True checksum_ok=True" in out
+
+
 @pytest.mark.parametrize("grid", ["1x4", "4x1", "1x2", "2x1"])
 def test_summa_rectangular_grids(grid):
     """Non-square grids use the common-refinement stage schedule."""
