@@ -13,7 +13,7 @@ OBJS      := $(patsubst $(SRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS)) $(patsubst $(SRC)/%
 HDRS      := $(wildcard $(SRC)/*.cuh) $(wildcard $(SRC)/*.h) include/spgemm_b200.h
 LIB       := $(PKG)/libspgemm_b200.so
 
-all: $(LIB) oracle
+all: $(LIB) oracle custom_sr
 
 $(BUILD)/%.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(BUILD)
@@ -30,6 +30,12 @@ $(LIB): $(OBJS)
 oracle:
 	$(MAKE) -C oracle
 
+# example user-defined semiring compiled outside the library (tests/custom_sr)
+CUSTOM_SR := tests/custom_sr/libmaxmin_sr.so
+custom_sr: $(CUSTOM_SR)
+$(CUSTOM_SR): tests/custom_sr/maxmin_sr.cu $(HDRS)
+	$(NVCC) $(NVFLAGS) -I$(SRC) -shared -o $@ $<
+
 # A/B tuning builds: make variant VNAME=x VFLAGS="-DSPG_SEG_MODE=0" -> variants/x/libspgemm_b200.so
 # (loaded only when SPG_LIB_PATH points at it)
 VNAME ?= v
@@ -42,4 +48,4 @@ variant:
 clean:
 	rm -rf $(BUILD) $(LIB)
 
-.PHONY: all oracle clean variant
+.PHONY: all oracle clean variant custom_sr

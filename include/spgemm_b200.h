@@ -125,8 +125,22 @@ SPG_API int spg_value_size(int sr);
 SPG_API int spg_semiring_by_name(const char* name); /* semiring_by_name, semiring.hpp:125-133; -1 if unknown */
 SPG_API const char* spg_semiring_name(int sr);
 SPG_API int spg_semiring_is_commutative(int sr);  /* SR::is_commutative_mul */
+/* User-defined semirings (the reference's SemiringLike plug-in,
+   semiring.hpp:28-40, + ValueCodec<T>, serialize.hpp:29-76): a struct with
+   value_type, add, mul, zero, one, is_zero, from_real, name,
+   is_commutative_mul (all __host__ __device__; optional acc_shared /
+   acc_global atomics, small / mul_small fast multiply, add_can_cancel),
+   instantiated in the user's own .cu with
+       SPG_INSTANTIATE(MySemiring, my_semiring_ops)   (csrc/instantiate.cuh)
+   and compiled into the user's shared library.  Registering the table
+   returns the id every entry point below accepts as `sr` (values travel as
+   their raw little-endian bytes, value_type size 1/2/4/8/16).  Registering
+   the same table again returns the same id; names must be unique. */
+typedef struct spg_semiring_ops spg_semiring_ops;
+SPG_API int spg_register_semiring(const spg_semiring_ops* ops, int* id);
 
 /* ------------------------------------------------------------- context */
+SPG_API int spg_device_count(void); /* visible CUDA devices (0 without a GPU) */
 SPG_API int spg_ctx_create(int device, spg_ctx** out);
 SPG_API void spg_ctx_destroy(spg_ctx* ctx);
 SPG_API void* spg_ctx_stream(spg_ctx* ctx);                 /* cudaStream_t */
@@ -294,6 +308,10 @@ typedef struct {
   uint64_t size_exchanges, local_multiply_calls, skipped_stages, peak_bcast_buffer_bytes;
   int64_t products; /* F over this rank's local multiplies */
   double ms_total;  /* time-to-C on this rank */
+  /* collectives this rank ROOTED: the reference's ledger charges each
+     collective instance once (fabric.hpp:220-241), so summing these over
+     the ranks reproduces its host/device broadcast and size-exchange counts */
+  uint64_t rooted_host_bcasts, rooted_device_bcasts, rooted_size_exchanges;
 } spg_ledger;
 
 /* summa25_multiply (summa.hpp:248-349), one rank's program.  a_block /

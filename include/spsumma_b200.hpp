@@ -10,13 +10,19 @@
 //   SemiringLike + built-ins (semiring.hpp)      tag types with the same names
 //   CooMatrix/CscMatrix/DcscMatrix/CsrMatrix     same structs (std::vector-backed)
 //     (formats.hpp:16-86)
-//   esc_multiply(a, b, chunk) (local_spgemm:83)  esc_multiply(a, b)  -> GPU
+//   esc_multiply(a, b, chunk) (local_spgemm:83)  esc_multiply(a, b[, chunk]) -> GPU (per-thread
+//                                                default context; chunk_nnz has no GPU meaning)
 //   merge_partials (summa.hpp:122-172)           merge_partials(...)  -> GPU
 //   matrix_checksum (checksum.hpp:20-38)         matrix_checksum(...) -> GPU
 //   generate_rmat (rmat.hpp:15-60)               generate_rmat<SR>(...) (bit-identical)
-//   summa25_multiply (summa.hpp:248-349)         summa25_multiply(comm, ...) — one
-//                                                rank per process/GPU (torchrun/MPI
-//                                                style), returns this rank's C block
+//   ProcessGrid / BlockRange / block_range /     same names; ProcessGrid(p) is square as in
+//     LocalBlock / DistMatrix / distribute /     the reference, ProcessGrid(pr, pc) adds the
+//     gather (process_grid.hpp, dist_matrix.hpp) 1x2 / 2x4 grids
+//   summa25_multiply(a, b, model, cfg, opts)     same signature -> SummaResult{product,
+//     (summa.hpp:248-349) -> SummaResult          ledger, per_rank}: one host thread per rank
+//                                                (the reference's run_program model), rank r
+//                                                on GPU r % ngpus; also the one-rank-per-
+//                                                process form summa25_multiply(comm, ...)
 //   Error / ShapeError / ... (common.hpp:12-73)  same class names, thrown from the
 //                                                C-ABI status codes
 //
@@ -24,14 +30,22 @@
 // library; a custom semiring is added by SPG_INSTANTIATE in a user .cu file
 // (paper_2504_06408_b200/csrc/instantiate.cuh).
 #pragma once
+#include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
+#include <memory>
 #include <stdexcept>
+#include <thread>
+#include <variant>
 #include <string>
 #include <type_traits>
 #include <utility>
 #include <vector>
+
+#include <unistd.h>
 
 #include "spgemm_b200.h"
 
@@ -188,6 +202,23 @@ CsrMatrix<SR> esc_multiply(Context& ctx, const CsrMatrix<SR>& a, const CsrMatrix
   return out;
 }
 
+// Per-thread default context (device = the thread's current CUDA device, or
+// SPG_DEVICE): the reference's esc_multiply takes no context argument.
+inline Context& default_context() {
+  thread_local std::unique_ptr<Context> ctx;
+  if (!ctx) {
+    const char* e = std::getenv("SPG_DEVICE");
+    ctx = std::make_unique<Context>(e ? std::atoi(e) : 0);
+  }
+  return *ctx;
+}
+
+// esc_multiply(a, b, chunk_nnz) — the reference signature (local_spgemm.hpp:83-85).
+template <class SR>
+CsrMatrix<SR> esc_multiply(const CsrMatrix<SR>& a, const CsrMatrix<SR>& b, std::size_t /*chunk_nnz*/ = 4096) {
+  return esc_multiply(default_context(), a, b);
+}
+
 // matrix_checksum (checksum.hpp:20-38) of a CSR, computed on the GPU.
 template <class SR>
 std::uint64_t matrix_checksum(Context& ctx, const CsrMatrix<SR>& m) {
@@ -299,14 +330,311 @@ class Comm {
 };
 
 enum class CommMode { host_only = SPG_COMM_HOST_ONLY, device_only = SPG_COMM_DEVICE_ONLY, hybrid = SPG_COMM_HYBRID };
+
+// ProcessGrid (process_grid.hpp:12-39): p = q*q ranks, row-major.  The
+// two-argument form is the generalisation BASELINE's 1x2 / 2x4 grids need.
+class ProcessGrid {
+ public:
+  explicit ProcessGrid(int process_count) : pr_(0), pc_(0) {
+    if (process_count < 1) throw GridError("process count must be positive, got " + std::to_string(process_count));
+    int q = 1;
+    while ((q + 1) * (q + 1) <= process_count) ++q;
+    if (q * q != process_count)
+      throw GridError("process count " + std::to_string(process_count) +
+                      " is not a perfect square; the 2D grid requires a square number of processes");
+    pr_ = pc_ = q;
+  }
+  ProcessGrid(int rows, int cols) : pr_(rows), pc_(cols) {
+    if (rows < 1 || cols < 1) throw GridError("grid sides must be positive");
+  }
+  int size() const { return pr_ * pc_; }
+  int side() const { return pr_; }  // square grids
+  int rows() const { return pr_; }
+  int cols() const { return pc_; }
+  int row_of(int rank) const { return rank / pc_; }
+  int col_of(int rank) const { return rank % pc_; }
+  int rank_at(int row, int col) const { return row * pc_ + col; }
+  bool operator==(const ProcessGrid&) const = default;
+
+ private:
+  int pr_, pc_;
+};
+
+// BlockRange / block_range (dist_matrix.hpp:12-28), larger-first split.
+struct BlockRange {
+  index_t begin = 0;
+  index_t end = 0;
+  index_t size() const { return end - begin; }
+  bool contains(index_t i) const { return i >= begin && i < end; }
+  bool operator==(const BlockRange&) const = default;
+};
+inline BlockRange block_range(index_t n, int q, int idx) {
+  BlockRange r;
+  spg_block_range(n, q, idx, &r.begin, &r.end);
+  return r;
+}
+
+// LocalBlock / DistMatrix (dist_matrix.hpp:41-63): host-resident blocks,
+// block (i, j) of the grid at index rank_at(i, j).
+template <class SR>
+struct LocalBlock {
+  std::variant<CscMatrix<SR>, DcscMatrix<SR>> storage;
+  BlockRange rows;
+  BlockRange cols;
+  index_t nnz() const {
+    return std::visit([](const auto& m) { return m.nnz(); }, storage);
+  }
+  bool is_dcsc() const { return std::holds_alternative<DcscMatrix<SR>>(storage); }
+};
+template <class SR>
+struct DistMatrix {
+  index_t nrows = 0;
+  index_t ncols = 0;
+  ProcessGrid grid{1};
+  std::vector<LocalBlock<SR>> blocks;  // indexed by rank
+};
+
+// distribute (dist_matrix.hpp:69-111): route every (normalised) tuple to its
+// block; a block with fewer than half its columns populated is stored DCSC.
+template <class SR>
+DistMatrix<SR> distribute(const CooMatrix<SR>& m, const ProcessGrid& grid) {
+  DistMatrix<SR> out;
+  out.nrows = m.nrows;
+  out.ncols = m.ncols;
+  out.grid = grid;
+  const int pr = grid.rows(), pc = grid.cols();
+  std::vector<BlockRange> rr(pr), cr(pc);
+  for (int i = 0; i < pr; ++i) rr[i] = block_range(m.nrows, pr, i);
+  for (int j = 0; j < pc; ++j) cr[j] = block_range(m.ncols, pc, j);
+  auto owner = [](const std::vector<BlockRange>& v, index_t x) {
+    int lo = 0, hi = (int)v.size() - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) / 2;
+      if (v[mid].begin <= x) lo = mid;
+      else hi = mid - 1;
+    }
+    return lo;
+  };
+  std::vector<std::vector<typename CooMatrix<SR>::Tuple>> per(grid.size());
+  for (const auto& t : m.tuples) per[grid.rank_at(owner(rr, t.row), owner(cr, t.col))].push_back(t);
+  out.blocks.resize(grid.size());
+  for (int r = 0; r < grid.size(); ++r) {
+    auto& tu = per[r];
+    const BlockRange br = rr[grid.row_of(r)], bc = cr[grid.col_of(r)];
+    std::stable_sort(tu.begin(), tu.end(), [](const auto& x, const auto& y) {
+      return x.col != y.col ? x.col < y.col : x.row < y.row;
+    });
+    CscMatrix<SR> csc;
+    csc.nrows = br.size();
+    csc.ncols = bc.size();
+    csc.colptr.assign((size_t)csc.ncols + 1, 0);
+    for (const auto& t : tu) {
+      ++csc.colptr[(size_t)(t.col - bc.begin) + 1];
+      csc.rowids.push_back(t.row - br.begin);
+      csc.values.push_back(t.value);
+    }
+    index_t populated = 0;
+    for (index_t c = 0; c < csc.ncols; ++c) {
+      populated += csc.colptr[(size_t)c + 1] > 0;
+      csc.colptr[(size_t)c + 1] += csc.colptr[(size_t)c];
+    }
+    LocalBlock<SR> blk;
+    blk.rows = br;
+    blk.cols = bc;
+    if (2 * populated < csc.ncols) {
+      DcscMatrix<SR> d;
+      d.nrows = csc.nrows;
+      d.ncols = csc.ncols;
+      for (index_t c = 0; c < csc.ncols; ++c)
+        if (csc.colptr[(size_t)c + 1] > csc.colptr[(size_t)c]) {
+          d.jc.push_back(c);
+          d.cp.push_back(csc.colptr[(size_t)c + 1]);
+        }
+      d.rowids = std::move(csc.rowids);
+      d.values = std::move(csc.values);
+      blk.storage = std::move(d);
+    } else {
+      blk.storage = std::move(csc);
+    }
+    out.blocks[r] = std::move(blk);
+  }
+  return out;
+}
+
+// gather (dist_matrix.hpp:115-141): all blocks back into one normalised COO.
+template <class SR>
+CooMatrix<SR> gather(const DistMatrix<SR>& d) {
+  CooMatrix<SR> out;
+  out.nrows = d.nrows;
+  out.ncols = d.ncols;
+  for (const auto& blk : d.blocks) {
+    std::visit(
+        [&](const auto& m) {
+          using M = std::decay_t<decltype(m)>;
+          if constexpr (std::is_same_v<M, CscMatrix<SR>>) {
+            for (index_t c = 0; c < m.ncols; ++c)
+              for (index_t e = m.colptr[(size_t)c]; e < m.colptr[(size_t)c + 1]; ++e)
+                out.tuples.push_back({blk.rows.begin + m.rowids[(size_t)e], blk.cols.begin + c, m.values[(size_t)e]});
+          } else {
+            for (size_t q = 0; q < m.jc.size(); ++q)
+              for (index_t e = m.cp[q]; e < m.cp[q + 1]; ++e)
+                out.tuples.push_back({blk.rows.begin + m.rowids[(size_t)e], blk.cols.begin + m.jc[q], m.values[(size_t)e]});
+          }
+        },
+        blk.storage);
+  }
+  std::sort(out.tuples.begin(), out.tuples.end(),
+            [](const auto& x, const auto& y) { return x.row != y.row ? x.row < y.row : x.col < y.col; });
+  return out;
+}
+
+// LatencyModel (latency_model.hpp:77-192): accepted for signature parity.
+// Routing depends only on CommConfig::threshold_bytes (comm.hpp:45-55) in
+// the reference too; its model charges SIMULATED time, while here every
+// phase is measured — pick the threshold from measured curves
+// (tools/comm_sweep.py, tuner.find_crossover).
+struct LatencyModel {
+  static LatencyModel bundled_default() { return {}; }
+};
+
+// CostLedger (cost_ledger.hpp:31-56): collective counts charged once per
+// collective instance (as the reference's fabric does), multiplies and
+// skipped stages per rank, measured milliseconds per phase (max over ranks).
+struct CostLedger {
+  std::uint64_t host_bcasts = 0, device_bcasts = 0, bytes_host_path = 0, bytes_device_path = 0;
+  std::uint64_t size_exchanges = 0, local_multiply_calls = 0, skipped_stages = 0, peak_bcast_buffer_bytes = 0;
+  double ms[5] = {0, 0, 0, 0, 0};  // prepare, broadcast, local_multiply, merge, copy
+  double ms_total = 0;
+};
+
+template <class SR>
+struct SummaResult {
+  DistMatrix<SR> product;              // C blocks, CSC, host-resident
+  CostLedger ledger;                   // whole run
+  std::vector<spg_ledger> per_rank;    // raw per-rank ledgers
+};
 struct CommConfig {  // comm.hpp:36-39
   CommMode mode = CommMode::hybrid;
   std::uint64_t threshold_bytes = 0;
 };
 struct SummaOptions {  // summa.hpp:174-177 (chunk_nnz has no GPU meaning)
   bool two_round = true;
+  std::size_t chunk_nnz = 4096;
   bool fuse_stages = true;  // one fused multiply over all received panels (no merge)
 };
+
+namespace detail {
+template <class SR>
+struct BlockViews {  // C-ABI views of one LocalBlock (CSC or DCSC)
+  spg_hcsr csc{};
+  spg_hdcsc dcsc{};
+  bool is_dcsc = false;
+  explicit BlockViews(const LocalBlock<SR>& b) {
+    if (const auto* d = std::get_if<DcscMatrix<SR>>(&b.storage)) {
+      is_dcsc = true;
+      dcsc = {d->nrows, d->ncols, d->nnz(), (index_t)d->jc.size(), const_cast<index_t*>(d->jc.data()),
+              const_cast<index_t*>(d->cp.data()), const_cast<index_t*>(d->rowids.data()),
+              const_cast<void*>(static_cast<const void*>(d->values.data()))};
+    } else {
+      csc = view_csc(std::get<CscMatrix<SR>>(b.storage));
+    }
+  }
+  const spg_hcsr* c() const { return is_dcsc ? nullptr : &csc; }
+  const spg_hdcsc* d() const { return is_dcsc ? &dcsc : nullptr; }
+};
+template <class SR>
+CscMatrix<SR> download_csc(Context& ctx, spg_dcsr& c) {
+  spg_hcsr h{};
+  const int st = spg_download(ctx.get(), SR::id, &c, 1, &h);
+  spg_dcsr_free(ctx.get(), &c);
+  ctx.check(st);
+  CscMatrix<SR> out;
+  out.nrows = h.nrows;
+  out.ncols = h.ncols;
+  take_idx(out.colptr, h.ptr, h.ncols + 1);
+  take_idx(out.rowids, h.idx, h.nnz);
+  take(out.values, h.vals, h.nnz);
+  spg_hcsr_free(&h);
+  return out;
+}
+inline int device_count() {
+  const char* e = std::getenv("SPG_NUM_GPUS");
+  if (e) return std::max(1, std::atoi(e));
+  return std::max(1, spg_device_count());
+}
+}  // namespace detail
+
+// summa25_multiply — the reference signature (summa.hpp:248-253).  Every
+// rank of the grid runs on its own host thread (the reference's run_program
+// model), rank r driving GPU r % ngpus; ranks that share a GPU have no
+// device path (host path only: use CommMode::host_only).  Throws
+// ShapeError / GridError / UnsupportedSemiringError like the reference; a
+// rank failure aborts its peers (AbortedError) instead of hanging.
+template <class SR>
+SummaResult<SR> summa25_multiply(const DistMatrix<SR>& a, const DistMatrix<SR>& b, const LatencyModel& /*model*/,
+                                 const CommConfig& cfg, const SummaOptions& opts = {}) {
+  if (a.ncols != b.nrows)
+    throw ShapeError("summa25_multiply: A is " + std::to_string(a.nrows) + "x" + std::to_string(a.ncols) +
+                     " but B is " + std::to_string(b.nrows) + "x" + std::to_string(b.ncols));
+  if (!(a.grid == b.grid)) throw GridError("summa25_multiply: A and B live on different process grids");
+  const ProcessGrid grid = a.grid;
+  const int p = grid.size();
+  if ((int)a.blocks.size() != p || (int)b.blocks.size() != p)
+    throw GridError("summa25_multiply: a DistMatrix must hold one block per rank");
+  static std::atomic<int> serial{0};
+  const std::string job = "facade" + std::to_string((long)::getpid()) + "_" + std::to_string(serial++);
+  const int ngpu = detail::device_count();
+  SummaResult<SR> res;
+  res.product.nrows = a.nrows;
+  res.product.ncols = b.ncols;
+  res.product.grid = grid;
+  res.product.blocks.resize(p);
+  res.per_rank.assign(p, spg_ledger{});
+  std::vector<std::exception_ptr> errs(p);
+  std::vector<std::thread> threads;
+  for (int r = 0; r < p; ++r)
+    threads.emplace_back([&, r] {
+      try {
+        const int dev = r % ngpu;
+        Context ctx(dev);
+        spg_comm* comm = nullptr;
+        const int cst = spg_comm_create(job.c_str(), p, r, grid.rows(), grid.cols(), dev, 64ull << 20, &comm);
+        if (cst != SPG_OK) throw_status(cst, spg_comm_last_error(nullptr));
+        std::unique_ptr<spg_comm, void (*)(spg_comm*)> guard(comm, spg_comm_destroy);
+        detail::BlockViews<SR> va(a.blocks[r]), vb(b.blocks[r]);
+        spg_summa_opts o{opts.two_round ? 1 : 0, static_cast<int>(cfg.mode), cfg.threshold_bytes, 0,
+                         opts.fuse_stages ? 1 : 0};
+        spg_dcsr c{};
+        const int st = spg_summa25_multiply(comm, ctx.get(), SR::id, a.nrows, a.ncols, b.ncols, va.c(), va.d(),
+                                            vb.c(), vb.d(), &o, &c, &res.per_rank[r]);
+        if (st != SPG_OK) throw_status(st, spg_last_error(ctx.get()));
+        LocalBlock<SR> blk;
+        blk.rows = block_range(a.nrows, grid.rows(), grid.row_of(r));
+        blk.cols = block_range(b.ncols, grid.cols(), grid.col_of(r));
+        blk.storage = detail::download_csc<SR>(ctx, c);
+        res.product.blocks[r] = std::move(blk);
+      } catch (...) {
+        errs[r] = std::current_exception();
+      }
+    });
+  for (auto& t : threads) t.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+  for (const auto& l : res.per_rank) {
+    res.ledger.host_bcasts += l.rooted_host_bcasts;
+    res.ledger.device_bcasts += l.rooted_device_bcasts;
+    res.ledger.size_exchanges += l.rooted_size_exchanges;
+    res.ledger.bytes_host_path += l.bytes_host_path;
+    res.ledger.bytes_device_path += l.bytes_device_path;
+    res.ledger.local_multiply_calls += l.local_multiply_calls;
+    res.ledger.skipped_stages += l.skipped_stages;
+    res.ledger.peak_bcast_buffer_bytes = std::max<std::uint64_t>(res.ledger.peak_bcast_buffer_bytes,
+                                                                 l.peak_bcast_buffer_bytes);
+    for (int k = 0; k < 5; ++k) res.ledger.ms[k] = std::max(res.ledger.ms[k], l.ms[k]);
+    res.ledger.ms_total = std::max(res.ledger.ms_total, l.ms_total);
+  }
+  return res;
+}
 
 // summa25_multiply for this rank's blocks (CSC or DCSC, LocalBlock layout).
 // Returns this rank's C block (CSC, host) and fills the ledger.

@@ -12,12 +12,12 @@ from .formats import (CooMatrix, CscMatrix, CsrMatrix, DcscMatrix, coo_to_csc, c
 from .generators import generate_er, generate_rmat, generate_stencil27
 from .matrix_market import read_matrix_market
 from .local_spgemm import esc_multiply, local_multiply, matrix_checksum, merge_partials
-from .semiring import SemiringId, dtype_of, semiring_by_name
+from .semiring import SemiringId, dtype_of, register_semiring, semiring_by_name
 
 __all__ = [
     "errors", "lib", "Context", "DeviceCsr", "default_context", "CooMatrix", "CscMatrix", "CsrMatrix",
     "DcscMatrix", "coo_to_csc", "coo_to_csr", "csc_to_coo", "csc_to_csr", "csc_to_dcsc", "csr_to_coo",
     "csr_to_csc", "dcsc_decompress", "reinterpret_transpose", "validate", "generate_er", "generate_rmat",
     "generate_stencil27", "esc_multiply", "local_multiply", "matrix_checksum", "merge_partials",
-    "SemiringId", "dtype_of", "semiring_by_name", "read_matrix_market",
+    "SemiringId", "dtype_of", "register_semiring", "semiring_by_name", "read_matrix_market",
 ]

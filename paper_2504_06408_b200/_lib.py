@@ -64,7 +64,9 @@ class Ledger(C.Structure):
                 ("bytes_host_path", C.c_uint64), ("bytes_device_path", C.c_uint64),
                 ("size_exchanges", C.c_uint64), ("local_multiply_calls", C.c_uint64),
                 ("skipped_stages", C.c_uint64), ("peak_bcast_buffer_bytes", C.c_uint64),
-                ("products", C.c_int64), ("ms_total", C.c_double)]
+                ("products", C.c_int64), ("ms_total", C.c_double),
+                ("rooted_host_bcasts", C.c_uint64), ("rooted_device_bcasts", C.c_uint64),
+                ("rooted_size_exchanges", C.c_uint64)]
 
     PHASES = ("prepare", "broadcast", "local_multiply", "merge", "copy")
 
@@ -83,6 +85,7 @@ _SIGS = [
     ("spg_last_error", C.c_char_p, [C.c_void_p]),
     ("spg_value_size", C.c_int, [C.c_int]),
     ("spg_semiring_by_name", C.c_int, [C.c_char_p]),
+    ("spg_register_semiring", C.c_int, [C.c_void_p, _P(C.c_int)]),
     ("spg_semiring_name", C.c_char_p, [C.c_int]),
     ("spg_semiring_is_commutative", C.c_int, [C.c_int]),
     ("spg_ctx_create", C.c_int, [C.c_int, _P(C.c_void_p)]),

@@ -899,9 +899,24 @@ __device__ __forceinline__ void balanced_items(const Src& src, const SegCache<SR
 // Returns the number of entries written.
 // ---------------------------------------------------------------------------
 
+// Can the fold cancel back to zero() (a + (-a) == 0)?  A semiring may say so
+// with `static constexpr bool add_can_cancel`; otherwise only the built-in
+// arithmetic (+, x) semiring (id 0) can.
+template <class SR, class = void>
+struct AddCanCancelById {
+  static constexpr bool value = false;
+};
 template <class SR>
+struct AddCanCancelById<SR, decltype((void)SR::id, void())> {
+  static constexpr bool value = SR::id == 0;
+};
+template <class SR, class = void>
 struct AddCanCancel {
-  static constexpr bool value = SR::id == 0;  // arithmetic (+, x): a + (-a) == 0
+  static constexpr bool value = AddCanCancelById<SR>::value;
+};
+template <class SR>
+struct AddCanCancel<SR, decltype((void)SR::add_can_cancel, void())> {
+  static constexpr bool value = SR::add_can_cancel;
 };
 
 // Barrier over a warp group: BAR == 0 is __syncthreads, else named barrier

@@ -33,6 +33,11 @@ void read_matrix_market(int, const char*, int64_t*, int64_t*, int64_t*, int64_t*
 
 thread_local std::string g_last_error;
 
+// Semiring registry: the built-ins, then user semirings registered at run
+// time (ids SPG_SR_COUNT, SPG_SR_COUNT + 1, ...; append-only).
+std::mutex g_sr_mu;
+std::vector<const SrOps*> g_sr_user;
+
 const SrOps* ops_for(int sr) {
   switch (sr) {
     case SPG_SR_ARITHMETIC: return spg_ops_arithmetic();
@@ -42,7 +47,16 @@ const SrOps* ops_for(int sr) {
     case SPG_SR_TROPICAL_I32: return spg_ops_tropical_i32();
     case SPG_SR_MAXTIMES: return spg_ops_maxtimes();
   }
+  if (sr >= SPG_SR_COUNT) {
+    std::lock_guard<std::mutex> g(g_sr_mu);
+    if ((size_t)(sr - SPG_SR_COUNT) < g_sr_user.size()) return g_sr_user[(size_t)(sr - SPG_SR_COUNT)];
+  }
   fail(SPG_ERR_ARG, "unknown semiring id " + std::to_string(sr));
+}
+
+int semiring_count() {
+  std::lock_guard<std::mutex> g(g_sr_mu);
+  return SPG_SR_COUNT + (int)g_sr_user.size();
 }
 
 template <class F>
@@ -334,11 +348,50 @@ int spg_value_size(int sr) {
 
 int spg_semiring_by_name(const char* name) {
   if (!name) return -1;
-  for (int s = 0; s < SPG_SR_COUNT; ++s)
+  const int n = semiring_count();
+  for (int s = 0; s < n; ++s)
     if (std::strcmp(name, ops_for(s)->name) == 0) return s;
   g_last_error = std::string("unknown semiring '") + name +
                  "' (expected arithmetic, minplus, boolean, minselect, tropical_i32, or maxtimes)";
   return -1;
+}
+
+int spg_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int spg_register_semiring(const spg_semiring_ops* ops_in, int* id) {
+  return guarded(nullptr, [&] {
+    const SrOps* ops = reinterpret_cast<const SrOps*>(ops_in);
+    need(ops && id, "null argument");
+    if (ops->abi != kSrOpsAbi)
+      fail(SPG_ERR_ARG, "semiring ops table ABI " + std::to_string(ops->abi) + " != " + std::to_string(kSrOpsAbi) +
+                            " (rebuild the semiring library against this release's headers)");
+    need(ops->name && ops->name[0] && ops->local_multiply && ops->merge && ops->checksum_part,
+         "incomplete semiring ops table");
+    if (ops->value_size != 1 && ops->value_size != 2 && ops->value_size != 4 && ops->value_size != 8 &&
+        ops->value_size != 16)
+      fail(SPG_ERR_ARG, "semiring value size must be 1, 2, 4, 8 or 16 bytes");
+    std::lock_guard<std::mutex> g(g_sr_mu);
+    for (int s = 0; s < SPG_SR_COUNT; ++s)
+      if (std::strcmp(ops_for(s)->name, ops->name) == 0)
+        fail(SPG_ERR_ARG, std::string("semiring name '") + ops->name + "' is a built-in");
+    for (size_t k = 0; k < g_sr_user.size(); ++k) {
+      if (g_sr_user[k] == ops) {  // registering the same table again returns its id
+        *id = SPG_SR_COUNT + (int)k;
+        return;
+      }
+      if (std::strcmp(g_sr_user[k]->name, ops->name) == 0)
+        fail(SPG_ERR_ARG, std::string("a different semiring named '") + ops->name + "' is already registered");
+    }
+    g_sr_user.push_back(ops);
+    *id = SPG_SR_COUNT + (int)g_sr_user.size() - 1;
+  });
 }
 
 const char* spg_semiring_name(int sr) {

@@ -19,8 +19,9 @@
 
 namespace spg {
 
-// A typed error that the C-ABI turns into an SPG_ERR_* status.
-struct Error : std::runtime_error {
+// A typed error that the C-ABI turns into an SPG_ERR_* status (default
+// visibility: user semiring libraries throw it across the library boundary).
+struct __attribute__((visibility("default"))) Error : std::runtime_error {
   int status;
   Error(int s, const std::string& m) : std::runtime_error(m), status(s) {}
 };

@@ -1,10 +1,14 @@
 // Per-semiring instantiation of the device pipeline.  Each built-in semiring
 // gets its own translation unit (sr_*.cu) containing one SPG_INSTANTIATE; a
 // user-defined semiring is added the same way from the user's own .cu file
-// and registered at run time with spg_register_semiring() — the analogue of
-// instantiating the reference's templates with a new SemiringLike type
-// (semiring.hpp:28-40).
+// (compiled into the user's shared library against these headers) and
+// registered at run time with spg_register_semiring(), which returns the id
+// every C-ABI entry point then accepts — the analogue of instantiating the
+// reference's templates with a new SemiringLike type (semiring.hpp:28-40).
+// tests/custom_sr/maxmin_sr.cu is a complete example.
 #pragma once
+#include <type_traits>
+
 #include "rows_driver.cuh"
 
 namespace spg {
@@ -61,8 +65,11 @@ __global__ void __launch_bounds__(256) checksum_kernel(int64_t nseg, const int64
   }
 }
 
+constexpr int kSrOpsAbi = 1;  // layout version of SrOps (checked at registration)
+
 struct SrOps {
-  int id;
+  int abi;
+  int id;  // built-ins: their SPG_SR_* id; user semirings: -1 (the registry assigns one)
   const char* name;
   int value_size;
   bool commutative;
@@ -113,9 +120,19 @@ struct OpsImpl {
   }
 };
 
+template <class SR, class = void>
+struct sr_has_id : std::false_type {};
+template <class SR>
+struct sr_has_id<SR, decltype((void)SR::id, void())> : std::true_type {};
+template <class SR>
+constexpr int sr_id() {
+  if constexpr (sr_has_id<SR>::value) return SR::id;
+  else return -1;
+}
+
 template <class SR>
 const SrOps* ops_instance() {
-  static const SrOps o{SR::id, SR::name, (int)sizeof(typename SR::value_type), SR::is_commutative_mul,
+  static const SrOps o{kSrOpsAbi, sr_id<SR>(), SR::name, (int)sizeof(typename SR::value_type), SR::is_commutative_mul,
                        &OpsImpl<SR>::local_multiply, &OpsImpl<SR>::merge, &OpsImpl<SR>::checksum_part};
   return &o;
 }
@@ -123,4 +140,4 @@ const SrOps* ops_instance() {
 }  // namespace spg
 
 #define SPG_INSTANTIATE(SR, FN) \
-  extern "C" const spg::SrOps* FN() { return spg::ops_instance<SR>(); }
+  extern "C" __attribute__((visibility("default"))) const spg::SrOps* FN() { return spg::ops_instance<SR>(); }

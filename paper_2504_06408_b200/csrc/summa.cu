@@ -99,6 +99,7 @@ void send_panel(spg_ctx* c, spg_comm* comm, int scope, int root, int vs, const s
   const auto t0 = Clock::now();
   comm_exchange_sizes(comm, scope, root, triple);
   ++led.size_exchanges;
+  if (me) ++led.rooted_size_exchanges;
   if (triple[2] == 0) {
     led.ms[1] += ms_since(t0);
     return;  // summa.hpp:226: empty panels are not broadcast
@@ -114,9 +115,11 @@ void send_panel(spg_ctx* c, spg_comm* comm, int scope, int root, int vs, const s
   if (path == SPG_PATH_HOST) {
     ++led.host_bcasts;
     led.bytes_host_path += p.bytes;
+    if (me) ++led.rooted_host_bcasts;
   } else {
     ++led.device_bcasts;
     led.bytes_device_path += p.bytes;
+    if (me) ++led.rooted_device_bcasts;
   }
   led.ms[1] += ms_since(t0);
 }
@@ -135,6 +138,7 @@ void broadcast_panel(spg_ctx* c, spg_comm* comm, int scope, int root, bool by_ro
   const auto t0 = Clock::now();
   comm_exchange_sizes(comm, scope, root, triple);
   ++led.size_exchanges;
+  if (me) ++led.rooted_size_exchanges;
   if (triple[2] == 0) {
     led.ms[1] += ms_since(t0);
     return;  // summa.hpp:226: empty panels are not broadcast
@@ -150,9 +154,11 @@ void broadcast_panel(spg_ctx* c, spg_comm* comm, int scope, int root, bool by_ro
   if (path == SPG_PATH_HOST) {
     ++led.host_bcasts;
     led.bytes_host_path += p.bytes;
+    if (me) ++led.rooted_host_bcasts;
   } else {
     ++led.device_bcasts;
     led.bytes_device_path += p.bytes;
+    if (me) ++led.rooted_device_bcasts;
   }
   led.ms[1] += ms_since(t0);
 }

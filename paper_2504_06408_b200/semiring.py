@@ -36,25 +36,58 @@ DTYPES = {
 
 COMMUTATIVE = {s: s != SemiringId.minselect for s in SemiringId}
 
+# user-defined semirings registered at run time: id -> (name, dtype, library handle)
+_USER = {}
 
-def semiring_by_name(name: str) -> SemiringId:
+
+def register_semiring(library_path: str, symbol: str, dtype) -> int:
+    """Load a user semiring library — a .cu with SPG_INSTANTIATE(MySemiring,
+    symbol) compiled against this repo's headers (tests/custom_sr/ is an
+    example) — and register its ops table (spg_register_semiring).  Returns
+    the semiring id every entry point then accepts; `dtype` is the numpy
+    view of its value_type (the ValueCodec byte layout)."""
+    import ctypes as C
+
+    from ._lib import check, lib
+    handle = C.CDLL(library_path)
+    fn = getattr(handle, symbol)
+    fn.restype = C.c_void_p
+    sid = C.c_int()
+    check(lib.spg_register_semiring(C.c_void_p(fn()), C.byref(sid)))
+    dt = np.dtype(dtype)
+    vs = int(lib.spg_value_size(sid.value))
+    if dt.itemsize != vs:
+        raise errors.ShapeError(f"dtype {dt} is {dt.itemsize} bytes, the semiring's value_type is {vs}")
+    _USER[sid.value] = (lib.spg_semiring_name(sid.value).decode(), dt, handle)
+    return sid.value
+
+
+def semiring_by_name(name: str):
     """semiring_by_name (semiring.hpp:125-133); MalformedInputError if unknown."""
     try:
         return SemiringId[name]
     except KeyError:
+        for sid, (n, _, _) in _USER.items():
+            if n == name:
+                return sid
         raise errors.MalformedInputError(
             f"unknown semiring '{name}' (expected arithmetic, minplus, boolean, minselect, "
             "tropical_i32, or maxtimes)") from None
 
 
-def as_id(sr) -> SemiringId:
+def as_id(sr):
     if isinstance(sr, str):
         return semiring_by_name(sr)
+    if int(sr) in _USER:
+        return int(sr)
     return SemiringId(int(sr))
 
 
 def dtype_of(sr) -> np.dtype:
-    return DTYPES[as_id(sr)]
+    sid = as_id(sr)
+    if sid in _USER:
+        return _USER[sid][1]
+    return DTYPES[sid]
 
 
 def zero(sr):

@@ -57,3 +57,29 @@ def test_facade_read_matrix_market(tmp_path):
     bad.write_text("%%MatrixMarket matrix coordinate real general\n3 3 2\n1 1 1\n")
     out = subprocess.run([exe, str(bad)], check=True, capture_output=True, text=True).stdout
     assert out.strip() == f"error MalformedInputError {bad}:3: file ends after 1 of 2 entries"
+
+
+def test_summa_facade_compiles_and_links():
+    assert os.path.exists(build_facade("summa_facade_main.cpp", os.path.join(ROOT, "build", "summa_facade_main")))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p", [1, 4])
+def test_summa_facade_matches_reference(golden, p):
+    """summa25_multiply(DistMatrix, DistMatrix, LatencyModel, CommConfig,
+    SummaOptions) -> SummaResult through the facade, one thread per rank:
+    gather(product) and the ledger's per-instance counters equal the
+    reference's summa25_multiply on the same input (golden section 6)."""
+    exe = build_facade("summa_facade_main.cpp", os.path.join(ROOT, "build", "summa_facade_main"))
+    out = subprocess.run([exe, str(p), "9", "8", "3", "0"], check=True, capture_output=True, text=True,
+                         timeout=600).stdout
+    kv = dict(x.split("=") for x in out.split())
+    key = f"summa_4_p{p}_r1"
+    led = golden[key + "_ledger"]
+    assert int(kv["checksum"]) == int(golden[key + "_csum"][0])
+    assert int(kv["nnz"]) == int(golden[key + "_nnz"][0])
+    assert int(kv["bcasts"]) == int(led[0] + led[1])
+    assert int(kv["size_exchanges"]) == int(led[4])
+    assert int(kv["multiplies"]) == int(led[5])
+    assert int(kv["skipped"]) == int(led[6])
+    assert kv["grid_error"] == "1"
