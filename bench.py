@@ -494,9 +494,15 @@ def run_summa(args):
     comm = Comm(job[0], world, rank, pr, pc, local, staging_bytes=64 << 20)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 
+    # C blocks larger than HBM (config 3 / 5 on 1-2 GPUs: 90-360 GB per rank)
+    # are streamed: column batches, each checksummed and released (§8f-2)
+    output = args.output
+    if output == "auto":
+        output = "checksum" if (args.config in (3, 5) and world <= 2) else "block"
+
     def step():
         c, led = summa25_multiply(comm, ctx, blk, blk, n, n, n, two_round=not args.one_round, mode=mode,
-                                  threshold=thr, threshold_col=thr_col, fuse_stages=not args.no_fuse)
+                                  threshold=thr, threshold_col=thr_col, fuse_stages=not args.no_fuse, output=output)
         return c, led
 
     for _ in range(args.warmup):
@@ -519,13 +525,13 @@ def run_summa(args):
             if len(times) < args.steps:
                 c.free()
     launches = ctx.kernel_launches() - launches0
-    part = checksum_part(c, blk.rows[0], blk.cols[0])
-    nnz_blk = c.nnz
+    part = checksum_part(c, blk.rows[0], blk.cols[0]) if output == "block" else leds[-1]["checksum_part"]
+    nnz_blk = c.nnz if output == "block" else leds[-1]["nnz_out"]
     c.free()
     # e2e: the same call plus the D2H read of this rank's C block (host
     # result); skipped (--e2e-steps 0) when C blocks exceed host RAM
     e2e_local, d2h = float("nan"), 0
-    if args.e2e_steps > 0:
+    if args.e2e_steps > 0 and output == "block":
         for k in range(2):  # k == 0: untimed warm-up of the pinned result buffers
             torch.cuda.synchronize()
             dist.barrier()
@@ -542,8 +548,10 @@ def run_summa(args):
 
     t = torch.tensor(times, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    # this rank's algorithmic bytes of its local multiply
+    balg_r = b_alg(leds[-1]["left_nnz"], blk.cols[1] - blk.cols[0], leds[-1]["products"], nnz_blk, wl["vs"])
     agg = torch.tensor([float(leds[-1]["products"]), float(nnz_blk), float(part & 0xFFFFFFFF), float(part >> 32),
-                        float(launches), float(d2h)], dtype=torch.float64)
+                        float(launches), float(d2h), float(balg_r)], dtype=torch.float64)
     dist.all_reduce(agg, op=dist.ReduceOp.SUM)
     e2e_t = torch.tensor([e2e_local], dtype=torch.float64)
     dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
@@ -560,6 +568,8 @@ def run_summa(args):
         peak, peak_kind = peaks()
         h2d = 8 * (blk.storage.ncols + 1) + (8 + wl["vs"]) * blk.storage.nnz
         nnz_c = int(agg[1])
+        golden = GOLDEN_CSUM.get((args.config, args.scale, args.ef, args.seed, bool(args.permute)))
+        achieved = float(agg[6]) / (ms * 1e-3) / 1e9
         line = {
             "metric": METRIC, "value": 2.0 * F / (ms * 1e-3) / 1e9, "unit": "Gflop/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -583,8 +593,14 @@ def run_summa(args):
                                         "multiply": round(float(x[4]), 2), "merge": round(float(x[5]), 2),
                                         "products": int(x[6])} for x in allr],
                        "l2": "flushed between steps (512 MB write)", "parallelism": f"summa{pr}x{pc}"},
-            "roofline": {"bound": "hbm", "achieved": None, "peak": peak, "unit": "GB/s", "frac": None,
-                         "traffic": None, "note": "per-kernel roofline is reported by the N=1 line"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * world, "unit": "GB/s",
+                         "frac": achieved / (peak * world), "traffic": None,
+                         "note": f"sum over ranks of each rank's local-multiply B_alg (SURVEY §8d) / time-to-C (max over "
+                                 f"ranks, broadcasts included) vs {world} x the {peak_kind} HBM peak"},
+            "parity": None if golden is None else bool(csum == golden),
+            "parity_check": {"checksum_C": csum, "golden": golden,
+                             "how": "sum over ranks of matrix_checksum terms (checksum.hpp:20-38) vs the CPU oracle's"},
+            "output": output,
             "cpu_baseline": None,
             "e2e": (None if args.e2e_steps <= 0 else
                     {"value": 2.0 * F / float(e2e_t[0]) / 1e9, "unit": "Gflop/s", "h2d_bytes_per_step": 2 * h2d,
@@ -626,6 +642,9 @@ def main():
                     help="use the generator's vertex order (default: relabel vertices by a seeded random "
                          "permutation, as CombBLAS does, so grid blocks carry equal work; F and nnz(C) unchanged)")
     ap.add_argument("--comm", default="hybrid", choices=["host", "device", "hybrid"])
+    ap.add_argument("--output", default="auto", choices=["auto", "block", "checksum"],
+                    help="SUMMA C block: materialised in HBM, or streamed in checksummed column batches (auto: "
+                         "streamed for configs 3 and 5 on 1-2 GPUs, whose C blocks exceed HBM)")
     ap.add_argument("--grid", default="", help="PRxPC process grid (default 1x1/1x2/2x2/2x4 by GPU count)")
     ap.add_argument("--threshold", type=int, default=-1, help="hybrid threshold bytes (-1: measured default)")
     args = ap.parse_args()

@@ -163,6 +163,11 @@ SPG_API int spg_ctx_set_pipeline(spg_ctx* ctx, int mode);
 SPG_API int spg_dcsr_alloc(spg_ctx* ctx, int sr, int64_t nrows, int64_t ncols, int64_t nseg,
                            int64_t nnz, spg_dcsr* out);
 SPG_API int spg_dcsr_free(spg_ctx* ctx, spg_dcsr* m);
+/* rows [row_begin, row_end) of A (x) B — the row-batched form of
+   spg_local_multiply (stream C out of HBM batch by batch: multiply a row range,
+   consume it — download / checksum — free it, next range) */
+SPG_API int spg_local_multiply_rows(spg_ctx* ctx, int sr, const spg_dcsr* a, const spg_dcsr* b,
+                                    int64_t row_begin, int64_t row_end, spg_dcsr* c, spg_mult_stats* stats);
 /* stream-ordered device -> host copy of `bytes` (synchronous on return) */
 SPG_API int spg_copy_to_host(spg_ctx* ctx, void* dst, const void* src, uint64_t bytes);
 /* H2D of a host CSR (or CSC) with int64 -> int32 index narrowing on device */
@@ -299,7 +304,16 @@ typedef struct {
   int fuse_stages;    /* 1: keep every received panel and run ONE fused local multiply over the
                          concatenated panels (no partials, no merge; fold order = ascending k);
                          0: the reference's per-stage multiplies + merge_partials */
+  int output;         /* SPG_SUMMA_OUT_BLOCK (0): this rank's C block in HBM;
+                         SPG_SUMMA_OUT_CHECKSUM (1): C larger than HBM — the fused multiply runs
+                         in column batches of the block (<= batch_bytes of C each), every batch
+                         is checksummed (matrix_checksum terms, checksum.hpp:20-38) and
+                         released; the ledger carries the block's checksum share and nnz and
+                         the returned block is empty */
+  uint64_t batch_bytes; /* batch size bound for output = 1 (0: 40% of free device memory) */
 } spg_summa_opts;
+#define SPG_SUMMA_OUT_BLOCK 0
+#define SPG_SUMMA_OUT_CHECKSUM 1
 
 /* CostLedger (cost_ledger.hpp:31-56) with measured instead of modelled time. */
 typedef struct {
@@ -312,6 +326,10 @@ typedef struct {
      collective instance once (fabric.hpp:220-241), so summing these over
      the ranks reproduces its host/device broadcast and size-exchange counts */
   uint64_t rooted_host_bcasts, rooted_device_bcasts, rooted_size_exchanges;
+  uint64_t checksum_part; /* output = SPG_SUMMA_OUT_CHECKSUM: this block's matrix_checksum terms */
+  int64_t nnz_out;        /* nnz of this rank's C block (both output modes) */
+  int64_t batches;        /* column batches of the streamed multiply (1 when materialised) */
+  int64_t left_nnz;       /* entries of the fused multiply's left operand (received B panels) */
 } spg_ledger;
 
 /* summa25_multiply (summa.hpp:248-349), one rank's program.  a_block /

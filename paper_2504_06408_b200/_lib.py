@@ -56,7 +56,8 @@ class Stage(C.Structure):
 
 class SummaOpts(C.Structure):
     _fields_ = [("two_round", C.c_int), ("comm_mode", C.c_int), ("threshold", C.c_uint64),
-                ("threshold_col", C.c_uint64), ("fuse_stages", C.c_int)]
+                ("threshold_col", C.c_uint64), ("fuse_stages", C.c_int), ("output", C.c_int),
+                ("batch_bytes", C.c_uint64)]
 
 
 class Ledger(C.Structure):
@@ -66,7 +67,8 @@ class Ledger(C.Structure):
                 ("skipped_stages", C.c_uint64), ("peak_bcast_buffer_bytes", C.c_uint64),
                 ("products", C.c_int64), ("ms_total", C.c_double),
                 ("rooted_host_bcasts", C.c_uint64), ("rooted_device_bcasts", C.c_uint64),
-                ("rooted_size_exchanges", C.c_uint64)]
+                ("rooted_size_exchanges", C.c_uint64), ("checksum_part", C.c_uint64), ("nnz_out", C.c_int64),
+                ("batches", C.c_int64), ("left_nnz", C.c_int64)]
 
     PHASES = ("prepare", "broadcast", "local_multiply", "merge", "copy")
 
@@ -99,6 +101,8 @@ _SIGS = [
     ("spg_dcsr_alloc", C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64, _P(DCsr)]),
     ("spg_dcsr_free", C.c_int, [C.c_void_p, _P(DCsr)]),
     ("spg_copy_to_host", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64]),
+    ("spg_local_multiply_rows", C.c_int, [C.c_void_p, C.c_int, _P(DCsr), _P(DCsr), C.c_int64, C.c_int64, _P(DCsr),
+                                          _P(MultStats)]),
     ("spg_upload", C.c_int, [C.c_void_p, C.c_int, _P(HCsr), C.c_int, _P(DCsr)]),
     ("spg_download", C.c_int, [C.c_void_p, C.c_int, _P(DCsr), C.c_int, _P(HCsr)]),
     ("spg_hcsr_free", None, [_P(HCsr)]),

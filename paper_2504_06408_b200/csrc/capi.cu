@@ -561,6 +561,25 @@ int spg_local_multiply(spg_ctx* c, int sr, const spg_dcsr* a, const spg_dcsr* b,
   });
 }
 
+int spg_local_multiply_rows(spg_ctx* c, int sr, const spg_dcsr* a, const spg_dcsr* b, int64_t row_begin,
+                            int64_t row_end, spg_dcsr* out, spg_mult_stats* st) {
+  return guarded(c, [&] {
+    need(c && a && b && out, "null argument");
+    use_device(c);
+    if (a->ncols != b->nrows)
+      fail(SPG_ERR_SHAPE, "cannot multiply " + std::to_string(a->nrows) + "x" + std::to_string(a->ncols) +
+                              " by " + std::to_string(b->nrows) + "x" + std::to_string(b->ncols));
+    if (row_begin < 0 || row_end < row_begin || row_end > a->nrows)
+      fail(SPG_ERR_INVALID_RANGE, "row range [" + std::to_string(row_begin) + ", " + std::to_string(row_end) +
+                                      ") outside 0.." + std::to_string(a->nrows));
+    if (b->ncols > INT32_MAX) fail(SPG_ERR_INVALID_RANGE, "output width exceeds int32 indices");
+    spg_dcsr v = *a;  // row window: the row pointers index the whole operand's entries
+    v.nrows = row_end - row_begin;
+    v.ptr = a->ptr + row_begin;
+    ops_for(sr)->local_multiply(c, &v, b, out, st);
+  });
+}
+
 int spg_merge_partials(spg_ctx* c, int sr, int nparts, const spg_dcsr* parts, const int* stages,
                        const int* rounds, int64_t block_rows, int64_t block_cols, spg_dcsr* out,
                        spg_mult_stats* st) {

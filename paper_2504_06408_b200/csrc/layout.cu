@@ -128,6 +128,31 @@ int blocks_for(spg_ctx* c, int64_t n, int threads = 256) {
 
 }  // namespace
 
+// products of every row of L (x) R: F_i = sum over L's entries (i, k) of nnz(R row k)
+__global__ void row_products_kernel(int64_t nrows, const int64_t* __restrict__ lptr, const int32_t* __restrict__ lidx,
+                                    const int64_t* __restrict__ rptr, int64_t* __restrict__ f) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < nrows; i += nwarps) {
+    int64_t acc = 0;
+    for (int64_t s = lptr[i] + lane; s < lptr[i + 1]; s += 32) {
+      const int32_t k = lidx[s];
+      acc += rptr[k + 1] - rptr[k];
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) f[i] = acc;
+  }
+}
+
+void row_products(spg_ctx* c, const spg_dcsr& l, const spg_dcsr& r, int64_t* f) {
+  if (l.nrows <= 0) return;
+  const int grid = (int)std::min<int64_t>((l.nrows + 7) / 8, (int64_t)c->sm_count * 16);
+  row_products_kernel<<<grid, 256, 0, c->stream>>>(l.nrows, l.ptr, l.idx, r.ptr, f);
+  SPG_LAUNCH_CHECK();
+  ++c->launches;
+}
+
 void exclusive_scan_i64(spg_ctx* c, const int64_t* in, int64_t* out, int64_t n) {
   size_t bytes = 0;
   SPG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, c->stream));

@@ -66,6 +66,8 @@ void slice_cols_fill(spg_ctx* c, const spg_dcsr& m, int64_t b, int64_t e, int vs
 void dcsc_colptr(spg_ctx* c, int64_t ncols, int64_t njc, const int64_t* jc, const int64_t* cp,
                  int64_t* colptr);
 void exclusive_scan_i64(spg_ctx* c, const int64_t* in, int64_t* out, int64_t n);
+// F_i (products of row i of L (x) R) for every row of l
+void row_products(spg_ctx* c, const spg_dcsr& l, const spg_dcsr& r, int64_t* f);
 
 // Horizontal concatenation of K CSR matrices with equal row counts: row i of
 // the result is row i of part 0, then part 1, ... with part p's columns shifted

@@ -182,6 +182,10 @@ extern "C" int spg_summa25_multiply(spg_comm* comm, spg_ctx* c, int sr, int64_t 
                "' has a non-commutative multiplication; the distributed transpose-reinterpretation path "
                "supports commutative semirings only");
     const int vs = ops->value_size;
+    if (opts->output == SPG_SUMMA_OUT_CHECKSUM && !opts->fuse_stages)
+      fail(SPG_ERR_ARG, "summa: output = checksum streams the fused multiply (fuse_stages = 1)");
+    if (opts->output != SPG_SUMMA_OUT_BLOCK && opts->output != SPG_SUMMA_OUT_CHECKSUM)
+      fail(SPG_ERR_ARG, "summa: unknown output mode");
     const int pr = comm_pr(comm), pc = comm_pc(comm), i = comm_grid_row(comm), j = comm_grid_col(comm);
     const int64_t inner = a_ncols;
     int64_t arb, are, acb, ace, brb, bre, bcb, bce;
@@ -368,7 +372,50 @@ extern "C" int spg_summa25_multiply(spg_comm* comm, spg_ctx* c, int sr, int64_t 
         if (L.nrows == 0 && R.nrows == 0) {
           L.nrows = block_cols;
         }
+        led.left_nnz = L.nnz;
         if (off == 0) {  // no inner dimension: empty product
+          ct.nrows = block_cols;
+          ct.ncols = block_rows;
+          ct.ptr = dalloc<int64_t>(c, block_cols + 1);
+          ct.idx = dalloc<int32_t>(c, 1);
+          ct.vals = dalloc<char>(c, vs);
+          SPG_CUDA(cudaMemsetAsync(ct.ptr, 0, sizeof(int64_t) * (block_cols + 1), c->stream));
+        } else if (opts->output == SPG_SUMMA_OUT_CHECKSUM) {
+          // C block larger than HBM: the fused product in column batches of
+          // the block (rows of C^T), each checksummed and released
+          DBuf<int64_t> f(c, (size_t)L.nrows);
+          row_products(c, L, R, f.p);
+          std::vector<int64_t> hf((size_t)L.nrows);
+          SPG_CUDA(cudaMemcpyAsync(hf.data(), f.p, sizeof(int64_t) * L.nrows, cudaMemcpyDeviceToHost, c->stream));
+          SPG_CUDA(cudaStreamSynchronize(c->stream));
+          const uint64_t budget = opts->batch_bytes ? opts->batch_bytes : (uint64_t)(mem_available(c) * 0.25);
+          const uint64_t per = 4 + (uint64_t)vs;  // bytes per C entry
+          for (int64_t r0 = 0; r0 < L.nrows;) {
+            int64_t r1 = r0;
+            uint64_t acc = 0;
+            while (r1 < L.nrows) {
+              const uint64_t e = (uint64_t)std::min<int64_t>(hf[r1], R.ncols) * per;  // nnz <= min(F, width)
+              if (r1 > r0 && acc + e > budget) break;
+              acc += e;
+              ++r1;
+            }
+            spg_dcsr lv = L;
+            lv.nrows = r1 - r0;
+            lv.ptr = L.ptr + r0;
+            spg_dcsr cb{};
+            spg_mult_stats bs{};
+            ops->local_multiply(c, &lv, &R, &cb, &bs);
+            spg_dcsr csc = cb;  // CSR of C^T rows [r0, r1) == CSC of C columns bcb + [r0, r1)
+            csc.nrows = block_rows;
+            csc.ncols = r1 - r0;
+            led.checksum_part += ops->checksum_part(c, &csc, 1, arb, bcb + r0);
+            led.nnz_out += cb.nnz;
+            ms.products += bs.products;
+            free_dcsr(c, &cb);
+            ++led.batches;
+            ++led.local_multiply_calls;
+            r0 = r1;
+          }
           ct.nrows = block_cols;
           ct.ncols = block_rows;
           ct.ptr = dalloc<int64_t>(c, block_cols + 1);
@@ -378,6 +425,8 @@ extern "C" int spg_summa25_multiply(spg_comm* comm, spg_ctx* c, int sr, int64_t 
         } else {
           ops->local_multiply(c, &L, &R, &ct, &ms);
           ++led.local_multiply_calls;
+          led.nnz_out = ct.nnz;
+          led.batches = 1;
         }
         led.products += ms.products;
         *c_out = ct;
@@ -417,6 +466,8 @@ extern "C" int spg_summa25_multiply(spg_comm* comm, spg_ctx* c, int sr, int64_t 
         }
         SPG_CUDA(cudaStreamSynchronize(c->stream));
         led.ms[3] += ms_since(t0);
+        led.nnz_out = c_out->nnz;
+        led.batches = 1;
       }
     } catch (...) {
       free_parts();

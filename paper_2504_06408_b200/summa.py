@@ -145,16 +145,22 @@ class Comm:
 
 def summa25_multiply(comm: Comm, ctx: Context, a_block: LocalBlock, b_block: LocalBlock, a_nrows: int,
                      a_ncols: int, b_ncols: int, two_round: bool = True, mode: int = HYBRID,
-                     threshold: int = 0, sr=None, fuse_stages: bool = True, threshold_col: int = 0):
+                     threshold: int = 0, sr=None, fuse_stages: bool = True, threshold_col: int = 0,
+                     output: str = "block", batch_bytes: int = 0):
     """One rank's summa25_multiply.  Returns (C block as DeviceCsr CSC, ledger dict).
 
     fuse_stages=True keeps every received panel and runs one fused local
     multiply over the concatenated panels (no partials, no merge); False runs
-    the reference's per-stage multiplies followed by merge_partials."""
+    the reference's per-stage multiplies followed by merge_partials.
+    output="checksum" streams a C block larger than HBM: the fused multiply
+    runs in column batches (<= batch_bytes of C each), each batch is
+    checksummed and released; ledger["checksum_part"] / ["nnz_out"] carry the
+    block's share and the returned block is empty."""
     sr = as_id(sr if sr is not None else a_block.storage.sr)
     ah, ad, ka = _block_structs(a_block)
     bh, bd, kb = _block_structs(b_block)
-    opts = SummaOpts(int(two_round), int(mode), int(threshold), int(threshold_col), int(fuse_stages))
+    opts = SummaOpts(int(two_round), int(mode), int(threshold), int(threshold_col), int(fuse_stages),
+                     {"block": 0, "checksum": 1}[output], int(batch_bytes))
     out = DCsr()
     led = Ledger()
     rc = lib.spg_summa25_multiply(comm.handle, ctx.handle, int(sr), int(a_nrows), int(a_ncols), int(b_ncols),

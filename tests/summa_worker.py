@@ -33,6 +33,8 @@ def main():
     ap.add_argument("--grid", default="", help="PRxPC (default: the BASELINE grid for the world size)")
     ap.add_argument("--gather", type=int, default=0, help="also gather C on rank 0 (GPU assembly) and compare")
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--output", default="block", choices=["block", "checksum"])
+    ap.add_argument("--batch-bytes", type=int, default=0)
     ap.add_argument("--golden-ledger", default="", help="golden.npz key prefix (summa_<sr>_p<p>_r<two>): compare the "
                     "distributed ledger counters with the reference's summa25_multiply")
     args = ap.parse_args()
@@ -62,8 +64,9 @@ def main():
     if not comm.has_device_path and args.mode != 0:
         raise SystemExit("ranks share a GPU: run with --mode 0 (host path)")
     c, led = summa25_multiply(comm, ctx, blk, blk, n, n, n, two_round=bool(args.two_round), mode=args.mode,
-                              threshold=args.threshold, fuse_stages=bool(args.fuse))
-    part = checksum_part(c, blk.rows[0], blk.cols[0])
+                              threshold=args.threshold, fuse_stages=bool(args.fuse), output=args.output,
+                              batch_bytes=args.batch_bytes)
+    part = checksum_part(c, blk.rows[0], blk.cols[0]) if args.output == "block" else led["checksum_part"]
     full = gather(comm, ctx, c, blk.rows, blk.cols, n, n, root=0) if args.gather else None
     got = c.download()  # CSC of the C block
 
@@ -77,6 +80,10 @@ def main():
     br, bc, bv = rr[sel] - rb, want_full.idx[sel] - cb, want_full.vals[sel]
     order = np.lexsort((br, bc))
     colptr = np.concatenate([[0], np.cumsum(np.bincount(bc, minlength=ce - cb))])
+    if args.output == "checksum":  # streamed: the block is not kept; nnz and checksum share are
+        got.colptr, got.rowids, got.values = colptr, br[order], bv[order]
+        assert led["nnz_out"] == br.size and c.nnz == 0, (led["nnz_out"], br.size, c.nnz)
+        assert args.batch_bytes == 0 or led["batches"] > 1 or br.size < 64
     ok = np.array_equal(got.colptr, colptr) and np.array_equal(got.rowids, br[order])
     if args.sr == 0:  # fp64 (+, x): summation order may differ; stated tolerance 1e-12
         x, y = got.values, bv[order]

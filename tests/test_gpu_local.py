@@ -278,3 +278,28 @@ def test_bitrank_drops_columns_whose_products_are_all_zero(bins_ctx):
     want = ob.orc_multiply(to_mat(a), to_mat(b))
     assert_same(got, want, 4)
     assert st["rows_per_bin"][8] == 1
+
+
+@pytest.mark.parametrize("sr", [2, 4])
+def test_row_batched_multiply_concatenates_to_the_full_product(ctx, sr):
+    """spg_local_multiply_rows: row windows of A (x) B (the row-batched form
+    used to stream C out of HBM) concatenate to the full product."""
+    import ctypes as C
+    from paper_2504_06408_b200._lib import DCsr, MultStats, check
+    a = coo_to_csr(generators.generate_rmat(sr, 12, 16.0, 2))
+    d = DeviceCsr.upload(ctx, a)
+    full = local_multiply(d, d).download()
+    cuts = [0, 1, 700, 701, 2500, a.nrows]
+    ptr, idx, vals = [np.zeros(1, np.int64)], [], []
+    for r0, r1 in zip(cuts[:-1], cuts[1:]):
+        out = DCsr()
+        check(lib.spg_local_multiply_rows(ctx.handle, sr, C.byref(d.d), C.byref(d.d), r0, r1, C.byref(out),
+                                          C.byref(MultStats())), ctx.handle)
+        part = DeviceCsr(ctx, sr, out).download()
+        assert part.nrows == r1 - r0
+        ptr.append(part.rowptr[1:] + ptr[-1][-1])
+        idx.append(part.colids)
+        vals.append(part.values)
+    assert np.array_equal(np.concatenate(ptr), full.rowptr)
+    assert np.array_equal(np.concatenate(idx), full.colids)
+    assert np.concatenate(vals).tobytes() == full.values.tobytes()

@@ -55,6 +55,18 @@ def test_summa_grids_on_one_gpu_host_path(grid, fuse):
     assert "blocks_ok=True checksum_ok=True" in out
 
 
+@pytest.mark.parametrize("grid", ["1x1", "1x2", "2x2"])
+def test_summa_streamed_checksum_output(grid):
+    """output = checksum (SURVEY §8f-2, C larger than HBM): the fused product
+    in many small column batches, each checksummed and released; the sum of
+    the ranks' shares equals the oracle's matrix_checksum of C."""
+    pr, pc = (int(x) for x in grid.split("x"))
+    for sr in (2, 4):
+        out = run_worker(pr * pc, "--sr", sr, "--scale", 11, "--grid", grid, "--mode", 0, "--output", "checksum",
+                         "--batch-bytes", 1 << 16)
+        assert "blocks_ok=True checksum_ok=True" in out
+
+
 @pytest.mark.parametrize("sr", [1, 2, 4])
 @pytest.mark.parametrize("two_round", [1, 0])
 def test_summa_2x2_ledger_matches_reference(sr, two_round):
