@@ -383,6 +383,8 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
   // ncols is not a multiple of W (e.g. ncols <= W/2), so take the larger
   const int wstride = std::max(npc * (512 / 32), std::max(npanels_for<V>(ncols_out, Geom<V>::kPanelW), 1) * (1024 / 32));
   DBuf<int32_t> wchunks(c, warp_emit ? (size_t)hcounts[kBinDense] * wstride * 2 : 1);
+  if (warp_emit)  // the 2-CTA rows fill fewer chunks than the stride holds: the rest must read as empty
+    SPG_CUDA(cudaMemsetAsync(wchunks.p, 0, sizeof(int32_t) * hcounts[kBinDense] * wstride * 2, c->stream));
   DBuf<int64_t> rowstart, chunks;
   DBuf<unsigned long long> bump(c, 1);
   if (cap > 0 && !slotted) {

@@ -303,3 +303,27 @@ def test_row_batched_multiply_concatenates_to_the_full_product(ctx, sr):
     assert np.array_equal(np.concatenate(ptr), full.rowptr)
     assert np.array_equal(np.concatenate(idx), full.colids)
     assert np.concatenate(vals).tobytes() == full.values.tobytes()
+
+
+@pytest.mark.parametrize("sr,ncols", [(4, 40000), (4, 12000), (0, 20000)])
+def test_heavy_and_dense_rows_share_the_chunk_table(bins_ctx, sr, ncols):
+    """Per-bin pipeline, U-slot mode: heavy dense rows (F > 262144, the
+    1-CTA/SM kernel with W-wide panels and 32 warps) and ordinary dense rows
+    (2-CTA kernel, W/2 panels, 16 warps) write per-warp chunk tables of
+    different sizes into one table — widths that are not a multiple of the
+    panel width used to overflow it."""
+    rng = np.random.default_rng(21)
+    from golden.make_golden import exact_values
+    nb = 64
+    lens = np.full(nb, min(ncols // 2, 9000))
+    bptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    bcols = np.concatenate([np.sort(rng.choice(ncols, L, replace=False)) for L in lens]).astype(np.int64)
+    b = CsrMatrix(sr, nb, ncols, bptr, bcols, exact_values(sr, rng, bcols.size))
+    rows = [np.arange(nb), np.arange(0, nb, 2), np.arange(5), np.arange(40)]  # F = 64 * L (heavy), ..., 5 * L
+    aptr = np.concatenate([[0], np.cumsum([len(x) for x in rows])]).astype(np.int64)
+    acols = np.concatenate(rows).astype(np.int64)
+    a = CsrMatrix(sr, len(rows), nb, aptr, acols, exact_values(sr, rng, acols.size))
+    st = {}
+    got = esc_multiply(a, b, ctx=bins_ctx, stats=st)
+    assert_same(got, ob.orc_multiply(to_mat(a), to_mat(b)), sr, rtol=RTOL if sr == 0 else None)
+    assert st["rows_per_bin"][6] >= 2 and st["output_mode"] == 0, st
