@@ -461,9 +461,6 @@ def run_summa(args):
         raise SystemExit(f"--grid {args.grid} does not hold {world} ranks")
     i, j = rank // pc, rank % pc
     mode = {"host": HOST_ONLY, "device": DEVICE_ONLY, "hybrid": HYBRID}[args.comm]
-    from paper_2504_06408_b200.summa import measured_threshold
-    thr = args.threshold if args.threshold >= 0 else measured_threshold(pc)      # row scope: fanout pc
-    thr_col = args.threshold if args.threshold >= 0 else measured_threshold(pr)  # column scope: fanout pr
 
     t_gen = time.time()
     sr, n = wl["sr"], wl["n"]
@@ -493,6 +490,17 @@ def run_summa(args):
     check(lib.spg_ctx_set_stream(ctx.handle, C.c_void_p(stream.cuda_stream)), ctx.handle)
     comm = Comm(job[0], world, rank, pr, pc, local, staging_bytes=64 << 20)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    # hybrid thresholds measured on THIS box at start-up (untimed), per scope
+    if args.threshold >= 0:
+        thr, thr_col, thr_info = args.threshold, args.threshold, {"source": "--threshold"}
+    else:
+        from paper_2504_06408_b200.summa import calibrated_thresholds
+
+        def _rmax(x):
+            tt = torch.tensor([x], dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            return float(tt[0])
+        thr, thr_col, thr_info = calibrated_thresholds(comm, local, dist.barrier, _rmax)
 
     # C blocks larger than HBM (config 3 / 5 on 1-2 GPUs: 90-360 GB per rank)
     # are streamed: column batches, each checksummed and released (§8f-2)
@@ -580,7 +588,7 @@ def run_summa(args):
                        "fuse_stages": not args.no_fuse,
                        "comm": args.comm,
                        "threshold_bytes": {"row_scope": thr, "col_scope": thr_col,
-                                           "source": "measured crossover (profiles/comm_fanout*.json)"},
+                                           "calibration": thr_info},
                        "products": F, "nnz_C": nnz_c, "checksum_C": csum,
                        "expected": wl.get("expect"),
                        "matches_expected": (None if not wl.get("expect") else

@@ -519,6 +519,22 @@ int ref_find_crossover_bundled(int fanout, uint64_t lo, uint64_t hi, uint64_t* o
   return 1;
 }
 
+// find_crossover on a model FILE (LatencyModel::load_file, latency_model.hpp:
+// 169-179): the reference's own tuner consuming curves measured on the box.
+// Returns 1 and writes *out on a crossover, 0 without one, -1 on error.
+int ref_find_crossover_file(const char* path, int fanout, uint64_t lo, uint64_t hi, uint64_t* out) {
+  try {
+    const auto m = LatencyModel::load_file(path);
+    const auto r = find_crossover(m, fanout, lo, hi);
+    if (!r) return 0;
+    *out = *r;
+    return 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 // Bundled model path costs (latency_model.hpp:104-109) for the sweep tests.
 double ref_bundled_host_total(uint64_t bytes, int fanout) {
   return LatencyModel::bundled_default().host_path_total(bytes, fanout);

@@ -15,7 +15,7 @@ simulated fabric:
     over ranks) and `wall=` the host-measured call time split in the same
     proportions — there is no latency model to simulate;
   * the default hybrid threshold is the crossover MEASURED on the box
-    (profiles/comm_fanout<f>.json via summa.measured_threshold), the analogue
+    (measured on the box at start-up: summa.calibrated_thresholds), the analogue
     of find_crossover(model) (tools/spsumma.cpp:186-195); --model is accepted
     and ignored;
   * --check-oracle compares against a host expand-sort-compress product of
@@ -236,12 +236,17 @@ def _run(job, a, blk, mode, threshold, threshold_col):
 
 
 def _thresholds(job, cfg_mode, threshold):
-    from .summa import HYBRID, measured_threshold
+    """Hybrid thresholds: the --threshold-bytes given, else the crossover
+    measured on this box at start-up (summa.calibrated_thresholds)."""
+    from .summa import HYBRID, calibrated_thresholds
     if threshold is not None:
         return threshold, threshold
     if cfg_mode != HYBRID:
         return 0, 0
-    return measured_threshold(max(job.pc, 2)), measured_threshold(max(job.pr, 2))
+    if job.world == 1:
+        return 0, 0
+    thr, thr_col, _ = calibrated_thresholds(job.comm, job.local, job.comm.barrier, job.max_over_ranks)
+    return thr, thr_col
 
 
 def cmd_multiply(args) -> int:

@@ -196,10 +196,33 @@ def checksum_seed(nrows: int, ncols: int) -> int:
     return int(lib.spg_checksum_seed(int(nrows), int(ncols)))
 
 
+def calibrated_thresholds(comm: "Comm", device: int, barrier, reduce_max, reps: int = 5) -> tuple:
+    """(row-scope, column-scope) hybrid thresholds MEASURED on this box at
+    start-up (tuner.calibrate_threshold over the real transports; cached per
+    GPU model and grid): the row scope has fanout pc, the column scope pr.
+    Collective over all ranks.  Returns (thr_row, thr_col, info)."""
+    import torch
+
+    from . import tuner
+    name = torch.cuda.get_device_name(device).replace(" ", "_")
+    key = f"{name}_{comm.pr}x{comm.pc}"
+    out, info = [], {}
+    for scope, fanout in ((0, comm.pc), (1, comm.pr)):
+        if fanout < 2:  # a one-rank scope never broadcasts
+            out.append(0)
+            info[("row", "col")[scope]] = {"threshold": 0, "source": "one-rank scope"}
+            continue
+        cal = tuner.calibrate_threshold(comm, scope, fanout, device, barrier, reduce_max, reps=reps, cache_key=key)
+        out.append(int(cal["threshold"]))
+        info[("row", "col")[scope]] = cal
+    return out[0], out[1], info
+
+
 def measured_threshold(fanout: int, default: int = 64 << 10) -> int:
-    """Hybrid threshold for a scope of `fanout` ranks: the crossover measured on
-    the box by tools/comm_sweep.py (profiles/comm_fanout<f>.json); the nearest
-    measured fanout is used when the exact one is missing."""
+    """Offline reference point only (tools / docs): the crossover recorded by
+    tools/comm_sweep.py in profiles/comm_fanout<f>.json on an earlier box.
+    The product path measures its threshold on the running box instead
+    (calibrated_thresholds)."""
     import json
     import os
     root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles")

@@ -71,13 +71,20 @@ def default_threshold_ladder(crossover: Optional[int]) -> List[int]:
     return ladder
 
 
+def broadcast_stages(fanout: int) -> int:
+    """broadcast_stages (latency_model.hpp:66-71): ceil(log2(f)) curve evaluations."""
+    if fanout < 1:
+        raise ValueError("broadcast fanout must be >= 1")
+    return int(fanout - 1).bit_length()
+
+
 def to_reference_json(curves: Dict[str, Curve]) -> dict:
     """The reference's model file layout (latency_model.hpp:135-148)."""
     return {"curves": {k: [[float(b), float(t)] for b, t in v] for k, v in curves.items()}}
 
 
 def measure_bcast_curves(comm, sizes: Sequence[int], reps: int = 10, scope: int = 0,
-                         barrier=None, reduce_max=None, device: int = 0) -> Dict[str, Curve]:
+                         barrier=None, reduce_max=None, device: int = 0, fanout: int = 2) -> Dict[str, Curve]:
     """Times spg_bcast on this rank's `scope` (0 = grid row, 1 = grid column)
     for every size through each path: the host path (root D2H into pinned
     shared memory, peers H2D, pipelined) and the device path (NCCL broadcast
@@ -117,11 +124,15 @@ def measure_bcast_curves(comm, sizes: Sequence[int], reps: int = 10, scope: int 
                 if r >= 2:
                     ts.append(time.perf_counter() - t0)
             out[key].append((float(nbytes), sorted(ts)[len(ts) // 2]))
-    # reference-format curves: host_bcast is what remains of the host path
-    # after the two staging copies (latency_model.hpp:104-106), floored at 1 ns
-    out["host_bcast"] = [(b, max(t - d - h, 1e-9)) for (b, t), (_, d), (_, h) in
+    # reference-format curves are PER BROADCAST STAGE: the reference prices a
+    # scope of f ranks as broadcast_stages(f) curve evaluations
+    # (latency_model.hpp:88-106), so the measured fanout-f totals are divided
+    # by that count; host_bcast is what remains of the host path after the
+    # two staging copies, floored at 1 ns
+    st = max(broadcast_stages(fanout), 1)
+    out["host_bcast"] = [(b, max(t - d - h, 1e-9) / st) for (b, t), (_, d), (_, h) in
                          zip(out["host_path_total"], out["copy_d2h"], out["copy_h2d"])]
-    out["device_bcast"] = list(out["device_path_total"])
+    out["device_bcast"] = [(b, t / st) for b, t in out["device_path_total"]]
     for k in out:  # the reference requires non-decreasing latencies
         pts, best = [], 0.0
         for b, t in out[k]:
@@ -131,8 +142,10 @@ def measure_bcast_curves(comm, sizes: Sequence[int], reps: int = 10, scope: int 
     return out
 
 
-def save_model(path: str, curves: Dict[str, Curve], extra: dict | None = None):
+def save_model(path: str, curves: Dict[str, Curve], extra: dict | None = None, fanout: int | None = None):
     doc = to_reference_json({k: curves[k] for k in ("host_bcast", "device_bcast", "copy_h2d", "copy_d2h")})
+    if fanout is not None:
+        doc["fanout"] = int(fanout)
     doc["measured"] = {k: [[b, t] for b, t in curves[k]] for k in ("host_path_total", "device_path_total")}
     if extra:
         doc.update(extra)
@@ -141,6 +154,60 @@ def save_model(path: str, curves: Dict[str, Curve], extra: dict | None = None):
 
 
 INFINITE_THRESHOLD = (1 << 64) - 1  # kInfiniteThreshold: every payload on the host path
+
+
+def model_path_totals(doc: dict, fanout: int):
+    """The reference's host_path_total / device_path_total (latency_model.hpp:
+    104-109) of a model file, as callables bytes -> seconds."""
+    cv = {k: [(float(b), float(t)) for b, t in v] for k, v in doc["curves"].items()}
+    st = broadcast_stages(fanout)
+
+    def host(b):
+        return curve_at(cv["copy_d2h"], b) + st * curve_at(cv["host_bcast"], b) + curve_at(cv["copy_h2d"], b)
+
+    def device(b):
+        return st * curve_at(cv["device_bcast"], b)
+    return host, device
+
+
+def calibrate_threshold(comm, scope: int, fanout: int, device: int, barrier, reduce_max, reps: int = 5,
+                        min_log2: int = 10, max_log2: int = 26, cache_key: str | None = None) -> dict:
+    """The hybrid threshold MEASURED on this box (north star: not hard-coded):
+    host and device broadcast paths timed through the real transports on the
+    `scope` communicator (fanout ranks) for 2^min_log2 .. 2^max_log2 bytes,
+    crossover by the reference's bisection.  Collective over the scope's
+    ranks.  Cached per GPU model/UUID set and fanout when `cache_key` is given
+    (SPG_CALIB_DIR, default ~/.cache/paper_2504_06408_b200): a fresh box
+    measures, a repeat run reuses.  Ranks sharing a GPU have no device path:
+    every payload takes the host path."""
+    import os
+    if not comm.has_device_path:
+        return {"threshold": INFINITE_THRESHOLD, "crossover": None, "source": "host path only (ranks share a GPU)"}
+    path = None
+    if cache_key:
+        d = os.environ.get("SPG_CALIB_DIR", os.path.join(os.path.expanduser("~"), ".cache", "paper_2504_06408_b200"))
+        path = os.path.join(d, f"calib_{cache_key}_f{fanout}_s{scope}.json")
+        if os.path.exists(path):
+            try:
+                with open(path) as f:
+                    doc = json.load(f)
+                return {**doc["calibration"], "source": f"cached measurement {path}"}
+            except (OSError, KeyError, ValueError):
+                pass
+    sizes = [1 << k for k in range(min_log2, max_log2 + 1)]
+    curves = measure_bcast_curves(comm, sizes, reps=reps, scope=scope, barrier=barrier, reduce_max=reduce_max,
+                                  device=device, fanout=fanout)
+    host, dev = curves["host_path_total"], curves["device_path_total"]
+    xo = find_crossover(host, dev, sizes[0], sizes[-1])
+    if xo is None:  # one path wins everywhere in range
+        thr = INFINITE_THRESHOLD if curve_at(host, sizes[-1]) < curve_at(dev, sizes[-1]) else 0
+    else:
+        thr = xo
+    cal = {"threshold": int(thr), "crossover": xo, "fanout": fanout, "sizes": [sizes[0], sizes[-1]], "reps": reps}
+    if path and comm.rank == 0:
+        os.makedirs(os.path.dirname(path), exist_ok=True)
+        save_model(path, curves, extra={"calibration": cal}, fanout=fanout)
+    return {**cal, "source": "measured on this box at start-up"}
 
 
 def crossover_warning(host, device, lo: int = 1, hi: int = 1 << 30) -> Optional[str]:

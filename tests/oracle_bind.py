@@ -70,6 +70,7 @@ if ref is not None:
     ref.ref_summa.argtypes = [C.c_int, _P(Coo), _P(Coo), C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint64,
                               _P(Coo), _P(C.c_uint64), _P(C.c_double)]
     ref.ref_find_crossover_bundled.argtypes = [C.c_int, C.c_uint64, C.c_uint64, _P(C.c_uint64)]
+    ref.ref_find_crossover_file.argtypes = [C.c_char_p, C.c_int, C.c_uint64, C.c_uint64, _P(C.c_uint64)]
     ref.ref_bundled_host_total.restype = C.c_double
     ref.ref_bundled_host_total.argtypes = [C.c_uint64, C.c_int]
     ref.ref_bundled_device_total.restype = C.c_double
@@ -274,6 +275,14 @@ def ref_summa(sr, nrows, ncols, rows, cols, vals, p, two_round=True, mode=2, thr
     if rc != 0:
         return rc, ref.ref_last_error().decode(), None, None
     return 0, _take_coo(sr, out), int(cs.value), list(led)
+
+
+def ref_find_crossover_file(path, fanout, lo, hi):
+    """The reference's find_crossover on LatencyModel::load_file(path); None without a crossover."""
+    out = C.c_uint64()
+    rc = ref.ref_find_crossover_file(path.encode(), fanout, lo, hi, C.byref(out))
+    assert rc >= 0, ref.ref_last_error()
+    return int(out.value) if rc == 1 else None
 
 
 def ref_find_crossover(fanout, lo, hi):

@@ -34,6 +34,7 @@ def _worker(rank, world, pr, pc, job, port, q):
             path = comm.bcast(0, root, buf.ctypes.data, nbytes, mode=2, threshold=1 << 40)
             assert path == 0
             assert np.array_equal(buf, (np.arange(nbytes) * (i + 3)) % 251)
+        comm.barrier()  # every rank is done broadcasting before rank 0 raises the abort below
         # a root outside the scope is a ProtocolError on the offending rank
         if world > 1:
             if rank == 0:

@@ -64,3 +64,48 @@ def test_crossover_warning():
     assert tuner.crossover_warning(host, [(1.0, 1e-5), (1e9, 0.05)]) is None
     msg = tuner.crossover_warning(host, [(1.0, 1e-7), (1e9, 0.05)])
     assert msg and "no host/device crossover" in msg
+
+
+def test_measured_model_files_are_reference_consumable():
+    """The measured curves stored under profiles/ are per broadcast stage, so
+    the reference's own LatencyModel::load_file + find_crossover
+    (latency_model.hpp:169-179, tuner.hpp:17-39, run through oracle/_ref)
+    reproduce the crossover measured on the box from the fanout totals."""
+    import json
+    import os
+
+    import oracle_bind as ob
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for f in (2, 4):
+        path = os.path.join(root, "profiles", f"comm_fanout{f}.json")
+        doc = json.load(open(path))
+        assert doc["fanout"] == f
+        measured = doc["sweep"]["crossover_bytes"]
+        lo, hi = doc["sweep"]["rows"][0]["bytes"], doc["sweep"]["rows"][-1]["bytes"]
+        # our bisection on the model's path totals == the reference's on the same file
+        host, dev = tuner.model_path_totals(doc, f)
+        ours = tuner.find_crossover(host, dev, lo, hi)
+        assert ob.ref_find_crossover_file(path, f, lo, hi) == ours
+        # and the model reproduces the measured totals' crossover to within the
+        # copy-curve split (the staging copies are separate curves in the model)
+        assert ours is not None and abs(math.log2(ours) - math.log2(measured)) < 1.0, (ours, measured)
+
+
+def test_save_model_round_trips_through_the_reference(tmp_path):
+    """tuner.save_model writes per-stage curves: a synthetic box whose fanout-4
+    TOTALS cross at a known size yields a file whose reference crossover at
+    fanout 4 is that size."""
+    import oracle_bind as ob
+    sizes = [float(1 << e) for e in range(10, 31)]
+    f = 4
+    tot_host = [(b, 20e-6 + b / 20e9) for b in sizes]    # cheaper start, less bandwidth
+    tot_dev = [(b, 60e-6 + b / 300e9) for b in sizes]
+    tiny = [(b, 1e-9 + b * 0) for b in sizes]
+    st = tuner.broadcast_stages(f)
+    curves = {"host_bcast": [(b, (t - 2e-9) / st) for b, t in tot_host], "device_bcast": [(b, t / st) for b, t in tot_dev],
+              "copy_h2d": tiny, "copy_d2h": tiny, "host_path_total": tot_host, "device_path_total": tot_dev}
+    p = str(tmp_path / "m.json")
+    tuner.save_model(p, curves, fanout=f)
+    want = tuner.find_crossover(tot_host, tot_dev, 1024, 1 << 30)
+    got = ob.ref_find_crossover_file(p, f, 1024, 1 << 30)
+    assert want is not None and abs(got - want) <= max(2, want // 1000)

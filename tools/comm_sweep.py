@@ -55,7 +55,7 @@ def main():
 
     sizes = [1 << k for k in range(args.min_log2, args.max_log2 + 1)]
     curves = tuner.measure_bcast_curves(comm, sizes, reps=args.reps, scope=0, barrier=dist.barrier,
-                                        reduce_max=reduce_max, device=local)
+                                        reduce_max=reduce_max, device=local, fanout=world)
     host, dev = curves["host_path_total"], curves["device_path_total"]
     xo = tuner.find_crossover(host, dev, sizes[0], sizes[-1])
     thr = xo if xo is not None else (sizes[-1] + 1 if host[-1][1] < dev[-1][1] else 0)
@@ -94,7 +94,7 @@ def main():
                   f"hybrid {r['hybrid_s'] * 1e6:10.1f} us  {'ok' if r['hybrid_le_min'] else 'SLOW'}",
                   file=sys.stderr)
         if args.out:
-            tuner.save_model(args.out, curves, extra={"sweep": verdict})
+            tuner.save_model(args.out, curves, extra={"sweep": verdict}, fanout=world)
     comm.close()
     dist.barrier()
     dist.destroy_process_group()

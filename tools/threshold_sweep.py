@@ -29,7 +29,7 @@ def main():
 
     from paper_2504_06408_b200 import Context, generators, tuner
     from paper_2504_06408_b200.semiring import as_id
-    from paper_2504_06408_b200.summa import Comm, grid_for, local_block, measured_threshold
+    from paper_2504_06408_b200.summa import Comm, calibrated_thresholds, grid_for, local_block
 
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -55,7 +55,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t[0])
 
-    star = measured_threshold(max(pc, pr))
+    thr_row, thr_col, _ = calibrated_thresholds(comm, local, dist.barrier, allmax)  # measured on this box
+    star = max(thr_row, thr_col) or None
     ladder = tuner.default_threshold_ladder(star)
     tuner.sweep_thresholds(comm, ctx, blk, n, ladder[:1], allsum, allmax)  # warm-up
     runs = [tuner.sweep_thresholds(comm, ctx, blk, n, ladder, allsum, allmax) for _ in range(args.reps)]
