@@ -182,8 +182,9 @@ extern "C" int spg_summa25_multiply(spg_comm* comm, spg_ctx* c, int sr, int64_t 
                "' has a non-commutative multiplication; the distributed transpose-reinterpretation path "
                "supports commutative semirings only");
     const int vs = ops->value_size;
-    if (opts->output == SPG_SUMMA_OUT_CHECKSUM && !opts->fuse_stages)
+    if (opts->output == SPG_SUMMA_OUT_CHECKSUM && opts->fuse_stages != 1)
       fail(SPG_ERR_ARG, "summa: output = checksum streams the fused multiply (fuse_stages = 1)");
+    if (opts->fuse_stages < 0 || opts->fuse_stages > 2) fail(SPG_ERR_ARG, "summa: fuse_stages must be 0, 1 or 2");
     if (opts->output != SPG_SUMMA_OUT_BLOCK && opts->output != SPG_SUMMA_OUT_CHECKSUM)
       fail(SPG_ERR_ARG, "summa: unknown output mode");
     const int pr = comm_pr(comm), pc = comm_pc(comm), i = comm_grid_row(comm), j = comm_grid_col(comm);
@@ -254,7 +255,11 @@ extern "C" int spg_summa25_multiply(spg_comm* comm, spg_ctx* c, int sr, int64_t 
     };
     const int64_t block_rows = are - arb, block_cols = bce - bcb;
     try {
-      if (opts->fuse_stages) {
+      // Fused groups: every panel of a group's rounds this rank roots is packed
+      // first, then the size exchanges and broadcasts are issued back to back
+      // (device ones stay in flight) and drained once — the per-stage host
+      // syncs no longer serialise them.
+      auto receive_group = [&](int r_lo, int r_hi) {
         // Fused: pack every panel this rank roots first, then exchange sizes and
         // issue all broadcasts back to back (device ones stay in flight), then
         // drain once — the per-stage host syncs no longer serialise them.
@@ -264,7 +269,7 @@ extern "C" int spg_summa25_multiply(spg_comm* comm, spg_ctx* c, int sr, int64_t 
           Panel a, b;
         };
         std::vector<Pending> pend;
-        for (int r = 0; r < rounds; ++r)
+        for (int r = r_lo; r < r_hi; ++r)
           for (int s = 0; s < ns; ++s) {
             const spg_stage& st = stages[s];
             int64_t hb, he;
@@ -291,7 +296,7 @@ extern "C" int spg_summa25_multiply(spg_comm* comm, spg_ctx* c, int sr, int64_t 
           kept.push_back({q.s, q.r, std::move(q.a), std::move(q.b), q.rows, block_cols});
         }
         if (total > led.peak_bcast_buffer_bytes) led.peak_bcast_buffer_bytes = total;
-      }
+      };
       for (int r = 0; r < (opts->fuse_stages ? 0 : rounds); ++r) {
         for (int s = 0; s < ns; ++s) {
           const spg_stage& st = stages[s];
@@ -329,7 +334,7 @@ extern "C" int spg_summa25_multiply(spg_comm* comm, spg_ctx* c, int sr, int64_t 
           }
         }
       }
-      if (opts->fuse_stages) {
+      auto multiply_kept = [&]() -> spg_dcsr {
         // C^T = [panB_0 | panB_1 | ...] (x) [panA_0; panA_1; ...]  in (stage, round) order
         // = ascending inner index k, so the fold order equals the serial reference's.
         const auto t0 = Clock::now();
@@ -429,11 +434,31 @@ extern "C" int spg_summa25_multiply(spg_comm* comm, spg_ctx* c, int sr, int64_t 
           led.batches = 1;
         }
         led.products += ms.products;
-        *c_out = ct;
-        c_out->nrows = block_rows;
-        c_out->ncols = block_cols;
         SPG_CUDA(cudaStreamSynchronize(c->stream));
         led.ms[2] += ms_since(t0);
+        return ct;
+      };
+      // fuse_stages 1: one fusion group (all rounds; peak buffer = every
+      // panel); 2: one group per round, the round products folded by the GPU
+      // merge (merge_partials, summa.hpp:122-172) — the 2.5D memory bound:
+      // only one round's panels are resident (SPEC acceptance 9).
+      const int groups = opts->fuse_stages == 2 ? rounds : 1;
+      if (opts->fuse_stages) {
+        for (int g = 0; g < groups; ++g) {
+          if (groups == 1) receive_group(0, rounds);
+          else receive_group(g, g + 1);
+          spg_dcsr ct = multiply_kept();
+          if (groups == 1) {
+            *c_out = ct;
+            c_out->nrows = block_rows;
+            c_out->ncols = block_cols;
+          } else {
+            parts.push_back({0, g, ct});
+          }
+        }
+      }
+      if (opts->fuse_stages && groups == 1) {
+        // done: c_out holds the fused product
       } else {
         // merge (summa.hpp:325-328), stage-major / round-minor
         const auto t0 = Clock::now();

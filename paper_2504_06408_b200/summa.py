@@ -149,9 +149,11 @@ def summa25_multiply(comm: Comm, ctx: Context, a_block: LocalBlock, b_block: Loc
                      output: str = "block", batch_bytes: int = 0):
     """One rank's summa25_multiply.  Returns (C block as DeviceCsr CSC, ledger dict).
 
-    fuse_stages=True keeps every received panel and runs one fused local
-    multiply over the concatenated panels (no partials, no merge); False runs
-    the reference's per-stage multiplies followed by merge_partials.
+    fuse_stages=True (1) keeps every received panel and runs one fused local
+    multiply over the concatenated panels (no partials, no merge); 2 fuses per
+    2.5D round and folds the round products with the GPU merge (only one
+    round's panels resident: the 2.5D memory bound); False (0) runs the
+    reference's per-stage multiplies followed by merge_partials.
     output="checksum" streams a C block larger than HBM: the fused multiply
     runs in column batches (<= batch_bytes of C each), each batch is
     checksummed and released; ledger["checksum_part"] / ["nnz_out"] carry the

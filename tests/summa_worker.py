@@ -64,7 +64,7 @@ def main():
     if not comm.has_device_path and args.mode != 0:
         raise SystemExit("ranks share a GPU: run with --mode 0 (host path)")
     c, led = summa25_multiply(comm, ctx, blk, blk, n, n, n, two_round=bool(args.two_round), mode=args.mode,
-                              threshold=args.threshold, fuse_stages=bool(args.fuse), output=args.output,
+                              threshold=args.threshold, fuse_stages=int(args.fuse), output=args.output,
                               batch_bytes=args.batch_bytes)
     part = checksum_part(c, blk.rows[0], blk.cols[0]) if args.output == "block" else led["checksum_part"]
     full = gather(comm, ctx, c, blk.rows, blk.cols, n, n, root=0) if args.gather else None
@@ -91,8 +91,8 @@ def main():
     else:
         ok = ok and got.values.tobytes() == bv[order].tobytes()
     t = torch.tensor([part & 0xFFFFFFFF, part >> 32, int(ok), led["local_multiply_calls"],
-                      led["host_bcasts"], led["device_bcasts"], led["size_exchanges"], led["skipped_stages"]],
-                     dtype=torch.int64)
+                      led["host_bcasts"], led["device_bcasts"], led["size_exchanges"], led["skipped_stages"],
+                      led["peak_bcast_buffer_bytes"]], dtype=torch.int64)
     parts = [torch.zeros_like(t) for _ in range(world)]
     dist.all_gather(parts, t)
     if rank == 0:
@@ -132,6 +132,7 @@ def main():
                   f"size exchanges {sx}/{q} vs {gl[4]}, multiplies {lm} vs {gl[5]}, skipped {sk} vs {gl[6]}: "
                   f"ledger_ok={led_ok}", flush=True)
             allok = allok and led_ok
+        print(f"[summa_worker] peak_bcast_buffer_bytes_max={max(int(p[8]) for p in parts)}", flush=True)
         print(f"[summa_worker] grid {pr}x{pc} sr={args.sr} s{args.scale} two_round={args.two_round} "
               f"mode={args.mode} fuse={args.fuse}: blocks_ok={allok} checksum_ok={cs_ok} ledger0={led}", flush=True)
         if not (allok and cs_ok):

@@ -55,6 +55,22 @@ def test_summa_grids_on_one_gpu_host_path(grid, fuse):
     assert "blocks_ok=True checksum_ok=True" in out
 
 
+@pytest.mark.parametrize("grid", ["1x2", "2x2", "2x4"])
+def test_summa_per_round_fusion_bounds_panel_memory(grid):
+    """fuse_stages = 2 (one fused multiply per 2.5D round, the two round
+    products folded by the GPU merge, merge_partials summa.hpp:122-172): C is
+    exact, and the peak broadcast-buffer bytes per rank in two-round mode
+    are at most the one-round peak (SPEC acceptance 9) — about half."""
+    pr, pc = (int(x) for x in grid.split("x"))
+    peaks = {}
+    for two in (1, 0):
+        out = run_worker(pr * pc, "--sr", 4, "--scale", 11, "--grid", grid, "--fuse", 2, "--mode", 0,
+                         "--two-round", two)
+        assert "blocks_ok=True checksum_ok=True" in out
+        peaks[two] = int(out.split("peak_bcast_buffer_bytes_max=")[1].split()[0])
+    assert 0 < peaks[1] <= peaks[0] and peaks[1] < 0.75 * peaks[0], peaks
+
+
 @pytest.mark.parametrize("grid", ["1x1", "1x2", "2x2"])
 def test_summa_streamed_checksum_output(grid):
     """output = checksum (SURVEY §8f-2, C larger than HBM): the fused product
