@@ -87,6 +87,7 @@ _SIGS = [
     ("spg_last_error", C.c_char_p, [C.c_void_p]),
     ("spg_value_size", C.c_int, [C.c_int]),
     ("spg_semiring_by_name", C.c_int, [C.c_char_p]),
+    ("spg_device_count", C.c_int, []),
     ("spg_register_semiring", C.c_int, [C.c_void_p, _P(C.c_int)]),
     ("spg_semiring_name", C.c_char_p, [C.c_int]),
     ("spg_semiring_is_commutative", C.c_int, [C.c_int]),

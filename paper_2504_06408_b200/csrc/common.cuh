@@ -15,6 +15,8 @@
 #include <string>
 #include <utility>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/spgemm_b200.h"
 
 namespace spg {
@@ -92,6 +94,15 @@ struct HostTrace {
     const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (ms >= lim) std::fprintf(stderr, "[spg-host] %s (%zu) %.3f ms\n", what, arg, ms);
   }
+};
+
+// NVTX range for profilers (nsys / ncu --nvtx): host-side phase markers,
+// no cost without an attached tool (NVTX v3, header-only).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 // Stream-ordered device allocation.  Large buffers come from the context's

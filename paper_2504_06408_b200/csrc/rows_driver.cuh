@@ -230,6 +230,7 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
               const spg_dcsr* r_for_panels = nullptr, bool* two_pass_out = nullptr) {
   using V = typename SR::value_type;
   const int64_t m = src_in.nrows;
+  NvtxRange nv_all("spg:row pipeline (per-bin)");
   PhaseTimer tm(c, st != nullptr);
   const uint64_t launches0 = c->launches;
   tm.mark(0);
@@ -661,6 +662,7 @@ bool run_rows_br(spg_ctx* c, const MulSource<SR>& src, const spg_dcsr* r, int64_
   const uint64_t launches0 = c->launches;
   tm.mark(0);
 
+  NvtxRange nv_all("spg:local_multiply (bitmap-rank)");
   // K1 analyse: F <= br_minf (<= 4096) rows go to the ESC / hash bins only
   DBuf<int64_t> prods(c, m), ub(c, m + 1), off(c, m + 1), rownnz(c, m + 1);
   DBuf<uint8_t> bins(c, m);
@@ -785,6 +787,7 @@ bool run_rows_br(spg_ctx* c, const MulSource<SR>& src, const spg_dcsr* r, int64_
     ++c->launches;
   }
   {  // symbolic (long rows) || numeric of the short rows into their slots
+    NvtxRange nv("spg:symbolic bitmaps + short rows");
     StreamFork fk(c, 3);
     if (nb > 0) {
       const size_t smem = sizeof(uint32_t) * (size_t)nwords + BrSegs<V>::bytes(kSymThreads) + 64;
@@ -876,6 +879,7 @@ bool run_rows_br(spg_ctx* c, const MulSource<SR>& src, const spg_dcsr* r, int64_
   SPG_CUDA(cudaMemsetAsync(zeros.p, 0, sizeof(unsigned long long), c->stream));
   SPG_CUDA(cudaMemsetAsync(rowzero.p, 0, sizeof(unsigned long long) * (size_t)m, c->stream));
   {  // numeric (long rows, straight into C) || compaction of the short rows
+    NvtxRange nv("spg:rank-space fold + short-row compaction");
     StreamFork fk(c, 2);
     if (nitems > 0) {
       const size_t smem = BrNumLayout<V>{nwords + 8, capv}.bytes(kNumThreads);

@@ -217,7 +217,9 @@ extern "C" int spg_summa25_multiply(spg_comm* comm, spg_ctx* c, int sr, int64_t 
                        a_csc->vals == b_csc->vals) ||
                       (a_dcsc && b_dcsc && a_dcsc->jc == b_dcsc->jc && a_dcsc->cp == b_dcsc->cp &&
                        a_dcsc->rowids == b_dcsc->rowids && a_dcsc->vals == b_dcsc->vals);
+    NvtxRange nv_summa("spg:summa25_multiply");
     {
+      NvtxRange nv("spg:summa prepare");
       const auto t0 = Clock::now();
       prepare_block(c, sr, a_csc, a_dcsc, &pa);
       if (!same) prepare_block(c, sr, b_csc, b_dcsc, &pb_own);
@@ -260,6 +262,7 @@ extern "C" int spg_summa25_multiply(spg_comm* comm, spg_ctx* c, int sr, int64_t 
       // (device ones stay in flight) and drained once — the per-stage host
       // syncs no longer serialise them.
       auto receive_group = [&](int r_lo, int r_hi) {
+        NvtxRange nv("spg:summa panels + broadcasts");
         // Fused: pack every panel this rank roots first, then exchange sizes and
         // issue all broadcasts back to back (device ones stay in flight), then
         // drain once — the per-stage host syncs no longer serialise them.
@@ -335,6 +338,7 @@ extern "C" int spg_summa25_multiply(spg_comm* comm, spg_ctx* c, int sr, int64_t 
         }
       }
       auto multiply_kept = [&]() -> spg_dcsr {
+        NvtxRange nv("spg:summa fused multiply");
         // C^T = [panB_0 | panB_1 | ...] (x) [panA_0; panA_1; ...]  in (stage, round) order
         // = ascending inner index k, so the fold order equals the serial reference's.
         const auto t0 = Clock::now();
