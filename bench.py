@@ -327,6 +327,9 @@ def run_single(args):
     # parity: the last timed C against the oracle's checksum of the same product
     csum = c.checksum()
     c.free()
+    # the dominant kernel's share: one untimed call with per-phase CUDA events
+    st2 = {}
+    local_multiply(d, d, stats=st2).free()
     golden = GOLDEN_CSUM.get((2, args.scale, args.ef, args.seed, bool(args.permute)))
     parity = None if golden is None else bool(csum == golden)
     ms = float(np.mean(times))
@@ -389,13 +392,28 @@ def run_single(args):
         cpu.pop("seconds", None)
         cpu.update(host_info())
 
-    traffic = None
+    traffic, fold_dram = None, None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(f"rmat{args.scale}")
+            tj = json.load(open(tp))
+            traffic = tj.get(f"rmat{args.scale}")
+            fold_dram = next((v["bytes"] for k, v in tj.get("per_kernel", {}).items() if "br_numeric" in k), None)
         except Exception:
             traffic = None
+    dominant = None
+    if st2.get("output_mode") == 3 and st2.get("ms_fold", 0) > 0:
+        # rank-space fold (br_numeric_kernel): gathers of R's (col, value) per product,
+        # C written once, the window bitmaps read back (SURVEY §8d terms)
+        fb = F * (4 + vs) + nnz_c * (4 + vs) + int(st2["bitmap_bytes"])
+        ach = fb / (st2["ms_fold"] * 1e-3) / 1e9
+        dominant = {"kernel": "br_numeric_kernel (rank-space fold into C)", "ms": st2["ms_fold"],
+                    "share_of_multiply": st2["ms_fold"] / st2["ms_total"], "algorithmic_bytes": fb,
+                    "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": fold_dram,
+                    "work_items": st2["fold_items"],
+                    "note": "phase time by CUDA events on the context stream around the fold (short-row "
+                            "compaction runs beside it); F and nnz(C) of the whole multiply (the long rows hold "
+                            "~99% of F); traffic = ncu dram bytes of the kernel (profiles/traffic.json)"}
     line = {
         "metric": METRIC, "value": gflops, "unit": "Gflop/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -412,7 +430,8 @@ def run_single(args):
                    "l2": "flushed between steps (512 MB write)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "note": f"B_alg of the whole local multiply (SURVEY §8d) / its event time; peak {peak_kind}"},
+                     "note": f"B_alg of the whole local multiply (SURVEY §8d) / its event time; peak {peak_kind}",
+                     "dominant_kernel": dominant},
         "parity": parity,
         "parity_check": {"checksum_C": csum, "golden": golden,
                          "how": "matrix_checksum (checksum.hpp:20-38) of the last timed C vs the CPU oracle's"},

@@ -116,6 +116,11 @@ typedef struct {
   int64_t output_mode;     /* 0: U-slot scratch + compaction, 1: exact claims + compaction,
                               2: two passes (count, then write into C),
                               3: bitmap-rank (long rows straight into C, short rows compacted) */
+  /* bitmap-rank pipeline (output_mode 3): the two phases of the long rows */
+  double ms_symbolic;      /* symbolic bitmaps (|| the short rows' kernels) + rowptr scan */
+  double ms_fold;          /* rank-space fold into C (|| the short rows' compaction) */
+  int64_t bitmap_bytes;    /* bitmap words streamed out by the symbolic pass and back in by the fold */
+  int64_t fold_items;      /* (row, rank window) work items of the fold */
 } spg_mult_stats;
 
 /* ---------------------------------------------------------------- misc */

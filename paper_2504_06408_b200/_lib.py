@@ -40,13 +40,17 @@ class MultStats(C.Structure):
     _fields_ = [("products", C.c_int64), ("nnz_out", C.c_int64),
                 ("rows_per_bin", C.c_int64 * 11), ("ms_analyse", C.c_double),
                 ("ms_numeric", C.c_double), ("ms_compact", C.c_double),
-                ("ms_total", C.c_double), ("kernels", C.c_int64), ("output_mode", C.c_int64)]
+                ("ms_total", C.c_double), ("kernels", C.c_int64), ("output_mode", C.c_int64),
+                ("ms_symbolic", C.c_double), ("ms_fold", C.c_double), ("bitmap_bytes", C.c_int64),
+                ("fold_items", C.c_int64)]
 
     def as_dict(self):
         return {"products": self.products, "nnz_out": self.nnz_out,
                 "rows_per_bin": list(self.rows_per_bin), "ms_analyse": self.ms_analyse,
                 "ms_numeric": self.ms_numeric, "ms_compact": self.ms_compact,
-                "ms_total": self.ms_total, "kernels": self.kernels, "output_mode": self.output_mode}
+                "ms_total": self.ms_total, "kernels": self.kernels, "output_mode": self.output_mode,
+                "ms_symbolic": self.ms_symbolic, "ms_fold": self.ms_fold, "bitmap_bytes": self.bitmap_bytes,
+                "fold_items": self.fold_items}
 
 
 class Stage(C.Structure):

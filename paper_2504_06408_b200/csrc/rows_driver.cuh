@@ -944,6 +944,10 @@ bool run_rows_br(spg_ctx* c, const MulSource<SR>& src, const spg_dcsr* r, int64_
     for (int b = 0; b < kNumBins; ++b) st->rows_per_bin[b] = (int64_t)hcounts[b];
     st->ms_numeric = ms_sym + ms_num;
     st->ms_compact = 0.0;
+    st->ms_symbolic = ms_sym;
+    st->ms_fold = ms_num;
+    st->bitmap_bytes = (int64_t)bm_bytes;
+    st->fold_items = nitems;
     st->ms_total = tm.between(0, 3);
     st->ms_analyse = st->ms_total - st->ms_numeric;
     st->kernels = (int64_t)(c->launches - launches0);
