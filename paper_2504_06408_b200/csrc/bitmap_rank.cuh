@@ -504,6 +504,7 @@ __global__ void __launch_bounds__(THREADS, MINB) br_numeric_kernel(
   __shared__ int s_cnt;
   __shared__ __align__(8) unsigned long long s_bar;  // bitmap bulk copy completion
   __shared__ bool s_issued;                          // this item's copy was issued ahead
+  __shared__ bool s_zero_seen;                       // a zero product was skipped in this item
   BR_T_INIT
   if (threadIdx.x == 0) {
     s_issued = false;
@@ -518,6 +519,7 @@ __global__ void __launch_bounds__(THREADS, MINB) br_numeric_kernel(
     // prefetched into L2 while this one is processed
     if (threadIdx.x == 0) {
       s_item = s_next;
+      s_zero_seen = false;
       long long nx = -1;
       if (s_next >= 0) {
         const unsigned long long w = atomicAdd(work, 1ull);
@@ -614,7 +616,10 @@ __global__ void __launch_bounds__(THREADS, MINB) br_numeric_kernel(
       BR_T(5);
       auto fold = [&](int32_t c, const V& v, auto fast) {
         if constexpr (!decltype(fast)::value) {
-          if (SR::is_zero(v)) return;  // add(x, zero) == x
+          if (SR::is_zero(v)) {  // add(x, zero) == x; its column may end up holding zero()
+            s_zero_seen = true;
+            return;
+          }
         }
         const int j = (c >> 5) - wb;
         const int rk = (int)pre16[j] + __popc(bm[j] & ((1u << (c & 31)) - 1u));
@@ -642,14 +647,18 @@ __global__ void __launch_bounds__(THREADS, MINB) br_numeric_kernel(
       }
     }
     // 4. values out (zero() entries counted for the drop-zeros fix-up)
-    int zc = 0;
-    for (int e = threadIdx.x; e < nr; e += THREADS) zc += SR::is_zero(acc[e]) ? 1 : 0;
-    smem_values_out<V>(cvals, base + r0, acc, nr, threadIdx.x, THREADS);
-    const int zt = Red(tmp.red).Sum(zc);
-    if (threadIdx.x == 0 && zt > 0) {
-      atomicAdd(rowzero + i, (unsigned long long)zt);
-      atomicAdd(zeros, (unsigned long long)zt);
+    // an entry folds to zero() only if a zero product was skipped or the add
+    // can cancel: count such entries only then (drop_zero_entries fix-up)
+    if (AddCanCancel<SR>::value || s_zero_seen) {
+      int zc = 0;
+      for (int e = threadIdx.x; e < nr; e += THREADS) zc += SR::is_zero(acc[e]) ? 1 : 0;
+      const int zt = Red(tmp.red).Sum(zc);
+      if (threadIdx.x == 0 && zt > 0) {
+        atomicAdd(rowzero + i, (unsigned long long)zt);
+        atomicAdd(zeros, (unsigned long long)zt);
+      }
     }
+    smem_values_out<V>(cvals, base + r0, acc, nr, threadIdx.x, THREADS);
     __syncthreads();
     BR_T(7);
   }
