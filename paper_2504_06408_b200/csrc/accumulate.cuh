@@ -1743,6 +1743,7 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
       balanced_items<SR, Src, NW>(src, cache, n, 0, [&](int32_t c, const V& v) {
         if (SR::is_zero(v)) return;
         uint32_t h = hash_slot((uint32_t)c, LOG2T);
+        int probes = 0;
         for (;;) {
           const int32_t k = *reinterpret_cast<volatile int32_t*>(&tkeys[h]);
           if (k == c) break;
@@ -1751,6 +1752,7 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
             if (prev == kEmptyKey || prev == c) break;
           }
           h = (h + 1) & (T - 1);
+          SPG_DCHECK(++probes < T);  // the bin keeps the table at most half full
         }
         atomic_accumulate<SR, true>(&tvals[h], v);
       });

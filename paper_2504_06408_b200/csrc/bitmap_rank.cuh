@@ -361,6 +361,7 @@ __global__ void __launch_bounds__(THREADS, MINB) br_symbolic_kernel(Src src, con
                                                              &s_cnt);
       BR_T(9);
       br_items<SR, Src, NW, SPG_BR_SYM_IPL, false, false>(src, nullptr, cs, nn, (int)(threadIdx.x >> 5), [&](int32_t c, const V&, auto) {
+        SPG_DCHECK(c >= 0 && (c >> 5) < nwords);
         atomicOr(&bm[c >> 5], 1u << (c & 31));
       });
       __syncthreads();
@@ -539,6 +540,7 @@ __global__ void __launch_bounds__(THREADS, MINB) br_numeric_kernel(
     const int p0 = w0.x, p1 = w1.x;                      // fine panels [p0, p1)
     const int r0 = w0.y, nr = w1.y - w0.y;               // output ranks [r0, r0 + nr)
     const int wb = p0 * wpp, nw = (p1 - p0) * wpp;       // bitmap words held
+    SPG_DCHECK(p0 >= 0 && p0 < p1 && p1 <= npf && nr >= 0 && nr <= capv && wb + nw <= nwords);
     // 1. the window's bitmap words: one bulk (TMA) copy into shared memory,
     //    completing on an mbarrier (issued at the end of the previous item's
     //    fold when this item was known then; else now)
@@ -591,6 +593,7 @@ __global__ void __launch_bounds__(THREADS, MINB) br_numeric_kernel(
           const uint32_t x = bm[j];
           pre16[j] = (uint16_t)rk;
           const uint32_t cb = (uint32_t)(wb + j) << 5;
+          SPG_DCHECK(rk + __popc(x) <= nr);
           if constexpr (sizeof(V) >= 4) {
             for (uint32_t y = x; y; y &= y - 1) stage[rk++] = cb + __ffs(y) - 1;
           } else {
@@ -622,7 +625,9 @@ __global__ void __launch_bounds__(THREADS, MINB) br_numeric_kernel(
           }
         }
         const int j = (c >> 5) - wb;
+        SPG_DCHECK(j >= 0 && j < nw);
         const int rk = (int)pre16[j] + __popc(bm[j] & ((1u << (c & 31)) - 1u));
+        SPG_DCHECK(rk >= 0 && rk < nr && (bm[j] >> (c & 31) & 1u));  // every product column is in the bitmap
         atomic_accumulate<SR, true>(&acc[rk], v);
       };
       constexpr int IPL = sizeof(V) > 4 ? 2 : SPG_BR_IPL;

@@ -96,6 +96,21 @@ struct HostTrace {
   }
 };
 
+// Device-side bounds checks of the checked build (make variant VNAME=checks
+// VFLAGS=-DSPG_CHECKS): a violated invariant traps the kernel (a CUDA error
+// on the next sync) instead of reading or writing out of bounds.  Used in
+// place of compute-sanitizer, which this GPU pool does not allow.
+#ifdef SPG_CHECKS
+#define SPG_DCHECK(cond) \
+  do {                   \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define SPG_DCHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 // NVTX range for profilers (nsys / ncu --nvtx): host-side phase markers,
 // no cost without an attached tool (NVTX v3, header-only).
 struct NvtxRange {

@@ -753,16 +753,22 @@ bool run_rows_br(spg_ctx* c, const MulSource<SR>& src, const spg_dcsr* r, int64_
   SPG_CUDA(cudaMemsetAsync(work.p, 0, 2 * sizeof(unsigned long long), c->stream));
   tm.mark(1);
 
-  constexpr int kSymThreads = 512, kNumThreads = 512;
+#ifndef SPG_BR_NUM_THREADS
+#define SPG_BR_NUM_THREADS 512  // fold CTA size
+#endif
+#ifndef SPG_BR_NUM_CTAS
+#define SPG_BR_NUM_CTAS 2  // fold CTAs per SM (shared memory split between them)
+#endif
+  constexpr int kSymThreads = 512, kNumThreads = SPG_BR_NUM_THREADS;
   // numeric geometry: 2 CTAs/SM when the bitmap is <= 32 KB, else 1; the rest
   // of the CTA's shared memory is the rank window's accumulator
-  auto num_kern = br_numeric_kernel<SR, Src, kNumThreads, 2>;
+  auto num_kern = br_numeric_kernel<SR, Src, kNumThreads, SPG_BR_NUM_CTAS>;
   int capv = 0;
   {
     cudaFuncAttributes fa{};
     SPG_CUDA(cudaFuncGetAttributes(&fa, num_kern));
     const size_t per_sm = 232448 - 2048;  // usable shared memory per SM, 1 KB reserved per CTA
-    const size_t num_budget = (nwords <= 8192 ? per_sm / 2 : per_sm) - fa.sharedSizeBytes - 256;
+    const size_t num_budget = (nwords <= 8192 ? per_sm / SPG_BR_NUM_CTAS : per_sm) - fa.sharedSizeBytes - 256;
     const BrNumLayout<V> l0{nwords + 8, 0};
     const size_t fixed = l0.bytes(kNumThreads);
     capv = fixed < num_budget ? (int)std::min<size_t>(65535, (num_budget - fixed) / sizeof(V)) & ~7 : 0;
