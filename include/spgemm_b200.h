@@ -115,7 +115,8 @@ typedef struct {
   int64_t kernels;         /* kernels launched by the call */
   int64_t output_mode;     /* 0: U-slot scratch + compaction, 1: exact claims + compaction,
                               2: two passes (count, then write into C),
-                              3: bitmap-rank (long rows straight into C, short rows compacted) */
+                              3: bitmap-rank (long rows straight into C, short rows compacted),
+                              4: pattern-only (Boolean: column-only count + emit passes) */
   /* bitmap-rank pipeline (output_mode 3): the two phases of the long rows */
   double ms_symbolic;      /* symbolic bitmaps (|| the short rows' kernels) + rowptr scan */
   double ms_fold;          /* rank-space fold into C (|| the short rows' compaction) */

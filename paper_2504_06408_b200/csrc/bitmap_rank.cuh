@@ -669,6 +669,117 @@ __global__ void __launch_bounds__(THREADS, MINB) br_numeric_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Pattern-only semirings (Boolean): every product of non-zero operands is
+// one() and the fold is idempotent, so C is the product's sparsity pattern.
+// br_pattern_kernel walks a row's products column-only, one column SUPER-PANEL
+// of SP columns at a time (a 64 KB shared-memory bitmap; each segment's slice
+// of the super-panel comes from the right operand's panel offsets), so any
+// output width works without stored bitmaps:
+//   MODE 0: nnz_i = sum of the super-panels' popcounts;
+//   MODE 1: (after the rowptr scan) the columns are emitted in order straight
+//           into C and the values set to one().
+// ---------------------------------------------------------------------------
+template <class SR, class Src, int THREADS, int MODE>
+__global__ void __launch_bounds__(THREADS, 3) br_pattern_kernel(Src src, const int64_t* __restrict__ rows,
+                                                                int64_t nrows_bin, int spw, int nsp,
+                                                                const int32_t* __restrict__ poff,
+                                                                unsigned long long* __restrict__ work,
+                                                                int64_t* __restrict__ rownnz,
+                                                                const int64_t* __restrict__ rowptr,
+                                                                int32_t* __restrict__ ccols,
+                                                                typename SR::value_type* __restrict__ cvals) {
+  using V = typename SR::value_type;
+  static_assert(!Src::kMultiSrc, "pattern path: local multiply sources only");
+  constexpr int NW = THREADS / 32;
+  using Scan = cub::BlockScan<int, THREADS>;
+  using Scan64 = cub::BlockScan<unsigned long long, THREADS>;
+  using Red = cub::BlockReduce<int, THREADS>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* bm = reinterpret_cast<uint32_t*>(smem_raw);  // [spw]
+  BrSegs<V> cs;
+  cs.carve(smem_raw + sizeof(uint32_t) * (size_t)spw, THREADS);
+  __shared__ union {
+    typename Scan::TempStorage scan;
+    typename Scan64::TempStorage scan64;
+    typename Red::TempStorage red;
+  } tmp;
+  __shared__ long long s_row;
+  __shared__ int s_any;
+  const int wpt = spw / THREADS;  // contiguous words per thread
+  const int w0 = threadIdx.x * wpt;
+  for (int q = threadIdx.x; q < spw; q += THREADS) bm[q] = 0u;
+  __syncthreads();
+  for (;;) {
+    if (threadIdx.x == 0) {
+      const unsigned long long r = atomicAdd(work, 1ull);
+      s_row = r < (unsigned long long)nrows_bin ? (long long)r : -1;
+    }
+    __syncthreads();
+    const long long r = s_row;
+    if (r < 0) break;
+    const int64_t i = rows[r];
+    const int64_t sb = src.seg_begin(i), nseg = src.seg_end(i) - sb;
+    int64_t run = MODE == 1 ? rowptr[i] : 0;  // next output position (MODE 1) / row count (MODE 0)
+    for (int sp = 0; sp < nsp; ++sp) {
+      if (threadIdx.x == 0) s_any = 0;
+      for (int64_t c0 = 0; c0 < nseg; c0 += THREADS) {
+        const int n = (int)(nseg - c0 < (int64_t)THREADS ? nseg - c0 : (int64_t)THREADS);
+        int dummy;
+        const int nn = br_seg_build<SR, Src, THREADS, Scan64>(
+            src, cs, br_seg_fetch_panels<SR>(src, poff, nsp, sp, sp + 1, nsp > 1, i, sb + c0, n), tmp.scan64, &dummy);
+        if (nn > 0 && threadIdx.x == 0) s_any = 1;
+        const int32_t cbase = sp * spw * 32;
+        br_items<SR, Src, NW, 2, false, false>(src, nullptr, cs, nn, (int)(threadIdx.x >> 5),
+                                               [&](int32_t c, const V&, auto) {
+                                                 const int cc = c - cbase;
+                                                 SPG_DCHECK(cc >= 0 && (cc >> 5) < spw);
+                                                 atomicOr(&bm[cc >> 5], 1u << (cc & 31));
+                                               });
+        __syncthreads();
+      }
+      if (!s_any) continue;  // no products in this super-panel: the bitmap is still clear
+      int cnt = 0;
+      for (int k = 0; k < wpt; ++k) cnt += __popc(bm[w0 + k]);
+      if constexpr (MODE == 0) {
+        run += Red(tmp.red).Sum(cnt);  // valid in thread 0, the only reader
+      } else {
+        int pre, tot;
+        Scan(tmp.scan).ExclusiveSum(cnt, pre, tot);
+        int64_t o = run + pre;
+        const int32_t cb = sp * spw * 32;
+        for (int k = 0; k < wpt; ++k) {
+          const int w = w0 + k;
+          for (uint32_t y = bm[w]; y; y &= y - 1) {
+            ccols[o] = cb + (w << 5) + __ffs(y) - 1;
+            cvals[o] = SR::one();
+            ++o;
+          }
+        }
+        run += tot;
+      }
+      __syncthreads();  // counts / emission read the bitmap before it is cleared
+      for (int k = 0; k < wpt; ++k) bm[w0 + k] = 0u;
+      __syncthreads();
+    }
+    if constexpr (MODE == 0) {
+      if (threadIdx.x == 0) rownnz[i] = run;
+    }
+    __syncthreads();
+  }
+}
+
+// non-zero check of operand values (pattern path eligibility)
+template <class SR>
+__global__ void count_zero_values_kernel(int64_t n, const typename SR::value_type* __restrict__ v,
+                                         unsigned long long* __restrict__ out) {
+  unsigned long long c = 0;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
+    c += SR::is_zero(v[u]) ? 1 : 0;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
 // Rare fix-up: drop entries whose value is the semiring zero (warp per row;
 // rows without such entries are copied as they are).
 template <class SR>

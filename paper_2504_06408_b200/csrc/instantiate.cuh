@@ -88,6 +88,7 @@ struct OpsImpl {
                              spg_mult_stats* st) {
     MulSource<SR> src{a->ptr, a->idx, static_cast<const V*>(a->vals),
                       b->ptr, b->idx, static_cast<const V*>(b->vals), a->nrows};
+    if (run_rows_pattern<SR>(c, src, b, b->ncols, out, st)) return;
     if (!run_rows_br<SR>(c, src, b, b->ncols, out, st)) run_rows<SR>(c, src, b->ncols, out, st, b);
   }
 

@@ -962,4 +962,227 @@ bool run_rows_br(spg_ctx* c, const MulSource<SR>& src, const spg_dcsr* r, int64_
   return true;
 }
 
+// ---------------------------------------------------------------------------
+// Pattern-only semirings (Boolean; semiring.cuh is_pattern_only): rows with
+// F > 2048 products get their columns from br_pattern_kernel (count pass,
+// rowptr scan, emit pass — any output width, column super-panels of up to
+// 2^19 columns, no stored bitmaps, values one()); shorter rows run the ESC /
+// hash kernels into U-slot scratch.  Not taken when an operand stores an
+// explicit zero() (its products must vanish): run_rows_br / run_rows then.
+// ---------------------------------------------------------------------------
+template <class SR>
+bool run_rows_pattern(spg_ctx* c, const MulSource<SR>& src, const spg_dcsr* r, int64_t ncols_out, spg_dcsr* out,
+                      spg_mult_stats* st) {
+  using V = typename SR::value_type;
+  using Src = MulSource<SR>;
+  if constexpr (!is_pattern_only<SR>::value) {
+    return false;
+  } else {
+    static const int on = [] {
+      const char* e = std::getenv("SPG_PATTERN");
+      return e ? std::atoi(e) : 1;
+    }();
+    const int64_t m = src.nrows;
+    if (!on || c->pipeline == SPG_PIPE_BINS || m == 0 || ncols_out <= 0 || r->nnz >= (int64_t{1} << 31) - 64)
+      return false;
+    // explicit zeros in either operand would have to vanish from C: not this path
+    {
+      int64_t lnnz = 0;
+      SPG_CUDA(cudaMemcpyAsync(&lnnz, src.lptr + m, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+      SPG_CUDA(cudaStreamSynchronize(c->stream));
+      DBuf<unsigned long long> z(c, 1);
+      SPG_CUDA(cudaMemsetAsync(z.p, 0, sizeof(unsigned long long), c->stream));
+      if (lnnz > 0) {
+        count_zero_values_kernel<SR><<<grid_for(c, lnnz, 256, 8), 256, 0, c->stream>>>(lnnz, src.lval, z.p);
+        SPG_LAUNCH_CHECK();
+      }
+      if (r->nnz > 0) {
+        count_zero_values_kernel<SR><<<grid_for(c, r->nnz, 256, 8), 256, 0, c->stream>>>(r->nnz, src.rval, z.p);
+        SPG_LAUNCH_CHECK();
+      }
+      c->launches += 2;
+      if (d2h_scalar(c, z.p) != 0) return false;
+    }
+    NvtxRange nv_all("spg:local_multiply (pattern)");
+    PhaseTimer tm(c, st != nullptr);
+    const uint64_t launches0 = c->launches;
+    tm.mark(0);
+    DBuf<int64_t> prods(c, m), ub(c, m + 1), off(c, m + 1), rownnz(c, m + 1);
+    DBuf<uint8_t> bins(c, m);
+    DBuf<int32_t> colmin(c, 1);
+    constexpr int64_t kLongF = 2048;
+    analyse_rows_kernel<SR, Src><<<grid_for(c, m, 8), 256, 0, c->stream>>>(
+        src, ncols_out, INT64_MAX, 0, 0, 0, 0, 0, kLongF, colmin.p, prods.p, ub.p, bins.p);
+    SPG_LAUNCH_CHECK();
+    ++c->launches;
+    SPG_CUDA(cudaMemsetAsync(ub.p + m, 0, sizeof(int64_t), c->stream));
+    SPG_CUDA(cudaMemsetAsync(rownnz.p + m, 0, sizeof(int64_t), c->stream));
+    exclusive_scan(c, ub.p, off.p, m + 1);
+    DBuf<unsigned long long> counts(c, kNumBins + 1);
+    SPG_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(unsigned long long) * (kNumBins + 1), c->stream));
+    bin_count_kernel<<<grid_for(c, m, 1024, 2), 1024, 0, c->stream>>>(bins.p, m, counts.p);
+    SPG_LAUNCH_CHECK();
+    ++c->launches;
+    unsigned long long hcounts[kNumBins];
+    int64_t scratch_total = 0;
+    SPG_CUDA(cudaMemcpyAsync(hcounts, counts.p, sizeof(hcounts), cudaMemcpyDeviceToHost, c->stream));
+    SPG_CUDA(cudaMemcpyAsync(&scratch_total, off.p + m, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    SPG_CUDA(cudaStreamSynchronize(c->stream));
+    const int64_t nb = (int64_t)hcounts[kBinBitmap];
+    size_t budget = c->scratch_budget;
+    if (budget == 0) budget = (size_t)(mem_available(c) * 0.45);
+    if ((size_t)scratch_total * (sizeof(int32_t) + sizeof(V)) > budget) return false;
+    DBuf<int32_t> sc_cols(c, (size_t)scratch_total + 16);
+    DBuf<V> sc_vals(c, (size_t)scratch_total + 16);
+    int64_t products = 0;
+    if (st) {
+      size_t bytes = 0;
+      DBuf<int64_t> fsum(c, 1);
+      SPG_CUDA(cub::DeviceReduce::Sum(nullptr, bytes, prods.p, fsum.p, m, c->stream));
+      ensure_cub_tmp(c, bytes);
+      SPG_CUDA(cub::DeviceReduce::Sum(c->cub_tmp, bytes, prods.p, fsum.p, m, c->stream));
+      ++c->launches;
+      products = d2h_scalar(c, fsum.p);
+    }
+    int end_bit = 0;
+    while ((int64_t{1} << end_bit) < ncols_out) ++end_bit;
+    DBuf<int64_t> lists(c, m);
+    DBuf<unsigned long long> cursor(c, kNumBins);
+    unsigned long long base[kNumBins];
+    {
+      unsigned long long acc = 0;
+      for (int b = 0; b < kNumBins; ++b) {
+        base[b] = acc;
+        if (b > 0) acc += hcounts[b];
+      }
+    }
+    SPG_CUDA(cudaMemcpyAsync(cursor.p, base, sizeof(base), cudaMemcpyHostToDevice, c->stream));
+    bin_scatter_kernel<<<grid_for(c, m, 1024, 2), 1024, 0, c->stream>>>(bins.p, m, cursor.p, lists.p);
+    SPG_LAUNCH_CHECK();
+    ++c->launches;
+    const int64_t* brows = lists.p + base[kBinBitmap];
+    DBuf<int64_t> bsorted, bk1, bk2;
+    if (nb > 1) {
+      bk1 = DBuf<int64_t>(c, nb);
+      bk2 = DBuf<int64_t>(c, nb);
+      bsorted = DBuf<int64_t>(c, nb);
+      gather_keys_kernel<<<grid_for(c, nb, 256, 4), 256, 0, c->stream>>>(brows, nb, prods.p, bk1.p);
+      SPG_LAUNCH_CHECK();
+      ++c->launches;
+      size_t bytes = 0;
+      SPG_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, bk1.p, bk2.p, brows, bsorted.p, (int)nb, 0,
+                                                          64, c->stream));
+      ensure_cub_tmp(c, bytes);
+      SPG_CUDA(cub::DeviceRadixSort::SortPairsDescending(c->cub_tmp, bytes, bk1.p, bk2.p, brows, bsorted.p, (int)nb,
+                                                          0, 64, c->stream));
+      ++c->launches;
+      brows = bsorted.p;
+    }
+    if (hcounts[kBinEmpty] > 0) {
+      zero_empty_rows_kernel<<<grid_for(c, m, 256, 4), 256, 0, c->stream>>>(bins.p, m, rownnz.p);
+      SPG_LAUNCH_CHECK();
+      ++c->launches;
+    }
+    // column super-panels: a 64 KB bitmap (<= 2^19 columns) per pass
+    const int spw = std::min(br_words(ncols_out), 16384);
+    const int64_t spc = (int64_t)spw * 32;
+    const int nsp = (int)((ncols_out + spc - 1) / spc);
+    DBuf<int32_t> poff;
+    if (nb > 0 && nsp > 1) {
+      poff = DBuf<int32_t>(c, (size_t)r->nrows * (nsp + 1));
+      panel_offsets_kernel<<<grid_for(c, r->nrows, 8), 256, 0, c->stream>>>(r->nrows, r->ptr, r->idx, nsp, (int)spc,
+                                                                            poff.p);
+      SPG_LAUNCH_CHECK();
+      ++c->launches;
+    }
+    DBuf<unsigned long long> work(c, 2);
+    SPG_CUDA(cudaMemsetAsync(work.p, 0, 2 * sizeof(unsigned long long), c->stream));
+    constexpr int kPT = 512;
+    const size_t psmem = sizeof(uint32_t) * (size_t)spw + BrSegs<V>::bytes(kPT) + 64;
+    tm.mark(1);
+    {  // count pass (long rows) || short rows into their slots
+      NvtxRange nv("spg:pattern count + short rows");
+      StreamFork fk(c, 3);
+      if (nb > 0) {
+        auto kern = br_pattern_kernel<SR, Src, kPT, 0>;
+        set_smem(kern, psmem);
+        kern<<<resident_grid(c, kern, kPT, psmem, nb), kPT, psmem, fk[0]>>>(src, brows, nb, spw, nsp, poff.p, work.p,
+                                                                            rownnz.p, nullptr, nullptr, nullptr);
+        SPG_LAUNCH_CHECK();
+        ++c->launches;
+      }
+      RowOut<V> o;
+      o.cols = sc_cols.p;
+      o.vals = sc_vals.p;
+      o.off = off.p;
+      o.rownnz = rownnz.p;
+      const int64_t* lb = lists.p;
+      if (hcounts[kBinHash8K] > 0)
+        launch_hash<SR, Src, 8192, 512>(c, fk[1], src, lb + base[kBinHash8K], hcounts[kBinHash8K], 256, end_bit, o);
+      if (hcounts[kBinHash4K] > 0)
+        launch_hash<SR, Src, 4096, 256>(c, fk[1], src, lb + base[kBinHash4K], hcounts[kBinHash4K], 256, end_bit, o);
+      if (hcounts[kBinHash2K] > 0)
+        launch_hash<SR, Src, 2048, 128>(c, fk[2], src, lb + base[kBinHash2K], hcounts[kBinHash2K], 256, end_bit, o);
+      if (hcounts[kBinEsc512] > 0)
+        launch_esc<SR, Src, 128, 4>(c, fk[2], src, lb + base[kBinEsc512], hcounts[kBinEsc512], end_bit, o);
+      if (hcounts[kBinWarpEsc] > 0) {
+        esc_warp_kernel<SR, Src><<<grid_for(c, hcounts[kBinWarpEsc], 8), 256, 0, fk[2]>>>(
+            src, lb + base[kBinWarpEsc], hcounts[kBinWarpEsc], o);
+        SPG_LAUNCH_CHECK();
+        ++c->launches;
+      }
+      for (int b : {(int)kBinDense, (int)kBinHashMax, (int)kBinBitRank, (int)kBinRankPanels})
+        if (hcounts[b] > 0) fail(SPG_ERR_INTERNAL, "pattern driver: unexpected bin");
+      fk.join();
+    }
+    out->ptr = dalloc<int64_t>(c, m + 1);
+    exclusive_scan(c, rownnz.p, out->ptr, m + 1);
+    const int64_t nnz = d2h_scalar(c, out->ptr + m);
+    tm.mark(2);
+    const float ms_cnt = tm.between(1, 2);
+    out->nrows = m;
+    out->ncols = ncols_out;
+    out->nnz = nnz;
+    out->idx = dalloc<int32_t>(c, (size_t)nnz);
+    out->vals = dalloc<V>(c, (size_t)nnz);
+    {  // emit pass (long rows, straight into C) || compaction of the short rows
+      NvtxRange nv("spg:pattern emit + short-row compaction");
+      StreamFork fk(c, 2);
+      if (nb > 0) {
+        auto kern = br_pattern_kernel<SR, Src, kPT, 1>;
+        set_smem(kern, psmem);
+        kern<<<resident_grid(c, kern, kPT, psmem, nb), kPT, psmem, fk[0]>>>(
+            src, brows, nb, spw, nsp, poff.p, work.p + 1, nullptr, out->ptr, out->idx, static_cast<V*>(out->vals));
+        SPG_LAUNCH_CHECK();
+        ++c->launches;
+      }
+      if (scratch_total > 0) {
+        compact_rows_kernel<V><<<grid_for(c, m, 8), 256, 0, fk[1]>>>(m, bins.p, off.p, out->ptr, sc_cols.p,
+                                                                   sc_vals.p, out->idx, static_cast<V*>(out->vals));
+        SPG_LAUNCH_CHECK();
+        ++c->launches;
+      }
+      fk.join();
+    }
+    tm.mark(3);
+    if (st) {
+      const float ms_emit = tm.between(2, 3);
+      st->products = products;
+      st->nnz_out = out->nnz;
+      for (int b = 0; b < kNumBins; ++b) st->rows_per_bin[b] = (int64_t)hcounts[b];
+      st->ms_numeric = ms_cnt + ms_emit;
+      st->ms_compact = 0.0;
+      st->ms_total = tm.between(0, 3);
+      st->ms_analyse = st->ms_total - st->ms_numeric;
+      st->kernels = (int64_t)(c->launches - launches0);
+      st->output_mode = 4;
+      st->ms_symbolic = ms_cnt;
+      st->ms_fold = ms_emit;
+      st->bitmap_bytes = 0;
+      st->fold_items = nb;
+    }
+    return true;
+  }
+}
+
 }  // namespace spg

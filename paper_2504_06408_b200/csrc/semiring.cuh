@@ -88,6 +88,9 @@ struct Boolean {
   SPG_HD static value_type one() { return 1; }
   SPG_HD static bool is_zero(value_type v) { return v == 0; }
   SPG_HD static value_type from_real(double x) { return x != 0.0 ? 1 : 0; }
+  // pattern-only: the product of two non-zeros is one() and the fold is
+  // idempotent, so C is the product's sparsity pattern with every value one()
+  static constexpr bool pattern_only = true;
 #ifdef __CUDACC__
   // OR with false is the identity and every writer of `true` writes the same
   // byte, so a plain store is a correct (race-free) accumulate.
@@ -189,6 +192,18 @@ struct has_acc<SR, decltype((void)SR::acc_shared((typename SR::value_type*)nullp
                                                  typename SR::value_type{}),
                             void())> {
   static constexpr bool value = true;
+};
+
+// Optional `pattern_only` (Boolean): mul(a, b) == one() for non-zero a, b and
+// add(one(), one()) == one(): C's values are all one(), only the pattern is
+// computed (two column-only passes, bitmap_rank.cuh: br_pattern_kernel).
+template <class SR, class = void>
+struct is_pattern_only {
+  static constexpr bool value = false;
+};
+template <class SR>
+struct is_pattern_only<SR, decltype((void)SR::pattern_only, void())> {
+  static constexpr bool value = SR::pattern_only;
 };
 
 // Optional fast multiply: a semiring may declare `small(v)` and

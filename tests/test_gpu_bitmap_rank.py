@@ -18,6 +18,7 @@ pytestmark = pytest.mark.gpu
 
 BIN_BITMAP = 10
 MODE_BITMAP = 3
+MODE_PATTERN = 4
 
 
 def _exact(sr, rng, n):
@@ -49,7 +50,7 @@ def test_rank_windows_against_oracle(ctx, sr):
     got = esc_multiply(a, b, ctx=ctx, stats=st)
     want = ob.orc_multiply(to_mat(a), to_mat(b))
     assert_same(got, want, sr, rtol=RTOL if sr == 0 else None)
-    assert st["output_mode"] == MODE_BITMAP
+    assert st["output_mode"] == (MODE_PATTERN if sr == 2 else MODE_BITMAP)
     lens = np.diff(b.rowptr)
     long_rows = sum(int(lens[a.colids[a.rowptr[i]:a.rowptr[i + 1]]].sum()) > 2048 for i in range(a.nrows))
     assert st["rows_per_bin"][BIN_BITMAP] == long_rows, st["rows_per_bin"]
@@ -64,14 +65,14 @@ def test_same_as_bins_pipeline_on_rmat(ctx, sr):
     d = DeviceCsr.upload(ctx, m)
     st = {}
     got = local_multiply(d, d, stats=st).download()
-    assert st["output_mode"] == MODE_BITMAP and st["rows_per_bin"][BIN_BITMAP] > 0
+    assert st["output_mode"] == (MODE_PATTERN if sr == 2 else MODE_BITMAP) and st["rows_per_bin"][BIN_BITMAP] > 0
     ctx.set_pipeline(ctx.PIPE_BINS)
     try:
         st2 = {}
         want = local_multiply(d, d, stats=st2).download()
     finally:
         ctx.set_pipeline(ctx.PIPE_AUTO)
-    assert st2["output_mode"] != MODE_BITMAP
+    assert st2["output_mode"] not in (MODE_BITMAP, MODE_PATTERN)
     assert_same(got, want, sr, rtol=RTOL if sr == 0 else None)
     assert_same(got, ob.orc_multiply(to_mat(m), to_mat(m)), sr, rtol=RTOL if sr == 0 else None)
 
@@ -140,3 +141,32 @@ def test_headline_config2_full_size_against_streaming_oracle(ctx):
     assert (z, f) == (1281547801, 2934326978)
     assert np.array_equal(rownnz, rn)
     assert csum == (ob.orc_seed(a.nrows, a.ncols) + s) % (1 << 64)
+
+
+@pytest.mark.parametrize("ncols", [3000, 200_000, 1_500_000])
+def test_boolean_pattern_path_any_width(ctx, ncols):
+    """Boolean (pattern-only): long rows take two column-only passes over
+    column super-panels of <= 2^19 columns (count, then emit straight into C
+    with every value one()) at any output width — 1.5M columns means three
+    super-panels per row.  An explicit false in an operand sends the call
+    down the general pipeline (its products must vanish)."""
+    rng = np.random.default_rng(17)
+    nb = 60
+    lens = rng.integers(200, min(ncols // 2, 4000), nb)
+    bptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    bcols = np.concatenate([np.sort(rng.choice(ncols, L, replace=False)) for L in lens]).astype(np.int64)
+    b = CsrMatrix(2, nb, ncols, bptr, bcols, np.ones(bcols.size, np.uint8))
+    rows = [np.sort(rng.choice(nb, k, replace=False)) for k in (1, 4, 12, 30, 60, 0, 2)]
+    aptr = np.concatenate([[0], np.cumsum([len(x) for x in rows])]).astype(np.int64)
+    acols = np.concatenate(rows).astype(np.int64)
+    a = CsrMatrix(2, len(rows), nb, aptr, acols, np.ones(acols.size, np.uint8))
+    st = {}
+    got = esc_multiply(a, b, ctx=ctx, stats=st)
+    assert_same(got, ob.orc_multiply(to_mat(a), to_mat(b)), 2)
+    assert st["output_mode"] == MODE_PATTERN and st["rows_per_bin"][BIN_BITMAP] >= 3, st
+    bz = CsrMatrix(2, nb, ncols, bptr, bcols, np.ones(bcols.size, np.uint8))
+    bz.values[::7] = 0  # explicit false entries
+    st2 = {}
+    got2 = esc_multiply(a, bz, ctx=ctx, stats=st2)
+    assert_same(got2, ob.orc_multiply(to_mat(a), to_mat(bz)), 2)
+    assert st2["output_mode"] != MODE_PATTERN
