@@ -706,6 +706,7 @@ __global__ void __launch_bounds__(THREADS, 3) br_pattern_kernel(Src src, const i
   } tmp;
   __shared__ long long s_row;
   __shared__ int s_any;
+  __shared__ int s_wcnt[NW];
   const int wpt = spw / THREADS;  // contiguous words per thread
   const int w0 = threadIdx.x * wpt;
   for (int q = threadIdx.x; q < spw; q += THREADS) bm[q] = 0u;
@@ -744,18 +745,53 @@ __global__ void __launch_bounds__(THREADS, 3) br_pattern_kernel(Src src, const i
       if constexpr (MODE == 0) {
         run += Red(tmp.red).Sum(cnt);  // valid in thread 0, the only reader
       } else {
-        int pre, tot;
-        Scan(tmp.scan).ExclusiveSum(cnt, pre, tot);
-        int64_t o = run + pre;
-        const int32_t cb = sp * spw * 32;
-        for (int k = 0; k < wpt; ++k) {
-          const int w = w0 + k;
-          for (uint32_t y = bm[w]; y; y &= y - 1) {
-            ccols[o] = cb + (w << 5) + __ffs(y) - 1;
-            cvals[o] = SR::one();
-            ++o;
-          }
+        // warp w owns the contiguous words [w * ww, (w + 1) * ww), lanes
+        // interleaved; per 32-word group a warp scan, then a flattened
+        // emission — lane e of every 32-output step finds its word by a
+        // shuffle search — so each store instruction writes 128 contiguous bytes
+        (void)cnt;
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        const int ww = spw / NW, wb0 = wid * ww;
+        int wc = 0;
+        for (int k = lane; k < ww; k += 32) wc += __popc(bm[wb0 + k]);
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) wc += __shfl_xor_sync(kFull, wc, d);
+        if (lane == 0) s_wcnt[wid] = wc;
+        __syncthreads();
+        int64_t o = run;
+        int tot = 0;
+        for (int q = 0; q < NW; ++q) {
+          const int v = s_wcnt[q];
+          if (q < wid) o += v;
+          tot += v;
         }
+        const int32_t cb = sp * spw * 32;
+        for (int g = 0; g < ww; g += 32) {
+          const uint32_t x = bm[wb0 + g + lane];
+          const int c = __popc(x);
+          int incl = c;
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            const int t = __shfl_up_sync(kFull, incl, d);
+            if (lane >= d) incl += t;
+          }
+          const int total = __shfl_sync(kFull, incl, 31);
+          const int excl = incl - c;
+          for (int q0 = 0; q0 < total; q0 += 32) {
+            const int q = q0 + lane;
+            int own = 0;
+#pragma unroll
+            for (int step = 16; step >= 1; step >>= 1) {
+              const int v = __shfl_sync(kFull, incl, own + step - 1);
+              if (v <= q) own += step;
+            }
+            const uint32_t xo = __shfl_sync(kFull, x, own);
+            const int eo = __shfl_sync(kFull, excl, own);
+            if (q < total) ccols[o + q] = cb + ((wb0 + g + own) << 5) + nth_set_bit(xo, q - eo);
+          }
+          o += total;
+        }
+        for (int e = threadIdx.x; e < tot; e += THREADS) cvals[run + e] = SR::one();  // coalesced
         run += tot;
       }
       __syncthreads();  // counts / emission read the bitmap before it is cleared
