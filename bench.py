@@ -458,7 +458,7 @@ def run_summa(args):
     from paper_2504_06408_b200 import Context, generators
     from paper_2504_06408_b200._lib import check, lib
     from paper_2504_06408_b200.summa import (DEVICE_ONLY, HOST_ONLY, HYBRID, Comm, checksum_part, checksum_seed,
-                                             grid_for, local_block, summa25_multiply)
+                                             distribute, grid_for, summa25_multiply)
 
     rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -482,6 +482,7 @@ def run_summa(args):
     mode = {"host": HOST_ONLY, "device": DEVICE_ONLY, "hybrid": HYBRID}[args.comm]
 
     t_gen = time.time()
+    ctx = Context(local)
     sr, n = wl["sr"], wl["n"]
     from paper_2504_06408_b200.summa import block_from_piece, block_range
     rr, cr = block_range(n, pr, i), block_range(n, pc, j)
@@ -489,7 +490,7 @@ def run_summa(args):
         coo = generators.generate_rmat(sr, args.scale, args.ef, args.seed)
         if args.permute:
             coo = generators.permute_symmetric(coo, args.seed)
-        blk = local_block(coo, pr, pc, i, j)
+        blk = distribute(ctx, coo, pr, pc, only_rank=rank)  # on the GPU: this rank's block only
         del coo
     elif wl["gen"] == "stencil27":
         blk = block_from_piece(generators.generate_stencil27_block(sr, wl["N"], rr, cr), rr, cr)
@@ -505,7 +506,6 @@ def run_summa(args):
         if hasattr(st, k):
             setattr(st, k, pinned_copy(getattr(st, k)))
     stream = torch.cuda.current_stream()
-    ctx = Context(local)
     check(lib.spg_ctx_set_stream(ctx.handle, C.c_void_p(stream.cuda_stream)), ctx.handle)
     comm = Comm(job[0], world, rank, pr, pc, local, staging_bytes=64 << 20)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")

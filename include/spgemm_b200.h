@@ -348,6 +348,32 @@ SPG_API int spg_summa25_multiply(spg_comm* comm, spg_ctx* ctx, int sr, int64_t a
                                  const spg_hdcsc* b_dcsc, const spg_summa_opts* opts,
                                  spg_dcsr* c_csc, spg_ledger* ledger);
 
+/* One rank's block as distribute builds it (LocalBlock, dist_matrix.hpp:41-53):
+ * global extents [row_begin, row_end) x [col_begin, col_end) and storage CSC
+ * (is_dcsc == 0, `csc`) or DCSC (is_dcsc == 1, `dcsc`); host arrays owned by
+ * the library (spg_block_free). */
+typedef struct {
+  int64_t row_begin, row_end, col_begin, col_end;
+  int is_dcsc;
+  spg_hcsr csc;
+  spg_hdcsc dcsc;
+} spg_block;
+
+/* distribute (dist_matrix.hpp:69-111) ON THE GPU: the host COO (global
+ * indices, any order, duplicates allowed) is uploaded once, every tuple is
+ * routed to the block owning it (block_index_of, dist_matrix.hpp:31-37) on a
+ * pr x pc grid (rank = i * pc + j), each block is built as coo_to_csc does
+ * (formats.hpp:138-180: stable column-major order, duplicates folded with
+ * SR::add in input order, zeros dropped) by one device radix sort, and a block
+ * with fewer than half of its columns populated is stored DCSC.  only_rank < 0
+ * builds all pr * pc blocks into blocks[rank]; only_rank >= 0 builds that
+ * rank's block alone into blocks[0] (one process per GPU).
+ * MalformedInputError for a tuple outside nrows x ncols. */
+SPG_API int spg_distribute(spg_ctx* ctx, int sr, int64_t nrows, int64_t ncols, int64_t nnz,
+                           const int64_t* rows, const int64_t* cols, const void* vals, int pr, int pc,
+                           int only_rank, spg_block* blocks);
+SPG_API void spg_block_free(spg_block* b);
+
 /* gather (dist_matrix.hpp gather): every rank's CSC block of C
  * (block-local indices, rows offset row_off, columns offset col_off) to world
  * rank `root`, assembled there ON THE GPU into the full nrows x ncols CSC

@@ -394,71 +394,61 @@ struct DistMatrix {
   std::vector<LocalBlock<SR>> blocks;  // indexed by rank
 };
 
-// distribute (dist_matrix.hpp:69-111): route every (normalised) tuple to its
-// block; a block with fewer than half its columns populated is stored DCSC.
+// distribute (dist_matrix.hpp:69-111) on the GPU (spg_distribute): the COO
+// is uploaded once, routed to its blocks and sorted column-major per block
+// by one device radix sort (coo_to_csc semantics, formats.hpp:138-180:
+// duplicates folded with SR::add in input order, zeros dropped); a block with
+// fewer than half of its columns populated is stored DCSC.
 template <class SR>
-DistMatrix<SR> distribute(const CooMatrix<SR>& m, const ProcessGrid& grid) {
+DistMatrix<SR> distribute(Context& ctx, const CooMatrix<SR>& m, const ProcessGrid& grid) {
+  const size_t n = m.tuples.size();
+  std::vector<index_t> rows(n), cols(n);
+  std::vector<typename SR::value_type> vals(n);
+  for (size_t k = 0; k < n; ++k) {
+    rows[k] = m.tuples[k].row;
+    cols[k] = m.tuples[k].col;
+    vals[k] = m.tuples[k].value;
+  }
+  std::vector<spg_block> raw((size_t)grid.size());
+  ctx.check(spg_distribute(ctx.get(), SR::id, m.nrows, m.ncols, (index_t)n, rows.data(), cols.data(), vals.data(),
+                           grid.rows(), grid.cols(), -1, raw.data()));
   DistMatrix<SR> out;
   out.nrows = m.nrows;
   out.ncols = m.ncols;
   out.grid = grid;
-  const int pr = grid.rows(), pc = grid.cols();
-  std::vector<BlockRange> rr(pr), cr(pc);
-  for (int i = 0; i < pr; ++i) rr[i] = block_range(m.nrows, pr, i);
-  for (int j = 0; j < pc; ++j) cr[j] = block_range(m.ncols, pc, j);
-  auto owner = [](const std::vector<BlockRange>& v, index_t x) {
-    int lo = 0, hi = (int)v.size() - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) / 2;
-      if (v[mid].begin <= x) lo = mid;
-      else hi = mid - 1;
-    }
-    return lo;
-  };
-  std::vector<std::vector<typename CooMatrix<SR>::Tuple>> per(grid.size());
-  for (const auto& t : m.tuples) per[grid.rank_at(owner(rr, t.row), owner(cr, t.col))].push_back(t);
-  out.blocks.resize(grid.size());
-  for (int r = 0; r < grid.size(); ++r) {
-    auto& tu = per[r];
-    const BlockRange br = rr[grid.row_of(r)], bc = cr[grid.col_of(r)];
-    std::stable_sort(tu.begin(), tu.end(), [](const auto& x, const auto& y) {
-      return x.col != y.col ? x.col < y.col : x.row < y.row;
-    });
-    CscMatrix<SR> csc;
-    csc.nrows = br.size();
-    csc.ncols = bc.size();
-    csc.colptr.assign((size_t)csc.ncols + 1, 0);
-    for (const auto& t : tu) {
-      ++csc.colptr[(size_t)(t.col - bc.begin) + 1];
-      csc.rowids.push_back(t.row - br.begin);
-      csc.values.push_back(t.value);
-    }
-    index_t populated = 0;
-    for (index_t c = 0; c < csc.ncols; ++c) {
-      populated += csc.colptr[(size_t)c + 1] > 0;
-      csc.colptr[(size_t)c + 1] += csc.colptr[(size_t)c];
-    }
-    LocalBlock<SR> blk;
-    blk.rows = br;
-    blk.cols = bc;
-    if (2 * populated < csc.ncols) {
+  out.blocks.resize(raw.size());
+  for (size_t r = 0; r < raw.size(); ++r) {
+    spg_block& b = raw[r];
+    LocalBlock<SR>& blk = out.blocks[r];
+    blk.rows = BlockRange{b.row_begin, b.row_end};
+    blk.cols = BlockRange{b.col_begin, b.col_end};
+    if (b.is_dcsc) {
       DcscMatrix<SR> d;
-      d.nrows = csc.nrows;
-      d.ncols = csc.ncols;
-      for (index_t c = 0; c < csc.ncols; ++c)
-        if (csc.colptr[(size_t)c + 1] > csc.colptr[(size_t)c]) {
-          d.jc.push_back(c);
-          d.cp.push_back(csc.colptr[(size_t)c + 1]);
-        }
-      d.rowids = std::move(csc.rowids);
-      d.values = std::move(csc.values);
+      d.nrows = b.dcsc.nrows;
+      d.ncols = b.dcsc.ncols;
+      detail::take_idx(d.jc, b.dcsc.jc, b.dcsc.njc);
+      detail::take_idx(d.cp, b.dcsc.cp, b.dcsc.njc + 1);
+      detail::take_idx(d.rowids, b.dcsc.rowids, b.dcsc.nnz);
+      detail::take(d.values, b.dcsc.vals, b.dcsc.nnz);
       blk.storage = std::move(d);
     } else {
-      blk.storage = std::move(csc);
+      CscMatrix<SR> c;
+      c.nrows = b.csc.nrows;
+      c.ncols = b.csc.ncols;
+      detail::take_idx(c.colptr, b.csc.ptr, b.csc.ncols + 1);
+      detail::take_idx(c.rowids, b.csc.idx, b.csc.nnz);
+      detail::take(c.values, b.csc.vals, b.csc.nnz);
+      blk.storage = std::move(c);
     }
-    out.blocks[r] = std::move(blk);
+    spg_block_free(&b);
   }
   return out;
+}
+
+// distribute(m, grid) — the reference signature, on the per-thread default context.
+template <class SR>
+DistMatrix<SR> distribute(const CooMatrix<SR>& m, const ProcessGrid& grid) {
+  return distribute(default_context(), m, grid);
 }
 
 // gather (dist_matrix.hpp:115-141): all blocks back into one normalised COO.

@@ -466,6 +466,27 @@ int ref_dcsc_roundtrip(int sr, const ref_csr* csc, int64_t* jc_len, ref_csr* out
   });
 }
 
+// distribute (dist_matrix.hpp:69-111) on a p-rank square grid: rank's block
+// as CSC (dcsc_decompress'ed when stored DCSC), its DCSC flag and extents.
+int ref_distribute_block(int sr, const ref_coo* m, int p, int rank, ref_csr* out, int* is_dcsc,
+                         int64_t* extents) {
+  return guarded([&] {
+    return with_ref_sr(sr, [&](auto t) {
+      using SR = typename decltype(t)::type;
+      const auto dm = distribute(to_coo<SR>(*m), ProcessGrid{p});
+      const auto& blk = dm.blocks.at(static_cast<std::size_t>(rank));
+      *is_dcsc = std::holds_alternative<DcscMatrix<SR>>(blk.storage) ? 1 : 0;
+      extents[0] = blk.rows.begin;
+      extents[1] = blk.rows.end;
+      extents[2] = blk.cols.begin;
+      extents[3] = blk.cols.end;
+      if (*is_dcsc) from_csc(dcsc_decompress(std::get<DcscMatrix<SR>>(blk.storage)), out);
+      else from_csc(std::get<CscMatrix<SR>>(blk.storage), out);
+      return 0;
+    });
+  });
+}
+
 // summa25_multiply(distribute(A, p), distribute(B, p), bundled model, cfg, opts)
 // then gather (summa.hpp:248-349, dist_matrix.hpp:69-141).  ledger receives
 // {host_bcasts, device_bcasts, bytes_host, bytes_device, size_exchanges,

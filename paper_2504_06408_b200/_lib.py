@@ -29,6 +29,13 @@ class HDcsc(C.Structure):
                 ("rowids", C.POINTER(C.c_int64)), ("vals", C.c_void_p)]
 
 
+class Block(C.Structure):
+    """spg_block: one rank's block as spg_distribute builds it."""
+
+    _fields_ = [("row_begin", C.c_int64), ("row_end", C.c_int64), ("col_begin", C.c_int64),
+                ("col_end", C.c_int64), ("is_dcsc", C.c_int), ("csc", HCsr), ("dcsc", HDcsc)]
+
+
 class DCsr(C.Structure):
     """spg_dcsr: device CSR/CSC (int64 offsets, int32 indices)."""
 
@@ -152,6 +159,9 @@ _SIGS = [
                             _P(C.c_int)]),
     ("spg_comm_set_device_transport", C.c_int, [C.c_void_p, C.c_int]),
     ("spg_comm_has_device_path", C.c_int, [C.c_void_p]),
+    ("spg_distribute", C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64, _i64p, _i64p, C.c_void_p,
+                                 C.c_int, C.c_int, C.c_int, _P(Block)]),
+    ("spg_block_free", None, [_P(Block)]),
     ("spg_gather", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, _P(DCsr), C.c_int64, C.c_int64, C.c_int64, C.c_int64,
                              C.c_int, _P(DCsr)]),
     ("spg_summa25_multiply", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64,

@@ -372,7 +372,8 @@ int spg_register_semiring(const spg_semiring_ops* ops_in, int* id) {
     if (ops->abi != kSrOpsAbi)
       fail(SPG_ERR_ARG, "semiring ops table ABI " + std::to_string(ops->abi) + " != " + std::to_string(kSrOpsAbi) +
                             " (rebuild the semiring library against this release's headers)");
-    need(ops->name && ops->name[0] && ops->local_multiply && ops->merge && ops->checksum_part,
+    need(ops->name && ops->name[0] && ops->local_multiply && ops->merge && ops->checksum_part &&
+             ops->fold_runs,
          "incomplete semiring ops table");
     if (ops->value_size != 1 && ops->value_size != 2 && ops->value_size != 4 && ops->value_size != 8 &&
         ops->value_size != 16)
@@ -854,6 +855,40 @@ int spg_coo_to_csr(int sr, int64_t nrows, int64_t ncols, int64_t nnz, const int6
 }
 
 void spg_free(void* p) { host_release(p); }
+
+void spg_block_free(spg_block* b) {
+  if (!b) return;
+  for (void* p : {(void*)b->csc.ptr, (void*)b->csc.idx, b->csc.vals, (void*)b->dcsc.jc, (void*)b->dcsc.cp,
+                  (void*)b->dcsc.rowids, b->dcsc.vals})
+    host_release(p);
+  std::memset(b, 0, sizeof(*b));
+}
+
+int spg_distribute(spg_ctx* c, int sr, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rows,
+                   const int64_t* cols, const void* vals, int pr, int pc, int only_rank, spg_block* blocks) {
+  const int nout = only_rank >= 0 ? 1 : std::max(pr, 0) * std::max(pc, 0);
+  if (blocks && pr > 0 && pc > 0) std::memset(blocks, 0, sizeof(spg_block) * (size_t)nout);
+  const int rc = guarded(c, [&] {
+    need(c && blocks && (nnz == 0 || (rows && cols && vals)), "null argument");
+    need(nrows >= 0 && ncols >= 0 && nnz >= 0, "negative dims");
+    if (pr < 1 || pc < 1) fail(SPG_ERR_GRID, "distribute: grid must be at least 1 x 1");
+    if (only_rank >= pr * pc) fail(SPG_ERR_GRID, "distribute: rank outside the grid");
+    if ((nrows + pr - 1) / pr > INT32_MAX || (ncols + pc - 1) / pc > INT32_MAX)
+      fail(SPG_ERR_INVALID_RANGE, "block dimension exceeds int32 indices");
+    use_device(c);
+    distribute_coo(c, ops_for(sr), nrows, ncols, nnz, rows, cols, vals, pr, pc, only_rank, blocks,
+                   [](size_t bytes) -> void* {
+                     try {
+                       return pinned().get(bytes);
+                     } catch (...) {
+                       return nullptr;
+                     }
+                   });
+  });
+  if (rc != SPG_OK && blocks && pr > 0 && pc > 0)
+    for (int k = 0; k < nout; ++k) spg_block_free(&blocks[k]);
+  return rc;
+}
 
 void* spg_host_alloc(uint64_t bytes) {
   try {

@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(256) checksum_kernel(int64_t nseg, const int64
   }
 }
 
-constexpr int kSrOpsAbi = 1;  // layout version of SrOps (checked at registration)
+constexpr int kSrOpsAbi = 2;  // layout version of SrOps (checked at registration)
 
 struct SrOps {
   int abi;
@@ -78,7 +78,29 @@ struct SrOps {
   void (*merge)(spg_ctx*, int, const spg_dcsr*, int64_t, int64_t, spg_dcsr*, spg_mult_stats*);
   // sum of tuple terms with coordinate offsets (no dims seed)
   uint64_t (*checksum_part)(spg_ctx*, const spg_dcsr*, int, int64_t, int64_t);
+  // distribute's duplicate fold (formats.hpp:160-170): run u covers sorted
+  // positions [heads[u], heads[u+1]) (the last ends at n); its values
+  // vin[order[p]] fold left to right with SR::add into vout[u]; keep[u] = the
+  // result is not SR::is_zero.
+  void (*fold_runs)(spg_ctx*, int64_t nu, const int64_t* heads, int64_t n, const int64_t* order,
+                    const void* vin, void* vout, uint8_t* keep);
 };
+
+// One thread per run of equal (rank, column, row) keys.
+template <class SR>
+__global__ void __launch_bounds__(256) fold_runs_kernel(int64_t nu, const int64_t* __restrict__ heads, int64_t n,
+                                                        const int64_t* __restrict__ order,
+                                                        const typename SR::value_type* __restrict__ vin,
+                                                        typename SR::value_type* __restrict__ vout,
+                                                        uint8_t* __restrict__ keep) {
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < nu; u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = heads[u], e = u + 1 < nu ? heads[u + 1] : n;
+    typename SR::value_type acc = vin[order[b]];
+    for (int64_t p = b + 1; p < e; ++p) acc = SR::add(acc, vin[order[p]]);
+    vout[u] = acc;
+    keep[u] = !SR::is_zero(acc);
+  }
+}
 
 template <class SR>
 struct OpsImpl {
@@ -119,6 +141,15 @@ struct OpsImpl {
     }
     return d2h_scalar(c, acc.p);
   }
+
+  static void fold_runs(spg_ctx* c, int64_t nu, const int64_t* heads, int64_t n, const int64_t* order,
+                        const void* vin, void* vout, uint8_t* keep) {
+    if (nu <= 0) return;
+    fold_runs_kernel<SR><<<grid_for(c, nu, 256, 8), 256, 0, c->stream>>>(
+        nu, heads, n, order, static_cast<const V*>(vin), static_cast<V*>(vout), keep);
+    SPG_LAUNCH_CHECK();
+    ++c->launches;
+  }
 };
 
 template <class SR, class = void>
@@ -134,7 +165,8 @@ constexpr int sr_id() {
 template <class SR>
 const SrOps* ops_instance() {
   static const SrOps o{kSrOpsAbi, sr_id<SR>(), SR::name, (int)sizeof(typename SR::value_type), SR::is_commutative_mul,
-                       &OpsImpl<SR>::local_multiply, &OpsImpl<SR>::merge, &OpsImpl<SR>::checksum_part};
+                       &OpsImpl<SR>::local_multiply, &OpsImpl<SR>::merge, &OpsImpl<SR>::checksum_part,
+                       &OpsImpl<SR>::fold_runs};
   return &o;
 }
 

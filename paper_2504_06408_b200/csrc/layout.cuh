@@ -37,6 +37,8 @@ struct VBytes;
 template <>
 struct VBytes<1> { using T = uint8_t; };
 template <>
+struct VBytes<2> { using T = uint16_t; };
+template <>
 struct VBytes<4> { using T = uint32_t; };
 template <>
 struct VBytes<8> { using T = unsigned long long; };
@@ -47,12 +49,20 @@ template <class F>
 void with_vs(int vs, F&& f) {
   switch (vs) {
     case 1: f(VBytes<1>{}); break;
+    case 2: f(VBytes<2>{}); break;
     case 4: f(VBytes<4>{}); break;
     case 8: f(VBytes<8>{}); break;
     case 16: f(VBytes<16>{}); break;
     default: fail(SPG_ERR_ARG, "unsupported value size " + std::to_string(vs));
   }
 }
+
+struct SrOps;
+// distribute + coo_to_csc on the device (distribute.cu); host arrays of the
+// blocks come from `halloc`.
+void distribute_coo(spg_ctx* c, const SrOps* ops, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rows,
+                    const int64_t* cols, const void* vals, int pr, int pc, int only_rank, spg_block* blocks,
+                    void* (*halloc)(size_t));
 
 void narrow_indices(spg_ctx* c, const int64_t* in, int32_t* out, int64_t n, int64_t bound);
 void widen_indices(spg_ctx* c, const int32_t* in, int64_t* out, int64_t n);

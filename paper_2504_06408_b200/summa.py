@@ -64,6 +64,45 @@ def local_block(m: CooMatrix, pr: int, pc: int, i: int, j: int) -> LocalBlock:
     return block_from_piece(piece, (rb, re), (cb, ce))
 
 
+def distribute(ctx: Context, m: CooMatrix, pr: int, pc: int, only_rank: int | None = None):
+    """distribute (dist_matrix.hpp:69-111) on the GPU (spg_distribute): the
+    COO is uploaded once, routed to its blocks, sorted column-major per block
+    by one device radix sort, duplicates folded with SR::add in input order
+    and zeros dropped (coo_to_csc, formats.hpp:138-180); a block with fewer
+    than half of its columns populated comes back DCSC.  Returns the list of
+    pr * pc LocalBlocks (rank = i * pc + j), or only `only_rank`'s block."""
+    from ._lib import Block
+    from .device import copy_out
+    from .semiring import dtype_of
+    rows = np.ascontiguousarray(m.rows, dtype=np.int64)
+    cols = np.ascontiguousarray(m.cols, dtype=np.int64)
+    vals = np.ascontiguousarray(m.values, dtype=dtype_of(m.sr))
+    n = 1 if only_rank is not None else pr * pc
+    out = (Block * n)()
+    i64 = C.POINTER(C.c_int64)
+    check(lib.spg_distribute(ctx.handle, int(m.sr), int(m.nrows), int(m.ncols), int(rows.shape[0]),
+                             rows.ctypes.data_as(i64), cols.ctypes.data_as(i64), vals.ctypes.data_as(C.c_void_p),
+                             int(pr), int(pc), -1 if only_rank is None else int(only_rank), out), ctx.handle)
+    dt = dtype_of(m.sr)
+    blocks = []
+    try:
+        for b in out:
+            if b.is_dcsc:
+                d = b.dcsc
+                st = DcscMatrix(m.sr, d.nrows, d.ncols, copy_out(d.jc, d.njc, np.int64),
+                                copy_out(d.cp, d.njc + 1, np.int64), copy_out(d.rowids, d.nnz, np.int64),
+                                copy_out(d.vals, d.nnz, dt))
+            else:
+                h = b.csc
+                st = CscMatrix(m.sr, h.nrows, h.ncols, copy_out(h.ptr, h.ncols + 1, np.int64),
+                               copy_out(h.idx, h.nnz, np.int64), copy_out(h.vals, h.nnz, dt))
+            blocks.append(LocalBlock(st, (b.row_begin, b.row_end), (b.col_begin, b.col_end)))
+    finally:
+        for b in out:
+            lib.spg_block_free(C.byref(b))
+    return blocks[0] if only_rank is not None else blocks
+
+
 def block_from_piece(piece: CooMatrix, rows: tuple, cols: tuple) -> LocalBlock:
     """LocalBlock from a block's COO in LOCAL indices (e.g. the block
     generators), DCSC when fewer than half of its columns are populated.

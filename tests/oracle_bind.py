@@ -67,6 +67,7 @@ if ref is not None:
     ref.ref_block_range.argtypes = [C.c_int64, C.c_int, C.c_int, _P(C.c_int64), _P(C.c_int64)]
     ref.ref_round_range.argtypes = [C.c_int64, C.c_int, C.c_int, _P(C.c_int64), _P(C.c_int64)]
     ref.ref_dcsc_roundtrip.argtypes = [C.c_int, _P(Csr), _P(C.c_int64), _P(Csr)]
+    ref.ref_distribute_block.argtypes = [C.c_int, _P(Coo), C.c_int, C.c_int, _P(Csr), _P(C.c_int), _P(C.c_int64)]
     ref.ref_summa.argtypes = [C.c_int, _P(Coo), _P(Coo), C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint64,
                               _P(Coo), _P(C.c_uint64), _P(C.c_double)]
     ref.ref_find_crossover_bundled.argtypes = [C.c_int, C.c_uint64, C.c_uint64, _P(C.c_uint64)]
@@ -229,6 +230,17 @@ def ref_coo_to_csc(sr, nrows, ncols, rows, cols, vals) -> Mat:
     out = Csr()
     _ok(ref.ref_coo_to_csc(sr, C.byref(_coo_struct(nrows, ncols, rows, cols, vals, sr)), C.byref(out)))
     return _take_csr(sr, out, csc=True, free=ref.ref_free)
+
+
+def ref_distribute_block(sr, nrows, ncols, rows, cols, vals, p, rank):
+    """The reference's distribute on a p-rank square grid: (block as CSC Mat,
+    is_dcsc, (row_begin, row_end, col_begin, col_end))."""
+    out = Csr()
+    flag = C.c_int()
+    ext = (C.c_int64 * 4)()
+    _ok(ref.ref_distribute_block(sr, C.byref(_coo_struct(nrows, ncols, rows, cols, vals, sr)), p, rank,
+                                 C.byref(out), C.byref(flag), ext))
+    return _take_csr(sr, out, csc=True, free=ref.ref_free), bool(flag.value), tuple(ext)
 
 
 def ref_checksum(m: Mat) -> int:

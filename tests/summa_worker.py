@@ -44,7 +44,7 @@ def main():
     import oracle_bind as ob
     from paper_2504_06408_b200 import Context, generators
     from paper_2504_06408_b200.formats import coo_to_csr
-    from paper_2504_06408_b200.summa import Comm, checksum_part, checksum_seed, gather, grid_for, local_block, \
+    from paper_2504_06408_b200.summa import Comm, checksum_part, checksum_seed, distribute, gather, grid_for, \
         summa25_multiply
 
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -58,8 +58,8 @@ def main():
 
     m = generators.generate_rmat(args.sr, args.scale, args.ef, args.seed)
     n = m.nrows
-    blk = local_block(m, pr, pc, i, j)
     ctx = Context(local)
+    blk = distribute(ctx, m, pr, pc, only_rank=rank)  # this rank's block, built on the GPU
     comm = Comm(job[0], world, rank, pr, pc, local, staging_bytes=args.staging)
     if not comm.has_device_path and args.mode != 0:
         raise SystemExit("ranks share a GPU: run with --mode 0 (host path)")

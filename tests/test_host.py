@@ -189,3 +189,19 @@ def test_dcsc_decompress_rejects_bad_input():
     d = formats.DcscMatrix(0, 3, 3, np.array([2, 1]), np.array([0, 1, 2]), np.array([0, 1]), np.ones(2))
     with pytest.raises(errors.MalformedInputError):
         formats.dcsc_decompress(d)
+
+
+@pytest.mark.parametrize("p", [1, 4, 9])
+def test_host_local_block_matches_reference_distribute(p):
+    """The host block builder (summa.local_block) against the reference's own
+    distribute on normalised R-MAT: extents, DCSC choice, CSC content."""
+    from paper_2504_06408_b200.summa import local_block
+    m = generators.generate_rmat(4, 9, 8.0, 5)
+    q = int(np.sqrt(p))
+    for rank in range(p):
+        blk = local_block(m, q, q, rank // q, rank % q)
+        want, want_dcsc, ext = ob.ref_distribute_block(4, m.nrows, m.ncols, m.rows, m.cols, m.values, p, rank)
+        assert blk.rows + blk.cols == ext and blk.is_dcsc == want_dcsc
+        csc = formats.dcsc_decompress(blk.storage) if blk.is_dcsc else blk.storage
+        assert np.array_equal(csc.colptr, want.ptr) and np.array_equal(csc.rowids, want.idx)
+        assert csc.values.tobytes() == want.vals.tobytes()
