@@ -104,10 +104,12 @@ typedef struct {
 typedef struct {
   int64_t products;        /* F: intermediate products (flops = 2F) */
   int64_t nnz_out;
-  int64_t rows_per_bin[11]; /* 0 empty, 1 warp-ESC, 2 block-ESC, 3/4/5 hash 4K/8K/2K, 6 dense panels,
+  int64_t rows_per_bin[12]; /* 0 empty, 1 warp-ESC, 2 block-ESC, 3/4/5 hash 4K/8K/2K, 6 dense panels,
                                7 hash max, 8 bit-rank (presence bitmap + ranked accumulator),
                                9 rank panels (bit-rank with accumulator panels in rank space),
-                               10 bitmap-rank (symbolic bitmap + ranked fold, written straight into C) */
+                               10 bitmap-rank (symbolic bitmap + ranked fold, written straight into C),
+                               11 wide rows (too wide for dense panels, too many outputs for a
+                                  shared-memory hash: products sorted in HBM, then folded) */
   double ms_analyse;       /* row products + binning + offsets */
   double ms_numeric;       /* accumulate kernels */
   double ms_compact;       /* output scan + compaction */
@@ -160,9 +162,13 @@ SPG_API int spg_ctx_set_scratch_budget(spg_ctx* ctx, uint64_t bytes);
    2048 products through the bitmap-rank kernels (symbolic bitmap pass, exact
    rowptr, values folded in rank space straight into C) whenever the output
    width fits a shared-memory bitmap; SPG_PIPE_BINS forces the per-bin
-   accumulators (hash / dense panels / bit-rank) with scratch + compaction. */
+   accumulators (hash / dense panels / bit-rank) with scratch + compaction;
+   SPG_PIPE_SORTED is SPG_PIPE_BINS with every dense-panel row sent to the
+   sort fallback (products sorted in HBM, then folded) that otherwise serves
+   only outputs too wide for dense panels. */
 #define SPG_PIPE_AUTO 0
 #define SPG_PIPE_BINS 1
+#define SPG_PIPE_SORTED 2
 SPG_API int spg_ctx_set_pipeline(spg_ctx* ctx, int mode);
 
 /* ---------------------------------------------------- device matrices */

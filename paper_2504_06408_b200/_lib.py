@@ -45,7 +45,7 @@ class DCsr(C.Structure):
 
 class MultStats(C.Structure):
     _fields_ = [("products", C.c_int64), ("nnz_out", C.c_int64),
-                ("rows_per_bin", C.c_int64 * 11), ("ms_analyse", C.c_double),
+                ("rows_per_bin", C.c_int64 * 12), ("ms_analyse", C.c_double),
                 ("ms_numeric", C.c_double), ("ms_compact", C.c_double),
                 ("ms_total", C.c_double), ("kernels", C.c_int64), ("output_mode", C.c_int64),
                 ("ms_symbolic", C.c_double), ("ms_fold", C.c_double), ("bitmap_bytes", C.c_int64),

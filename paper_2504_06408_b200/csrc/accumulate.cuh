@@ -51,7 +51,7 @@
 
 namespace spg {
 
-constexpr int kNumBins = 11;
+constexpr int kNumBins = 12;
 constexpr int32_t kEmptyKey = -1;
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -67,6 +67,7 @@ enum Bin : uint8_t {
   kBinBitRank = 8,   // F <= kBitRankMax, narrow C: presence bitmap + ranked accumulator
   kBinRankPanels = 9,  // longer rows in a bounded column window: bitmap ranks, accumulator panels in rank space
   kBinBitmap = 10,     // bitmap-rank pipeline (bitmap_rank.cuh): symbolic bitmap pass, then ranks, output direct into C
+  kBinWide = 11,       // dense-bin rows whose panels do not fit (very wide outputs): sort fallback (wide_rows.cuh)
 };
 
 // ---------------------------------------------------------------------------
@@ -1700,13 +1701,22 @@ struct HashSort {
   };
 };
 
-template <class SR, class Src, int T, int THREADS>
+// OPT (optimistic small table): rows are tried in a table sized for their
+// likely distinct count; a row whose distinct columns pass T/2 stops
+// inserting (at most THREADS more keys land, so probing always finds a free
+// slot), writes nothing and is listed in ovf_rows for a re-run in a full-size
+// table.  A stencil row (729 products, 125 outputs) then touches 512 slots
+// instead of 2048, at 4x the CTAs per SM.
+template <class SR, class Src, int T, int THREADS, bool OPT = false>
 __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64_t* __restrict__ rows,
                                                             int64_t nrows_bin, int cap, int end_bit,
-                                                            RowOut<typename SR::value_type> out) {
+                                                            RowOut<typename SR::value_type> out,
+                                                            unsigned long long* ovf_n = nullptr,
+                                                            int64_t* ovf_rows = nullptr) {
   using V = typename SR::value_type;
   using HS = HashSort<T, THREADS>;
   __shared__ long long s_base;
+  __shared__ int s_distinct, s_over;  // OPT only
   constexpr int SPT = T / THREADS;
   constexpr int NW = THREADS / 32;
   constexpr int NB = T / 2, NBT = NB / THREADS, kBucketMax = 32;
@@ -1734,6 +1744,10 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
       tkeys[e] = kEmptyKey;
       tvals[e] = SR::zero();
     }
+    if (OPT && threadIdx.x == 0) {
+      s_distinct = 0;
+      s_over = 0;
+    }
     const int64_t sb = src.seg_begin(i), nseg = src.seg_end(i) - sb;
     for (int64_t c0 = 0; c0 < nseg; c0 += cap) {
       const int n = (int)(nseg - c0 < (int64_t)cap ? nseg - c0 : (int64_t)cap);
@@ -1742,6 +1756,9 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
       cache.template prefix<THREADS, typename HS::Scan>(n, 0, tmp->scan);
       balanced_items<SR, Src, NW>(src, cache, n, 0, [&](int32_t c, const V& v) {
         if (SR::is_zero(v)) return;
+        if constexpr (OPT) {
+          if (*reinterpret_cast<volatile int*>(&s_over)) return;
+        }
         uint32_t h = hash_slot((uint32_t)c, LOG2T);
         int probes = 0;
         for (;;) {
@@ -1749,14 +1766,30 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
           if (k == c) break;
           if (k == kEmptyKey) {
             const int32_t prev = atomicCAS(&tkeys[h], kEmptyKey, c);
-            if (prev == kEmptyKey || prev == c) break;
+            if (prev == kEmptyKey) {
+              if constexpr (OPT) {
+                if (atomicAdd(&s_distinct, 1) >= T / 2) {
+                  s_over = 1;
+                  return;
+                }
+              }
+              break;
+            }
+            if (prev == c) break;
           }
           h = (h + 1) & (T - 1);
-          SPG_DCHECK(++probes < T);  // the bin keeps the table at most half full
+          SPG_DCHECK(++probes < T);  // the bin keeps the table at most half full (OPT: < T/2 + THREADS keys)
         }
         atomic_accumulate<SR, true>(&tvals[h], v);
       });
       __syncthreads();
+    }
+    if constexpr (OPT) {
+      if (s_over) {  // uniform after the barrier: re-run in the full-size table
+        if (threadIdx.x == 0) ovf_rows[atomicAdd(ovf_n, 1ull)] = i;
+        __syncthreads();
+        continue;
+      }
     }
     // occupied, non-zero slots -> staging.  Slots are taken striped (slot
     // t + q*THREADS: conflict-free shared loads); staging order is free, the

@@ -486,7 +486,7 @@ int spg_ctx_set_scratch_budget(spg_ctx* c, uint64_t bytes) {
 
 int spg_ctx_set_pipeline(spg_ctx* c, int mode) {
   return guarded(c, [&] {
-    need(c && (mode == SPG_PIPE_AUTO || mode == SPG_PIPE_BINS), "pipeline: unknown mode");
+    need(c && (mode == SPG_PIPE_AUTO || mode == SPG_PIPE_BINS || mode == SPG_PIPE_SORTED), "pipeline: unknown mode");
     c->pipeline = mode;
   });
 }

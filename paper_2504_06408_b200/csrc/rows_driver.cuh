@@ -51,6 +51,10 @@ inline int grid_for(spg_ctx* c, int64_t work_items, int per_block, int max_waves
   return (int)std::max<int64_t>(1, std::min<int64_t>(want, cap));
 }
 
+}  // namespace spg
+#include "wide_rows.cuh"  // uses exclusive_scan above
+namespace spg {
+
 // Forked side streams so independent bins overlap on the SMs.
 struct StreamFork {
   spg_ctx* c;
@@ -87,9 +91,10 @@ inline int resident_grid(spg_ctx* c, K kern, int threads, size_t smem, int64_t w
   return (int)std::max<int64_t>(1, std::min<int64_t>(work, cap));
 }
 
-template <class SR, class Src, int T, int THREADS>
+template <class SR, class Src, int T, int THREADS, bool OPT = false>
 void launch_hash(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* rows, int64_t n, int cap, int end_bit,
-                 const RowOut<typename SR::value_type>& out) {
+                 const RowOut<typename SR::value_type>& out, unsigned long long* ovf_n = nullptr,
+                 int64_t* ovf_rows = nullptr) {
   using V = typename SR::value_type;
   const size_t fixed = (size_t)T * (sizeof(V) + sizeof(int32_t) + sizeof(uint32_t)) +
                        ((sizeof(typename HashSort<T, THREADS>::Tmp) + 15) & ~size_t(15)) + 64;
@@ -99,9 +104,10 @@ void launch_hash(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* rows
   cap = std::min(cap, fit) & ~3;
   if (cap < 32) fail(SPG_ERR_INTERNAL, "hash bin: no shared memory left for the segment cache");
   const size_t smem = fixed + (size_t)cap * per;
-  auto kern = hash_rows_kernel<SR, Src, T, THREADS>;
+  auto kern = hash_rows_kernel<SR, Src, T, THREADS, OPT>;
   set_smem(kern, smem);
-  kern<<<resident_grid(c, kern, THREADS, smem, n), THREADS, smem, s>>>(src, rows, n, cap, end_bit, out);
+  kern<<<resident_grid(c, kern, THREADS, smem, n), THREADS, smem, s>>>(src, rows, n, cap, end_bit, out, ovf_n,
+                                                                        ovf_rows);
   SPG_LAUNCH_CHECK();
   ++c->launches;
 }
@@ -120,18 +126,32 @@ void launch_esc(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* rows,
 // Dense-panel geometry: (panel width, CTA size, smem budget per CTA).
 // cfg 0: 128 KB panel, 1024 threads, 1 CTA/SM; cfg 1: 64 KB, 512 threads,
 // 2 CTAs/SM; cfg 2: 32 KB, 512 threads, 3 CTAs/SM.  SPG_DENSE_CFG overrides.
-template <int W, int DT, class SR, class Src, int MINB = 1>
-void launch_dense_cfg(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* rows, int64_t n, int64_t ncols,
-                      size_t smem_budget, unsigned long long* work, const RowOut<typename SR::value_type>& out) {
+// Segments the dense kernel caches next to a W-column panel within
+// `smem_budget` (the per-segment panel offsets grow with the output width);
+// < 32 means the geometry does not fit and the rows take the sort fallback.
+template <int W, class SR, class Src>
+int dense_seg_cap(int64_t ncols, size_t smem_budget, size_t* smem_out = nullptr) {
   using V = typename SR::value_type;
-  const int np = (int)((ncols + W - 1) / W);
+  const int64_t np64 = (ncols + W - 1) / W;
+  if (np64 > (int64_t{1} << 20)) return 0;
+  const int np = (int)np64;
   const bool preall = kPreAll && np <= 32;  // per-row prefixes of every panel (small panel counts)
   const size_t per_seg = SegCache<SR, Src>::bytes_per_seg(np) + (preall ? sizeof(int) * np : 0);
   const size_t fixed = sizeof(V) * W + sizeof(uint32_t) * (W / 32) + (preall ? sizeof(int) * (np + 4) : 0);
   const size_t room = smem_budget > fixed + 64 ? smem_budget - fixed - 64 : 0;
   const int cap = (int)std::min<size_t>(8192, room / per_seg) & ~3;  // keeps 16-byte values aligned
+  if (smem_out) *smem_out = fixed + (size_t)cap * per_seg + 64;
+  return cap;
+}
+
+template <int W, int DT, class SR, class Src, int MINB = 1>
+void launch_dense_cfg(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* rows, int64_t n, int64_t ncols,
+                      size_t smem_budget, unsigned long long* work, const RowOut<typename SR::value_type>& out) {
+  const int np = (int)((ncols + W - 1) / W);
+  const bool preall = kPreAll && np <= 32;
+  size_t smem = 0;
+  const int cap = dense_seg_cap<W, SR, Src>(ncols, smem_budget, &smem);
   if (cap < 32) fail(SPG_ERR_INTERNAL, "dense panel: no room for the segment cache");
-  const size_t smem = fixed + (size_t)cap * per_seg + 64;
   auto kern = dense_panel_kernel<SR, Src, W, DT, MINB>;
   set_smem(kern, smem);
   kern<<<resident_grid(c, kern, DT, smem, n), DT, smem, s>>>(src, rows, n, np, cap, work, out, preall);
@@ -324,6 +344,20 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
     ++c->launches;
     products = d2h_scalar(c, fsum.p);
   }
+  // Dense-bin rows whose panel geometry does not fit next to the segment
+  // cache (very wide outputs with wide values) take the sort fallback (bin 11).
+  if (hcounts[kBinDense] > 0) {
+    constexpr int PW = Geom<V>::kPanelW;
+    const bool fits = dense_seg_cap<PW / 2, SR, Src>(ncols_out, 110 * 1024) >= 32 &&
+                      dense_seg_cap<PW, SR, Src>(ncols_out, 220 * 1024) >= 32;
+    if (!fits || c->pipeline == SPG_PIPE_SORTED) {
+      relabel_bin_kernel<<<grid_for(c, m, 1024, 2), 1024, 0, c->stream>>>(bins.p, m, kBinDense, kBinWide);
+      SPG_LAUNCH_CHECK();
+      ++c->launches;
+      hcounts[kBinWide] += hcounts[kBinDense];
+      hcounts[kBinDense] = 0;
+    }
+  }
 
   // Panels for the dense bin.
   const int W = dense_panel_width<V>();
@@ -471,10 +505,21 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
   }
   DBuf<unsigned long long> work(c, 2);
   float ms_numeric = 0.f, ms_compact = 0.f;
+  // 2K-slot hash rows (512 < F <= 1024) are first tried in a 512-slot table
+  // (many CTAs per SM, 4x fewer slots to clear and scan); rows with more than
+  // 256 distinct columns are re-run in the 2K table (SPG_HASH_OPT=0: off)
+  static const int hash_opt_on = [] {
+    const char* e = std::getenv("SPG_HASH_OPT");
+    return e ? std::atoi(e) : 1;
+  }();
+  const bool hash_opt = hash_opt_on && hcounts[kBinHash2K] > 0;
+  DBuf<unsigned long long> ovf_n(c, 1);
+  DBuf<int64_t> ovf_rows(c, hash_opt ? (size_t)hcounts[kBinHash2K] : 1);
 
   // One numeric pass over all bins with output placement `o`.
   auto numeric = [&](const RowOut<V>& o) {
     SPG_CUDA(cudaMemsetAsync(work.p, 0, 2 * sizeof(unsigned long long), c->stream));
+    if (hash_opt) SPG_CUDA(cudaMemsetAsync(ovf_n.p, 0, sizeof(unsigned long long), c->stream));
     const int64_t* lb = lists.p;
     StreamFork fk(c, 3);
     static const int plan = [] {  // SPG_STREAM_PLAN (default 1): heavy rows and rank panels on their own streams
@@ -498,7 +543,10 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
       launch_hash<SR, Src, 8192, 512>(c, fk[1], src, lb + base[kBinHash8K], hcounts[kBinHash8K], 256, end_bit, o);
     if (hcounts[kBinHash4K] > 0)
       launch_hash<SR, Src, 4096, 256>(c, fk[2], src, lb + base[kBinHash4K], hcounts[kBinHash4K], 256, end_bit, o);
-    if (hcounts[kBinHash2K] > 0)
+    if (hash_opt)
+      launch_hash<SR, Src, 512, 128, true>(c, fk[2], src, lb + base[kBinHash2K], hcounts[kBinHash2K], 64, end_bit, o,
+                                           ovf_n.p, ovf_rows.p);
+    else if (hcounts[kBinHash2K] > 0)
       launch_hash<SR, Src, 2048, 128>(c, fk[2], src, lb + base[kBinHash2K], hcounts[kBinHash2K], 256, end_bit, o);
     if (hcounts[kBinEsc512] > 0)
       launch_esc<SR, Src, 128, 4>(c, fk[2], src, lb + base[kBinEsc512], hcounts[kBinEsc512], end_bit, o);
@@ -533,6 +581,12 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
       ++c->launches;
     }
     fk.join();
+    if (hash_opt) {  // the rows that overflowed the 512-slot table
+      const int64_t nov = (int64_t)d2h_scalar(c, ovf_n.p);
+      if (nov > 0) launch_hash<SR, Src, 2048, 128>(c, c->stream, src, ovf_rows.p, nov, 256, end_bit, o);
+    }
+    if (hcounts[kBinWide] > 0)
+      run_wide_rows<SR, Src>(c, src, lb + base[kBinWide], (int64_t)hcounts[kBinWide], prods.p, o);
   };
 
   RowOut<V> first;
@@ -653,7 +707,7 @@ bool run_rows_br(spg_ctx* c, const MulSource<SR>& src, const spg_dcsr* r, int64_
     return std::min<int64_t>(e ? (int64_t)std::atoll(e) : 2048, 4096);
   }();
   const int64_t m = src.nrows;
-  if (!br_on || c->pipeline == SPG_PIPE_BINS || m == 0 || ncols_out <= 0 || ncols_out > kBrMaxCols)
+  if (!br_on || c->pipeline != SPG_PIPE_AUTO || m == 0 || ncols_out <= 0 || ncols_out > kBrMaxCols)
     return false;
   const int64_t nnz_r = r->nnz;
   if (nnz_r >= (int64_t{1} << 31) - 64) return false;  // 32-bit entry offsets
@@ -983,7 +1037,7 @@ bool run_rows_pattern(spg_ctx* c, const MulSource<SR>& src, const spg_dcsr* r, i
       return e ? std::atoi(e) : 1;
     }();
     const int64_t m = src.nrows;
-    if (!on || c->pipeline == SPG_PIPE_BINS || m == 0 || ncols_out <= 0 || r->nnz >= (int64_t{1} << 31) - 64)
+    if (!on || c->pipeline != SPG_PIPE_AUTO || m == 0 || ncols_out <= 0 || r->nnz >= (int64_t{1} << 31) - 64)
       return false;
     // explicit zeros in either operand would have to vanish from C: not this path
     {

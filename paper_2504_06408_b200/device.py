@@ -35,11 +35,13 @@ class Context:
     def set_scratch_budget(self, nbytes: int):
         check(lib.spg_ctx_set_scratch_budget(self.handle, int(nbytes)), self.handle)
 
-    PIPE_AUTO, PIPE_BINS = 0, 1
+    PIPE_AUTO, PIPE_BINS, PIPE_SORTED = 0, 1, 2
 
     def set_pipeline(self, mode: int):
         """PIPE_AUTO: bitmap-rank kernels for long rows when the output width
-        fits; PIPE_BINS: the per-bin accumulators with scratch + compaction."""
+        fits; PIPE_BINS: the per-bin accumulators with scratch + compaction;
+        PIPE_SORTED: PIPE_BINS with every dense-panel row on the sort fallback
+        (bin 11, otherwise only for outputs too wide for dense panels)."""
         check(lib.spg_ctx_set_pipeline(self.handle, int(mode)), self.handle)
 
     def close(self):

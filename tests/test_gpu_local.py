@@ -327,3 +327,58 @@ def test_heavy_and_dense_rows_share_the_chunk_table(bins_ctx, sr, ncols):
     got = esc_multiply(a, b, ctx=bins_ctx, stats=st)
     assert_same(got, ob.orc_multiply(to_mat(a), to_mat(b)), sr, rtol=RTOL if sr == 0 else None)
     assert st["rows_per_bin"][6] >= 2 and st["output_mode"] == 0, st
+
+
+BIN_WIDE = 11
+
+
+@pytest.mark.parametrize("sr", [0, 3, 5])
+def test_wide_rows_sort_fallback_at_4m_columns(ctx, sr):
+    """Rows with more distinct outputs than the largest shared-memory hash
+    (> 4096 for 8/16-byte values) over 4 M columns, where the dense panels'
+    per-segment offsets no longer fit shared memory (ER max-times at 1x1):
+    the products are sorted in HBM and folded in the reference's order
+    (bin 11), next to ordinary hash rows.  Overlapping right-operand rows make
+    duplicates; fp64 uses non-integer values."""
+    rng = np.random.default_rng(31 + sr)
+    from golden.make_golden import exact_values
+    ncols, nb, blen = 1 << 22, 80, 100
+    pool = np.sort(rng.choice(ncols, 12000, replace=False))
+    b_cols = [np.sort(rng.choice(pool, blen, replace=False)) for _ in range(nb)]
+    bptr = np.concatenate([[0], np.cumsum([len(x) for x in b_cols])]).astype(np.int64)
+    bc = np.concatenate(b_cols).astype(np.int64)
+    bv = rng.standard_normal(bc.size) if sr == 0 else exact_values(sr, rng, bc.size)
+    b = CsrMatrix(sr, nb, ncols, bptr, bc, bv)
+    rows = [np.arange(nb), np.arange(0, nb, 2), np.arange(10), np.zeros(0, np.int64), np.arange(70)]
+    aptr = np.concatenate([[0], np.cumsum([len(x) for x in rows])]).astype(np.int64)
+    ac = np.concatenate(rows).astype(np.int64)
+    av = rng.standard_normal(ac.size) if sr == 0 else exact_values(sr, rng, ac.size)
+    a = CsrMatrix(sr, len(rows), nb, aptr, ac, av)
+    st = {}
+    got = esc_multiply(a, b, ctx=ctx, stats=st)
+    assert_same(got, ob.orc_multiply(to_mat(a), to_mat(b)), sr, rtol=RTOL if sr == 0 else None)
+    assert st["rows_per_bin"][BIN_WIDE] >= 2, st["rows_per_bin"]
+
+
+@pytest.mark.parametrize("sr", [0, 1, 2, 4, 5])
+def test_sorted_pipeline_equals_oracle_on_dense_rows(ctx, sr):
+    """PIPE_SORTED sends every dense-panel row through the sort fallback:
+    long R-MAT rows (with exact cancellations possible for fp64) must give
+    the same C as the oracle, in every output mode the fallback serves."""
+    m = coo_to_csr(generators.generate_rmat(sr, 12, 16.0, 4))
+    d = DeviceCsr.upload(ctx, m)
+    ctx.set_pipeline(ctx.PIPE_SORTED)
+    try:
+        st = {}
+        got = local_multiply(d, d, stats=st).download()
+        assert st["rows_per_bin"][BIN_WIDE] > 0 and st["rows_per_bin"][6] == 0, st["rows_per_bin"]
+        ctx.set_scratch_budget(1 << 20)  # exact-claim / two-pass modes
+        st2 = {}
+        got2 = local_multiply(d, d, stats=st2).download()
+        assert st2["output_mode"] in (1, 2)
+    finally:
+        ctx.set_pipeline(ctx.PIPE_AUTO)
+        ctx.set_scratch_budget(0)
+    want = ob.orc_multiply(to_mat(m), to_mat(m))
+    assert_same(got, want, sr, rtol=RTOL if sr == 0 else None)
+    assert_same(got2, want, sr, rtol=RTOL if sr == 0 else None)

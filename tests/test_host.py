@@ -205,3 +205,15 @@ def test_host_local_block_matches_reference_distribute(p):
         csc = formats.dcsc_decompress(blk.storage) if blk.is_dcsc else blk.storage
         assert np.array_equal(csc.colptr, want.ptr) and np.array_equal(csc.rowids, want.idx)
         assert csc.values.tobytes() == want.vals.tobytes()
+
+
+def test_library_never_calls_exit():
+    """A __device__-only member called from host code compiles to a host stub
+    that calls exit(1) (the process vanishes with status 1, no error):
+    the shipped library must contain no call to exit."""
+    import shutil
+    import subprocess
+    if not shutil.which("objdump"):
+        pytest.skip("objdump not installed")
+    dis = subprocess.run(["objdump", "-d", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "<exit@plt>" not in dis
