@@ -446,6 +446,28 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
   bin_scatter_kernel<<<grid_for(c, m, 1024, 2), 1024, 0, c->stream>>>(bins.p, m, cursor.p, lists.p);
   SPG_LAUNCH_CHECK();
   ++c->launches;
+  // Row order inside each bin: the scatter's block arrival order scatters a
+  // bin's rows over ~300K-row spans, while neighbouring rows of A usually
+  // share right-operand rows — CTAs on nearby rows keep those in L2
+  // (27-point stencil: the right operand's rows i +- N^2 stay resident).
+  if (m >= 65536) {
+    int row_bits = 1;
+    while ((int64_t{1} << row_bits) < m) ++row_bits;
+    DBuf<int64_t> alt(c, m);
+    for (int b = 1; b < kNumBins; ++b) {
+      const int64_t nbin = (int64_t)hcounts[b];
+      if (b == kBinDense || nbin < 2) continue;  // dense rows are ordered by F below
+      cub::DoubleBuffer<int64_t> db(lists.p + base[b], alt.p + base[b]);
+      size_t bytes = 0;
+      SPG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, db, (int)nbin, 0, row_bits, c->stream));
+      ensure_cub_tmp(c, bytes);
+      SPG_CUDA(cub::DeviceRadixSort::SortKeys(c->cub_tmp, bytes, db, (int)nbin, 0, row_bits, c->stream));
+      ++c->launches;
+      if (db.Current() != lists.p + base[b])
+        SPG_CUDA(cudaMemcpyAsync(lists.p + base[b], db.Current(), sizeof(int64_t) * nbin, cudaMemcpyDeviceToDevice,
+                                 c->stream));
+    }
+  }
   // dense bin: largest rows first
   const int64_t nd = (int64_t)hcounts[kBinDense];
   const int64_t* dense_rows = lists.p + base[kBinDense];
