@@ -302,6 +302,9 @@ __device__ __forceinline__ void br_items(const Src& src, const BrPack<typename S
   }
 }
 
+#ifndef SPG_BR_EMIT_LIGHT
+#define SPG_BR_EMIT_LIGHT 4  // fold: words with more columns are expanded warp-cooperatively (0: lane loops)
+#endif
 #ifndef SPG_BR_IPL
 #define SPG_BR_IPL 4  // numeric: 32-item steps per warp iteration (loads in flight)
 #endif
@@ -586,6 +589,44 @@ __global__ void __launch_bounds__(THREADS, MINB) br_numeric_kernel(
       int start = incl - tcnt;
       for (int w = 0; w < wid; ++w) start += s_wsum[w];
       int rk = start + (tcnt - thi);  // rank of the first word visited (word rot of the chunk)
+      auto put = [&](int r, uint32_t col) {
+        if constexpr (sizeof(V) >= 4) stage[r] = col;
+        else ccols[base + r0 + r] = col;
+      };
+#if SPG_BR_EMIT_LIGHT > 0
+      // words with <= SPG_BR_EMIT_LIGHT columns: expanded by their lane;
+      // denser words: by the whole warp, one bit per lane (no lane waits
+      // for another lane's long bit loop)
+      for (int k = 0; k < L; ++k) {
+        if (k == L - rot) rk = start;  // wrapped to word 0 of the chunk
+        const int j = jt0 + ((k + rot) & (L - 1));
+        uint32_t x = 0u;
+        if (j < nw) {
+          x = bm[j];
+          pre16[j] = (uint16_t)rk;
+        }
+        const uint32_t cb = (uint32_t)(wb + j) << 5;
+        const int pc = __popc(x);
+        SPG_DCHECK(rk + pc <= nr);
+        if (pc <= SPG_BR_EMIT_LIGHT) {
+          uint32_t y = x;
+#pragma unroll
+          for (int u = 0; u < SPG_BR_EMIT_LIGHT; ++u)
+            if (y) {
+              put(rk + u, cb + __ffs(y) - 1);
+              y &= y - 1;
+            }
+        }
+        for (unsigned hm = __ballot_sync(kFull, pc > SPG_BR_EMIT_LIGHT); hm; hm &= hm - 1) {
+          const int srcl = __ffs(hm) - 1;
+          const uint32_t xh = __shfl_sync(kFull, x, srcl);
+          const int rh = __shfl_sync(kFull, rk, srcl);
+          const uint32_t cbh = __shfl_sync(kFull, cb, srcl);
+          if ((xh >> lane) & 1u) put(rh + __popc(xh & ((1u << lane) - 1u)), cbh + lane);
+        }
+        rk += pc;
+      }
+#else
       for (int k = 0; k < L; ++k) {
         if (k == L - rot) rk = start;  // wrapped to word 0 of the chunk
         const int j = jt0 + ((k + rot) & (L - 1));
@@ -594,13 +635,10 @@ __global__ void __launch_bounds__(THREADS, MINB) br_numeric_kernel(
           pre16[j] = (uint16_t)rk;
           const uint32_t cb = (uint32_t)(wb + j) << 5;
           SPG_DCHECK(rk + __popc(x) <= nr);
-          if constexpr (sizeof(V) >= 4) {
-            for (uint32_t y = x; y; y &= y - 1) stage[rk++] = cb + __ffs(y) - 1;
-          } else {
-            for (uint32_t y = x; y; y &= y - 1) ccols[base + r0 + rk++] = cb + __ffs(y) - 1;
-          }
+          for (uint32_t y = x; y; y &= y - 1) put(rk++, cb + __ffs(y) - 1);
         }
       }
+#endif
     }
     __syncthreads();
     BR_T(3);

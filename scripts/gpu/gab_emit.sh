@@ -1,0 +1,4 @@
+export VARIANTS="emit0 emit8"
+bash scripts/gpu/ab.sh
+bash scripts/gpu/ab.sh
+timeout 600 python -m pytest tests/test_gpu_bitmap_rank.py -x -q -m gpu 2>&1 | tail -2
