@@ -303,7 +303,7 @@ __device__ __forceinline__ void br_items(const Src& src, const BrPack<typename S
 }
 
 #ifndef SPG_BR_EMIT_LIGHT
-#define SPG_BR_EMIT_LIGHT 4  // fold: words with more columns are expanded warp-cooperatively (0: lane loops)
+#define SPG_BR_EMIT_LIGHT 0  // > 0: words with more columns expanded warp-cooperatively (measured slower: 4 -> +1.6 ms, 8 -> +0.7 ms)
 #endif
 #ifndef SPG_BR_IPL
 #define SPG_BR_IPL 4  // numeric: 32-item steps per warp iteration (loads in flight)

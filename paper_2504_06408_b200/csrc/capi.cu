@@ -248,6 +248,8 @@ class HostPool {
   uint64_t gen_ = 0;
 };
 
+constexpr double kGpuWiden = 0.0;  // share of index chunks widened on the GPU (measured: see DESIGN §6)
+
 void download(spg_ctx* c, int vs, const spg_dcsr* d, int is_csc, spg_hcsr* h) {
   const int64_t nseg = is_csc ? d->ncols : d->nrows;
   h->nrows = d->nrows;
@@ -261,19 +263,29 @@ void download(spg_ctx* c, int vs, const spg_dcsr* d, int is_csc, spg_hcsr* h) {
     // int32 indices cross PCIe in chunks through two pinned staging buffers
     // and are widened to the reference's int64 by host threads while the
     // next chunk (and finally the values) is in flight: 4 + V bytes per
-    // entry on the bus instead of 8 + V
+    // entry on the bus instead of 8 + V.  A fraction of the chunks
+    // (SPG_D2H_GPU_WIDEN, default kGpuWiden) is widened on the GPU and crosses
+    // as int64 instead, balancing PCIe bytes against host memory bandwidth.
     const int64_t chunk = std::min<int64_t>(int64_t(1) << 25, d->nnz);
     int32_t* stage[2] = {static_cast<int32_t*>(pinned().get(sizeof(int32_t) * chunk)),
                          static_cast<int32_t*>(pinned().get(sizeof(int32_t) * chunk))};
     cudaEvent_t ev[2];
     for (auto& e : ev) SPG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    auto widen = [&](int k) {
+    static const double gpu_frac = [] {
+      const char* e = std::getenv("SPG_D2H_GPU_WIDEN");
+      const double f = e ? std::atof(e) : kGpuWiden;
+      return f < 0 ? 0.0 : f > 1 ? 1.0 : f;
+    }();
+    DBuf<int64_t> dwide[2];
+    if (gpu_frac > 0)
+      for (auto& b : dwide) b = DBuf<int64_t>(c, (size_t)chunk);
+    auto widen = [&](int k, int slot) {
       const int64_t o = (int64_t)k * chunk, n = std::min<int64_t>(chunk, d->nnz - o);
       {
         HostTrace ht("download: wait chunk", (size_t)k);
-        SPG_CUDA(cudaEventSynchronize(ev[k & 1]));
+        SPG_CUDA(cudaEventSynchronize(ev[slot]));
       }
-      const int32_t* in = stage[k & 1];
+      const int32_t* in = stage[slot];
       int64_t* out = h->idx + o;
       HostTrace ht("download: widen chunk", (size_t)k);
       HostPool::get().parallel_for(n, [&](int64_t lo, int64_t hi) {
@@ -290,13 +302,26 @@ void download(spg_ctx* c, int vs, const spg_dcsr* d, int is_csc, spg_hcsr* h) {
     SPG_CUDA(cudaStreamWaitEvent(side, ready, 0));
     SPG_CUDA(cudaMemcpyAsync(h->vals, d->vals, (size_t)vs * d->nnz, cudaMemcpyDeviceToHost, side));
     try {
+      int hosted = 0, gpu = 0, pending = -1, pending_slot = 0;
       for (int k = 0; k < nch; ++k) {
         const int64_t o = (int64_t)k * chunk, n = std::min<int64_t>(chunk, d->nnz - o);
-        SPG_CUDA(cudaMemcpyAsync(stage[k & 1], d->idx + o, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
-        SPG_CUDA(cudaEventRecord(ev[k & 1], c->stream));
-        if (k > 0) widen(k - 1);
+        // Bresenham spread: chunk k goes wide on the GPU when the running share falls behind gpu_frac
+        if (gpu_frac > 0 && (double)(gpu + 1) <= gpu_frac * (double)(k + 1) + 1e-9) {
+          widen_indices(c, d->idx + o, dwide[gpu & 1].p, n);
+          SPG_CUDA(cudaMemcpyAsync(h->idx + o, dwide[gpu & 1].p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost,
+                                   c->stream));
+          ++gpu;
+          continue;
+        }
+        const int slot = hosted & 1;
+        SPG_CUDA(cudaMemcpyAsync(stage[slot], d->idx + o, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
+        SPG_CUDA(cudaEventRecord(ev[slot], c->stream));
+        if (pending >= 0) widen(pending, pending_slot);  // the chunk before this one (its slot is the other)
+        pending = k;
+        pending_slot = slot;
+        ++hosted;
       }
-      widen(nch - 1);
+      if (pending >= 0) widen(pending, pending_slot);
       SPG_CUDA(cudaStreamSynchronize(side));
     } catch (...) {
       cudaStreamSynchronize(side);
