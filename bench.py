@@ -343,7 +343,7 @@ def run_single(args):
     unpin = pin(a.rowptr, a.colids, a.values)  # inputs in pinned host memory
     e2e_times = []
     h2d = 2 * (8 * (a.nrows + 1) + 8 * a.nnz + vs * a.nnz)
-    d2h = 8 * (a.nrows + 1) + (4 + vs) * nnz_c  # int32 indices cross PCIe, widened on the host
+    d2h = 8 * (a.nrows + 1) + (8 + vs) * nnz_c  # int64 indices (widened on the GPU) + values cross PCIe
     for k in range(args.e2e_steps + (1 if args.e2e_steps > 0 else 0)):
         t0 = time.perf_counter()
         ch = esc_multiply(a, a, ctx=ctx)
@@ -569,7 +569,7 @@ def run_summa(args):
             if k == 0:
                 del host_c
                 c2.free()
-        d2h = 8 * (host_c.ncols + 1) + (4 + wl["vs"]) * host_c.nnz  # int32 indices on the bus
+        d2h = 8 * (host_c.ncols + 1) + (8 + wl["vs"]) * host_c.nnz  # int64 indices (widened on the GPU) + values
         del host_c
         c2.free()
 

@@ -248,7 +248,10 @@ class HostPool {
   uint64_t gen_ = 0;
 };
 
-constexpr double kGpuWiden = 0.0;  // share of index chunks widened on the GPU (measured: see DESIGN §6)
+// share of index chunks widened on the GPU: config-2 e2e 0.340 s at 0 (host
+// widening bound), 0.307 s at 0.4 and at 1 (PCIe bound, ~55 GB/s) — 1 leaves
+// the host threads idle
+constexpr double kGpuWiden = 1.0;
 
 void download(spg_ctx* c, int vs, const spg_dcsr* d, int is_csc, spg_hcsr* h) {
   const int64_t nseg = is_csc ? d->ncols : d->nrows;
@@ -277,8 +280,17 @@ void download(spg_ctx* c, int vs, const spg_dcsr* d, int is_csc, spg_hcsr* h) {
       return f < 0 ? 0.0 : f > 1 ? 1.0 : f;
     }();
     DBuf<int64_t> dwide[2];
-    if (gpu_frac > 0)
-      for (auto& b : dwide) b = DBuf<int64_t>(c, (size_t)chunk);
+    double frac = gpu_frac;
+    if (frac > 0) {  // no room for the two device staging buffers: widen everything on the host
+      for (auto& b : dwide) {
+        int64_t* p = try_dalloc<int64_t>(c, (size_t)chunk);
+        if (!p) {
+          frac = 0;
+          break;
+        }
+        b = DBuf<int64_t>::adopt(c, p, (size_t)chunk);
+      }
+    }
     auto widen = [&](int k, int slot) {
       const int64_t o = (int64_t)k * chunk, n = std::min<int64_t>(chunk, d->nnz - o);
       {
@@ -306,7 +318,7 @@ void download(spg_ctx* c, int vs, const spg_dcsr* d, int is_csc, spg_hcsr* h) {
       for (int k = 0; k < nch; ++k) {
         const int64_t o = (int64_t)k * chunk, n = std::min<int64_t>(chunk, d->nnz - o);
         // Bresenham spread: chunk k goes wide on the GPU when the running share falls behind gpu_frac
-        if (gpu_frac > 0 && (double)(gpu + 1) <= gpu_frac * (double)(k + 1) + 1e-9) {
+        if (frac > 0 && (double)(gpu + 1) <= frac * (double)(k + 1) + 1e-9) {
           widen_indices(c, d->idx + o, dwide[gpu & 1].p, n);
           SPG_CUDA(cudaMemcpyAsync(h->idx + o, dwide[gpu & 1].p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost,
                                    c->stream));

@@ -382,3 +382,30 @@ def test_sorted_pipeline_equals_oracle_on_dense_rows(ctx, sr):
     want = ob.orc_multiply(to_mat(m), to_mat(m))
     assert_same(got, want, sr, rtol=RTOL if sr == 0 else None)
     assert_same(got2, want, sr, rtol=RTOL if sr == 0 else None)
+
+
+def test_download_with_split_index_widening():
+    """The host result's int64 column indices come back in 2^25-entry chunks,
+    a share widened on the GPU (crossing PCIe as int64) and the rest widened
+    by host threads from int32 staging (SPG_D2H_GPU_WIDEN=0.5 here, read once
+    per process): the host C equals the device C (checksum of the uploaded
+    host result vs the device checksum)."""
+    import os
+    import subprocess
+    import sys
+    code = """
+import sys
+from paper_2504_06408_b200 import Context, DeviceCsr, esc_multiply, generators, local_multiply, matrix_checksum
+a = generators.coo_to_csr_fast(generators.generate_rmat(4, 16, 16.0, 3))
+ctx = Context(0)
+c = esc_multiply(a, a, ctx=ctx)
+assert c.nnz > 2 * (1 << 25), c.nnz
+d = DeviceCsr.upload(ctx, a)
+dc = local_multiply(d, d)
+assert matrix_checksum(c, ctx) == dc.checksum()
+print("ok", c.nnz)
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {**os.environ, "SPG_D2H_GPU_WIDEN": "0.5", "PYTHONPATH": root}
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.startswith("ok"), r.stdout + r.stderr
