@@ -409,3 +409,31 @@ print("ok", c.nnz)
     env = {**os.environ, "SPG_D2H_GPU_WIDEN": "0.5", "PYTHONPATH": root}
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.startswith("ok"), r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("sr", [0, 4, 5])
+def test_optimistic_small_hash_and_overflow_rerun(bins_ctx, sr):
+    """2K-slot bin rows (512 < F <= 1024) run first in a 512-slot table: rows
+    with <= 256 distinct columns finish there, rows with more stop inserting
+    and are re-run in the 2K table — both kinds side by side, against the
+    oracle."""
+    rng = np.random.default_rng(77 + sr)
+    from golden.make_golden import exact_values
+    ncols, nb, blen = 1_000_000, 40, 25  # column spans > 2^18: no bit-rank window
+    narrow = np.sort(rng.choice(ncols, 200, replace=False))
+    b_cols = [np.sort(rng.choice(narrow if k < nb // 2 else ncols, blen, replace=False)) for k in range(nb)]
+    bptr = np.concatenate([[0], np.cumsum([len(x) for x in b_cols])]).astype(np.int64)
+    bc = np.concatenate(b_cols).astype(np.int64)
+    b = CsrMatrix(sr, nb, ncols, bptr, bc, exact_values(sr, rng, bc.size))
+    lo, hi = np.arange(nb // 2), np.arange(nb // 2, nb)
+    # F = 550 / 550 / 525 products; <= 250, ~500, <= 225 distinct columns
+    rows = [np.concatenate([lo, hi[:2]]), np.concatenate([lo[:2], hi]), np.concatenate([lo, hi[:1]])]
+    aptr = np.concatenate([[0], np.cumsum([len(x) for x in rows])]).astype(np.int64)
+    ac = np.concatenate(rows).astype(np.int64)
+    a = CsrMatrix(sr, len(rows), nb, aptr, ac, exact_values(sr, rng, ac.size))
+    st = {}
+    got = esc_multiply(a, b, ctx=bins_ctx, stats=st)
+    assert_same(got, ob.orc_multiply(to_mat(a), to_mat(b)), sr, rtol=RTOL if sr == 0 else None)
+    assert st["rows_per_bin"][5] == 3, st["rows_per_bin"]
+    nnz = np.diff(got.rowptr)
+    assert nnz[0] <= 256 < nnz[1]  # one row fits the small table, one overflows
