@@ -305,6 +305,9 @@ __device__ __forceinline__ void br_items(const Src& src, const BrPack<typename S
 #ifndef SPG_BR_EMIT_LIGHT
 #define SPG_BR_EMIT_LIGHT 0  // > 0: words with more columns expanded warp-cooperatively (measured slower: 4 -> +1.6 ms, 8 -> +0.7 ms)
 #endif
+#ifndef SPG_BR_EMIT_FLAT
+#define SPG_BR_EMIT_FLAT 1  // fold emission: one bit loop across a lane's words (0: a bit loop per word)
+#endif
 #ifndef SPG_BR_IPL
 #define SPG_BR_IPL 4  // numeric: 32-item steps per warp iteration (loads in flight)
 #endif
@@ -625,6 +628,31 @@ __global__ void __launch_bounds__(THREADS, MINB) br_numeric_kernel(
           if ((xh >> lane) & 1u) put(rh + __popc(xh & ((1u << lane) - 1u)), cbh + lane);
         }
         rk += pc;
+      }
+#elif SPG_BR_EMIT_FLAT
+      // one loop over all the columns of the lane's L words (a word is
+      // entered when the previous one is exhausted): the warp runs
+      // max-over-lanes(columns + words) steps instead of, per word,
+      // max-over-lanes(columns of that word)
+      {
+        int k = -1;
+        uint32_t y = 0u, cb = 0u;
+        for (;;) {
+          while (y == 0u && k + 1 < L) {
+            ++k;
+            if (k == L - rot) rk = start;  // wrapped to word 0 of the chunk
+            const int j = jt0 + ((k + rot) & (L - 1));
+            if (j < nw) {
+              y = bm[j];
+              pre16[j] = (uint16_t)rk;
+              cb = (uint32_t)(wb + j) << 5;
+              SPG_DCHECK(rk + __popc(y) <= nr);
+            }
+          }
+          if (y == 0u) break;
+          put(rk++, cb + __ffs(y) - 1);
+          y &= y - 1;
+        }
       }
 #else
       for (int k = 0; k < L; ++k) {
