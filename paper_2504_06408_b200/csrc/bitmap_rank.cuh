@@ -306,7 +306,7 @@ __device__ __forceinline__ void br_items(const Src& src, const BrPack<typename S
 #define SPG_BR_EMIT_LIGHT 0  // > 0: words with more columns expanded warp-cooperatively (measured slower: 4 -> +1.6 ms, 8 -> +0.7 ms)
 #endif
 #ifndef SPG_BR_EMIT_FLAT
-#define SPG_BR_EMIT_FLAT 1  // fold emission: one bit loop across a lane's words (0: a bit loop per word)
+#define SPG_BR_EMIT_FLAT 0  // 1: one bit loop across a lane's words (measured slower: 21.2 vs 19.0 ms)
 #endif
 #ifndef SPG_BR_IPL
 #define SPG_BR_IPL 4  // numeric: 32-item steps per warp iteration (loads in flight)
