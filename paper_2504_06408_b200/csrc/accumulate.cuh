@@ -1707,12 +1707,17 @@ struct HashSort {
 // slot), writes nothing and is listed in ovf_rows for a re-run in a full-size
 // table.  A stencil row (729 products, 125 outputs) then touches 512 slots
 // instead of 2048, at 4x the CTAs per SM.
-template <class SR, class Src, int T, int THREADS, bool OPT = false>
+// GRED: the slot values live in a per-CTA table in global memory (gtab,
+// zero on entry and left zero) and fold with acc_global (a native L2
+// reduction for fp64 +, instead of a shared-memory CAS loop); after a row's
+// fold its occupied slots are copied into shared memory and re-zeroed.
+template <class SR, class Src, int T, int THREADS, bool OPT = false, bool GRED = false>
 __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64_t* __restrict__ rows,
                                                             int64_t nrows_bin, int cap, int end_bit,
                                                             RowOut<typename SR::value_type> out,
                                                             unsigned long long* ovf_n = nullptr,
-                                                            int64_t* ovf_rows = nullptr) {
+                                                            int64_t* ovf_rows = nullptr,
+                                                            typename SR::value_type* gtab = nullptr) {
   using V = typename SR::value_type;
   using HS = HashSort<T, THREADS>;
   __shared__ long long s_base;
@@ -1738,11 +1743,12 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
   SegCache<SR, Src> cache;
   cache.carve(reinterpret_cast<unsigned char*>(tmp) + ((sizeof(typename HS::Tmp) + 15) & ~size_t(15)), cap, 1);
   const int shift = end_bit > LOG2T - 1 ? end_bit - (LOG2T - 1) : 0;
+  V* gv = GRED ? gtab + (size_t)blockIdx.x * T : nullptr;
   for (int64_t r = blockIdx.x; r < nrows_bin; r += gridDim.x) {
     const int64_t i = rows[r];
     for (int e = threadIdx.x; e < T; e += THREADS) {
       tkeys[e] = kEmptyKey;
-      tvals[e] = SR::zero();
+      if constexpr (!GRED) tvals[e] = SR::zero();
     }
     if (OPT && threadIdx.x == 0) {
       s_distinct = 0;
@@ -1780,9 +1786,28 @@ __global__ void __launch_bounds__(THREADS) hash_rows_kernel(Src src, const int64
           h = (h + 1) & (T - 1);
           SPG_DCHECK(++probes < T);  // the bin keeps the table at most half full (OPT: < T/2 + THREADS keys)
         }
-        atomic_accumulate<SR, true>(&tvals[h], v);
+        if constexpr (GRED) {
+          if constexpr (std::is_same<V, double>::value)  // fire-and-forget L2 reduction (no returned value)
+            asm volatile("red.global.add.f64 [%0], %1;" ::"l"(gv + h), "d"(v) : "memory");
+          else
+            SR::acc_global(&gv[h], v);
+        } else {
+          atomic_accumulate<SR, true>(&tvals[h], v);
+        }
       });
+      if constexpr (GRED) __threadfence_block();  // the reductions land before any thread reads gv
       __syncthreads();
+    }
+    if constexpr (GRED) {  // occupied slots: value into shared memory, global slot back to zero
+#pragma unroll 4
+      for (int q = 0; q < SPT; ++q) {
+        const int e = threadIdx.x + q * THREADS;
+        if (tkeys[e] != kEmptyKey) {
+          tvals[e] = gv[e];
+          gv[e] = SR::zero();
+        }
+      }
+      __threadfence_block();  // zeros visible before the next row's reductions (after the barriers below)
     }
     if constexpr (OPT) {
       if (s_over) {  // uniform after the barrier: re-run in the full-size table

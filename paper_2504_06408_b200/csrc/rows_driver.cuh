@@ -91,10 +91,14 @@ inline int resident_grid(spg_ctx* c, K kern, int threads, size_t smem, int64_t w
   return (int)std::max<int64_t>(1, std::min<int64_t>(work, cap));
 }
 
+// gtab (optional, gtab_slots entries, zero and left zero): per-CTA value
+// tables in global memory for semirings with a native L2 reduction
+// (has_red_global: fp64 +); the shared-memory table is used otherwise, or
+// when the resident grid needs more slots than gtab holds.
 template <class SR, class Src, int T, int THREADS, bool OPT = false>
 void launch_hash(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* rows, int64_t n, int cap, int end_bit,
                  const RowOut<typename SR::value_type>& out, unsigned long long* ovf_n = nullptr,
-                 int64_t* ovf_rows = nullptr) {
+                 int64_t* ovf_rows = nullptr, typename SR::value_type* gtab = nullptr, size_t gtab_slots = 0) {
   using V = typename SR::value_type;
   const size_t fixed = (size_t)T * (sizeof(V) + sizeof(int32_t) + sizeof(uint32_t)) +
                        ((sizeof(typename HashSort<T, THREADS>::Tmp) + 15) & ~size_t(15)) + 64;
@@ -104,10 +108,27 @@ void launch_hash(spg_ctx* c, cudaStream_t s, const Src& src, const int64_t* rows
   cap = std::min(cap, fit) & ~3;
   if (cap < 32) fail(SPG_ERR_INTERNAL, "hash bin: no shared memory left for the segment cache");
   const size_t smem = fixed + (size_t)cap * per;
-  auto kern = hash_rows_kernel<SR, Src, T, THREADS, OPT>;
+  if constexpr (has_red_global<SR>::value) {
+    static const int gred_on = [] {  // SPG_HASH_GRED=1: L2-reduction tables (config 4: 231 vs 222 ms, kept off)
+      const char* e = std::getenv("SPG_HASH_GRED");
+      return e ? std::atoi(e) : 0;
+    }();
+    if (gred_on && gtab) {
+      auto kern = hash_rows_kernel<SR, Src, T, THREADS, OPT, true>;
+      set_smem(kern, smem);
+      const int grid = resident_grid(c, kern, THREADS, smem, n);
+      if ((size_t)grid * T <= gtab_slots) {
+        kern<<<grid, THREADS, smem, s>>>(src, rows, n, cap, end_bit, out, ovf_n, ovf_rows, gtab);
+        SPG_LAUNCH_CHECK();
+        ++c->launches;
+        return;
+      }
+    }
+  }
+  auto kern = hash_rows_kernel<SR, Src, T, THREADS, OPT, false>;
   set_smem(kern, smem);
   kern<<<resident_grid(c, kern, THREADS, smem, n), THREADS, smem, s>>>(src, rows, n, cap, end_bit, out, ovf_n,
-                                                                        ovf_rows);
+                                                                        ovf_rows, nullptr);
   SPG_LAUNCH_CHECK();
   ++c->launches;
 }
@@ -537,6 +558,19 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
   const bool hash_opt = hash_opt_on && hcounts[kBinHash2K] > 0;
   DBuf<unsigned long long> ovf_n(c, 1);
   DBuf<int64_t> ovf_rows(c, hash_opt ? (size_t)hcounts[kBinHash2K] : 1);
+  // global value tables for the 512- / 2K-slot hash bins (fp64 +): zeroed
+  // once, left zero by every launch
+  DBuf<V> gtab;
+  size_t gtab_slots = 0;
+  static const int gred_env = [] {
+    const char* e = std::getenv("SPG_HASH_GRED");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (has_red_global<SR>::value && gred_env && hcounts[kBinHash2K] > 0) {
+    gtab_slots = (size_t)c->sm_count * 16 * 2048;
+    gtab = DBuf<V>(c, gtab_slots);
+    SPG_CUDA(cudaMemsetAsync(gtab.p, 0, sizeof(V) * gtab_slots, c->stream));
+  }
 
   // One numeric pass over all bins with output placement `o`.
   auto numeric = [&](const RowOut<V>& o) {
@@ -567,9 +601,10 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
       launch_hash<SR, Src, 4096, 256>(c, fk[2], src, lb + base[kBinHash4K], hcounts[kBinHash4K], 256, end_bit, o);
     if (hash_opt)
       launch_hash<SR, Src, 512, 128, true>(c, fk[2], src, lb + base[kBinHash2K], hcounts[kBinHash2K], 64, end_bit, o,
-                                           ovf_n.p, ovf_rows.p);
+                                           ovf_n.p, ovf_rows.p, gtab.p, gtab_slots);
     else if (hcounts[kBinHash2K] > 0)
-      launch_hash<SR, Src, 2048, 128>(c, fk[2], src, lb + base[kBinHash2K], hcounts[kBinHash2K], 256, end_bit, o);
+      launch_hash<SR, Src, 2048, 128>(c, fk[2], src, lb + base[kBinHash2K], hcounts[kBinHash2K], 256, end_bit, o,
+                                      nullptr, nullptr, gtab.p, gtab_slots);
     if (hcounts[kBinEsc512] > 0)
       launch_esc<SR, Src, 128, 4>(c, fk[2], src, lb + base[kBinEsc512], hcounts[kBinEsc512], end_bit, o);
     if (hcounts[kBinBitRank] > 0) {
@@ -605,7 +640,9 @@ void run_rows(spg_ctx* c, const Src& src_in, int64_t ncols_out, spg_dcsr* out, s
     fk.join();
     if (hash_opt) {  // the rows that overflowed the 512-slot table
       const int64_t nov = (int64_t)d2h_scalar(c, ovf_n.p);
-      if (nov > 0) launch_hash<SR, Src, 2048, 128>(c, c->stream, src, ovf_rows.p, nov, 256, end_bit, o);
+      if (nov > 0)
+        launch_hash<SR, Src, 2048, 128>(c, c->stream, src, ovf_rows.p, nov, 256, end_bit, o, nullptr, nullptr, gtab.p,
+                                        gtab_slots);
     }
     if (hcounts[kBinWide] > 0)
       run_wide_rows<SR, Src>(c, src, lb + base[kBinWide], (int64_t)hcounts[kBinWide], prods.p, o);

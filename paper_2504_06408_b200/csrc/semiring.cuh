@@ -61,6 +61,9 @@ struct Arithmetic {
   __device__ __forceinline__ static value_type acc_shared(value_type* p, value_type v) { return atomicAdd(p, v); }
   __device__ __forceinline__ static value_type acc_global(value_type* p, value_type v) { return atomicAdd(p, v); }
 #endif
+  // fp64 add has a native L2 reduction (RED.ADD.F64) but no shared-memory
+  // one (a CAS loop): hash accumulators may keep their values in global memory
+  static constexpr bool red_global = true;
 };
 
 struct MinPlus {
@@ -192,6 +195,17 @@ struct has_acc<SR, decltype((void)SR::acc_shared((typename SR::value_type*)nullp
                                                  typename SR::value_type{}),
                             void())> {
   static constexpr bool value = true;
+};
+
+// Optional `red_global`: acc_global is a native fire-and-forget L2 reduction
+// that beats the shared-memory accumulate (fp64 +).
+template <class SR, class = void>
+struct has_red_global {
+  static constexpr bool value = false;
+};
+template <class SR>
+struct has_red_global<SR, decltype((void)SR::red_global, void())> {
+  static constexpr bool value = SR::red_global;
 };
 
 // Optional `pattern_only` (Boolean): mul(a, b) == one() for non-zero a, b and
