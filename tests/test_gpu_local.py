@@ -181,11 +181,15 @@ def test_wide_output_uses_hash_bins(bins_ctx, sr):
     assert sum(st["rows_per_bin"][i] for i in (3, 4, 7)) >= 2, st["rows_per_bin"]
 
 
+@pytest.mark.parametrize("sorted_rows", [False, True])
 @pytest.mark.parametrize("sr", [1, 2, 4])
-def test_merge_dense_panels_against_oracle(bins_ctx, sr):
+def test_merge_dense_panels_against_oracle(bins_ctx, sr, sorted_rows):
     """Merging long partial rows over a wide block takes the dense panel path
-    with per-partial binary-searched panel bounds; checked against the oracle
+    with per-partial binary-searched panel bounds (or, PIPE_SORTED, the sort
+    fallback of bin 11, folding in partial order); checked against the oracle
     product [I I I] . vstack(partials)."""
+    if sorted_rows:
+        bins_ctx.set_pipeline(bins_ctx.PIPE_SORTED)
     rng = np.random.default_rng(3)
     from golden.make_golden import exact_values
     nrows, ncols, K = 6, 200_000, 3
@@ -206,7 +210,7 @@ def test_merge_dense_panels_against_oracle(bins_ctx, sr):
     want = ob.orc_multiply(L, R)
     assert np.array_equal(out.colptr, want.ptr) and np.array_equal(out.rowids, want.idx)
     assert out.values.tobytes() == want.vals.tobytes()
-    assert st["rows_per_bin"][6] == nrows
+    assert st["rows_per_bin"][11 if sorted_rows else 6] == nrows
 
 
 @pytest.mark.parametrize("N", [7, 24])
