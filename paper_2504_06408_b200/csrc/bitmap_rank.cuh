@@ -763,8 +763,9 @@ __global__ void __launch_bounds__(THREADS, 3) br_pattern_kernel(Src src, const i
   using Red = cub::BlockReduce<int, THREADS>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* bm = reinterpret_cast<uint32_t*>(smem_raw);  // [spw]
+  uint32_t* sm = bm + spw;                                // [spw / 32] summary: bit w = word w non-empty
   BrSegs<V> cs;
-  cs.carve(smem_raw + sizeof(uint32_t) * (size_t)spw, THREADS);
+  cs.carve(smem_raw + sizeof(uint32_t) * ((size_t)spw + spw / 32), THREADS);
   __shared__ union {
     typename Scan::TempStorage scan;
     typename Scan64::TempStorage scan64;
@@ -773,9 +774,11 @@ __global__ void __launch_bounds__(THREADS, 3) br_pattern_kernel(Src src, const i
   __shared__ long long s_row;
   __shared__ int s_any;
   __shared__ int s_wcnt[NW];
-  const int wpt = spw / THREADS;  // contiguous words per thread
+  const int wpt = spw / THREADS;  // contiguous words per thread (<= 32: inside one summary word)
   const int w0 = threadIdx.x * wpt;
+  const uint32_t my_mask = wpt >= 32 ? 0xffffffffu : ((1u << wpt) - 1u) << (w0 & 31);  // my words in sm[w0 >> 5]
   for (int q = threadIdx.x; q < spw; q += THREADS) bm[q] = 0u;
+  for (int q = threadIdx.x; q < spw / 32; q += THREADS) sm[q] = 0u;
   __syncthreads();
   for (;;) {
     if (threadIdx.x == 0) {
@@ -802,12 +805,16 @@ __global__ void __launch_bounds__(THREADS, 3) br_pattern_kernel(Src src, const i
                                                  const int cc = c - cbase;
                                                  SPG_DCHECK(cc >= 0 && (cc >> 5) < spw);
                                                  atomicOr(&bm[cc >> 5], 1u << (cc & 31));
+                                                 atomicOr(&sm[cc >> 10], 1u << ((cc >> 5) & 31));
                                                });
         __syncthreads();
       }
       if (!s_any) continue;  // no products in this super-panel: the bitmap is still clear
+      // only the words the summary marks non-empty are read (and cleared):
+      // a row's outputs fill ~1 % of a 4 M-column output's words
+      const uint32_t mine = sm[w0 >> 5] & my_mask;
       int cnt = 0;
-      for (int k = 0; k < wpt; ++k) cnt += __popc(bm[w0 + k]);
+      for (uint32_t y = mine; y; y &= y - 1) cnt += __popc(bm[(w0 & ~31) + __ffs(y) - 1]);
       if constexpr (MODE == 0) {
         run += Red(tmp.red).Sum(cnt);  // valid in thread 0, the only reader
       } else {
@@ -819,7 +826,8 @@ __global__ void __launch_bounds__(THREADS, 3) br_pattern_kernel(Src src, const i
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
         const int ww = spw / NW, wb0 = wid * ww;
         int wc = 0;
-        for (int k = lane; k < ww; k += 32) wc += __popc(bm[wb0 + k]);
+        for (int k = lane; k < ww; k += 32)
+          if (sm[(wb0 + k) >> 5] & (1u << ((wb0 + k) & 31))) wc += __popc(bm[wb0 + k]);
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) wc += __shfl_xor_sync(kFull, wc, d);
         if (lane == 0) s_wcnt[wid] = wc;
@@ -833,7 +841,9 @@ __global__ void __launch_bounds__(THREADS, 3) br_pattern_kernel(Src src, const i
         }
         const int32_t cb = sp * spw * 32;
         for (int g = 0; g < ww; g += 32) {
-          const uint32_t x = bm[wb0 + g + lane];
+          const uint32_t sg = sm[(wb0 + g) >> 5];  // the group's 32 words (warp-uniform)
+          if (sg == 0u) continue;
+          const uint32_t x = (sg >> lane) & 1u ? bm[wb0 + g + lane] : 0u;
           const int c = __popc(x);
           int incl = c;
 #pragma unroll
@@ -861,7 +871,9 @@ __global__ void __launch_bounds__(THREADS, 3) br_pattern_kernel(Src src, const i
         run += tot;
       }
       __syncthreads();  // counts / emission read the bitmap before it is cleared
-      for (int k = 0; k < wpt; ++k) bm[w0 + k] = 0u;
+      for (uint32_t y = mine; y; y &= y - 1) bm[(w0 & ~31) + __ffs(y) - 1] = 0u;
+      __syncthreads();  // every thread read its summary bits before they are cleared
+      for (int q = threadIdx.x; q < spw / 32; q += THREADS) sm[q] = 0u;
       __syncthreads();
     }
     if constexpr (MODE == 0) {

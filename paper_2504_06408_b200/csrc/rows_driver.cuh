@@ -1211,7 +1211,7 @@ bool run_rows_pattern(spg_ctx* c, const MulSource<SR>& src, const spg_dcsr* r, i
     DBuf<unsigned long long> work(c, 2);
     SPG_CUDA(cudaMemsetAsync(work.p, 0, 2 * sizeof(unsigned long long), c->stream));
     constexpr int kPT = 512;
-    const size_t psmem = sizeof(uint32_t) * (size_t)spw + BrSegs<V>::bytes(kPT) + 64;
+    const size_t psmem = sizeof(uint32_t) * ((size_t)spw + spw / 32) + BrSegs<V>::bytes(kPT) + 64;
     tm.mark(1);
     {  // count pass (long rows) || short rows into their slots
       NvtxRange nv("spg:pattern count + short rows");
