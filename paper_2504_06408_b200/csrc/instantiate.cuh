@@ -34,6 +34,18 @@ SPG_HD uint64_t tuple_hash(int64_t row, int64_t col, const V& v) {
   return splitmix64(h);
 }
 
+// tuple_hash with the segment's coordinate hashed once: `seg_h` is
+// splitmix64(row) (CSR segment) or splitmix64(col + golden) (CSC segment).
+template <class V>
+SPG_HD uint64_t tuple_hash_seg(uint64_t seg_h, int64_t other, bool is_csc, const V& v) {
+  const uint8_t* b = reinterpret_cast<const uint8_t*>(&v);
+  uint64_t fh = 0xcbf29ce484222325ULL;
+#pragma unroll
+  for (int k = 0; k < (int)sizeof(V); ++k) fh = (fh ^ b[k]) * 0x100000001b3ULL;
+  const uint64_t oh = is_csc ? splitmix64((uint64_t)other) : splitmix64((uint64_t)other + 0x9e3779b97f4a7c15ULL);
+  return splitmix64(seg_h ^ oh ^ fh);
+}
+
 // K8: order-free content checksum, warp per segment, one atomic per CTA.
 template <class V>
 __global__ void __launch_bounds__(256) checksum_kernel(int64_t nseg, const int64_t* __restrict__ ptr,
@@ -48,11 +60,11 @@ __global__ void __launch_bounds__(256) checksum_kernel(int64_t nseg, const int64
   unsigned long long acc = 0;
   for (int64_t s = warp; s < nseg; s += nwarps) {
     const int64_t b = ptr[s], e = ptr[s + 1];
-    for (int64_t t = b + lane; t < e; t += 32) {
-      const int64_t other = idx[t];
-      acc += is_csc ? tuple_hash(other + row_off, s + col_off, vals[t])
-                    : tuple_hash(s + row_off, other + col_off, vals[t]);
-    }
+    if (b == e) continue;
+    const uint64_t seg_h = is_csc ? splitmix64((uint64_t)(s + col_off) + 0x9e3779b97f4a7c15ULL)
+                                  : splitmix64((uint64_t)(s + row_off));
+    const int64_t ooff = is_csc ? row_off : col_off;
+    for (int64_t t = b + lane; t < e; t += 32) acc += tuple_hash_seg(seg_h, idx[t] + ooff, is_csc != 0, vals[t]);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
