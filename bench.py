@@ -33,12 +33,22 @@ GRIDS = {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}
 # matrix_checksum (checksum.hpp:20-38) of C = A.A from the CPU oracle's streaming
 # restatement (oracle/spg_oracle.cpp, pinned to the reference): the bench
 # checks its own C against these after the timed loop ("parity" in the line).
-# key: (config, scale, edge factor, seed, permuted)
+# keys: R-MAT (config, scale, edge factor, seed, permuted); stencil (4, N);
+# ER (5, log2 n, d, seed) — configs 4 and 5 from tools/golden_checksums.py
 GOLDEN_CSUM = {
     (2, 18, 16.0, 1, True): 7149000290918998130,
     (2, 18, 16.0, 1, False): 10351070082044141371,
     (3, 22, 16.0, 1, True): 216229255003959338,
+    (4, 252): 16022149531309518969,  # nnz(C) = 1971935064, products = 11512557512
 }
+
+
+def golden_key(args):
+    if args.config == 4:
+        return (4, args.stencil_n)
+    if args.config == 5:
+        return (5, args.er_log2, args.er_d, args.seed)
+    return (args.config, args.scale, args.ef, args.seed, bool(args.permute))
 
 
 def log(*a):
@@ -595,7 +605,7 @@ def run_summa(args):
         peak, peak_kind = peaks()
         h2d = 8 * (blk.storage.ncols + 1) + (8 + wl["vs"]) * blk.storage.nnz
         nnz_c = int(agg[1])
-        golden = GOLDEN_CSUM.get((args.config, args.scale, args.ef, args.seed, bool(args.permute)))
+        golden = GOLDEN_CSUM.get(golden_key(args))
         achieved = float(agg[6]) / (ms * 1e-3) / 1e9
         line = {
             "metric": METRIC, "value": 2.0 * F / (ms * 1e-3) / 1e9, "unit": "Gflop/s", "n_gpus": world,
