@@ -40,6 +40,7 @@ GOLDEN_CSUM = {
     (2, 18, 16.0, 1, False): 10351070082044141371,
     (3, 22, 16.0, 1, True): 216229255003959338,
     (4, 252): 16022149531309518969,  # nnz(C) = 1971935064, products = 11512557512
+    (5, 22, 64, 1): 3744257256882867897,  # nnz(C) = 17171350284, products = 17179606120
 }
 
 
