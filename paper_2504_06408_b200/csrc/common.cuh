@@ -132,6 +132,7 @@ inline cudaError_t pool_alloc(spg_ctx* c, void** p, size_t bytes) {
 // Returns every cached large block to the pool and the pools' idle reserve
 // to the device.
 inline void release_cached(spg_ctx* c) {
+  HostTrace ht("release_cached (out of memory)", c->big_cached);
   for (auto& kv : c->big_free) cudaFreeAsync(kv.second, c->stream);
   c->big_free.clear();
   c->big_cached = 0;
@@ -147,9 +148,15 @@ inline void* dalloc_bytes(spg_ctx* c, size_t bytes, bool allow_fail) {
   HostTrace ht("cudaMallocAsync", bytes);
   const bool big = bytes >= kBigAlloc;
   if (big) {
-    bytes = (bytes + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1);
+    // size classes: rounded up to 1/16 of the request's power of two (>= 2 MB),
+    // so the slightly different buffers of consecutive calls (streamed
+    // batches) reuse one cached block instead of growing the pool — a fresh
+    // 30 GB block costs 0.2-1.2 s of mapping
+    int lg = 63 - __builtin_clzll((unsigned long long)bytes);
+    const size_t gran = std::max<size_t>(size_t(2) << 20, size_t(1) << (lg > 4 ? lg - 4 : 0));
+    bytes = (bytes + gran - 1) / gran * gran;
     auto it = c->big_free.lower_bound(bytes);
-    if (it != c->big_free.end() && it->first <= bytes + bytes / 8) {
+    if (it != c->big_free.end() && it->first <= bytes + bytes / 2) {  // the smallest cached fit, <= 1.5x
       p = it->second;
       c->big_live[p] = it->first;
       c->big_cached -= it->first;

@@ -397,8 +397,15 @@ extern "C" int spg_summa25_multiply(spg_comm* comm, spg_ctx* c, int sr, int64_t 
           std::vector<int64_t> hf((size_t)L.nrows);
           SPG_CUDA(cudaMemcpyAsync(hf.data(), f.p, sizeof(int64_t) * L.nrows, cudaMemcpyDeviceToHost, c->stream));
           SPG_CUDA(cudaStreamSynchronize(c->stream));
-          const uint64_t budget = opts->batch_bytes ? opts->batch_bytes : (uint64_t)(mem_available(c) * 0.25);
+          const uint64_t budget0 = opts->batch_bytes ? opts->batch_bytes : (uint64_t)(mem_available(c) * 0.25);
           const uint64_t per = 4 + (uint64_t)vs;  // bytes per C entry
+          // equal batches (total / ceil(total / budget)): consecutive batches
+          // then need equal buffers, which the block cache hands back instead
+          // of growing the pool (a fresh 30 GB block costs up to 1 s to map)
+          uint64_t total_b = 0;
+          for (int64_t r = 0; r < L.nrows; ++r) total_b += (uint64_t)std::min<int64_t>(hf[r], R.ncols) * per;
+          const uint64_t nbat = std::max<uint64_t>(1, (total_b + budget0 - 1) / std::max<uint64_t>(budget0, 1));
+          const uint64_t budget = std::min<uint64_t>(budget0, (total_b / nbat) + (total_b / nbat) / 32);  // +3 %: no stub batch
           for (int64_t r0 = 0; r0 < L.nrows;) {
             int64_t r1 = r0;
             uint64_t acc = 0;
@@ -413,7 +420,15 @@ extern "C" int spg_summa25_multiply(spg_comm* comm, spg_ctx* c, int sr, int64_t 
             lv.ptr = L.ptr + r0;
             spg_dcsr cb{};
             spg_mult_stats bs{};
+            const auto tb = Clock::now();
             ops->local_multiply(c, &lv, &R, &cb, &bs);
+            if (HostTrace::limit_ms() >= 0)
+              std::fprintf(stderr, "[spg-host] summa batch rows [%lld, %lld) products %lld nnz %lld mode %lld: %.1f ms "
+                                   "(analyse %.1f numeric %.1f compact %.1f) budget %.1f GB, available %.1f GB, "
+                                   "cached %.1f GB\n",
+                           (long long)r0, (long long)r1, (long long)bs.products, (long long)cb.nnz,
+                           (long long)bs.output_mode, ms_since(tb), bs.ms_analyse, bs.ms_numeric, bs.ms_compact,
+                           budget / 1e9, mem_available(c) / 1e9, c->big_cached / 1e9);
             spg_dcsr csc = cb;  // CSR of C^T rows [r0, r1) == CSC of C columns bcb + [r0, r1)
             csc.nrows = block_rows;
             csc.ncols = r1 - r0;
