@@ -824,10 +824,12 @@ __global__ void __launch_bounds__(THREADS, 3) br_pattern_kernel(Src src, const i
         // shuffle search — so each store instruction writes 128 contiguous bytes
         (void)cnt;
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-        const int ww = spw / NW, wb0 = wid * ww;
+        const int ww = spw / NW, wb0 = wid * ww;  // ww <= 1024 words: <= 32 groups of 32 words
+        // lane l holds the summary word of the warp's group l; only non-empty
+        // groups and, inside them, non-empty words are visited
+        const uint32_t swl = lane < (ww >> 5) ? sm[(wb0 >> 5) + lane] : 0u;
         int wc = 0;
-        for (int k = lane; k < ww; k += 32)
-          if (sm[(wb0 + k) >> 5] & (1u << ((wb0 + k) & 31))) wc += __popc(bm[wb0 + k]);
+        for (uint32_t y = swl; y; y &= y - 1) wc += __popc(bm[wb0 + (lane << 5) + __ffs(y) - 1]);
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) wc += __shfl_xor_sync(kFull, wc, d);
         if (lane == 0) s_wcnt[wid] = wc;
@@ -840,9 +842,10 @@ __global__ void __launch_bounds__(THREADS, 3) br_pattern_kernel(Src src, const i
           tot += v;
         }
         const int32_t cb = sp * spw * 32;
-        for (int g = 0; g < ww; g += 32) {
-          const uint32_t sg = sm[(wb0 + g) >> 5];  // the group's 32 words (warp-uniform)
-          if (sg == 0u) continue;
+        for (unsigned gm = __ballot_sync(kFull, swl != 0u); gm; gm &= gm - 1) {
+          const int gl = __ffs(gm) - 1;
+          const uint32_t sg = __shfl_sync(kFull, swl, gl);  // the group's 32 words (warp-uniform)
+          const int g = gl << 5;
           const uint32_t x = (sg >> lane) & 1u ? bm[wb0 + g + lane] : 0u;
           const int c = __popc(x);
           int incl = c;
