@@ -848,6 +848,12 @@ __global__ void __launch_bounds__(THREADS, 3) br_pattern_kernel(Src src, const i
           const int g = gl << 5;
           const uint32_t x = (sg >> lane) & 1u ? bm[wb0 + g + lane] : 0u;
           const int c = __popc(x);
+          if (__all_sync(kFull, c <= 1)) {  // sparse group: one column per non-empty word, ranks by ballot
+            const unsigned m = __ballot_sync(kFull, c != 0);
+            if (c) ccols[o + __popc(m & ((1u << lane) - 1u))] = cb + ((wb0 + g + lane) << 5) + __ffs(x) - 1;
+            o += __popc(m);
+            continue;
+          }
           int incl = c;
 #pragma unroll
           for (int d = 1; d < 32; d <<= 1) {
