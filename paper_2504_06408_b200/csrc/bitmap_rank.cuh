@@ -848,10 +848,15 @@ __global__ void __launch_bounds__(THREADS, 3) br_pattern_kernel(Src src, const i
           const int g = gl << 5;
           const uint32_t x = (sg >> lane) & 1u ? bm[wb0 + g + lane] : 0u;
           const int c = __popc(x);
-          if (__all_sync(kFull, c <= 1)) {  // sparse group: one column per non-empty word, ranks by ballot
-            const unsigned m = __ballot_sync(kFull, c != 0);
-            if (c) ccols[o + __popc(m & ((1u << lane) - 1u))] = cb + ((wb0 + g + lane) << 5) + __ffs(x) - 1;
-            o += __popc(m);
+          if (__reduce_max_sync(kFull, (unsigned)c) <= 3u) {
+            // sparse group (<= 3 columns per word): a lane's first rank is
+            // sum_k popc(ballot(c >= k) below it); each lane writes its own
+            const unsigned m1 = __ballot_sync(kFull, c >= 1), m2 = __ballot_sync(kFull, c >= 2),
+                           m3 = __ballot_sync(kFull, c >= 3), lt = (1u << lane) - 1u;
+            int pos = __popc(m1 & lt) + __popc(m2 & lt) + __popc(m3 & lt);
+            const uint32_t wcb = cb + ((uint32_t)(wb0 + g + lane) << 5);
+            for (uint32_t y = x; y; y &= y - 1) ccols[o + pos++] = wcb + __ffs(y) - 1;
+            o += __popc(m1) + __popc(m2) + __popc(m3);
             continue;
           }
           int incl = c;
