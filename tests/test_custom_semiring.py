@@ -99,3 +99,29 @@ def test_custom_semiring_device_path_and_checksum(ctx, maxmin):
     got = c.download()
     _check(got, a, a)
     assert c.checksum() == matrix_checksum(got, ctx=ctx)
+
+
+@pytest.mark.gpu
+def test_custom_semiring_distribute_folds_duplicates(ctx, maxmin):
+    """spg_distribute with the user's semiring: duplicate tuples fold with the
+    user's add (max) through the fold_runs entry of its ops table, and the
+    (max, min) zero (INT32_MIN) is dropped."""
+    from paper_2504_06408_b200.formats import CooMatrix, dcsc_decompress
+    from paper_2504_06408_b200.summa import distribute
+    rng = np.random.default_rng(9)
+    n, nnz = 120, 3000
+    r = rng.integers(0, n, nnz)
+    c = rng.integers(0, n, nnz)
+    v = rng.integers(-50, 1000, nnz).astype(np.int32)
+    v[rng.random(nnz) < 0.05] = NEG
+    m = CooMatrix(maxmin, n, n, r, c, v)
+    want = np.full((n, n), NEG, dtype=np.int64)
+    np.maximum.at(want, (r, c), v.astype(np.int64))
+    for blk in distribute(ctx, m, 2, 2):
+        s = dcsc_decompress(blk.storage) if blk.is_dcsc else blk.storage
+        (rb, re), (cb, ce) = blk.rows, blk.cols
+        d = np.full((re - rb, ce - cb), NEG, dtype=np.int64)
+        cols = np.repeat(np.arange(ce - cb), np.diff(s.colptr))
+        d[s.rowids, cols] = s.values
+        assert np.array_equal(d, want[rb:re, cb:ce])
+        assert not np.any(s.values == NEG)
