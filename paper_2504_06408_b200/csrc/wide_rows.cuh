@@ -39,6 +39,7 @@ __global__ void __launch_bounds__(256) wide_expand_kernel(Src src, const int64_t
       V mult;
       src.seg(i, s, -1, b, len, sid, mult);
       for (int t = lane; t < len; t += 32) {
+        SPG_DCHECK(o + t < poffs[j + 1]);  // the row's products fit its counted range
         keys[o + t] = hi | (uint32_t)src.col(sid, b + t);
         vals[o + t] = src.item(mult, src.val(sid, b + t));
       }
@@ -103,6 +104,7 @@ __global__ void wide_store_kernel(int64_t nu, const int64_t* __restrict__ keep, 
     if (!keep[u]) continue;
     const int64_t j = (int64_t)(ukeys[u] >> 32);
     if (base[j] < 0) continue;
+    SPG_DCHECK(kpos[u] >= kb[j]);
     const int64_t d = base[j] + (kpos[u] - kb[j]);
     o.cols[d] = (int32_t)(uint32_t)ukeys[u];
     o.vals[d] = uvals[u];
