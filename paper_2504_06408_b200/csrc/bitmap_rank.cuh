@@ -302,6 +302,9 @@ __device__ __forceinline__ void br_items(const Src& src, const BrPack<typename S
   }
 }
 
+#ifndef SPG_BR_SKIP
+#define SPG_BR_SKIP 0  // 1: read the slot first, skip atomics that cannot change it (measured slower: 19.8 vs 19.1 ms)
+#endif
 #ifndef SPG_BR_EMIT_LIGHT
 #define SPG_BR_EMIT_LIGHT 0  // > 0: words with more columns expanded warp-cooperatively (measured slower: 4 -> +1.6 ms, 8 -> +0.7 ms)
 #endif
@@ -694,6 +697,9 @@ __global__ void __launch_bounds__(THREADS, MINB) br_numeric_kernel(
         SPG_DCHECK(j >= 0 && j < nw);
         const int rk = (int)pre16[j] + __popc(bm[j] & ((1u << (c & 31)) - 1u));
         SPG_DCHECK(rk >= 0 && rk < nr && (bm[j] >> (c & 31) & 1u));  // every product column is in the bitmap
+        if constexpr (SPG_BR_SKIP && has_improves<SR>::value) {
+          if (!SR::improves(v, *reinterpret_cast<volatile V*>(&acc[rk]))) return;  // cannot lower the slot
+        }
         atomic_accumulate<SR, true>(&acc[rk], v);
       };
       constexpr int IPL = sizeof(V) > 4 ? 2 : SPG_BR_IPL;

@@ -158,6 +158,8 @@ struct TropicalI32 {
   // fast path (see has_mul_small): |a|, |b| < 2^29 => a + b neither saturates nor hits zero()
   SPG_HD static bool small(value_type v) { return v > -(1 << 29) && v < (1 << 29); }
   SPG_HD static value_type mul_small(value_type a, value_type b) { return a + b; }
+  // add(cur, v) != cur: a fold may skip the atomic when v cannot change the slot
+  SPG_HD static bool improves(value_type v, value_type cur) { return v < cur; }
 #ifdef __CUDACC__
   __device__ __forceinline__ static value_type acc_shared(value_type* p, value_type v) { return atomicMin(p, v); }
   __device__ __forceinline__ static value_type acc_global(value_type* p, value_type v) { return atomicMin(p, v); }
@@ -194,6 +196,18 @@ template <class SR>
 struct has_acc<SR, decltype((void)SR::acc_shared((typename SR::value_type*)nullptr,
                                                  typename SR::value_type{}),
                             void())> {
+  static constexpr bool value = true;
+};
+
+// Optional `improves(v, cur)` (idempotent, monotone adds such as min): true
+// iff add(cur, v) != cur, so a fold may read the slot and skip the atomic
+// when the product cannot change it (hub columns receive many products).
+template <class SR, class = void>
+struct has_improves {
+  static constexpr bool value = false;
+};
+template <class SR>
+struct has_improves<SR, decltype((void)SR::improves(typename SR::value_type{}, typename SR::value_type{}), void())> {
   static constexpr bool value = true;
 };
 
