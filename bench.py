@@ -44,6 +44,19 @@ GOLDEN_CSUM = {
 }
 
 
+def d2h_index_bytes(nnz):
+    """Column-index bytes of a host download: 2^25-entry chunks, a share
+    (SPG_D2H_GPU_WIDEN, library default 0.1) widened on the GPU and sent as
+    int64, the rest sent as int32 and widened on the host."""
+    chunk = 1 << 25
+    nch = (nnz + chunk - 1) // chunk
+    frac = min(max(float(os.environ.get("SPG_D2H_GPU_WIDEN", "0.1")), 0.0), 1.0)
+    gpu = sum(1 for k in range(nch) if frac > 0 and int(frac * (k + 1) + 1e-9) > int(frac * k + 1e-9))
+    wide = sum(min(chunk, nnz - k * chunk) for k in range(nch)
+               if frac > 0 and int(frac * (k + 1) + 1e-9) > int(frac * k + 1e-9))
+    return 4 * nnz + 4 * wide if gpu else 4 * nnz
+
+
 def golden_key(args):
     if args.config == 4:
         return (4, args.stencil_n)
@@ -354,7 +367,7 @@ def run_single(args):
     unpin = pin(a.rowptr, a.colids, a.values)  # inputs in pinned host memory
     e2e_times = []
     h2d = 2 * (8 * (a.nrows + 1) + 8 * a.nnz + vs * a.nnz)
-    d2h = 8 * (a.nrows + 1) + (8 + vs) * nnz_c  # int64 indices (widened on the GPU) + values cross PCIe
+    d2h = 8 * (a.nrows + 1) + vs * nnz_c + d2h_index_bytes(nnz_c)  # rowptr + values + column indices
     for k in range(args.e2e_steps + (1 if args.e2e_steps > 0 else 0)):
         t0 = time.perf_counter()
         ch = esc_multiply(a, a, ctx=ctx)
@@ -580,7 +593,7 @@ def run_summa(args):
             if k == 0:
                 del host_c
                 c2.free()
-        d2h = 8 * (host_c.ncols + 1) + (8 + wl["vs"]) * host_c.nnz  # int64 indices (widened on the GPU) + values
+        d2h = 8 * (host_c.ncols + 1) + wl["vs"] * host_c.nnz + d2h_index_bytes(host_c.nnz)
         del host_c
         c2.free()
 

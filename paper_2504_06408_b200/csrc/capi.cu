@@ -26,6 +26,7 @@ extern "C" const spg::SrOps* spg_ops_maxtimes();
 
 namespace spg {
 void gen_rmat(int, int, double, uint64_t, int64_t*, int64_t*, int64_t**, int64_t**, void**);
+void widen_i32_to_i64(const int32_t* in, int64_t* out, int64_t n);  // hostwiden.cpp
 void gen_er(int, int64_t, int, uint64_t, int, int64_t, int64_t, int64_t, int64_t, int64_t*, int64_t**, int64_t**,
             void**);
 void gen_stencil27(int, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t*, int64_t*, int64_t**, int64_t**, void**);
@@ -248,10 +249,11 @@ class HostPool {
   uint64_t gen_ = 0;
 };
 
-// share of index chunks widened on the GPU: config-2 e2e 0.340 s at 0 (host
-// widening bound), 0.307 s at 0.4 and at 1 (PCIe bound, ~55 GB/s) — 1 leaves
-// the host threads idle
-constexpr double kGpuWiden = 1.0;
+// share of index chunks widened on the GPU (the rest cross PCIe as int32 and
+// are widened by host threads with streaming stores, hostwiden.cpp):
+// config-2 e2e 0.301 s at 0, 0.270-0.276 s at 0.1, 0.272-0.281 s at 0.2,
+// 0.305-0.355 s at 1 (all int64 on the bus: PCIe bound)
+constexpr double kGpuWiden = 0.1;
 
 void download(spg_ctx* c, int vs, const spg_dcsr* d, int is_csc, spg_hcsr* h) {
   const int64_t nseg = is_csc ? d->ncols : d->nrows;
@@ -300,9 +302,7 @@ void download(spg_ctx* c, int vs, const spg_dcsr* d, int is_csc, spg_hcsr* h) {
       const int32_t* in = stage[slot];
       int64_t* out = h->idx + o;
       HostTrace ht("download: widen chunk", (size_t)k);
-      HostPool::get().parallel_for(n, [&](int64_t lo, int64_t hi) {
-        for (int64_t e = lo; e < hi; ++e) out[e] = in[e];
-      });
+      HostPool::get().parallel_for(n, [&](int64_t lo, int64_t hi) { widen_i32_to_i64(in + lo, out + lo, hi - lo); });
     };
     const int nch = (int)((d->nnz + chunk - 1) / chunk);
     // values on a side stream, concurrently with the index pipeline
