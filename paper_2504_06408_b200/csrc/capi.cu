@@ -3,6 +3,7 @@
 // points and the host-array drop-ins.  Every function converts C++
 // exceptions into an SPG_ERR_* status + last-error message.
 #include <algorithm>
+#include <atomic>
 #include <condition_variable>
 #include <cstdlib>
 #include <cstring>
@@ -97,7 +98,9 @@ void need(bool ok, const char* what) {
 
 void use_device(spg_ctx* c) { SPG_CUDA(cudaSetDevice(c->device)); }
 
-// Host CSR/CSC -> device (int64 -> int32 narrowing on device).
+void upload_indices(spg_ctx* c, const int64_t* h, int32_t* d, int64_t n, int64_t bound);  // below
+
+// Host CSR/CSC -> device (int64 indices narrowed to int32 on the way).
 void upload(spg_ctx* c, int vs, const spg_hcsr* h, int is_csc, spg_dcsr* d) {
   const int64_t nseg = is_csc ? h->ncols : h->nrows;
   const int64_t bound = is_csc ? h->nrows : h->ncols;
@@ -114,10 +117,9 @@ void upload(spg_ctx* c, int vs, const spg_hcsr* h, int is_csc, spg_dcsr* d) {
   d->vals = dalloc<char>(c, (size_t)vs * h->nnz);
   SPG_CUDA(cudaMemcpyAsync(d->ptr, h->ptr, sizeof(int64_t) * (nseg + 1), cudaMemcpyHostToDevice, c->stream));
   if (h->nnz > 0) {
-    DBuf<int64_t> wide(c, h->nnz);
-    SPG_CUDA(cudaMemcpyAsync(wide.p, h->idx, sizeof(int64_t) * h->nnz, cudaMemcpyHostToDevice, c->stream));
-    narrow_indices(c, wide.p, d->idx, h->nnz, bound);
+    // values first: their copy runs while host threads narrow the first index chunks
     SPG_CUDA(cudaMemcpyAsync(d->vals, h->vals, (size_t)vs * h->nnz, cudaMemcpyHostToDevice, c->stream));
+    upload_indices(c, h->idx, d->idx, h->nnz, bound);
   }
 }
 
@@ -254,6 +256,61 @@ class HostPool {
 // config-2 e2e 0.301 s at 0, 0.270-0.276 s at 0.1, 0.272-0.281 s at 0.2,
 // 0.305-0.355 s at 1 (all int64 on the bus: PCIe bound)
 constexpr double kGpuWiden = 0.1;
+
+bool narrow_i64_to_i32(const int64_t* in, int32_t* out, int64_t n, int64_t bound);  // hostwiden.cpp
+
+// int64 host indices -> int32 device indices.  Large arrays cross PCIe as
+// int32: host threads narrow (and range-check) 2^25-entry chunks into two
+// pinned staging buffers while the previous chunk is in flight — half the
+// bytes on the bus.  Small arrays (and SPG_H2D_HOST_NARROW=0) go as int64 and
+// are narrowed by a device kernel.  MalformedInputError on an index outside
+// [0, bound) either way.
+void upload_indices(spg_ctx* c, const int64_t* h, int32_t* d, int64_t n, int64_t bound) {
+  if (n <= 0) return;
+  static const int host_narrow = [] {
+    const char* e = std::getenv("SPG_H2D_HOST_NARROW");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (!host_narrow || n < (int64_t(1) << 22)) {
+    DBuf<int64_t> wide(c, n);
+    SPG_CUDA(cudaMemcpyAsync(wide.p, h, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream));
+    narrow_indices(c, wide.p, d, n, bound);
+    return;
+  }
+  const int64_t chunk = std::min<int64_t>(int64_t(1) << 25, n);
+  int32_t* stage[2] = {static_cast<int32_t*>(pinned().get(sizeof(int32_t) * chunk)),
+                       static_cast<int32_t*>(pinned().get(sizeof(int32_t) * chunk))};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  std::atomic<bool> bad{false};
+  auto cleanup = [&] {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    host_release(stage[0]);
+    host_release(stage[1]);
+  };
+  try {
+    for (auto& e : ev) SPG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    const int64_t nch = (n + chunk - 1) / chunk;
+    for (int64_t k = 0; k < nch; ++k) {
+      const int64_t o = k * chunk, m = std::min<int64_t>(chunk, n - o);
+      const int slot = (int)(k & 1);
+      if (k >= 2) SPG_CUDA(cudaEventSynchronize(ev[slot]));  // the copy out of this stage is done
+      int32_t* st = stage[slot];
+      HostPool::get().parallel_for(m, [&](int64_t lo, int64_t hi) {
+        if (!narrow_i64_to_i32(h + o + lo, st + lo, hi - lo, bound)) bad = true;
+      });
+      SPG_CUDA(cudaMemcpyAsync(d + o, st, sizeof(int32_t) * m, cudaMemcpyHostToDevice, c->stream));
+      SPG_CUDA(cudaEventRecord(ev[slot], c->stream));
+    }
+    SPG_CUDA(cudaStreamSynchronize(c->stream));
+  } catch (...) {
+    cudaStreamSynchronize(c->stream);
+    cleanup();
+    throw;
+  }
+  cleanup();
+  if (bad) fail(SPG_ERR_MALFORMED, "index outside [0, " + std::to_string(bound) + ")");
+}
 
 void download(spg_ctx* c, int vs, const spg_dcsr* d, int is_csc, spg_hcsr* h) {
   const int64_t nseg = is_csc ? d->ncols : d->nrows;
@@ -745,10 +802,8 @@ void prepare_block(spg_ctx* c, int sr, const spg_hcsr* csc, const spg_hdcsc* dcs
     SPG_CUDA(cudaMemcpyAsync(cp.p, dcsc->cp, sizeof(int64_t) * (dcsc->njc + 1), cudaMemcpyHostToDevice, c->stream));
     dcsc_colptr(c, dcsc->ncols, dcsc->njc, jc.p, cp.p, out->ptr);
     if (dcsc->nnz > 0) {
-      DBuf<int64_t> wide(c, dcsc->nnz);
-      SPG_CUDA(cudaMemcpyAsync(wide.p, dcsc->rowids, sizeof(int64_t) * dcsc->nnz, cudaMemcpyHostToDevice, c->stream));
-      narrow_indices(c, wide.p, out->idx, dcsc->nnz, dcsc->nrows);
       SPG_CUDA(cudaMemcpyAsync(out->vals, dcsc->vals, (size_t)vs * dcsc->nnz, cudaMemcpyHostToDevice, c->stream));
+      upload_indices(c, dcsc->rowids, out->idx, dcsc->nnz, dcsc->nrows);
     }
   } else {
     spg_dcsr d{};

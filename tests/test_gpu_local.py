@@ -441,3 +441,22 @@ def test_optimistic_small_hash_and_overflow_rerun(bins_ctx, sr):
     assert st["rows_per_bin"][5] == 3, st["rows_per_bin"]
     nnz = np.diff(got.rowptr)
     assert nnz[0] <= 256 < nnz[1]  # one row fits the small table, one overflows
+
+
+def test_large_upload_narrows_on_host_and_checks_range(ctx):
+    """Uploads of >= 2^22 indices cross PCIe as int32, narrowed and
+    range-checked by host threads (two chunks of 2^25 here): the device matrix
+    equals the host one, and an index outside the block raises
+    MalformedInputError as the device narrowing does."""
+    rng = np.random.default_rng(8)
+    n, ncols, per = 1 << 20, 1 << 22, 40
+    ptr = np.arange(0, n * per + 1, per, dtype=np.int64)
+    idx = np.sort(rng.integers(0, ncols, (n, per)), axis=1).reshape(-1).astype(np.int64)
+    vals = rng.integers(0, 100, idx.size).astype(np.int32)
+    m = CsrMatrix(4, n, ncols, ptr, idx, vals)
+    got = DeviceCsr.upload(ctx, m).download()
+    assert np.array_equal(got.colids, idx) and np.array_equal(got.rowptr, ptr)
+    bad = idx.copy()
+    bad[idx.size - 7] = ncols  # one column id past the block
+    with pytest.raises(errors.MalformedInputError):
+        DeviceCsr.upload(ctx, CsrMatrix(4, n, ncols, ptr, bad, vals))
