@@ -44,13 +44,14 @@ GOLDEN_CSUM = {
 }
 
 
-def d2h_index_bytes(nnz):
+def d2h_index_bytes(nnz, procs=1):
     """Column-index bytes of a host download: 2^25-entry chunks, a share
-    (SPG_D2H_GPU_WIDEN, library default 0.1) widened on the GPU and sent as
-    int64, the rest sent as int32 and widened on the host."""
+    (SPG_D2H_GPU_WIDEN; library default 0.1 for one process on the host, 1
+    when several share it) widened on the GPU and sent as int64, the rest
+    sent as int32 and widened on the host."""
     chunk = 1 << 25
     nch = (nnz + chunk - 1) // chunk
-    frac = min(max(float(os.environ.get("SPG_D2H_GPU_WIDEN", "0.1")), 0.0), 1.0)
+    frac = min(max(float(os.environ.get("SPG_D2H_GPU_WIDEN", "0.1" if procs == 1 else "1")), 0.0), 1.0)
     gpu = sum(1 for k in range(nch) if frac > 0 and int(frac * (k + 1) + 1e-9) > int(frac * k + 1e-9))
     wide = sum(min(chunk, nnz - k * chunk) for k in range(nch)
                if frac > 0 and int(frac * (k + 1) + 1e-9) > int(frac * k + 1e-9))
@@ -593,7 +594,7 @@ def run_summa(args):
             if k == 0:
                 del host_c
                 c2.free()
-        d2h = 8 * (host_c.ncols + 1) + wl["vs"] * host_c.nnz + d2h_index_bytes(host_c.nnz)
+        d2h = 8 * (host_c.ncols + 1) + wl["vs"] * host_c.nnz + d2h_index_bytes(host_c.nnz, world)
         del host_c
         c2.free()
 

@@ -274,6 +274,8 @@ int comm_bcast(spg_comm* c, int scope, int root, void* buf, uint64_t bytes, int 
   return path;
 }
 
+void note_host_procs(int n);  // capi.cu: host-side download policy
+
 }  // namespace spg
 
 using namespace spg;
@@ -316,6 +318,7 @@ int spg_comm_create(const char* job, int world, int rank, int pr, int pc, int de
                              std::to_string(world) + " ranks");
     if (rank < 0 || rank >= world) fail(SPG_ERR_GRID, "rank outside the grid");
     c = new spg_comm();
+    spg::note_host_procs(world);  // one node: every rank of the job is on this host
     c->name = std::string("/spg_") + job;
     c->world = world;
     c->rank = rank;
