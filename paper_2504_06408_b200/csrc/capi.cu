@@ -275,7 +275,9 @@ void upload_indices(spg_ctx* c, const int64_t* h, int32_t* d, int64_t n, int64_t
     const char* e = std::getenv("SPG_H2D_HOST_NARROW");
     return e ? std::atoi(e) : 1;
   }();
-  if (!host_narrow || n < (int64_t(1) << 22)) {
+  // (several processes of a job on this host: their threads would share its
+  // memory bandwidth, so the indices go as int64 and narrow on each GPU)
+  if (!host_narrow || n < (int64_t(1) << 22) || g_host_procs.load() > 1) {
     DBuf<int64_t> wide(c, n);
     SPG_CUDA(cudaMemcpyAsync(wide.p, h, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream));
     narrow_indices(c, wide.p, d, n, bound);
